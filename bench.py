@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""Benchmark of one Lloyd iteration (arXiv 2405.12052) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NS|C1..C5]
+                    [--scaling strong|weak] [--impl ours|reference]
+
+A "step" is one pass of the whole hot path over the workload: assign + fused
+per-cluster reduction, deterministic merge, (NCCL allreduce when N > 1), and
+the update (means, E, inertia, stop flag) -- SURVEY.md §8(a) rows a1-a9.
+Inputs are resident in HBM before the timed region; W warm-up steps, then
+exactly K steps between CUDA events on the context's stream, bracketed by a
+barrier and a device synchronize, max over ranks.  The dataset (1.2 GB per
+GPU at the default workload) is larger than the 126 MB L2, so no flush is
+needed between steps.
+
+For N > 1 launch with torchrun (one process per GPU); the library's own NCCL
+communicator is created from a unique id broadcast over torch.distributed.
+
+Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import dataclasses
+import json
+import os
+import platform
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0      # /opt/skills/guides/B200_PROFILING.md fallback
+SMS = 148
+FP32_LANES_PER_SM = 128
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--workload", default="NS")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong")
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--e2e-iters", type=int, default=20)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU time of the oracle baseline sample")
+    ap.add_argument("--ref-seconds", type=float, default=60.0,
+                    help="--impl reference: target CPU time of the whole run")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p.get("sm_max_mhz", 1965.0)), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, 1965.0, "fallback"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor()
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML sampling thread)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index: int, period_s: float = 0.005):
+        self.samples, self.reasons = [], 0
+        self.period = period_s
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - depends on the box
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            self.sample()
+            time.sleep(self.period)
+
+    def sample(self):
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            pass
+
+    def __enter__(self):
+        if self.ok:
+            self.sample()
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+            self.sample()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        names = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle baseline (rank 0, N = 1 only) and the reference arm
+# ---------------------------------------------------------------------------
+def oracle_sample(w, target_s: float):
+    """Times the oracle (as it stands, single thread) on a prefix of the
+    workload: whole Lloyd iterations (oracle.step) until ~target_s of CPU."""
+    import oracle
+    from paper_2405_12052_b200 import datagen
+    n = min(w.N, 2_000_000 if w.K <= 16 else 100_000)
+    X = datagen.generate(w, 0, n, N=w.N)
+    mu = X[datagen.init_indices(w, N=n, K=w.K)].astype(np.float64) if w.planted_sites == 0 \
+        else X[:w.K].astype(np.float64) + np.arange(w.K)[:, None]
+    t0 = time.perf_counter()
+    r = oracle.step(X, mu)
+    one = time.perf_counter() - t0
+    iters = max(1, int(target_s / max(one, 1e-6)) - 1)
+    mu = r["mu_next"]
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        mu = oracle.step(X, mu)["mu_next"]
+    dt = time.perf_counter() - t0
+    return dict(value=n * iters / dt, n=n, iters=iters, seconds=dt)
+
+
+def run_reference(args, w):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0  # under torchrun only rank 0 runs the oracle
+    import oracle
+    from paper_2405_12052_b200 import datagen
+    # size the per-step sample so the whole run takes ~args.ref_seconds of CPU
+    n_cal = min(w.N, 20_000)
+    Xc = datagen.generate(w, 0, n_cal, N=w.N)
+    muc = Xc[:w.K].astype(np.float64) + 0.5
+    t0 = time.perf_counter()
+    oracle.step(Xc, muc)
+    per_point = (time.perf_counter() - t0) / n_cal
+    n = int(args.ref_seconds / max(1, args.steps + args.warmup) / per_point)
+    n = max(min(w.N, 2 * w.K, 1000), min(w.N, n))
+    X = datagen.generate(w, 0, n, N=w.N)
+    mu = X[datagen.init_indices(w, N=n, K=w.K)].astype(np.float64)
+    for _ in range(args.warmup):
+        mu = oracle.step(X, mu)["mu_next"]
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        mu = oracle.step(X, mu)["mu_next"]
+    dt = time.perf_counter() - t0
+    value = n * args.steps / dt
+    sample = (f"{n} of {w.N} points (prefix of the seeded {w.name} workload), "
+              f"{args.steps} whole Lloyd iterations (oracle.step)")
+    line = {
+        "impl": "reference", "metric": "Lloyd points·iter/s", "value": value,
+        "unit": "points·iter/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps * (w.N / n),
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": workload_config(w, args.gpus, args.scaling),
+        "cpu_baseline": {"value": value, "unit": "points·iter/s", "cores": 1,
+                         "kind": "oracle", "sample": sample, "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": "points·iter/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(w, P, scaling):
+    per_gpu = w.N // P if scaling == "strong" else w.N
+    return {"workload": w.name, "N": w.N if scaling == "strong" else w.N * P, "d": w.d,
+            "K": w.K, "per_gpu_N": per_gpu, "blobs": w.M, "tol": 0.0,
+            "parallelism": f"dp{P}",
+            "l2": f"inputs larger than L2 ({per_gpu * w.d * 4 / 1e6:.0f} MB per GPU vs 126 MB)"
+            if per_gpu * w.d * 4 > 126e6 else "inputs fit in L2 (no flush)"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    from paper_2405_12052_b200 import datagen
+    w = datagen.WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, w)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2405_12052_b200 import kmeans as km
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    P = world
+    assert P == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    distributed = P > 1
+    comm = None
+    if distributed:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        uid = [km.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = km.comm_init(P, uid[0], rank, local)
+
+    def barrier():
+        if distributed:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if not distributed:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # shard (contiguous ceiling partition, PAPER.md:97 / SPEC.md:236)
+    global_N = w.N if args.scaling == "strong" else w.N * P
+    a, b = datagen.shard_range(global_N, P, rank)
+    gen_w = w if args.scaling == "strong" else dataclasses.replace(w, N=global_N)
+    Xh = torch.empty((b - a, w.d), dtype=torch.float32, pin_memory=True)
+    datagen.generate(gen_w, a, b - a, N=global_N, out=Xh.numpy())
+    init = datagen.init_indices(gen_w, N=global_N, K=w.K)
+
+    ctx = km.Context(Xh, w.K, device=local, comm=comm, global_offset=a, global_N=global_N)
+    info = ctx.info()
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    ctx.start(init_idx=init, tol=0.0, max_iter=1 << 30)
+
+    # warm-up (also instantiates the CUDA graph)
+    ctx.iterate(args.warmup)
+    ctx.poll()
+    barrier()
+
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.info()["kernel_launches"]
+    with ClockSampler(local) as clocks:
+        barrier()
+        e0.record(stream)
+        ctx.iterate(args.steps)
+        e1.record(stream)
+        e1.synchronize()
+        barrier()
+    launches = ctx.info()["kernel_launches"] - launches0
+    ms = e0.elapsed_time(e1)
+    ms = max_over_ranks(ms)
+    st = ctx.poll()
+    assert st["iters"] == args.warmup + args.steps, st
+
+    value = global_N * args.steps / (ms / 1e3)   # whole-job points·iter/s
+    ms_per_step = ms / args.steps
+
+    # ---- dominant kernel alone (roofline): assign + fused reduction ------------
+    reps = max(20, min(args.steps, 200))
+    ctx.profile_assign(3)
+    torch.cuda.synchronize()
+    a0 = torch.cuda.Event(enable_timing=True)
+    a1 = torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    ctx.profile_assign(reps)
+    a1.record(stream)
+    a1.synchronize()
+    t_assign = a0.elapsed_time(a1) / reps / 1e3        # s per launch
+    n_local = b - a
+    hbm_gbs, sm_max_mhz, peak_src = peaks()
+    clk = clocks.summary()
+    bytes_per_launch = 4.0 * w.d * n_local                      # read every point once
+    lane_ops_per_launch = 2.0 * w.d * w.K * n_local             # form D: d FADD, 1 FMUL, d-1 FFMA
+    fp32_peak = SMS * FP32_LANES_PER_SM * sm_max_mhz * 1e6 / 1e12   # T lane-ops/s
+    achieved_gbs = bytes_per_launch / t_assign / 1e9
+    achieved_tops = lane_ops_per_launch / t_assign / 1e12
+    t_hbm = bytes_per_launch / (hbm_gbs * 1e9)
+    t_alu = lane_ops_per_launch / (fp32_peak * 1e12)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        key = f"{w.name}:P{P}:{args.scaling}"
+        traffic = tj.get(key)
+    except Exception:
+        pass
+    if t_alu >= t_hbm:
+        roofline = {"bound": "alu", "achieved": achieved_tops, "peak": fp32_peak,
+                    "unit": "TFLOP/s", "op": "FP32 lane-op (FADD, FMUL, FFMA = 1 each)",
+                    "frac": achieved_tops / fp32_peak, "traffic": traffic,
+                    "kernel": "k_assign_small" if info["path"] == 0 else "k_assign_large",
+                    "kernel_ms": t_assign * 1e3,
+                    "kernel_share_of_step": t_assign * 1e3 / ms_per_step,
+                    "peak_source": f"148 SMs x 128 FP32 lanes x {sm_max_mhz:.0f} MHz"}
+    else:
+        roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_gbs, "unit": "GB/s",
+                    "frac": achieved_gbs / hbm_gbs, "traffic": traffic,
+                    "kernel": "k_assign_small" if info["path"] == 0 else "k_assign_large",
+                    "kernel_ms": t_assign * 1e3,
+                    "kernel_share_of_step": t_assign * 1e3 / ms_per_step,
+                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
+    roofline_hbm = {"achieved": achieved_gbs, "peak": hbm_gbs, "unit": "GB/s",
+                    "frac": achieved_gbs / hbm_gbs,
+                    "step_frac": (bytes_per_launch / (ms_per_step / 1e3) / 1e9) / hbm_gbs,
+                    "peak_source": peak_src}
+
+    # ---- end to end through the public API with host buffers ------------------------
+    e2e = None
+    if not args.no_e2e:
+        labels_h = torch.empty(n_local, dtype=torch.int32, pin_memory=True)
+        ctx.close()
+        barrier()
+        t0 = time.perf_counter()
+        c2 = km.Context(Xh, w.K, device=local, comm=comm, global_offset=a, global_N=global_N)
+        r = c2.fit(init, 0.0, args.e2e_iters, out_labels=labels_h, traces=False)
+        c2.close()
+        dt = time.perf_counter() - t0
+        barrier()
+        dt = max_over_ranks(dt)
+        assert r["iters"] == args.e2e_iters
+        e2e = {"value": global_N * args.e2e_iters / dt, "unit": "points·iter/s",
+               "h2d_bytes_per_step": int(Xh.numel() * 4 + 8 * w.K),
+               "d2h_bytes_per_step": int(n_local * 4 + 8 * w.K * w.d + 16),
+               "step": f"one kmeans_create + kmeans_fit_ctx ({args.e2e_iters} iterations, "
+                       "labels out) + kmeans_destroy call from pinned host memory",
+               "seconds_per_step": dt}
+    else:
+        ctx.close()
+
+    cpu = None
+    if rank == 0 and P == 1 and not args.no_cpu_baseline:
+        s = oracle_sample(w, args.cpu_seconds)
+        cpu = {"value": s["value"], "unit": "points·iter/s", "cores": 1, "kind": "oracle",
+               "sample": f"{s['iters']} Lloyd iterations (oracle.step) on the first {s['n']} "
+                         f"points of {w.name}, single-threaded C oracle, {s['seconds']:.1f} s",
+               "cpu": cpu_model(), "host_cores": os.cpu_count()}
+
+    if distributed:
+        km.comm_destroy(comm)
+    if rank == 0:
+        line = {
+            "metric": "Lloyd points·iter/s", "value": value, "unit": "points·iter/s",
+            "n_gpus": P, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(w, P, args.scaling),
+            "roofline": roofline, "roofline_hbm": roofline_hbm,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "kernels_per_step": info["kernels_per_iter"],
+            "clocks": clk,
+            "launch": {"grid": info["grid"], "block": info["block"],
+                       "smem_bytes": info["smem_bytes"], "path": info["path"]},
+        }
+        print(json.dumps(line), flush=True)
+    if distributed:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

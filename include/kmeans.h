@@ -1,0 +1,195 @@
+/*
+ * kmeans.h -- C ABI of the B200-native Lloyd iteration (arXiv 2405.12052).
+ *
+ * The operation is one Lloyd iteration of PAPER.md (§THE LLOYD'S ALGORITHM,
+ * lines 39-64, and §SERIAL LLOYD'S ALGORITHM, lines 65-70):
+ *
+ *   reassignment  z_i^{t+1} = argmin_k ||x_i - mu_k^t||_2^2
+ *   mean          mu_k^{t+1} = sum_i 1(z_i^{t+1}=k) x_i
+ *                              / sum_i 1(z_i^{t+1}=k)
+ *   error         E = sum_k ||mu_k^{t+1} - mu_k^t||_2^2
+ *   stop          E < tol, or t = max_iter
+ *
+ * with the numerical contract of DESIGN.md "Readings" (R1-R16): fp32 points,
+ * centroids staged once per iteration fp64 -> fp32 (round to nearest even),
+ * form-D distance e_j = x_j - c_j, s = e_0*e_0, s = fma(e_j, e_j, s), argmin
+ * with the lowest index winning ties, fp64 sums / means / E / inertia, int64
+ * counts, empty clusters keep mu^t, labels 0-based.
+ *
+ * Conventions for every function:
+ *   - Returns a kmeans_status; nothing throws across the ABI.
+ *   - Validation happens before any device work; outputs are written only on
+ *     KMEANS_OK.
+ *   - Every pointer argument may be host memory (pageable or pinned) or device
+ *     memory of the context's device (CUDA unified addressing decides); the
+ *     caller owns it, and the library never keeps it past the call.
+ *   - After KMEANS_ECUDA or KMEANS_ENCCL a context is unusable (sticky error);
+ *     only kmeans_destroy is valid.
+ *   - A context is not thread-safe; distinct contexts are independent.
+ *   - kmeans_last_error() returns a thread-local message for the last failure.
+ *
+ * Supported shapes: d in {2, 3} (the paper's 2D and 3D datasets, PAPER.md:37,
+ * 72); 1 <= K <= KMEANS_MAX_K; K <= N (global N when distributed).
+ */
+#ifndef KMEANS_H
+#define KMEANS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KMEANS_ABI_VERSION 1
+#define KMEANS_MAX_K 1024
+
+typedef struct kmeans_ctx kmeans_ctx; /* opaque */
+
+typedef enum kmeans_status {
+    KMEANS_OK = 0,
+    KMEANS_EINVAL = -1,     /* NULL where required; N < 1; d not in {2,3}; K < 1;
+                               K > N or K > KMEANS_MAX_K; tol < 0 or NaN; max_iter < 1;
+                               init_idx entry outside [0, N) or repeated */
+    KMEANS_ENONFINITE = -2, /* NaN/Inf in points or centroids */
+    KMEANS_ENOMEM = -3,     /* device or host allocation failed */
+    KMEANS_ECUDA = -4,      /* CUDA error (sticky) */
+    KMEANS_ENCCL = -5,      /* NCCL error, or library built without NCCL (sticky) */
+    KMEANS_ESTATE = -6      /* call out of order, e.g. kmeans_update before kmeans_assign */
+} kmeans_status;
+
+typedef enum kmeans_layout {
+    KMEANS_LAYOUT_AOS = 0,  /* N x d row-major (point-major), the default */
+    KMEANS_LAYOUT_SOA = 1   /* d x N row-major, the paper's X in R^{d x N} */
+} kmeans_layout;
+
+typedef struct kmeans_opts {
+    int device;             /* CUDA ordinal; -1 = current device */
+    void* stream;           /* cudaStream_t to run on; NULL = a context-owned stream */
+    int layout;             /* kmeans_layout of `points` */
+    void* nccl_comm;        /* ncclComm_t (see kmeans_comm_init); NULL = single GPU.
+                               When set, the context is one rank of a data-parallel
+                               group: it owns the contiguous shard
+                               [global_offset, global_offset + N) of global_N points,
+                               and every compute call is collective over the group. */
+    int64_t global_offset;  /* first global index of this rank's shard */
+    int64_t global_N;       /* total points over all ranks; 0 = N */
+} kmeans_opts;
+
+/* Fills *opts with the defaults above. */
+void kmeans_opts_init(kmeans_opts* opts);
+
+/* Creates a context holding a device-resident copy of `points` (N points of
+ * dimension d, layout per opts), laid out internally as SoA fp32.  K is the
+ * number of clusters every later call uses.  Checks every coordinate for
+ * NaN/Inf (KMEANS_ENONFINITE). */
+kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, int d, int K,
+                            const kmeans_opts* opts);
+
+/* One reassignment step plus the fused per-cluster reduction at the given
+ * centroids mu^t (K x d fp64, row-major).  Distributed: the
+ * partials are summed over all ranks (collective), labels stay local.
+ * Outputs (each may be NULL):
+ *   labels  : N int32, z_i^{t+1} for this rank's points
+ *   inertia : J(z^{t+1}, mu^t) = sum_i ||x_i - c_{z_i}||^2 (fp32 distances summed
+ *             in fp64), global
+ *   counts  : K int64, global
+ *   sums    : K x d fp64, global per-cluster coordinate sums
+ * Enables one following kmeans_update. */
+kmeans_status kmeans_assign(kmeans_ctx* ctx, const double* centroids, int32_t* labels,
+                            double* inertia, int64_t* counts, double* sums);
+
+/* The mean step after kmeans_assign: writes
+ * mu^{t+1} (K x d fp64) to `centroids` (empty clusters keep the mu^t given to
+ * kmeans_assign) and E to *shift_E (either may be NULL).
+ * KMEANS_ESTATE unless directly preceded by a successful kmeans_assign. */
+kmeans_status kmeans_update(kmeans_ctx* ctx, double* centroids, double* shift_E);
+
+/* The whole serial Lloyd run of PAPER.md:65-70 on one GPU:
+ *   mu^0 = x[init_idx[k]] (K distinct indices in [0, N)),
+ *   loop { assign; update } until E < tol or max_iter iterations.
+ * points: N x d row-major fp32.  Outputs: labels z^{iters} (N, may be NULL),
+ * centroids mu^{iters} (K x d), iters in [1, max_iter], inertia = J of the
+ * last iteration.  Non-convergence at max_iter is KMEANS_OK. */
+kmeans_status kmeans_fit(const float* points, int64_t N, int d, int K, const int64_t* init_idx,
+                         double tol, int max_iter, int32_t* labels, double* centroids,
+                         int* iters, double* inertia);
+
+/* kmeans_fit on an existing context; collective when distributed (init_idx
+ * are global indices; labels are this rank's N).  E_trace / J_trace (may be
+ * NULL) receive E and J of every iteration (max_iter entries of room). */
+kmeans_status kmeans_fit_ctx(kmeans_ctx* ctx, const int64_t* init_idx, double tol,
+                             int max_iter, int32_t* labels, double* centroids, int* iters,
+                             double* inertia, double* E_trace, double* J_trace);
+
+/* ---- device-resident loop (asynchronous; used by kmeans_fit_ctx and bench) ---- */
+
+/* Resets the iteration state: mu^0 from init_idx (K global indices) or, if
+ * init_idx is NULL, from `centroids` (K x d fp64); t = 0; stop rule
+ * (tol, max_iter).  Synchronous. */
+kmeans_status kmeans_start(kmeans_ctx* ctx, const int64_t* init_idx, const double* centroids,
+                           double tol, int max_iter);
+
+/* Enqueues n Lloyd iterations on the context's stream (a captured CUDA graph
+ * per iteration: assign+reduce, merge, [allreduce], update).  Iterations
+ * after the stop rule fired are no-ops.  Returns without synchronising. */
+kmeans_status kmeans_iterate(kmeans_ctx* ctx, int n);
+
+/* Synchronises the stream and reads the state: completed iterations, stop
+ * flag, last E and J (any may be NULL). */
+kmeans_status kmeans_poll(kmeans_ctx* ctx, int* iters, int* done, double* E, double* J);
+
+/* Copies the current centroids mu^t (K x d fp64).  Synchronous. */
+kmeans_status kmeans_read_centroids(kmeans_ctx* ctx, double* centroids);
+
+/* Writes z^{t} = argmin_k ||x_i - fl32(mu_k^{t-1})|| for this rank's points,
+ * i.e. the labels of the last completed iteration (t >= 1).  Synchronous. */
+kmeans_status kmeans_final_labels(kmeans_ctx* ctx, int32_t* labels);
+
+/* Profiling aid (bench.py's roofline): enqueues n launches of the
+ * assign+reduce kernel alone at the current mu^t (no merge / update, the
+ * iteration state is unchanged).  Returns without synchronising. */
+kmeans_status kmeans_profile_assign(kmeans_ctx* ctx, int n);
+
+/* The cudaStream_t the context runs on. */
+kmeans_status kmeans_get_stream(kmeans_ctx* ctx, void** stream);
+
+typedef struct kmeans_info {
+    int64_t N, global_N, global_offset, ldx;
+    int d, K;
+    int grid;               /* blocks of the assign kernel (a multiple of the SM count) */
+    int block;              /* threads per block of the assign kernel */
+    int smem_bytes;         /* dynamic shared memory of the assign kernel */
+    int path;               /* 0 = register-centroid path (K <= 16), 1 = shared-memory path */
+    int kernels_per_iter;   /* kernels of this library launched per iteration */
+    int64_t kernel_launches;/* kernels of this library launched so far by this context */
+    int nranks, rank;
+} kmeans_info;
+
+kmeans_status kmeans_get_info(kmeans_ctx* ctx, kmeans_info* info);
+
+/* ---- multi-GPU plumbing (NCCL) ---- */
+
+/* Writes a fresh NCCL unique id (128 bytes) to id; rank 0 calls it and the
+ * caller broadcasts it (e.g. over torch.distributed). */
+kmeans_status kmeans_comm_unique_id(unsigned char id[128]);
+
+/* Creates an NCCL communicator for `rank` of `nranks` on CUDA device `device`
+ * (collective over the ranks). *comm receives an ncclComm_t. */
+kmeans_status kmeans_comm_init(void** comm, int nranks, const unsigned char id[128], int rank,
+                               int device);
+
+kmeans_status kmeans_comm_destroy(void* comm);
+
+/* NULL-safe; frees all device memory of the context (not the caller's stream
+ * or communicator). */
+void kmeans_destroy(kmeans_ctx* ctx);
+
+const char* kmeans_status_string(kmeans_status s);
+const char* kmeans_last_error(void);
+int kmeans_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KMEANS_H */

@@ -1,0 +1,859 @@
+// runtime.cu -- host runtime (kmeans_ctx) and the C ABI of include/kmeans.h.
+//
+// One context = one GPU's shard of the points, resident in HBM as padded SoA
+// fp32, plus the iteration state (mu ping-pong buffers, per-block partials,
+// merged partials, DevState, E/J traces).  One Lloyd iteration is captured once
+// into a CUDA graph [assign+reduce -> merge -> (NCCL allreduce) -> update] and
+// replayed; the stop rule lives on the device (DevState::done), so the host only
+// polls between graph replays.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#ifdef KMEANS_WITH_NCCL
+#include <nccl.h>
+#endif
+
+#include "../../include/kmeans.h"
+#include "kernels.cuh"
+
+using km::DevState;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+}
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+}  // namespace
+
+struct kmeans_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int64_t N = 0, ldx = 0, global_N = 0, global_offset = 0;
+    int d = 0, K = 0;
+    void* comm = nullptr;
+    int nranks = 1, rank = 0;
+
+    float* X = nullptr;          // d x ldx SoA fp32
+    double* mu = nullptr;        // 2 x Kpad x d (ping-pong by t & 1)
+    double* part = nullptr;      // nE x G per-block partials
+    double* red = nullptr;       // nE merged partials
+    DevState* st = nullptr;
+    double* trace_E = nullptr;
+    double* trace_J = nullptr;
+    int trace_cap = 0;
+    int32_t* labels = nullptr;   // ldx, lazily
+    int64_t* idx_dev = nullptr;  // K
+    int* flag = nullptr;
+
+    int G = 0, tpb = 0, smem = 0, path = 0;
+    int nE = 0;
+    cudaGraphExec_t graph = nullptr;
+    int64_t launches = 0;
+    kmeans_status sticky = KMEANS_OK;
+    bool assigned = false;
+    std::vector<double> mu_host;   // mu^t given to the last kmeans_assign
+};
+
+namespace {
+
+constexpr int kKernelsPerIter = 3;  // assign, merge, update
+
+kmeans_status cuda_fail(kmeans_ctx* c, cudaError_t e, const char* what) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    if (c) c->sticky = KMEANS_ECUDA;
+    return KMEANS_ECUDA;
+}
+
+#define CK(call)                                                      \
+    do {                                                              \
+        cudaError_t _e = (call);                                      \
+        if (_e != cudaSuccess) return cuda_fail(ctx, _e, #call);      \
+    } while (0)
+
+#define CHECK_CTX(c)                                                  \
+    do {                                                              \
+        if (!(c)) { set_error("NULL context"); return KMEANS_EINVAL; } \
+        if ((c)->sticky != KMEANS_OK) {                               \
+            set_error("context is in a sticky error state");          \
+            return (c)->sticky;                                       \
+        }                                                             \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// --- kernel selection --------------------------------------------------------
+using AssignFn = void (*)(const float*, int64_t, int64_t, int, const double*, const DevState*,
+                          int, int, double*, int32_t*);
+
+template <int D, int MODE>
+AssignFn pick_small(int K) {
+    if (K <= 4) return km::k_assign_small<D, 4, MODE>;
+    if (K <= 8) return km::k_assign_small<D, 8, MODE>;
+    return km::k_assign_small<D, 16, MODE>;
+}
+
+AssignFn pick_assign(int d, int K, int mode) {
+    const bool small = K <= 16;
+    if (d == 2) {
+        if (small) {
+            if (mode == 1) return pick_small<2, 1>(K);
+            if (mode == 2) return pick_small<2, 2>(K);
+            return pick_small<2, 3>(K);
+        }
+        if (mode == 1) return km::k_assign_large<2, 1>;
+        if (mode == 2) return km::k_assign_large<2, 2>;
+        return km::k_assign_large<2, 3>;
+    }
+    if (small) {
+        if (mode == 1) return pick_small<3, 1>(K);
+        if (mode == 2) return pick_small<3, 2>(K);
+        return pick_small<3, 3>(K);
+    }
+    if (mode == 1) return km::k_assign_large<3, 1>;
+    if (mode == 2) return km::k_assign_large<3, 2>;
+    return km::k_assign_large<3, 3>;
+}
+
+int small_kp(int K) { return K <= 4 ? 4 : (K <= 8 ? 8 : 16); }
+
+int small_smem(int d, int K) {
+    const int kp = small_kp(K);
+    return kp * km::kSmallTPB * (16 + (d == 3 ? 8 : 0) + 4) + (km::kSmallTPB / 32) * 8;
+}
+
+int large_smem(int d, int K, int tpb) {
+    const int W = tpb / 32;
+    return K * 16 + W * K * d * 8 + (W * K + 1) * 4 + 8 + W * 8;
+}
+
+kmeans_status configure(kmeans_ctx* ctx) {
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, ctx->device));
+    const int sms = prop.multiProcessorCount;
+    const int maxSmem = (int)prop.sharedMemPerBlockOptin;
+    if (ctx->K <= 16) {
+        ctx->path = 0;
+        ctx->tpb = km::kSmallTPB;
+        ctx->smem = small_smem(ctx->d, ctx->K);
+    } else {
+        ctx->path = 1;
+        int tpb = km::kLargeTPBMax;
+        while (tpb > 64 && large_smem(ctx->d, ctx->K, tpb) > maxSmem - 4096) tpb -= 32;
+        ctx->tpb = tpb;
+        ctx->smem = large_smem(ctx->d, ctx->K, tpb);
+        if (ctx->smem > maxSmem) {
+            set_error("K=%d needs %d B of shared memory (max %d)", ctx->K, ctx->smem, maxSmem);
+            return KMEANS_EINVAL;
+        }
+    }
+    int occ = 0;
+    for (int mode = 1; mode <= 3; ++mode) {
+        AssignFn f = pick_assign(ctx->d, ctx->K, mode);
+        CK(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                ctx->smem));
+    }
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ, (const void*)pick_assign(ctx->d, ctx->K, 1), ctx->tpb, ctx->smem));
+    occ = std::max(occ, 1);
+    ctx->G = sms * occ;  // persistent grid: every SM busy, static tile schedule
+    ctx->nE = ctx->K * ctx->d + ctx->K + 1;
+    return KMEANS_OK;
+}
+
+kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_done) {
+    AssignFn f = pick_assign(ctx->d, ctx->K, mode);
+    if ((mode & km::kModeLabels) && !ctx->labels) {
+        CK(cudaMalloc(&ctx->labels, sizeof(int32_t) * ctx->ldx));
+    }
+    f<<<ctx->G, ctx->tpb, ctx->smem, ctx->stream>>>(ctx->X, ctx->ldx, ctx->N, ctx->K, ctx->mu,
+                                                    ctx->st, mu_sel, ignore_done, ctx->part,
+                                                    ctx->labels);
+    ctx->launches += 1;
+    CK(cudaGetLastError());
+    return KMEANS_OK;
+}
+
+kmeans_status launch_merge(kmeans_ctx* ctx, int ignore_done) {
+    const int wpb = 8;
+    km::k_merge<<<(ctx->nE + wpb - 1) / wpb, wpb * 32, 0, ctx->stream>>>(
+        ctx->part, ctx->G, ctx->nE, ctx->red, ctx->st, ignore_done);
+    ctx->launches += 1;
+    CK(cudaGetLastError());
+    return KMEANS_OK;
+}
+
+kmeans_status allreduce(kmeans_ctx* ctx, double* buf, size_t count) {
+    if (!ctx->comm) return KMEANS_OK;
+#ifdef KMEANS_WITH_NCCL
+    ncclResult_t r = ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)ctx->comm,
+                                   ctx->stream);
+    if (r != ncclSuccess) {
+        set_error("ncclAllReduce: %s", ncclGetErrorString(r));
+        ctx->sticky = KMEANS_ENCCL;
+        return KMEANS_ENCCL;
+    }
+    return KMEANS_OK;
+#else
+    (void)buf;
+    (void)count;
+    set_error("library built without NCCL");
+    ctx->sticky = KMEANS_ENCCL;
+    return KMEANS_ENCCL;
+#endif
+}
+
+kmeans_status launch_update(kmeans_ctx* ctx) {
+    const int tpb = 256;
+    if (ctx->d == 2)
+        km::k_update<2><<<1, tpb, 0, ctx->stream>>>(ctx->mu, ctx->K, ctx->red, ctx->st,
+                                                    ctx->trace_E, ctx->trace_J, ctx->trace_cap);
+    else
+        km::k_update<3><<<1, tpb, 0, ctx->stream>>>(ctx->mu, ctx->K, ctx->red, ctx->st,
+                                                    ctx->trace_E, ctx->trace_J, ctx->trace_cap);
+    ctx->launches += 1;
+    CK(cudaGetLastError());
+    return KMEANS_OK;
+}
+
+// One iteration: assign+reduce, merge, [allreduce], update.
+kmeans_status enqueue_iteration(kmeans_ctx* ctx) {
+    kmeans_status s;
+    if ((s = launch_assign(ctx, km::kModeReduce, 0, 0)) != KMEANS_OK) return s;
+    if ((s = launch_merge(ctx, 0)) != KMEANS_OK) return s;
+    if ((s = allreduce(ctx, ctx->red, ctx->nE)) != KMEANS_OK) return s;
+    return launch_update(ctx);
+}
+
+kmeans_status ensure_graph(kmeans_ctx* ctx) {
+    if (ctx->graph) return KMEANS_OK;
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    const int64_t before = ctx->launches;
+    kmeans_status s = enqueue_iteration(ctx);
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+    ctx->launches = before;  // capture is not a launch
+    if (s != KMEANS_OK) {
+        if (g) cudaGraphDestroy(g);
+        return s;
+    }
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&ctx->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate");
+    return KMEANS_OK;
+}
+
+kmeans_status sync(kmeans_ctx* ctx) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    return KMEANS_OK;
+}
+
+kmeans_status read_state(kmeans_ctx* ctx, DevState* h) {
+    CK(cudaMemcpyAsync(h, ctx->st, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return KMEANS_OK;
+}
+
+kmeans_status write_state(kmeans_ctx* ctx, int t, int done, int max_iter, double tol) {
+    DevState h{};
+    h.t = t;
+    h.done = done;
+    h.max_iter = max_iter;
+    h.tol = tol;
+    CK(cudaMemcpyAsync(ctx->st, &h, sizeof(DevState), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));  // h is a stack object
+    return KMEANS_OK;
+}
+
+kmeans_status ensure_trace(kmeans_ctx* ctx, int cap) {
+    if (cap <= ctx->trace_cap) return KMEANS_OK;
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->graph) {
+        cudaGraphExecDestroy(ctx->graph);  // captured the old trace pointers
+        ctx->graph = nullptr;
+    }
+    cudaFree(ctx->trace_E);
+    cudaFree(ctx->trace_J);
+    ctx->trace_E = ctx->trace_J = nullptr;
+    ctx->trace_cap = 0;
+    if (cudaMalloc(&ctx->trace_E, sizeof(double) * cap) != cudaSuccess ||
+        cudaMalloc(&ctx->trace_J, sizeof(double) * cap) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("trace allocation failed");
+        return KMEANS_ENOMEM;
+    }
+    ctx->trace_cap = cap;
+    return KMEANS_OK;
+}
+
+// Reads K init indices (host or device memory) and validates them against
+// [0, global_N): distinct and in range.
+kmeans_status fetch_init_idx(kmeans_ctx* ctx, const int64_t* init_idx, std::vector<int64_t>& out) {
+    out.resize(ctx->K);
+    CK(cudaMemcpy(out.data(), init_idx, sizeof(int64_t) * ctx->K, cudaMemcpyDefault));
+    std::vector<int64_t> s(out);
+    std::sort(s.begin(), s.end());
+    for (int k = 0; k < ctx->K; ++k) {
+        if (s[k] < 0 || s[k] >= ctx->global_N) {
+            set_error("init_idx[%d] out of range [0, %lld)", k, (long long)ctx->global_N);
+            return KMEANS_EINVAL;
+        }
+        if (k && s[k] == s[k - 1]) {
+            set_error("init_idx holds %lld twice", (long long)s[k]);
+            return KMEANS_EINVAL;
+        }
+    }
+    return KMEANS_OK;
+}
+
+kmeans_status fetch_centroids(kmeans_ctx* ctx, const double* cent, std::vector<double>& out) {
+    const size_t n = (size_t)ctx->K * ctx->d;
+    out.resize(n);
+    CK(cudaMemcpy(out.data(), cent, sizeof(double) * n, cudaMemcpyDefault));
+    for (size_t q = 0; q < n; ++q) {
+        if (!std::isfinite(out[q])) {
+            set_error("centroid entry %zu is not finite", q);
+            return KMEANS_ENONFINITE;
+        }
+    }
+    return KMEANS_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+int kmeans_abi_version(void) { return KMEANS_ABI_VERSION; }
+
+const char* kmeans_last_error(void) { return g_last_error.c_str(); }
+
+const char* kmeans_status_string(kmeans_status s) {
+    switch (s) {
+        case KMEANS_OK: return "KMEANS_OK";
+        case KMEANS_EINVAL: return "KMEANS_EINVAL: invalid argument";
+        case KMEANS_ENONFINITE: return "KMEANS_ENONFINITE: NaN or Inf in input";
+        case KMEANS_ENOMEM: return "KMEANS_ENOMEM: allocation failed";
+        case KMEANS_ECUDA: return "KMEANS_ECUDA: CUDA error";
+        case KMEANS_ENCCL: return "KMEANS_ENCCL: NCCL error";
+        case KMEANS_ESTATE: return "KMEANS_ESTATE: call out of order";
+    }
+    return "unknown kmeans_status";
+}
+
+void kmeans_opts_init(kmeans_opts* o) {
+    if (!o) return;
+    o->device = -1;
+    o->stream = nullptr;
+    o->layout = KMEANS_LAYOUT_AOS;
+    o->nccl_comm = nullptr;
+    o->global_offset = 0;
+    o->global_N = 0;
+}
+
+void kmeans_destroy(kmeans_ctx* ctx) {
+    if (!ctx) return;
+    {
+        DeviceGuard g(ctx->device);
+        if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+        if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+        cudaFree(ctx->X);
+        cudaFree(ctx->mu);
+        cudaFree(ctx->part);
+        cudaFree(ctx->red);
+        cudaFree(ctx->st);
+        cudaFree(ctx->trace_E);
+        cudaFree(ctx->trace_J);
+        cudaFree(ctx->labels);
+        cudaFree(ctx->idx_dev);
+        cudaFree(ctx->flag);
+        if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+        cudaGetLastError();
+    }
+    delete ctx;
+}
+
+kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, int d, int K,
+                            const kmeans_opts* opts_in) {
+    if (!out) {
+        set_error("out is NULL");
+        return KMEANS_EINVAL;
+    }
+    *out = nullptr;
+    kmeans_opts opts;
+    kmeans_opts_init(&opts);
+    if (opts_in) opts = *opts_in;
+    const int64_t gN = opts.global_N > 0 ? opts.global_N : N;
+    if (!points || N < 1 || (d != 2 && d != 3) || K < 1 || K > KMEANS_MAX_K || K > gN ||
+        (opts.layout != KMEANS_LAYOUT_AOS && opts.layout != KMEANS_LAYOUT_SOA) ||
+        opts.global_offset < 0 || opts.global_offset + N > gN || (!opts.nccl_comm && gN != N)) {
+        set_error("invalid argument (N=%lld d=%d K=%d global_N=%lld offset=%lld)", (long long)N, d,
+                  K, (long long)gN, (long long)opts.global_offset);
+        return KMEANS_EINVAL;
+    }
+#ifndef KMEANS_WITH_NCCL
+    if (opts.nccl_comm) {
+        set_error("library built without NCCL");
+        return KMEANS_ENCCL;
+    }
+#endif
+    kmeans_ctx* ctx = new kmeans_ctx();
+    int dev = opts.device;
+    if (dev < 0) {
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) {
+            delete ctx;
+            set_error("cudaGetDevice: %s", cudaGetErrorString(e));
+            return KMEANS_ECUDA;
+        }
+    }
+    ctx->device = dev;
+    DeviceGuard guard(dev);
+    ctx->N = N;
+    ctx->d = d;
+    ctx->K = K;
+    ctx->global_N = gN;
+    ctx->global_offset = opts.global_offset;
+    ctx->comm = opts.nccl_comm;
+    ctx->ldx = round_up(N + km::kPadPoints, km::kPadPoints);
+#ifdef KMEANS_WITH_NCCL
+    if (ctx->comm) {
+        ncclCommCount((ncclComm_t)ctx->comm, &ctx->nranks);
+        ncclCommUserRank((ncclComm_t)ctx->comm, &ctx->rank);
+    }
+#endif
+    auto fail = [&](kmeans_status s) {
+        kmeans_destroy(ctx);
+        return s;
+    };
+    cudaError_t e;
+    if (opts.stream) {
+        ctx->stream = (cudaStream_t)opts.stream;
+    } else {
+        e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            cuda_fail(nullptr, e, "cudaStreamCreate");
+            return fail(KMEANS_ECUDA);
+        }
+        ctx->own_stream = true;
+    }
+    kmeans_status s = configure(ctx);
+    if (s != KMEANS_OK) return fail(s);
+
+    const int Kpad = K + 16;
+    size_t bytesX = sizeof(float) * (size_t)d * ctx->ldx;
+    if (cudaMalloc(&ctx->X, bytesX) != cudaSuccess ||
+        cudaMalloc(&ctx->mu, sizeof(double) * 2 * Kpad * d) != cudaSuccess ||
+        cudaMalloc(&ctx->part, sizeof(double) * (size_t)ctx->nE * ctx->G) != cudaSuccess ||
+        cudaMalloc(&ctx->red, sizeof(double) * ctx->nE) != cudaSuccess ||
+        cudaMalloc(&ctx->st, sizeof(DevState)) != cudaSuccess ||
+        cudaMalloc(&ctx->idx_dev, sizeof(int64_t) * K) != cudaSuccess ||
+        cudaMalloc(&ctx->flag, sizeof(int)) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("device allocation failed (%zu bytes of points)", bytesX);
+        return fail(KMEANS_ENOMEM);
+    }
+    if ((s = ensure_trace(ctx, 64)) != KMEANS_OK) return fail(s);
+    if (cudaMemsetAsync(ctx->mu, 0, sizeof(double) * 2 * Kpad * d, ctx->stream) != cudaSuccess ||
+        cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream) != cudaSuccess ||
+        cudaMemsetAsync(ctx->st, 0, sizeof(DevState), ctx->stream) != cudaSuccess) {
+        cuda_fail(ctx, cudaGetLastError(), "cudaMemsetAsync");
+        return fail(KMEANS_ECUDA);
+    }
+
+    // Ingest: host or device input -> padded SoA, with the non-finite check.
+    cudaPointerAttributes attr;
+    bool on_device = false;
+    if (cudaPointerGetAttributes(&attr, points) == cudaSuccess)
+        on_device = attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+    cudaGetLastError();
+    const float* src = points;
+    float* staging = nullptr;
+    if (!on_device) {
+        if (cudaMalloc(&staging, sizeof(float) * (size_t)N * d) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("staging allocation failed");
+            return fail(KMEANS_ENOMEM);
+        }
+        e = cudaMemcpyAsync(staging, points, sizeof(float) * (size_t)N * d,
+                            cudaMemcpyHostToDevice, ctx->stream);
+        if (e != cudaSuccess) {
+            cudaFree(staging);
+            cuda_fail(ctx, e, "H2D points");
+            return fail(KMEANS_ECUDA);
+        }
+        src = staging;
+    }
+    const int64_t si = opts.layout == KMEANS_LAYOUT_AOS ? d : 1;
+    const int64_t sj = opts.layout == KMEANS_LAYOUT_AOS ? 1 : N;
+    {
+        int blocks = (int)std::min<int64_t>((ctx->ldx + 255) / 256, 148 * 16);
+        km::k_prep<<<blocks, 256, 0, ctx->stream>>>(src, N, d, si, sj, ctx->X, ctx->ldx,
+                                                    ctx->flag);
+        ctx->launches += 1;
+    }
+    int hflag = 0;
+    e = cudaMemcpyAsync(&hflag, ctx->flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (staging) cudaFree(staging);
+    if (e != cudaSuccess) {
+        cuda_fail(ctx, e, "k_prep");
+        return fail(KMEANS_ECUDA);
+    }
+    if (hflag) {
+        set_error("points contain NaN or Inf");
+        return fail(KMEANS_ENONFINITE);
+    }
+    *out = ctx;
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_start(kmeans_ctx* ctx, const int64_t* init_idx, const double* centroids,
+                           double tol, int max_iter) {
+    CHECK_CTX(ctx);
+    if ((!init_idx && !centroids) || !(tol >= 0.0) || max_iter < 1) {
+        set_error("kmeans_start: need init_idx or centroids, tol >= 0, max_iter >= 1");
+        return KMEANS_EINVAL;
+    }
+    DeviceGuard g(ctx->device);
+    kmeans_status s;
+    if (init_idx) {
+        std::vector<int64_t> idx;
+        if ((s = fetch_init_idx(ctx, init_idx, idx)) != KMEANS_OK) return s;
+        CK(cudaMemcpyAsync(ctx->idx_dev, idx.data(), sizeof(int64_t) * ctx->K,
+                           cudaMemcpyHostToDevice, ctx->stream));
+        const int n = ctx->K * ctx->d;
+        km::k_init_gather<<<(n + 255) / 256, 256, 0, ctx->stream>>>(
+            ctx->X, ctx->ldx, ctx->d, ctx->K, ctx->idx_dev, ctx->global_offset, ctx->N, ctx->mu);
+        ctx->launches += 1;
+        CK(cudaGetLastError());
+        // CC1: assemble mu^0 from the owners (exact: one x plus zeros)
+        if ((s = allreduce(ctx, ctx->mu, (size_t)n)) != KMEANS_OK) return s;
+        CK(cudaStreamSynchronize(ctx->stream));  // idx vector lifetime
+    } else {
+        std::vector<double> c;
+        if ((s = fetch_centroids(ctx, centroids, c)) != KMEANS_OK) return s;
+        CK(cudaMemcpyAsync(ctx->mu, c.data(), sizeof(double) * c.size(), cudaMemcpyHostToDevice,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    if ((s = ensure_trace(ctx, max_iter)) != KMEANS_OK) return s;
+    ctx->assigned = false;
+    return write_state(ctx, 0, 0, max_iter, tol);
+}
+
+kmeans_status kmeans_iterate(kmeans_ctx* ctx, int n) {
+    CHECK_CTX(ctx);
+    if (n < 0) {
+        set_error("n < 0");
+        return KMEANS_EINVAL;
+    }
+    DeviceGuard g(ctx->device);
+    kmeans_status s = ensure_graph(ctx);
+    if (s != KMEANS_OK) return s;
+    for (int i = 0; i < n; ++i) {
+        CK(cudaGraphLaunch(ctx->graph, ctx->stream));
+        ctx->launches += kKernelsPerIter;
+    }
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_poll(kmeans_ctx* ctx, int* iters, int* done, double* E, double* J) {
+    CHECK_CTX(ctx);
+    DeviceGuard g(ctx->device);
+    DevState h;
+    kmeans_status s = read_state(ctx, &h);
+    if (s != KMEANS_OK) return s;
+    if (iters) *iters = h.t;
+    if (done) *done = h.done;
+    if (E) *E = h.E;
+    if (J) *J = h.J;
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_read_centroids(kmeans_ctx* ctx, double* centroids) {
+    CHECK_CTX(ctx);
+    if (!centroids) {
+        set_error("centroids is NULL");
+        return KMEANS_EINVAL;
+    }
+    DeviceGuard g(ctx->device);
+    DevState h;
+    kmeans_status s = read_state(ctx, &h);
+    if (s != KMEANS_OK) return s;
+    const size_t n = (size_t)ctx->K * ctx->d;
+    CK(cudaMemcpyAsync(centroids, ctx->mu + (size_t)(h.t & 1) * n, sizeof(double) * n,
+                       cudaMemcpyDefault, ctx->stream));
+    return sync(ctx);
+}
+
+kmeans_status kmeans_final_labels(kmeans_ctx* ctx, int32_t* labels) {
+    CHECK_CTX(ctx);
+    if (!labels) {
+        set_error("labels is NULL");
+        return KMEANS_EINVAL;
+    }
+    DeviceGuard g(ctx->device);
+    DevState h;
+    kmeans_status s = read_state(ctx, &h);
+    if (s != KMEANS_OK) return s;
+    if (h.t < 1) {
+        set_error("no completed iteration");
+        return KMEANS_ESTATE;
+    }
+    // z^t = argmin over fl32(mu^{t-1}): mu_sel = 1 selects buffer (t-1) & 1.
+    if ((s = launch_assign(ctx, km::kModeLabels, 1, 1)) != KMEANS_OK) return s;
+    CK(cudaMemcpyAsync(labels, ctx->labels, sizeof(int32_t) * ctx->N, cudaMemcpyDefault,
+                       ctx->stream));
+    return sync(ctx);
+}
+
+kmeans_status kmeans_assign(kmeans_ctx* ctx, const double* centroids, int32_t* labels,
+                            double* inertia, int64_t* counts, double* sums) {
+    CHECK_CTX(ctx);
+    if (!centroids) {
+        set_error("centroids is NULL");
+        return KMEANS_EINVAL;
+    }
+    DeviceGuard g(ctx->device);
+    kmeans_status s;
+    std::vector<double> c;
+    if ((s = fetch_centroids(ctx, centroids, c)) != KMEANS_OK) return s;
+    ctx->assigned = false;
+    const size_t n = c.size();
+    CK(cudaMemcpyAsync(ctx->mu, c.data(), sizeof(double) * n, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    if ((s = write_state(ctx, 0, 0, 0x7fffffff, -1.0)) != KMEANS_OK) return s;
+    const int mode = km::kModeReduce | (labels ? km::kModeLabels : 0);
+    if ((s = launch_assign(ctx, mode, 0, 1)) != KMEANS_OK) return s;
+    if ((s = launch_merge(ctx, 1)) != KMEANS_OK) return s;
+    if ((s = allreduce(ctx, ctx->red, ctx->nE)) != KMEANS_OK) return s;
+    std::vector<double> red(ctx->nE);
+    CK(cudaMemcpyAsync(red.data(), ctx->red, sizeof(double) * ctx->nE, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    if (labels)
+        CK(cudaMemcpyAsync(labels, ctx->labels, sizeof(int32_t) * ctx->N, cudaMemcpyDefault,
+                           ctx->stream));
+    if ((s = sync(ctx)) != KMEANS_OK) return s;
+    const int K = ctx->K, d = ctx->d;
+    if (inertia) CK(cudaMemcpy(inertia, &red[(size_t)K * d + K], sizeof(double), cudaMemcpyDefault));
+    if (counts) {
+        std::vector<int64_t> cn(K);
+        for (int k = 0; k < K; ++k) cn[k] = (int64_t)red[(size_t)K * d + k];
+        CK(cudaMemcpy(counts, cn.data(), sizeof(int64_t) * K, cudaMemcpyDefault));
+    }
+    if (sums) CK(cudaMemcpy(sums, red.data(), sizeof(double) * K * d, cudaMemcpyDefault));
+    ctx->mu_host = c;
+    ctx->assigned = true;
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_update(kmeans_ctx* ctx, double* centroids, double* shift_E) {
+    CHECK_CTX(ctx);
+    if (!ctx->assigned) {
+        set_error("kmeans_update needs a preceding kmeans_assign");
+        return KMEANS_ESTATE;
+    }
+    DeviceGuard g(ctx->device);
+    kmeans_status s;
+    if ((s = launch_update(ctx)) != KMEANS_OK) return s;
+    DevState h;
+    if ((s = read_state(ctx, &h)) != KMEANS_OK) return s;
+    const size_t n = (size_t)ctx->K * ctx->d;
+    if (centroids) {
+        CK(cudaMemcpyAsync(centroids, ctx->mu + n /* buffer 1 = mu^{t+1} */, sizeof(double) * n,
+                           cudaMemcpyDefault, ctx->stream));
+        if ((s = sync(ctx)) != KMEANS_OK) return s;
+    }
+    if (shift_E) CK(cudaMemcpy(shift_E, &h.E, sizeof(double), cudaMemcpyDefault));
+    ctx->assigned = false;
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_fit_ctx(kmeans_ctx* ctx, const int64_t* init_idx, double tol, int max_iter,
+                             int32_t* labels, double* centroids, int* iters, double* inertia,
+                             double* E_trace, double* J_trace) {
+    CHECK_CTX(ctx);
+    if (!init_idx || !centroids || !iters || !inertia || !(tol >= 0.0) || max_iter < 1) {
+        set_error("kmeans_fit_ctx: invalid argument");
+        return KMEANS_EINVAL;
+    }
+    DeviceGuard g(ctx->device);
+    kmeans_status s = kmeans_start(ctx, init_idx, nullptr, tol, max_iter);
+    if (s != KMEANS_OK) return s;
+    // Graph replays in chunks; the device stop flag turns surplus iterations
+    // into no-ops, the host polls once per chunk.
+    int chunk = 4, t = 0, done = 0;
+    while (!done) {
+        const int n = std::min(chunk, max_iter - t);
+        if ((s = kmeans_iterate(ctx, n)) != KMEANS_OK) return s;
+        if ((s = kmeans_poll(ctx, &t, &done, nullptr, nullptr)) != KMEANS_OK) return s;
+        chunk = std::min(chunk * 2, 64);
+    }
+    DevState h;
+    if ((s = read_state(ctx, &h)) != KMEANS_OK) return s;
+    if (labels && (s = kmeans_final_labels(ctx, labels)) != KMEANS_OK) return s;
+    const size_t n = (size_t)ctx->K * ctx->d;
+    CK(cudaMemcpyAsync(centroids, ctx->mu + (size_t)(h.t & 1) * n, sizeof(double) * n,
+                       cudaMemcpyDefault, ctx->stream));
+    if (E_trace)
+        CK(cudaMemcpyAsync(E_trace, ctx->trace_E, sizeof(double) * h.t, cudaMemcpyDefault,
+                           ctx->stream));
+    if (J_trace)
+        CK(cudaMemcpyAsync(J_trace, ctx->trace_J, sizeof(double) * h.t, cudaMemcpyDefault,
+                           ctx->stream));
+    if ((s = sync(ctx)) != KMEANS_OK) return s;
+    CK(cudaMemcpy(iters, &h.t, sizeof(int), cudaMemcpyDefault));
+    CK(cudaMemcpy(inertia, &h.J, sizeof(double), cudaMemcpyDefault));
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_fit(const float* points, int64_t N, int d, int K, const int64_t* init_idx,
+                         double tol, int max_iter, int32_t* labels, double* centroids, int* iters,
+                         double* inertia) {
+    if (!init_idx || !centroids || !iters || !inertia || !(tol >= 0.0) || max_iter < 1) {
+        set_error("kmeans_fit: invalid argument");
+        return KMEANS_EINVAL;
+    }
+    kmeans_ctx* ctx = nullptr;
+    kmeans_status s = kmeans_create(&ctx, points, N, d, K, nullptr);
+    if (s != KMEANS_OK) return s;
+    s = kmeans_fit_ctx(ctx, init_idx, tol, max_iter, labels, centroids, iters, inertia, nullptr,
+                       nullptr);
+    kmeans_destroy(ctx);
+    return s;
+}
+
+kmeans_status kmeans_profile_assign(kmeans_ctx* ctx, int n) {
+    CHECK_CTX(ctx);
+    if (n < 0) {
+        set_error("n < 0");
+        return KMEANS_EINVAL;
+    }
+    DeviceGuard g(ctx->device);
+    for (int i = 0; i < n; ++i) {
+        kmeans_status s = launch_assign(ctx, km::kModeReduce, 0, 1);
+        if (s != KMEANS_OK) return s;
+    }
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_get_stream(kmeans_ctx* ctx, void** stream) {
+    CHECK_CTX(ctx);
+    if (!stream) return KMEANS_EINVAL;
+    *stream = (void*)ctx->stream;
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_get_info(kmeans_ctx* ctx, kmeans_info* info) {
+    if (!ctx || !info) {
+        set_error("NULL argument");
+        return KMEANS_EINVAL;
+    }
+    info->N = ctx->N;
+    info->global_N = ctx->global_N;
+    info->global_offset = ctx->global_offset;
+    info->ldx = ctx->ldx;
+    info->d = ctx->d;
+    info->K = ctx->K;
+    info->grid = ctx->G;
+    info->block = ctx->tpb;
+    info->smem_bytes = ctx->smem;
+    info->path = ctx->path;
+    info->kernels_per_iter = kKernelsPerIter;
+    info->kernel_launches = ctx->launches;
+    info->nranks = ctx->nranks;
+    info->rank = ctx->rank;
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_comm_unique_id(unsigned char id[128]) {
+    if (!id) return KMEANS_EINVAL;
+#ifdef KMEANS_WITH_NCCL
+    ncclUniqueId u;
+    ncclResult_t r = ncclGetUniqueId(&u);
+    if (r != ncclSuccess) {
+        set_error("ncclGetUniqueId: %s", ncclGetErrorString(r));
+        return KMEANS_ENCCL;
+    }
+    memcpy(id, u.internal, 128);
+    return KMEANS_OK;
+#else
+    set_error("library built without NCCL");
+    return KMEANS_ENCCL;
+#endif
+}
+
+kmeans_status kmeans_comm_init(void** comm, int nranks, const unsigned char id[128], int rank,
+                               int device) {
+    if (!comm || !id || nranks < 1 || rank < 0 || rank >= nranks) {
+        set_error("kmeans_comm_init: invalid argument");
+        return KMEANS_EINVAL;
+    }
+#ifdef KMEANS_WITH_NCCL
+    if (device >= 0) cudaSetDevice(device);
+    ncclUniqueId u;
+    memcpy(u.internal, id, 128);
+    ncclComm_t c = nullptr;
+    ncclResult_t r = ncclCommInitRank(&c, nranks, u, rank);
+    if (r != ncclSuccess) {
+        set_error("ncclCommInitRank: %s", ncclGetErrorString(r));
+        return KMEANS_ENCCL;
+    }
+    *comm = (void*)c;
+    return KMEANS_OK;
+#else
+    (void)device;
+    set_error("library built without NCCL");
+    return KMEANS_ENCCL;
+#endif
+}
+
+kmeans_status kmeans_comm_destroy(void* comm) {
+    if (!comm) return KMEANS_OK;
+#ifdef KMEANS_WITH_NCCL
+    ncclResult_t r = ncclCommDestroy((ncclComm_t)comm);
+    if (r != ncclSuccess) {
+        set_error("ncclCommDestroy: %s", ncclGetErrorString(r));
+        return KMEANS_ENCCL;
+    }
+    return KMEANS_OK;
+#else
+    set_error("library built without NCCL");
+    return KMEANS_ENCCL;
+#endif
+}
+
+}  // extern "C"

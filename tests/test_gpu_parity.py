@@ -1,0 +1,367 @@
+"""GPU parity: the sm_100a path through the C ABI against the CPU oracle.
+
+Bars (BASELINE.json north_star):
+  - labels: bit-exact per step, given identical fp64 input centroids;
+  - counts: exact;
+  - sums, inertia, mu^{t+1}: within 1e-9 relative in the sense of reading R13
+    (|delta| <= 1e-9 * scale, scale = sum of |x| over the cluster, since an fp64
+    sum's rounding error scales with sum|x|, not with |sum x|);
+  - E per step: |dE| <= 1e-9 * max(E, 1e-3 * sum ||mu||^2) plus the error E
+    inherits from mu (R13);
+  - full runs on well-separated blobs: iters exact, labels exact, centroids
+    within 1e-6 relative.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2405_12052_b200 import datagen
+from paper_2405_12052_b200 import kmeans as km
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-9
+
+
+def cluster_abs_scale(X, labels, K):
+    """sum_i |x_ij| over each cluster (the scale of fp64 summation error)."""
+    d = X.shape[1]
+    s = np.zeros((K, d))
+    for j in range(d):
+        s[:, j] = np.bincount(labels, weights=np.abs(X[:, j].astype(np.float64)), minlength=K)
+    return s
+
+
+def check_step(X, mu, ctx=None, tag=""):
+    """One Lloyd step on the GPU vs the oracle at identical mu^t."""
+    N, d = X.shape
+    K = mu.shape[0]
+    own = ctx is None
+    if own:
+        ctx = km.Context(X, K)
+    try:
+        g = ctx.assign(mu)
+        mu_next, E = ctx.update()
+    finally:
+        if own:
+            ctx.close()
+    o = oracle.step(X, mu)
+    lab_g, lab_o = g["labels"], o["labels"]
+    bad = np.nonzero(lab_g != lab_o)[0]
+    assert bad.size == 0, f"{tag}: {bad.size} labels differ, first at {bad[:5]}"
+    assert np.array_equal(g["counts"], o["counts"]), tag
+    scale = cluster_abs_scale(X, lab_o, K)
+    assert np.all(np.abs(g["sums"] - o["sums"]) <= REL * scale + 1e-300), tag
+    assert abs(g["inertia"] - o["J"]) <= REL * max(o["J"], 1e-300), tag
+    n = np.maximum(o["counts"], 1)[:, None]
+    mscale = np.maximum(np.abs(o["mu_next"]), scale / n)
+    assert np.all(np.abs(mu_next - o["mu_next"]) <= REL * mscale + 1e-300), tag
+    # E inherits |d mu| * 2 |mu_next - mu| per entry, plus its own rounding
+    dmu = REL * mscale
+    e_tol = np.sum(2 * np.abs(o["mu_next"] - mu) * dmu + dmu ** 2) + \
+        REL * max(o["E"], 1e-3 * float(np.sum(mu ** 2)))
+    assert abs(E - o["E"]) <= e_tol, f"{tag}: E {E} vs {o['E']}"
+    return g, o
+
+
+def perturbed_centroids(X, K, seed):
+    """K data points plus fp64 noise that is not fp32-representable (so the
+    fp64 -> fp32 staging rounding is exercised)."""
+    rng = np.random.default_rng(seed)
+    idx = rng.choice(X.shape[0], K, replace=False)
+    return X[idx].astype(np.float64) + rng.normal(0, 0.3, (K, X.shape[1]))
+
+
+# --------------------------------------------------------------------------
+# per-step parity over the configs (small N) and K / ragged-N sweeps
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("name,N", [("C1", 10_000), ("C2", 200_000), ("C3", 300_001),
+                                    ("NS", 250_003), ("C5", 60_000)])
+def test_step_parity_configs(name, N):
+    w = datagen.WORKLOADS[name]
+    X = datagen.generate(w, N=N)
+    init = datagen.init_indices(w, N=N)
+    mu0 = X[init].astype(np.float64)
+    check_step(X, mu0, tag=f"{name} init")
+    check_step(X, perturbed_centroids(X, w.K, 5), tag=f"{name} perturbed")
+
+
+@pytest.mark.parametrize("d", [2, 3])
+@pytest.mark.parametrize("K", [1, 2, 3, 5, 8, 11, 13, 16, 17, 31, 64, 100, 257])
+def test_step_parity_k_sweep(d, K):
+    w = datagen.WORKLOADS["NS" if d == 3 else "C3"]
+    N = 20_011
+    X = datagen.generate(w, N=N)
+    check_step(X, perturbed_centroids(X, K, K), tag=f"d={d} K={K}")
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 7, 511, 512, 513, 1023, 1025, 4097, 65_537])
+def test_step_parity_ragged_n(N):
+    w = datagen.WORKLOADS["NS"]
+    X = datagen.generate(w, N=max(N, 16))[:N].copy()
+    for K in sorted({1, min(N, 5), min(N, 16), min(N, 40)}):
+        check_step(X, perturbed_centroids(X, K, N + K), tag=f"N={N} K={K}")
+
+
+def test_step_parity_exact_ties_and_empty_clusters():
+    """Integer data -> exact fp32 distances -> genuine ties (lowest k wins);
+    duplicated centroids -> clusters that stay empty (keep mu^t)."""
+    rng = np.random.default_rng(1)
+    X = rng.integers(-4, 5, (50_000, 3)).astype(np.float32)
+    C = rng.integers(-4, 5, (12, 3)).astype(np.float64)
+    C[7] = C[2]
+    C[9] = C[2]
+    C[11] = [1000.0, 1000.0, 1000.0]
+    g, o = check_step(X, C, tag="ties")
+    assert g["counts"][7] == 0 and g["counts"][9] == 0 and g["counts"][11] == 0
+    X2 = rng.integers(-3, 4, (40_000, 2)).astype(np.float32)
+    C2 = np.array([[0, 0], [0, 0], [1, 1], [-1, 1], [1, 1], [2, -2], [0, 3], [-3, 0],
+                   [3, 3], [1, 1], [0, 0], [-2, -2], [2, 2], [-1, -1], [1, -1], [3, -3],
+                   [0, 1], [1, 0], [0, -1], [-1, 0]], np.float64)
+    check_step(X2, C2, tag="ties 2D K=20 (large path)")
+    check_step(X2, C2[:16], tag="ties 2D K=16 (small path)")
+
+
+def test_step_parity_soa_layout_and_device_input():
+    import torch
+    w = datagen.WORKLOADS["NS"]
+    X = datagen.generate(w, N=30_000)
+    mu = perturbed_centroids(X, 16, 3)
+    o = oracle.step(X, mu)
+    Xs = np.ascontiguousarray(X.T)
+    with km.Context(Xs, 16, layout="soa") as c:
+        g = c.assign(mu)
+        assert np.array_equal(g["labels"], o["labels"])
+    Xd = torch.from_numpy(X).cuda()
+    lab = torch.empty(30_000, dtype=torch.int32, device="cuda")
+    with km.Context(Xd, 16) as c:
+        g = c.assign(torch.from_numpy(mu).cuda(), out_labels=lab)
+        assert np.array_equal(lab.cpu().numpy(), o["labels"])
+        assert np.array_equal(g["counts"], o["counts"])
+
+
+# --------------------------------------------------------------------------
+# full runs
+# --------------------------------------------------------------------------
+def check_fit(X, K, init, tol, max_iter, tag=""):
+    o = oracle.fit(X, K, init, tol, max_iter)
+    with km.Context(X, K) as c:
+        g = c.fit(init, tol, max_iter)
+    assert g["iters"] == o["iters"], f"{tag}: iters {g['iters']} vs {o['iters']}"
+    assert np.array_equal(g["labels"], o["labels"]), tag
+    np.testing.assert_allclose(g["centroids"], o["centroids"], rtol=1e-6, atol=1e-9)
+    assert abs(g["inertia"] - o["inertia"]) <= 1e-6 * max(o["inertia"], 1e-300)
+    return g, o
+
+
+@pytest.mark.parametrize("name,N", [("C1", 10_000), ("C2", 300_000), ("C3", 200_000),
+                                    ("NS", 1_000_000)])
+def test_full_run_parity_one_init_per_blob(name, N):
+    w = datagen.WORKLOADS[name]
+    X = datagen.generate(w, N=N)
+    init = datagen.one_per_blob_init(w, N=N)
+    g, o = check_fit(X, w.M, init, w.tol, w.max_iter, tag=name)
+    np.testing.assert_allclose(g["centroids"], w.centers(), atol=0.05)
+
+
+def test_full_run_parity_c1_seeded_init():
+    """BASELINE.json configs[0]: N=1e4 2D blobs, K=4, seeded init, tol 1e-6, max_iter 100."""
+    w = datagen.WORKLOADS["C1"]
+    X = datagen.generate(w)
+    init = datagen.init_indices(w)
+    g, o = check_fit(X, w.K, init, w.tol, w.max_iter, tag="C1")
+    with km.Context(X, w.K) as c:
+        r = c.fit(init, w.tol, w.max_iter)
+    np.testing.assert_allclose(r["E_trace"], o["E_trace"], rtol=1e-6, atol=1e-12)
+    np.testing.assert_allclose(r["J_trace"], o["J_trace"], rtol=1e-9)
+
+
+def test_kmeans_fit_convenience_call():
+    w = datagen.WORKLOADS["C1"]
+    X = datagen.generate(w)
+    init = datagen.init_indices(w)
+    o = oracle.fit(X, w.K, init, w.tol, w.max_iter)
+    g = km.fit(X, w.K, init, w.tol, w.max_iter)
+    assert g["iters"] == o["iters"]
+    assert np.array_equal(g["labels"], o["labels"])
+    np.testing.assert_allclose(g["centroids"], o["centroids"], rtol=1e-6)
+
+
+@pytest.mark.parametrize("name", ["w1.json", "w2.json", "w3.json", "w4.json"])
+def test_hand_worked_runs_on_gpu(golden_dir, name):
+    """Tiny integer examples: every sum is exact in any order, so the GPU's
+    per-iteration E and J must equal the hand-derived values exactly."""
+    g = json.load(open(os.path.join(golden_dir, name)))
+    X = np.array(g["points"], np.float32)
+    K = len(g["init_idx"])
+    with km.Context(X, K) as c:
+        r = c.fit(g["init_idx"], g["tol"], g["max_iter"])
+    assert r["iters"] == g["iters"]
+    assert r["labels"].tolist() == g["labels"]
+    assert r["centroids"].tolist() == g["centroids"]
+    assert r["E_trace"].tolist() == [it["E"] for it in g["per_iter"]]
+    assert r["J_trace"].tolist() == [it["J"] for it in g["per_iter"]]
+    assert r["inertia"] == g["inertia"]
+
+
+def test_special_cases_k1_kn_tol0_maxiter1():
+    rng = np.random.default_rng(8)
+    X = rng.normal(0, 1, (9, 2)).astype(np.float32)
+    init = rng.permutation(9)
+    with km.Context(X, 9) as c:
+        r = c.fit(init, 1e-6, 10)
+    assert r["iters"] == 1 and r["inertia"] == 0.0
+    for k, i in enumerate(init):
+        assert r["labels"][i] == k
+    X = datagen.generate(datagen.WORKLOADS["NS"], N=5000)
+    o = oracle.fit(X, 1, [3], 1e-6, 10)
+    with km.Context(X, 1) as c:
+        r = c.fit([3], 1e-6, 10)
+    assert r["iters"] == o["iters"] == 2
+    np.testing.assert_allclose(r["centroids"], o["centroids"], rtol=1e-12)
+    init = datagen.init_indices(datagen.WORKLOADS["NS"], N=5000)
+    with km.Context(X, 16) as c:
+        r0 = c.fit(init, 0.0, 9)
+        r1 = c.fit(init, 1e-6, 1)
+    assert r0["iters"] == 9 and r1["iters"] == 1
+
+
+def test_errors():
+    X = datagen.generate(datagen.WORKLOADS["C1"], N=100)
+    Xn = X.copy()
+    Xn[17, 1] = np.inf
+    with pytest.raises(km.KMeansError) as e:
+        km.Context(Xn, 4)
+    assert e.value.name == "KMEANS_ENONFINITE"
+    with km.Context(X, 4) as c:
+        with pytest.raises(km.KMeansError) as e:
+            c.update()
+        assert e.value.name == "KMEANS_ESTATE"
+        with pytest.raises(km.KMeansError) as e:
+            c.fit([1, 2, 2, 3], 1e-6, 10)
+        assert e.value.name == "KMEANS_EINVAL"
+        with pytest.raises(km.KMeansError) as e:
+            c.fit([1, 2, 3, 100], 1e-6, 10)
+        assert e.value.name == "KMEANS_EINVAL"
+        bad = np.zeros((4, 2))
+        bad[2, 0] = np.nan
+        with pytest.raises(km.KMeansError) as e:
+            c.assign(bad)
+        assert e.value.name == "KMEANS_ENONFINITE"
+        # the context is still usable after argument errors
+        r = c.fit([1, 2, 3, 4], 1e-6, 10)
+        assert r["iters"] >= 1
+
+
+def test_deterministic_bitwise():
+    w = datagen.WORKLOADS["NS"]
+    X = datagen.generate(w, N=400_000)
+    init = datagen.init_indices(w, N=400_000)
+    with km.Context(X, 16) as c:
+        a = c.fit(init, 0.0, 6)
+        b = c.fit(init, 0.0, 6)
+    with km.Context(X, 16) as c:
+        e = c.fit(init, 0.0, 6)
+    for r in (b, e):
+        assert np.array_equal(a["labels"], r["labels"])
+        assert np.array_equal(a["centroids"], r["centroids"])
+        assert np.array_equal(a["E_trace"], r["E_trace"])
+        assert np.array_equal(a["J_trace"], r["J_trace"])
+
+
+# --------------------------------------------------------------------------
+# sharding (T4'): P contexts on one device, partials summed in rank order
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_fake_sharding_matches_oracle(P):
+    w = datagen.WORKLOADS["NS"]
+    N = 100_003
+    X = datagen.generate(w, N=N)
+    mu = perturbed_centroids(X, 16, P)
+    o = oracle.step(X, mu)
+    counts = np.zeros(16, np.int64)
+    sums = np.zeros((16, 3))
+    J = 0.0
+    labels = []
+    for r in range(P):
+        a, b = datagen.shard_range(N, P, r)
+        Xs = datagen.generate(w, a, b - a, N=N)
+        with km.Context(Xs, 16) as c:
+            g = c.assign(mu)
+        labels.append(g["labels"])
+        counts += g["counts"]
+        sums += g["sums"]
+        J += g["inertia"]
+    assert np.array_equal(np.concatenate(labels), o["labels"])
+    assert np.array_equal(counts, o["counts"])
+    scale = cluster_abs_scale(X, o["labels"], 16)
+    assert np.all(np.abs(sums - o["sums"]) <= REL * scale)
+    assert abs(J - o["J"]) <= REL * o["J"]
+
+
+def test_nccl_single_rank_communicator_path():
+    """The distributed code path (NCCL allreduce inside the graph, CC1 init
+    gather) with a 1-rank communicator equals the single-GPU path."""
+    w = datagen.WORKLOADS["C2"]
+    N = 200_000
+    X = datagen.generate(w, N=N)
+    init = datagen.one_per_blob_init(w, N=N)
+    uid = km.comm_unique_id()
+    comm = km.comm_init(1, uid, 0, 0)
+    try:
+        with km.Context(X, w.M, comm=comm, global_offset=0, global_N=N) as c:
+            rd = c.fit(init, w.tol, w.max_iter)
+            assert c.info()["nranks"] == 1
+    finally:
+        km.comm_destroy(comm)
+    with km.Context(X, w.M) as c:
+        rs = c.fit(init, w.tol, w.max_iter)
+    assert rd["iters"] == rs["iters"]
+    assert np.array_equal(rd["labels"], rs["labels"])
+    assert np.array_equal(rd["centroids"], rs["centroids"])
+
+
+# --------------------------------------------------------------------------
+# full-size checks in the launch configuration bench.py times
+# --------------------------------------------------------------------------
+@pytest.mark.slow
+def test_full_size_ns_step_parity():
+    """BASELINE north-star size (N=1e8, 3D, K=16): one full step against the
+    oracle on all N points (labels bit-exact, counts exact, sums / J / mu / E
+    per R13), through the same Context configuration bench.py uses."""
+    w = datagen.WORKLOADS["NS"]
+    X = datagen.generate(w)
+    mu = X[datagen.init_indices(w)].astype(np.float64)
+    with km.Context(X, w.K) as c:
+        info = c.info()
+        assert info["path"] == 0 and info["grid"] % 148 == 0
+        check_step(X, mu, ctx=c, tag="NS full")
+
+
+@pytest.mark.slow
+def test_full_size_c5_sampled_parity():
+    """C5 (N=5e7, 3D, K=1024, forced empty clusters): labels of a sample
+    against the oracle one by one; properties at full size (counts sum to N,
+    the 56 forced-empty clusters are empty, sums add up to sum x)."""
+    w = datagen.WORKLOADS["C5"]
+    X = datagen.generate(w)
+    init = datagen.init_indices(w)
+    mu = X[init].astype(np.float64)
+    with km.Context(X, w.K) as c:
+        g = c.assign(mu)
+    rng = np.random.default_rng(0)
+    sample = np.sort(rng.choice(w.N, 200_000, replace=False))
+    sample = np.concatenate([datagen.planted_indices(w), sample])
+    o = oracle.partials(X[sample], mu)
+    assert np.array_equal(g["labels"][sample], o["labels"])
+    assert g["counts"].sum() == w.N
+    for s in range(w.planted_sites):
+        ks = list(range(8 * s, 8 * s + 8))
+        assert g["counts"][ks[0]] >= 8
+        assert all(g["counts"][k] == 0 for k in ks[1:])
+    tot = g["sums"].sum(axis=0)
+    ref = X.astype(np.float64).sum(axis=0)
+    assert np.all(np.abs(tot - ref) <= 1e-9 * np.abs(X).astype(np.float64).sum(axis=0))
