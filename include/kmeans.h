@@ -156,10 +156,11 @@ kmeans_status kmeans_get_stream(kmeans_ctx* ctx, void** stream);
 typedef struct kmeans_info {
     int64_t N, global_N, global_offset, ldx;
     int d, K;
-    int grid;               /* blocks of the assign kernel (a multiple of the SM count) */
+    int grid;               /* blocks of the assign kernel: 2048-point chunks (path 0) or
+                               a persistent multiple of the SM count (path 1) */
     int block;              /* threads per block of the assign kernel */
     int smem_bytes;         /* dynamic shared memory of the assign kernel */
-    int path;               /* 0 = register-centroid path (K <= 16), 1 = shared-memory path */
+    int path;               /* 0 = chunked register-centroid path (K <= 16), 1 = shared-memory path */
     int kernels_per_iter;   /* kernels of this library launched per iteration */
     int64_t kernel_launches;/* kernels of this library launched so far by this context */
     int nranks, rank;

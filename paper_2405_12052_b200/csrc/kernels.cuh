@@ -3,9 +3,11 @@
 // Step map:
 //   k_prep          AoS/SoA fp32 input -> padded SoA fp32, non-finite check (create only)
 //   k_init_gather   mu^0_k = (double) x[init_idx[k]]
-//   k_assign_small  K <= 16: centroids in registers, form-D distances with packed
-//                   f32x2 FADD2/FMUL2/FFMA2, exact argmin (lowest index on ties),
-//                   per-thread private fp64 smem accumulators, per-block partials
+//   k_assign_chunk  K <= 16: one-warp blocks over fixed 2048-point chunks fed by
+//                   TMA bulk copies; centroids in registers, form-D distances with
+//                   packed f32x2 FADD2/FMUL2/FFMA2, exact argmin (lowest index on
+//                   ties), per-lane private fp64 smem columns, per-chunk partial
+//                   rows merged per 64-chunk group by the last arriving chunk
 //                                                                        PAPER.md:45-52
 //   k_assign_large  16 < K <= 1024: centroids in smem, per-warp fp64 accumulators
 //                   updated in lane order (conflicting lanes serialised by
@@ -35,9 +37,7 @@ struct DevState {
     double J;
 };
 
-constexpr int kSmallTPB = 256;     // threads per block, small-K path
 constexpr int kLargeTPBMax = 256;  // threads per block (max), large-K path
-constexpr int kPadPoints = 1024;   // SoA arrays padded so any tile start < N is in bounds
 
 __device__ __forceinline__ float pos_inf() { return __int_as_float(0x7f800000); }
 
@@ -47,9 +47,20 @@ __device__ __forceinline__ float2 ld_stream2(const float* p) {
 }
 
 // ---------------------------------------------------------------------------
-// k_prep: out[j * ldx + i] = in[i * si + j * sj] for i < N, 0 for N <= i < ldx.
-// Any non-finite coordinate sets *flag (integer atomic, order-free).
+// Internal point layout: AoSoA tiles of 64 points:
+//   tile t = points [64t, 64t+64): x[64] | y[64] | (z[64])     (D*256 bytes)
+// so one warp-tile is one contiguous TMA bulk copy, and a lane's 2 consecutive
+// points of one coordinate are one 8-byte float2.
 // ---------------------------------------------------------------------------
+constexpr int kWarpTile = 64;
+
+template <int D>
+__device__ __forceinline__ const float* tile_coord(const float* X, int64_t p, int j) {
+    return X + (p >> 6) * (D * kWarpTile) + j * kWarpTile + (p & 63);
+}
+
+// k_prep: tiled[p] <- in[p * si + j * sj] for p < N, 0 for N <= p < ldx.
+// Any non-finite coordinate sets *flag (integer atomic, order-free).
 __global__ void k_prep(const float* __restrict__ in, int64_t N, int d, int64_t si, int64_t sj,
                        float* __restrict__ out, int64_t ldx, int* __restrict__ flag) {
     int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -61,7 +72,7 @@ __global__ void k_prep(const float* __restrict__ in, int64_t N, int d, int64_t s
                 v = in[i * si + (int64_t)j * sj];
                 bad |= !isfinite(v);
             }
-            out[(int64_t)j * ldx + i] = v;
+            out[(i >> 6) * (d * kWarpTile) + j * kWarpTile + (i & 63)] = v;
         }
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
@@ -69,14 +80,16 @@ __global__ void k_prep(const float* __restrict__ in, int64_t N, int d, int64_t s
 
 // mu^0_k = (double) x_{idx_k} for the indices this rank owns, 0 elsewhere (the
 // allreduce over ranks then assembles mu^0 exactly: one x plus zeros).
-__global__ void k_init_gather(const float* __restrict__ X, int64_t ldx, int d, int K,
+__global__ void k_init_gather(const float* __restrict__ X, int d, int K,
                               const int64_t* __restrict__ idx, int64_t offset, int64_t n_local,
                               double* __restrict__ mu0) {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= K * d) return;
     int k = q / d, j = q % d;
     int64_t i = idx[k] - offset;
-    mu0[q] = (i >= 0 && i < n_local) ? (double)X[(int64_t)j * ldx + i] : 0.0;
+    mu0[q] = (i >= 0 && i < n_local)
+                 ? (double)X[(i >> 6) * (d * kWarpTile) + j * kWarpTile + (i & 63)]
+                 : 0.0;
 }
 
 // Per-block partial layout: part[e * G + b], e in [0, K*D + K + 1):
@@ -88,21 +101,168 @@ __global__ void k_init_gather(const float* __restrict__ X, int64_t ldx, int d, i
 enum : int { kModeReduce = 1, kModeLabels = 2 };
 
 // ---------------------------------------------------------------------------
-// Small-K path.  KP = compile-time padded K (4, 8 or 16); padded slots have
-// c = +inf so their distance is +inf and never wins (strict <).
-// Each thread handles 2 consecutive points per tile (float2 loads, packed math).
+// Exact argmin used by the small-K path.  KP = compile-time padded K (4, 8 or
+// 16); padded slots have c = +inf so their distance is +inf and never wins.
+//
+// Argmin (exact, lowest index on ties): m = min_k d_k by a 3-input FMNMX tree
+// (min is exact and order-free for non-NaN values), then the lowest k with
+// d_k == m by short descending select chains and an integer min.  This is the same (value, index) the
+// ascending strict-< scan of the oracle returns.
 // ---------------------------------------------------------------------------
+template <int KP>
+__device__ __forceinline__ void exact_argmin(const float (&d)[KP], float& m, int& lab) {
+    float t[KP];
+#pragma unroll
+    for (int k = 0; k < KP; ++k) t[k] = d[k];
+    int n = KP;
+#pragma unroll
+    for (int level = 0; level < 4; ++level) {
+        if (n > 1) {
+            int w = 0;
+#pragma unroll
+            for (int k = 0; k < KP; k += 3) {
+                if (k < n) {
+                    float v = t[k];
+                    if (k + 1 < n) v = fminf(v, t[k + 1]);
+                    if (k + 2 < n) v = fminf(v, t[k + 2]);
+                    t[w++] = v;
+                }
+            }
+            n = w;
+        }
+    }
+    m = t[0];
+    // lowest k with d_k == m: descending select chains over groups of 4 (each
+    // yields its lowest match or KP), then the minimum over the groups.
+    int g[KP / 4];
+#pragma unroll
+    for (int q = 0; q < KP / 4; ++q) {
+        int l = KP;
+#pragma unroll
+        for (int k = 4 * q + 3; k >= 4 * q; --k) l = (d[k] == m) ? k : l;
+        g[q] = l;
+    }
+    int l = g[0];
+#pragma unroll
+    for (int q = 1; q < KP / 4; ++q) l = min(l, g[q]);
+    lab = l;
+}
+
+// ---------------------------------------------------------------------------
+// Small-K path (K <= 16): k_assign_chunk.
+//
+// Work unit = one 2048-point chunk processed by a one-warp block.  Blocks are
+// scheduled by the hardware as SMs free up, so warps the issue arbiter starves
+// do not hold up the grid, and the result stays deterministic: a chunk's
+// partial row depends only on its own points, summed in a fixed order.  The
+// point stream is fed by TMA bulk copies (cp.async.bulk, one per 128-point
+// warp-tile) into a kStages-deep shared-memory ring completed on mbarriers.
+//
+// Per lane: 4 points per warp-tile (2 float2 groups), packed f32x2 form-D math,
+// centroids (negated fp32) in registers, exact argmin, private fp64 column.
+// Partials: one coalesced row per chunk; k_merge_rows sums each group of
+// kGroupChunks rows in ascending order, k_merge sums the groups.  No atomics.
+// ---------------------------------------------------------------------------
+constexpr int kLaneTile = 2 * kWarpTile;                 // 128 points per warp-tile
+constexpr int kChunkTiles = 16;
+constexpr int kChunkPoints = kLaneTile * kChunkTiles;    // 2048
+constexpr int kStages = 3;
+constexpr int kGroupChunks = 64;
+constexpr int kRowDoubles = 16 * 4 + 2;                  // [k][Sx Sy Sz n] + J + pad
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int D, int KP>
+struct ChunkSmem {
+    double2 A[KP][32];                  // {Sx, Sy} per (k, lane)
+    double2 B[KP][32];                  // {Sz, n|pad} per (k, lane)
+    float ring[kStages][D * kLaneTile]; // two AoSoA tiles (one warp-tile) per stage
+    uint64_t bar[kStages];
+};
+
+template <int D, int KP>
+__device__ __forceinline__ void form_d_pair(const float (&nc)[KP][D], float2 x, float2 y, float2 z,
+                                            float (&d0)[KP], float (&d1)[KP]) {
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+        float2 e0 = __fadd2_rn(x, make_float2(nc[k][0], nc[k][0]));
+        float2 e1 = __fadd2_rn(y, make_float2(nc[k][1], nc[k][1]));
+        float2 sq = __fmul2_rn(e0, e0);
+        sq = __ffma2_rn(e1, e1, sq);
+        if (D == 3) {
+            float2 e2 = __fadd2_rn(z, make_float2(nc[k][2], nc[k][2]));
+            sq = __ffma2_rn(e2, e2, sq);
+        }
+        d0[k] = sq.x;
+        d1[k] = sq.y;
+    }
+}
+
 template <int D, int KP, int MODE>
-__global__ void __launch_bounds__(kSmallTPB, 2)
-k_assign_small(const float* __restrict__ X, int64_t ldx, int64_t n, int K,
+__global__ void __launch_bounds__(32, 10)
+k_assign_chunk(const float* __restrict__ X, int64_t n, int K,
                const double* __restrict__ mu_buf, const DevState* __restrict__ st,
-               int mu_sel, int ignore_done, double* __restrict__ part,
+               int mu_sel, int ignore_done, double* __restrict__ cpart,
                int32_t* __restrict__ labels) {
     if (!ignore_done && st->done) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ChunkSmem<D, KP>& S = *reinterpret_cast<ChunkSmem<D, KP>*>(smem_raw);
+    constexpr int kTileFloats = D * kLaneTile;
+    constexpr unsigned kTileBytes = kTileFloats * 4;
+    const int lane = threadIdx.x;
+    const int chunk = blockIdx.x;
+    const int64_t base = (int64_t)chunk * kChunkPoints;
+    const int64_t rem = n - base;
+    const int64_t ntile64 = (rem + kLaneTile - 1) / kLaneTile;
+    const int ntile = ntile64 < kChunkTiles ? (int)ntile64 : kChunkTiles;
+    const int nfull = rem >= kChunkPoints ? kChunkTiles : (int)(rem / kLaneTile);
+    const float* src = X + (base >> 6) * (D * kWarpTile);   // first AoSoA tile of the chunk
+
+    // kick off the point stream first (its latency overlaps the staging below)
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < kStages; ++s) mbar_init(&S.bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+        for (int s = 0; s < kStages; ++s) {
+            if (s < ntile) {
+                mbar_expect_tx(&S.bar[s], kTileBytes);
+                bulk_g2s(S.ring[s], src + s * kTileFloats, kTileBytes, &S.bar[s]);
+            }
+        }
+    }
+
     const int t_it = st->t;
     const double* mu = mu_buf + (size_t)((t_it - mu_sel) & 1) * K * D;
-
-    // Stage: c_k = fl32(mu_k^t) (RN), kept negated so that x + (-c) == x - c.
+    // Stage: c_k = fl32(mu_k^t) (RN), negated so that x + (-c) == x - c.
     float nc[KP][D];
 #pragma unroll
     for (int k = 0; k < KP; ++k) {
@@ -110,145 +270,136 @@ k_assign_small(const float* __restrict__ X, int64_t ldx, int64_t n, int K,
         for (int j = 0; j < D; ++j)
             nc[k][j] = (k < K) ? -__double2float_rn(__ldg(&mu[k * D + j])) : -pos_inf();
     }
-
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int tid = threadIdx.x;
-    double2* accA = reinterpret_cast<double2*>(smem_raw);                 // [KP][TPB] (sx, sy)
-    double* accZ = reinterpret_cast<double*>(accA + KP * kSmallTPB);       // [KP][TPB] sz (D==3)
-    int* accN = reinterpret_cast<int*>(accZ + (D == 3 ? KP * kSmallTPB : 0));  // [KP][TPB]
-    double* warpJ = reinterpret_cast<double*>(accN + KP * kSmallTPB);      // [TPB/32]
-
     if (MODE & kModeReduce) {
 #pragma unroll
         for (int k = 0; k < KP; ++k) {
-            accA[k * kSmallTPB + tid] = make_double2(0.0, 0.0);
-            if (D == 3) accZ[k * kSmallTPB + tid] = 0.0;
-            accN[k * kSmallTPB + tid] = 0;
+            S.A[k][lane] = make_double2(0.0, 0.0);
+            S.B[k][lane] = make_double2(0.0, 0.0);
         }
     }
     double J = 0.0;
+    __syncwarp();
 
-    const float* X0 = X;
-    const float* X1 = X + ldx;
-    const float* X2 = X + 2 * ldx;
-    constexpr int kTile = 2 * kSmallTPB;
-    const int64_t n_tiles = (n + kTile - 1) / kTile;
+    auto accumulate = [&](int l, float px, float py, float pz) {
+        double2 a = S.A[l][lane], b = S.B[l][lane];
+        a.x += (double)px;
+        a.y += (double)py;
+        if (D == 3) b.x += (double)pz;
+        int2 c = *reinterpret_cast<int2*>(&b.y);
+        c.x += 1;
+        b.y = *reinterpret_cast<double*>(&c);
+        S.A[l][lane] = a;
+        S.B[l][lane] = b;
+    };
 
-    int64_t tile = blockIdx.x;
-    float2 px, py, pz = make_float2(0.f, 0.f);
-    if (tile < n_tiles) {
-        int64_t p = tile * kTile + 2 * tid;
-        px = ld_stream2(X0 + p);
-        py = ld_stream2(X1 + p);
-        if (D == 3) pz = ld_stream2(X2 + p);
-    }
-    for (; tile < n_tiles; tile += gridDim.x) {
-        const int64_t p = tile * kTile + 2 * tid;
-        const float2 x = px, y = py, z = pz;
-        // prefetch the next tile of this block (1-deep register pipeline)
-        const int64_t nt = tile + gridDim.x;
-        if (nt < n_tiles) {
-            int64_t q = nt * kTile + 2 * tid;
-            px = ld_stream2(X0 + q);
-            py = ld_stream2(X1 + q);
-            if (D == 3) pz = ld_stream2(X2 + q);
+    // One warp-tile: wait for its stage, refill the stage consumed one tile ago
+    // (its values are in registers and already used), assign, accumulate.
+    auto tile_step = [&](int i, bool checked) {
+        const int s = i % kStages;
+        mbar_wait(&S.bar[s], (unsigned)(i / kStages) & 1u);
+        const float* rg = S.ring[s];
+        const float2 xa = reinterpret_cast<const float2*>(rg)[lane];
+        const float2 ya = reinterpret_cast<const float2*>(rg + kWarpTile)[lane];
+        const float2 za = (D == 3) ? reinterpret_cast<const float2*>(rg + 2 * kWarpTile)[lane]
+                                   : make_float2(0.f, 0.f);
+        const float* rb = rg + D * kWarpTile;
+        const float2 xb = reinterpret_cast<const float2*>(rb)[lane];
+        const float2 yb = reinterpret_cast<const float2*>(rb + kWarpTile)[lane];
+        const float2 zb = (D == 3) ? reinterpret_cast<const float2*>(rb + 2 * kWarpTile)[lane]
+                                   : make_float2(0.f, 0.f);
+        __syncwarp();
+        const int r = i - 1 + kStages;   // tile refilled into stage (i-1) % kStages
+        if (lane == 0 && i >= 1 && r < ntile) {
+            const int sr = (i - 1) % kStages;
+            mbar_expect_tx(&S.bar[sr], kTileBytes);
+            bulk_g2s(S.ring[sr], src + (int64_t)r * kTileFloats, kTileBytes, &S.bar[sr]);
         }
 
-        // Reassignment, form D, both points at once.
-        float b0, b1;
-        int l0 = 0, l1 = 0;
-        {
-            float2 e0 = __fadd2_rn(x, make_float2(nc[0][0], nc[0][0]));
-            float2 e1 = __fadd2_rn(y, make_float2(nc[0][1], nc[0][1]));
-            float2 s = __fmul2_rn(e0, e0);
-            s = __ffma2_rn(e1, e1, s);
-            if (D == 3) {
-                float2 e2 = __fadd2_rn(z, make_float2(nc[0][2], nc[0][2]));
-                s = __ffma2_rn(e2, e2, s);
-            }
-            b0 = s.x;
-            b1 = s.y;
-        }
-#pragma unroll
-        for (int k = 1; k < KP; ++k) {
-            float2 e0 = __fadd2_rn(x, make_float2(nc[k][0], nc[k][0]));
-            float2 e1 = __fadd2_rn(y, make_float2(nc[k][1], nc[k][1]));
-            float2 s = __fmul2_rn(e0, e0);
-            s = __ffma2_rn(e1, e1, s);
-            if (D == 3) {
-                float2 e2 = __fadd2_rn(z, make_float2(nc[k][2], nc[k][2]));
-                s = __ffma2_rn(e2, e2, s);
-            }
-            if (s.x < b0) { b0 = s.x; l0 = k; }
-            if (s.y < b1) { b1 = s.y; l1 = k; }
-        }
+        // Reassignment, form D, 4 points per lane.
+        float da0[KP], da1[KP], db0[KP], db1[KP];
+        form_d_pair<D, KP>(nc, xa, ya, za, da0, da1);
+        form_d_pair<D, KP>(nc, xb, yb, zb, db0, db1);
+        float m[4];
+        int l[4];
+        exact_argmin<KP>(da0, m[0], l[0]);
+        exact_argmin<KP>(da1, m[1], l[1]);
+        exact_argmin<KP>(db0, m[2], l[2]);
+        exact_argmin<KP>(db1, m[3], l[3]);
 
-        const bool v0 = p < n, v1 = p + 1 < n;
+        const int64_t pa = base + (int64_t)i * kLaneTile + 2 * lane;
+        const int64_t pb = pa + kWarpTile;
         if (MODE & kModeLabels) {
-            // labels buffer is padded like X: the pair store is always in bounds
-            *reinterpret_cast<int2*>(labels + p) = make_int2(l0, l1);
+            *reinterpret_cast<int2*>(labels + pa) = make_int2(l[0], l[1]);
+            *reinterpret_cast<int2*>(labels + pb) = make_int2(l[2], l[3]);
         }
         if (MODE & kModeReduce) {
-            // Fused mean numerator/denominator, private column.
-            if (v0) {
-                int a = l0 * kSmallTPB + tid;
-                double2 sxy = accA[a];
-                sxy.x += (double)x.x;
-                sxy.y += (double)y.x;
-                accA[a] = sxy;
-                if (D == 3) accZ[a] += (double)z.x;
-                accN[a] += 1;
-                J += (double)b0;
-            }
-            if (v1) {
-                int a = l1 * kSmallTPB + tid;
-                double2 sxy = accA[a];
-                sxy.x += (double)x.y;
-                sxy.y += (double)y.y;
-                accA[a] = sxy;
-                if (D == 3) accZ[a] += (double)z.y;
-                accN[a] += 1;
-                J += (double)b1;
-            }
+            // Fused numerator / denominator of the mean, in the
+            // fixed point order a0, a1, b0, b1.
+            if (!checked || pa < n) { accumulate(l[0], xa.x, ya.x, za.x); J += (double)m[0]; }
+            if (!checked || pa + 1 < n) { accumulate(l[1], xa.y, ya.y, za.y); J += (double)m[1]; }
+            if (!checked || pb < n) { accumulate(l[2], xb.x, yb.x, zb.x); J += (double)m[2]; }
+            if (!checked || pb + 1 < n) { accumulate(l[3], xb.y, yb.y, zb.y); J += (double)m[3]; }
         }
-    }
+    };
 
+#pragma unroll 1
+    for (int i = 0; i < nfull; ++i) tile_step(i, false);
+    if (nfull < ntile) tile_step(nfull, true);   // the ragged last tile of the last chunk
     if (!(MODE & kModeReduce)) return;
 
-    // Block reduction in a fixed order: lane l sums threads l, l+32, ... in
-    // ascending order, then a butterfly over the 32 lanes.
-    const int lane = tid & 31, warp = tid >> 5;
-    constexpr int W = kSmallTPB / 32;
-    {
-        double j = J;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) j += __shfl_xor_sync(0xffffffffu, j, o);
-        if (lane == 0) warpJ[warp] = j;
-    }
-    __syncthreads();
-    const int G = gridDim.x;
-    const int nE = K * D + K + 1;
-    for (int e = warp; e < nE; e += W) {
-        double v = 0.0;
-        if (e < K * D) {
-            const int k = e / D, j = e % D;
-#pragma unroll
-            for (int r = 0; r < kSmallTPB / 32; ++r) {
-                const int a = k * kSmallTPB + r * 32 + lane;
-                v += (j == 0) ? accA[a].x : (j == 1) ? accA[a].y : accZ[a];
-            }
-        } else if (e < K * D + K) {
-            const int k = e - K * D;
-            long long c = 0;
-#pragma unroll
-            for (int r = 0; r < kSmallTPB / 32; ++r) c += accN[k * kSmallTPB + r * 32 + lane];
-            v = (double)c;
-        } else {
-            v = (lane < W) ? warpJ[lane] : 0.0;
+    // ---- chunk partial: row[4k + j] = sum over lanes, fixed rotation order ----
+    __syncwarp();
+    // lane L owns double2 entry (k = L >> 1, half = L & 1); the 8 lanes of one
+    // LDS.128 phase read distinct columns -> conflict-free.
+    const int k = lane >> 1;
+    const double2* col = (lane & 1) ? &S.B[0][0] : &S.A[0][0];
+    double v0 = 0.0, v1 = 0.0;
+    long long cnt = 0;
+    if (k < KP) {
+#pragma unroll 8
+        for (int r = 0; r < 32; ++r) {
+            const int t = (r + lane) & 31;
+            const double2 w = col[k * 32 + t];
+            v0 += w.x;
+            if (lane & 1) cnt += reinterpret_cast<const int2*>(&w.y)->x;
+            else v1 += w.y;
         }
+    }
+    double jj = J;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) part[(size_t)e * G + blockIdx.x] = v;
+    for (int o = 16; o > 0; o >>= 1) jj += __shfl_xor_sync(0xffffffffu, jj, o);
+    double* row = cpart + (size_t)chunk * kRowDoubles;
+    // row layout [k][Sx, Sy, Sz, n] (k < KP), then J at 64
+    const double2 out = (lane & 1) ? make_double2(v0, (double)cnt) : make_double2(v0, v1);
+    reinterpret_cast<double2*>(row)[lane] = (k < KP) ? out : make_double2(0.0, 0.0);
+    if (lane == 0) row[64] = jj;
+}
+
+// ---------------------------------------------------------------------------
+// k_merge_rows: group g sums the rows of chunks [64g, 64g + 64) in ascending
+// chunk order and scatters them to gpart[e][g] (the layout k_merge sums).
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(96)
+k_merge_rows(const double* __restrict__ cpart, int n_chunks, int K, double* __restrict__ gpart,
+             int n_groups, const DevState* __restrict__ st, int ignore_done) {
+    if (!ignore_done && st->done) return;
+    const int q = threadIdx.x;            // row entry
+    if (q > 64) return;
+    const int g = blockIdx.x;
+    const int c0 = g * kGroupChunks;
+    const int c1 = min(n_chunks, c0 + kGroupChunks);
+    double v = 0.0;
+#pragma unroll 8
+    for (int c = c0; c < c1; ++c) v += cpart[(size_t)c * kRowDoubles + q];
+    if (q == 64) {
+        gpart[(size_t)(K * D + K) * n_groups + g] = v;
+        return;
+    }
+    const int k = q >> 2, j = q & 3;
+    if (k < K) {
+        if (j < D) gpart[(size_t)(k * D + j) * n_groups + g] = v;
+        else if (j == 3) gpart[(size_t)(K * D + k) * n_groups + g] = v;
     }
 }
 
@@ -297,17 +448,14 @@ k_assign_large(const float* __restrict__ X, int64_t ldx, int64_t n, int K,
     int* myN = accN + warp * K;
     double J = 0.0;
 
-    const float* X0 = X;
-    const float* X1 = X + ldx;
-    const float* X2 = X + 2 * ldx;
     const int tileN = 2 * nthr;
     const int64_t n_tiles = (n + tileN - 1) / tileN;
 
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const int64_t p = tile * tileN + 2 * tid;
-        const float2 x = ld_stream2(X0 + p);
-        const float2 y = ld_stream2(X1 + p);
-        const float2 z = (D == 3) ? ld_stream2(X2 + p) : make_float2(0.f, 0.f);
+        const float2 x = ld_stream2(tile_coord<D>(X, p, 0));
+        const float2 y = ld_stream2(tile_coord<D>(X, p, 1));
+        const float2 z = (D == 3) ? ld_stream2(tile_coord<D>(X, p, 2)) : make_float2(0.f, 0.f);
 
         float b0 = pos_inf(), b1 = pos_inf();
         int l0 = 0, l1 = 0;

@@ -52,7 +52,7 @@ struct kmeans_ctx {
     void* comm = nullptr;
     int nranks = 1, rank = 0;
 
-    float* X = nullptr;          // d x ldx SoA fp32
+    float* X = nullptr;          // AoSoA fp32: ldx/64 tiles of [x64 y64 (z64)]
     double* mu = nullptr;        // 2 x Kpad x d (ping-pong by t & 1)
     double* part = nullptr;      // nE x G per-block partials
     double* red = nullptr;       // nE merged partials
@@ -64,7 +64,9 @@ struct kmeans_ctx {
     int64_t* idx_dev = nullptr;  // K
     int* flag = nullptr;
 
-    int G = 0, tpb = 0, smem = 0, path = 0;
+    int G = 0, tpb = 0, smem = 0, path = 0;   // G = columns of part (blocks or groups)
+    int n_chunks = 0;
+    double* cpart = nullptr;      // n_chunks x kRowDoubles chunk partials (path 0)
     int nE = 0;
     cudaGraphExec_t graph = nullptr;
     int64_t launches = 0;
@@ -75,7 +77,8 @@ struct kmeans_ctx {
 
 namespace {
 
-constexpr int kKernelsPerIter = 3;  // assign, merge, update
+// kernels of this library per iteration: assign (+ merge_rows on path 0), merge, update
+int kernels_per_iter(const kmeans_ctx* ctx) { return ctx->path == 0 ? 4 : 3; }
 
 kmeans_status cuda_fail(kmeans_ctx* c, cudaError_t e, const char* what) {
     set_error("%s: %s", what, cudaGetErrorString(e));
@@ -112,43 +115,51 @@ struct DeviceGuard {
 };
 
 // --- kernel selection --------------------------------------------------------
-using AssignFn = void (*)(const float*, int64_t, int64_t, int, const double*, const DevState*,
-                          int, int, double*, int32_t*);
+// path 0 (K <= 16): k_assign_chunk, one-warp blocks over 2048-point chunks.
+// path 1 (K > 16):  k_assign_large, persistent blocks, smem centroids.
+using ChunkFn = void (*)(const float*, int64_t, int, const double*, const DevState*, int, int,
+                         double*, int32_t*);
+using LargeFn = void (*)(const float*, int64_t, int64_t, int, const double*, const DevState*,
+                         int, int, double*, int32_t*);
+
+int small_kp(int K) { return K <= 4 ? 4 : (K <= 8 ? 8 : 16); }
 
 template <int D, int MODE>
-AssignFn pick_small(int K) {
-    if (K <= 4) return km::k_assign_small<D, 4, MODE>;
-    if (K <= 8) return km::k_assign_small<D, 8, MODE>;
-    return km::k_assign_small<D, 16, MODE>;
+ChunkFn pick_chunk_kp(int K) {
+    if (K <= 4) return km::k_assign_chunk<D, 4, MODE>;
+    if (K <= 8) return km::k_assign_chunk<D, 8, MODE>;
+    return km::k_assign_chunk<D, 16, MODE>;
 }
 
-AssignFn pick_assign(int d, int K, int mode) {
-    const bool small = K <= 16;
+ChunkFn pick_chunk(int d, int K, int mode) {
     if (d == 2) {
-        if (small) {
-            if (mode == 1) return pick_small<2, 1>(K);
-            if (mode == 2) return pick_small<2, 2>(K);
-            return pick_small<2, 3>(K);
-        }
+        if (mode == 1) return pick_chunk_kp<2, 1>(K);
+        if (mode == 2) return pick_chunk_kp<2, 2>(K);
+        return pick_chunk_kp<2, 3>(K);
+    }
+    if (mode == 1) return pick_chunk_kp<3, 1>(K);
+    if (mode == 2) return pick_chunk_kp<3, 2>(K);
+    return pick_chunk_kp<3, 3>(K);
+}
+
+int chunk_smem(int d, int K) {
+    const int kp = small_kp(K);
+    if (d == 2)
+        return kp == 4 ? sizeof(km::ChunkSmem<2, 4>)
+                       : (kp == 8 ? sizeof(km::ChunkSmem<2, 8>) : sizeof(km::ChunkSmem<2, 16>));
+    return kp == 4 ? sizeof(km::ChunkSmem<3, 4>)
+                   : (kp == 8 ? sizeof(km::ChunkSmem<3, 8>) : sizeof(km::ChunkSmem<3, 16>));
+}
+
+LargeFn pick_large(int d, int mode) {
+    if (d == 2) {
         if (mode == 1) return km::k_assign_large<2, 1>;
         if (mode == 2) return km::k_assign_large<2, 2>;
         return km::k_assign_large<2, 3>;
     }
-    if (small) {
-        if (mode == 1) return pick_small<3, 1>(K);
-        if (mode == 2) return pick_small<3, 2>(K);
-        return pick_small<3, 3>(K);
-    }
     if (mode == 1) return km::k_assign_large<3, 1>;
     if (mode == 2) return km::k_assign_large<3, 2>;
     return km::k_assign_large<3, 3>;
-}
-
-int small_kp(int K) { return K <= 4 ? 4 : (K <= 8 ? 8 : 16); }
-
-int small_smem(int d, int K) {
-    const int kp = small_kp(K);
-    return kp * km::kSmallTPB * (16 + (d == 3 ? 8 : 0) + 4) + (km::kSmallTPB / 32) * 8;
 }
 
 int large_smem(int d, int K, int tpb) {
@@ -161,10 +172,16 @@ kmeans_status configure(kmeans_ctx* ctx) {
     CK(cudaGetDeviceProperties(&prop, ctx->device));
     const int sms = prop.multiProcessorCount;
     const int maxSmem = (int)prop.sharedMemPerBlockOptin;
+    ctx->nE = ctx->K * ctx->d + ctx->K + 1;
     if (ctx->K <= 16) {
         ctx->path = 0;
-        ctx->tpb = km::kSmallTPB;
-        ctx->smem = small_smem(ctx->d, ctx->K);
+        ctx->tpb = 32;
+        ctx->smem = chunk_smem(ctx->d, ctx->K);
+        for (int mode = 1; mode <= 3; ++mode)
+            CK(cudaFuncSetAttribute((const void*)pick_chunk(ctx->d, ctx->K, mode),
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
+        ctx->n_chunks = (int)((ctx->N + km::kChunkPoints - 1) / km::kChunkPoints);
+        ctx->G = (ctx->n_chunks + km::kGroupChunks - 1) / km::kGroupChunks;  // groups
     } else {
         ctx->path = 1;
         int tpb = km::kLargeTPBMax;
@@ -175,29 +192,43 @@ kmeans_status configure(kmeans_ctx* ctx) {
             set_error("K=%d needs %d B of shared memory (max %d)", ctx->K, ctx->smem, maxSmem);
             return KMEANS_EINVAL;
         }
+        for (int mode = 1; mode <= 3; ++mode)
+            CK(cudaFuncSetAttribute((const void*)pick_large(ctx->d, mode),
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &occ, (const void*)pick_large(ctx->d, 1), ctx->tpb, ctx->smem));
+        occ = std::max(occ, 1);
+        ctx->G = sms * occ;  // persistent grid: every SM busy, static tile schedule
     }
-    int occ = 0;
-    for (int mode = 1; mode <= 3; ++mode) {
-        AssignFn f = pick_assign(ctx->d, ctx->K, mode);
-        CK(cudaFuncSetAttribute((const void*)f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                ctx->smem));
-    }
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &occ, (const void*)pick_assign(ctx->d, ctx->K, 1), ctx->tpb, ctx->smem));
-    occ = std::max(occ, 1);
-    ctx->G = sms * occ;  // persistent grid: every SM busy, static tile schedule
-    ctx->nE = ctx->K * ctx->d + ctx->K + 1;
     return KMEANS_OK;
 }
 
 kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_done) {
-    AssignFn f = pick_assign(ctx->d, ctx->K, mode);
     if ((mode & km::kModeLabels) && !ctx->labels) {
         CK(cudaMalloc(&ctx->labels, sizeof(int32_t) * ctx->ldx));
     }
-    f<<<ctx->G, ctx->tpb, ctx->smem, ctx->stream>>>(ctx->X, ctx->ldx, ctx->N, ctx->K, ctx->mu,
-                                                    ctx->st, mu_sel, ignore_done, ctx->part,
-                                                    ctx->labels);
+    if (ctx->path == 0) {
+        ChunkFn f = pick_chunk(ctx->d, ctx->K, mode);
+        f<<<ctx->n_chunks, 32, ctx->smem, ctx->stream>>>(ctx->X, ctx->N, ctx->K, ctx->mu, ctx->st,
+                                                         mu_sel, ignore_done, ctx->cpart,
+                                                         ctx->labels);
+        if (mode & km::kModeReduce) {
+            // chunk rows -> group columns of part (fixed ascending order)
+            if (ctx->d == 2)
+                km::k_merge_rows<2><<<ctx->G, 96, 0, ctx->stream>>>(
+                    ctx->cpart, ctx->n_chunks, ctx->K, ctx->part, ctx->G, ctx->st, ignore_done);
+            else
+                km::k_merge_rows<3><<<ctx->G, 96, 0, ctx->stream>>>(
+                    ctx->cpart, ctx->n_chunks, ctx->K, ctx->part, ctx->G, ctx->st, ignore_done);
+            ctx->launches += 1;
+        }
+    } else {
+        LargeFn f = pick_large(ctx->d, mode);
+        f<<<ctx->G, ctx->tpb, ctx->smem, ctx->stream>>>(ctx->X, ctx->ldx, ctx->N, ctx->K, ctx->mu,
+                                                        ctx->st, mu_sel, ignore_done, ctx->part,
+                                                        ctx->labels);
+    }
     ctx->launches += 1;
     CK(cudaGetLastError());
     return KMEANS_OK;
@@ -399,6 +430,7 @@ void kmeans_destroy(kmeans_ctx* ctx) {
         cudaFree(ctx->labels);
         cudaFree(ctx->idx_dev);
         cudaFree(ctx->flag);
+        cudaFree(ctx->cpart);
         if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
         cudaGetLastError();
     }
@@ -447,7 +479,8 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
     ctx->global_N = gN;
     ctx->global_offset = opts.global_offset;
     ctx->comm = opts.nccl_comm;
-    ctx->ldx = round_up(N + km::kPadPoints, km::kPadPoints);
+    // padded so every full 2048-point chunk (and every large-path tile) is in bounds
+    ctx->ldx = round_up(N, km::kChunkPoints) + km::kChunkPoints;
 #ifdef KMEANS_WITH_NCCL
     if (ctx->comm) {
         ncclCommCount((ncclComm_t)ctx->comm, &ctx->nranks);
@@ -480,6 +513,9 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
         cudaMalloc(&ctx->red, sizeof(double) * ctx->nE) != cudaSuccess ||
         cudaMalloc(&ctx->st, sizeof(DevState)) != cudaSuccess ||
         cudaMalloc(&ctx->idx_dev, sizeof(int64_t) * K) != cudaSuccess ||
+        (ctx->path == 0 &&
+         cudaMalloc(&ctx->cpart, sizeof(double) * km::kRowDoubles * (size_t)ctx->n_chunks) !=
+             cudaSuccess) ||
         cudaMalloc(&ctx->flag, sizeof(int)) != cudaSuccess) {
         cudaGetLastError();
         set_error("device allocation failed (%zu bytes of points)", bytesX);
@@ -488,6 +524,9 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
     if ((s = ensure_trace(ctx, 64)) != KMEANS_OK) return fail(s);
     if (cudaMemsetAsync(ctx->mu, 0, sizeof(double) * 2 * Kpad * d, ctx->stream) != cudaSuccess ||
         cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream) != cudaSuccess ||
+        (ctx->path == 0 &&
+         cudaMemsetAsync(ctx->cpart, 0, sizeof(double) * km::kRowDoubles * (size_t)ctx->n_chunks,
+                         ctx->stream) != cudaSuccess) ||
         cudaMemsetAsync(ctx->st, 0, sizeof(DevState), ctx->stream) != cudaSuccess) {
         cuda_fail(ctx, cudaGetLastError(), "cudaMemsetAsync");
         return fail(KMEANS_ECUDA);
@@ -556,7 +595,7 @@ kmeans_status kmeans_start(kmeans_ctx* ctx, const int64_t* init_idx, const doubl
                            cudaMemcpyHostToDevice, ctx->stream));
         const int n = ctx->K * ctx->d;
         km::k_init_gather<<<(n + 255) / 256, 256, 0, ctx->stream>>>(
-            ctx->X, ctx->ldx, ctx->d, ctx->K, ctx->idx_dev, ctx->global_offset, ctx->N, ctx->mu);
+            ctx->X, ctx->d, ctx->K, ctx->idx_dev, ctx->global_offset, ctx->N, ctx->mu);
         ctx->launches += 1;
         CK(cudaGetLastError());
         // CC1: assemble mu^0 from the owners (exact: one x plus zeros)
@@ -585,7 +624,7 @@ kmeans_status kmeans_iterate(kmeans_ctx* ctx, int n) {
     if (s != KMEANS_OK) return s;
     for (int i = 0; i < n; ++i) {
         CK(cudaGraphLaunch(ctx->graph, ctx->stream));
-        ctx->launches += kKernelsPerIter;
+        ctx->launches += kernels_per_iter(ctx);
     }
     return KMEANS_OK;
 }
@@ -788,11 +827,11 @@ kmeans_status kmeans_get_info(kmeans_ctx* ctx, kmeans_info* info) {
     info->ldx = ctx->ldx;
     info->d = ctx->d;
     info->K = ctx->K;
-    info->grid = ctx->G;
+    info->grid = ctx->path == 0 ? ctx->n_chunks : ctx->G;
     info->block = ctx->tpb;
     info->smem_bytes = ctx->smem;
     info->path = ctx->path;
-    info->kernels_per_iter = kKernelsPerIter;
+    info->kernels_per_iter = kernels_per_iter(ctx);
     info->kernel_launches = ctx->launches;
     info->nranks = ctx->nranks;
     info->rank = ctx->rank;

@@ -337,7 +337,7 @@ def test_full_size_ns_step_parity():
     mu = X[datagen.init_indices(w)].astype(np.float64)
     with km.Context(X, w.K) as c:
         info = c.info()
-        assert info["path"] == 0 and info["grid"] % 148 == 0
+        assert info["path"] == 0 and info["grid"] == (w.N + 2047) // 2048
         check_step(X, mu, ctx=c, tag="NS full")
 
 
