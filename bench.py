@@ -235,10 +235,9 @@ def main():
     distributed = P > 1
     comm = None
     if distributed:
+        from paper_2405_12052_b200 import dist as kdist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        uid = [km.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        comm = km.comm_init(P, uid[0], rank, local)
+        comm = kdist.init_comm(rank, P, local)
 
     def barrier():
         if distributed:

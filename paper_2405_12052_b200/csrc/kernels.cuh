@@ -206,6 +206,7 @@ struct ChunkSmem {
     double2 B[KP][32];                  // {Sz, n|pad} per (k, lane)
     float ring[kStages][D * kLaneTile]; // two AoSoA tiles (one warp-tile) per stage
     uint64_t bar[kStages];
+    float cst[KP * D];                  // staged negated fp32 centroids
 };
 
 template <int D, int KP>
@@ -262,14 +263,10 @@ k_assign_chunk(const float* __restrict__ X, int64_t n, int K,
 
     const int t_it = st->t;
     const double* mu = mu_buf + (size_t)((t_it - mu_sel) & 1) * K * D;
-    // Stage: c_k = fl32(mu_k^t) (RN), negated so that x + (-c) == x - c.
-    float nc[KP][D];
-#pragma unroll
-    for (int k = 0; k < KP; ++k) {
-#pragma unroll
-        for (int j = 0; j < D; ++j)
-            nc[k][j] = (k < K) ? -__double2float_rn(__ldg(&mu[k * D + j])) : -pos_inf();
-    }
+    // Stage: c_k = fl32(mu_k^t) (RN), negated so that x + (-c) == x - c; each
+    // lane converts <= 2 entries, the warp shares them through smem.
+    for (int q = lane; q < KP * D; q += 32)
+        S.cst[q] = (q < K * D) ? -__double2float_rn(__ldg(&mu[q])) : -pos_inf();
     if (MODE & kModeReduce) {
 #pragma unroll
         for (int k = 0; k < KP; ++k) {
@@ -277,8 +274,14 @@ k_assign_chunk(const float* __restrict__ X, int64_t n, int K,
             S.B[k][lane] = make_double2(0.0, 0.0);
         }
     }
-    double J = 0.0;
     __syncwarp();
+    float nc[KP][D];
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) nc[k][j] = S.cst[k * D + j];
+    }
+    double J = 0.0;
 
     auto accumulate = [&](int l, float px, float py, float pz) {
         double2 a = S.A[l][lane], b = S.B[l][lane];
@@ -292,21 +295,26 @@ k_assign_chunk(const float* __restrict__ X, int64_t n, int K,
         S.B[l][lane] = b;
     };
 
-    // One warp-tile: wait for its stage, refill the stage consumed one tile ago
-    // (its values are in registers and already used), assign, accumulate.
-    auto tile_step = [&](int i, bool checked) {
+    // Points of one warp-tile held by a lane: a = (2L, 2L+1), b = (64+2L, 64+2L+1).
+    struct Pts {
+        float2 xa, ya, za, xb, yb, zb;
+    };
+    // Wait for tile i's stage, read this lane's points, refill the stage that
+    // tile i-1 used (its values are in registers and consumed by then).
+    auto fetch = [&](int i) {
         const int s = i % kStages;
         mbar_wait(&S.bar[s], (unsigned)(i / kStages) & 1u);
         const float* rg = S.ring[s];
-        const float2 xa = reinterpret_cast<const float2*>(rg)[lane];
-        const float2 ya = reinterpret_cast<const float2*>(rg + kWarpTile)[lane];
-        const float2 za = (D == 3) ? reinterpret_cast<const float2*>(rg + 2 * kWarpTile)[lane]
-                                   : make_float2(0.f, 0.f);
         const float* rb = rg + D * kWarpTile;
-        const float2 xb = reinterpret_cast<const float2*>(rb)[lane];
-        const float2 yb = reinterpret_cast<const float2*>(rb + kWarpTile)[lane];
-        const float2 zb = (D == 3) ? reinterpret_cast<const float2*>(rb + 2 * kWarpTile)[lane]
-                                   : make_float2(0.f, 0.f);
+        Pts P;
+        P.xa = reinterpret_cast<const float2*>(rg)[lane];
+        P.ya = reinterpret_cast<const float2*>(rg + kWarpTile)[lane];
+        P.za = (D == 3) ? reinterpret_cast<const float2*>(rg + 2 * kWarpTile)[lane]
+                        : make_float2(0.f, 0.f);
+        P.xb = reinterpret_cast<const float2*>(rb)[lane];
+        P.yb = reinterpret_cast<const float2*>(rb + kWarpTile)[lane];
+        P.zb = (D == 3) ? reinterpret_cast<const float2*>(rb + 2 * kWarpTile)[lane]
+                        : make_float2(0.f, 0.f);
         __syncwarp();
         const int r = i - 1 + kStages;   // tile refilled into stage (i-1) % kStages
         if (lane == 0 && i >= 1 && r < ntile) {
@@ -314,37 +322,77 @@ k_assign_chunk(const float* __restrict__ X, int64_t n, int K,
             mbar_expect_tx(&S.bar[sr], kTileBytes);
             bulk_g2s(S.ring[sr], src + (int64_t)r * kTileFloats, kTileBytes, &S.bar[sr]);
         }
-
-        // Reassignment, form D, 4 points per lane.
+        return P;
+    };
+    // Reassignment, form D, 4 points per lane.
+    auto assign = [&](int i, const Pts& P, float (&m)[4], int (&l)[4]) {
         float da0[KP], da1[KP], db0[KP], db1[KP];
-        form_d_pair<D, KP>(nc, xa, ya, za, da0, da1);
-        form_d_pair<D, KP>(nc, xb, yb, zb, db0, db1);
-        float m[4];
-        int l[4];
+        form_d_pair<D, KP>(nc, P.xa, P.ya, P.za, da0, da1);
+        form_d_pair<D, KP>(nc, P.xb, P.yb, P.zb, db0, db1);
         exact_argmin<KP>(da0, m[0], l[0]);
         exact_argmin<KP>(da1, m[1], l[1]);
         exact_argmin<KP>(db0, m[2], l[2]);
         exact_argmin<KP>(db1, m[3], l[3]);
-
-        const int64_t pa = base + (int64_t)i * kLaneTile + 2 * lane;
-        const int64_t pb = pa + kWarpTile;
         if (MODE & kModeLabels) {
+            const int64_t pa = base + (int64_t)i * kLaneTile + 2 * lane;
             *reinterpret_cast<int2*>(labels + pa) = make_int2(l[0], l[1]);
-            *reinterpret_cast<int2*>(labels + pb) = make_int2(l[2], l[3]);
-        }
-        if (MODE & kModeReduce) {
-            // Fused numerator / denominator of the mean, in the
-            // fixed point order a0, a1, b0, b1.
-            if (!checked || pa < n) { accumulate(l[0], xa.x, ya.x, za.x); J += (double)m[0]; }
-            if (!checked || pa + 1 < n) { accumulate(l[1], xa.y, ya.y, za.y); J += (double)m[1]; }
-            if (!checked || pb < n) { accumulate(l[2], xb.x, yb.x, zb.x); J += (double)m[2]; }
-            if (!checked || pb + 1 < n) { accumulate(l[3], xb.y, yb.y, zb.y); J += (double)m[3]; }
+            *reinterpret_cast<int2*>(labels + pa + kWarpTile) = make_int2(l[2], l[3]);
         }
     };
+    // Fused numerator / denominator of the mean, points in the
+    // fixed order a0, a1, b0, b1.
+    auto reduce_full = [&](const Pts& P, const float (&m)[4], const int (&l)[4]) {
+        if (!(MODE & kModeReduce)) return;
+        accumulate(l[0], P.xa.x, P.ya.x, P.za.x);
+        accumulate(l[1], P.xa.y, P.ya.y, P.za.y);
+        accumulate(l[2], P.xb.x, P.yb.x, P.zb.x);
+        accumulate(l[3], P.xb.y, P.yb.y, P.zb.y);
+        J += (double)m[0];
+        J += (double)m[1];
+        J += (double)m[2];
+        J += (double)m[3];
+    };
+    auto reduce_checked = [&](int i, const Pts& P, const float (&m)[4], const int (&l)[4]) {
+        if (!(MODE & kModeReduce)) return;
+        const int64_t pa = base + (int64_t)i * kLaneTile + 2 * lane, pb = pa + kWarpTile;
+        if (pa < n) { accumulate(l[0], P.xa.x, P.ya.x, P.za.x); J += (double)m[0]; }
+        if (pa + 1 < n) { accumulate(l[1], P.xa.y, P.ya.y, P.za.y); J += (double)m[1]; }
+        if (pb < n) { accumulate(l[2], P.xb.x, P.yb.x, P.zb.x); J += (double)m[2]; }
+        if (pb + 1 < n) { accumulate(l[3], P.xb.y, P.yb.y, P.zb.y); J += (double)m[3]; }
+    };
 
+    if (nfull == kChunkTiles) {
+        // Full chunk: software pipeline unrolled by 2 -- the smem reduction of
+        // one tile sits in the same basic block as the distance math of the next,
+        // so the scheduler interleaves them.
+        float mA[4], mB[4];
+        int lA[4], lB[4];
+        Pts A = fetch(0);
+        assign(0, A, mA, lA);
 #pragma unroll 1
-    for (int i = 0; i < nfull; ++i) tile_step(i, false);
-    if (nfull < ntile) tile_step(nfull, true);   // the ragged last tile of the last chunk
+        for (int i = 1; i < kChunkTiles - 1; i += 2) {
+            const Pts B = fetch(i);
+            reduce_full(A, mA, lA);
+            assign(i, B, mB, lB);
+            A = fetch(i + 1);
+            reduce_full(B, mB, lB);
+            assign(i + 1, A, mA, lA);
+        }
+        const Pts B = fetch(kChunkTiles - 1);
+        reduce_full(A, mA, lA);
+        assign(kChunkTiles - 1, B, mB, lB);
+        reduce_full(B, mB, lB);
+    } else {
+        // the last chunk: plain loop with per-point bounds
+#pragma unroll 1
+        for (int i = 0; i < ntile; ++i) {
+            const Pts P = fetch(i);
+            float m[4];
+            int l[4];
+            assign(i, P, m, l);
+            reduce_checked(i, P, m, l);
+        }
+    }
     if (!(MODE & kModeReduce)) return;
 
     // ---- chunk partial: row[4k + j] = sum over lanes, fixed rotation order ----

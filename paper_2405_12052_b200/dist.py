@@ -1,0 +1,34 @@
+"""Multi-GPU plumbing (host side): one process per GPU, launched by torchrun.
+
+The data-parallel split follows the paper's OpenMP design -- "the dataset is
+to be divided among the number of threads" -- as contiguous
+ceiling-partition shards (datagen.shard_range).  Each rank keeps its shard in
+HBM; the only exchange per iteration is one allreduce of the K*(d+1)+1
+partials (sums, counts, inertia), done by the library's own NCCL communicator
+inside the iteration's CUDA graph.  This module only creates that
+communicator: rank 0 draws an NCCL unique id, torch.distributed broadcasts it
+(any backend, gloo included), every rank calls kmeans_comm_init.
+"""
+from __future__ import annotations
+
+from . import datagen
+from . import kmeans as km
+
+
+def shard(global_N: int, world: int, rank: int) -> tuple[int, int]:
+    """[a, b) owned by `rank` (contiguous ceiling partition)."""
+    return datagen.shard_range(global_N, world, rank)
+
+
+def broadcast_unique_id(rank: int, group=None) -> bytes:
+    """Rank 0's NCCL unique id, broadcast over torch.distributed."""
+    import torch.distributed as dist
+    obj = [km.comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
+
+
+def init_comm(rank: int, world: int, device: int, group=None) -> int:
+    """Create the library's NCCL communicator for this rank (collective)."""
+    uid = broadcast_unique_id(rank, group)
+    return km.comm_init(world, uid, rank, device)
