@@ -56,6 +56,9 @@ def parse():
                     help="--impl reference: target CPU time of the whole run")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sort", action="store_true",
+                    help="keep the caller's point order (full-scan assign kernel)")
+    ap.add_argument("--no-fullscan-roofline", action="store_true")
     return ap.parse_args()
 
 
@@ -259,7 +262,8 @@ def main():
     datagen.generate(gen_w, a, b - a, N=global_N, out=Xh.numpy())
     init = datagen.init_indices(gen_w, N=global_N, K=w.K)
 
-    ctx = km.Context(Xh, w.K, device=local, comm=comm, global_offset=a, global_N=global_N)
+    ctx = km.Context(Xh, w.K, device=local, comm=comm, global_offset=a, global_N=global_N,
+                     sort=not args.no_sort)
     info = ctx.info()
     stream = torch.cuda.ExternalStream(ctx.stream)
     ctx.start(init_idx=init, tol=0.0, max_iter=1 << 30)
@@ -289,53 +293,68 @@ def main():
     ms_per_step = ms / args.steps
 
     # ---- dominant kernel alone (roofline): assign + fused reduction ------------
-    reps = max(20, min(args.steps, 200))
-    ctx.profile_assign(3)
-    torch.cuda.synchronize()
-    a0 = torch.cuda.Event(enable_timing=True)
-    a1 = torch.cuda.Event(enable_timing=True)
-    a0.record(stream)
-    ctx.profile_assign(reps)
-    a1.record(stream)
-    a1.synchronize()
-    t_assign = a0.elapsed_time(a1) / reps / 1e3        # s per launch
+    def time_assign(c):
+        st_ = torch.cuda.ExternalStream(c.stream)
+        reps = max(20, min(args.steps, 200))
+        c.profile_assign(3)
+        torch.cuda.synchronize()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(st_)
+        c.profile_assign(reps)
+        a1.record(st_)
+        a1.synchronize()
+        return a0.elapsed_time(a1) / reps / 1e3        # s per launch
+
     n_local = b - a
     hbm_gbs, sm_max_mhz, peak_src = peaks()
     clk = clocks.summary()
     bytes_per_launch = 4.0 * w.d * n_local                      # read every point once
     lane_ops_per_launch = 2.0 * w.d * w.K * n_local             # form D: d FADD, 1 FMUL, d-1 FFMA
     fp32_peak = SMS * FP32_LANES_PER_SM * sm_max_mhz * 1e6 / 1e12   # T lane-ops/s
-    achieved_gbs = bytes_per_launch / t_assign / 1e9
-    achieved_tops = lane_ops_per_launch / t_assign / 1e12
-    t_hbm = bytes_per_launch / (hbm_gbs * 1e9)
-    t_alu = lane_ops_per_launch / (fp32_peak * 1e12)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            tj = json.load(f)
-        key = f"{w.name}:P{P}:{args.scaling}"
-        traffic = tj.get(key)
+            traffic = json.load(f).get(f"{w.name}:P{P}:{args.scaling}:{'sorted' if info['sorted'] else 'unsorted'}")
     except Exception:
         pass
-    if t_alu >= t_hbm:
-        roofline = {"bound": "alu", "achieved": achieved_tops, "peak": fp32_peak,
-                    "unit": "TFLOP/s", "op": "FP32 lane-op (FADD, FMUL, FFMA = 1 each)",
-                    "frac": achieved_tops / fp32_peak, "traffic": traffic,
-                    "kernel": "k_assign_small" if info["path"] == 0 else "k_assign_large",
-                    "kernel_ms": t_assign * 1e3,
-                    "kernel_share_of_step": t_assign * 1e3 / ms_per_step,
-                    "peak_source": f"148 SMs x 128 FP32 lanes x {sm_max_mhz:.0f} MHz"}
-    else:
-        roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_gbs, "unit": "GB/s",
-                    "frac": achieved_gbs / hbm_gbs, "traffic": traffic,
-                    "kernel": "k_assign_small" if info["path"] == 0 else "k_assign_large",
-                    "kernel_ms": t_assign * 1e3,
-                    "kernel_share_of_step": t_assign * 1e3 / ms_per_step,
-                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
-    roofline_hbm = {"achieved": achieved_gbs, "peak": hbm_gbs, "unit": "GB/s",
-                    "frac": achieved_gbs / hbm_gbs,
+
+    def roofline_of(t_kernel, kernel, sorted_path):
+        ach_gbs = bytes_per_launch / t_kernel / 1e9
+        ach_tops = lane_ops_per_launch / t_kernel / 1e12
+        common = {"kernel": kernel, "kernel_ms": t_kernel * 1e3,
+                  "kernel_share_of_step": t_kernel * 1e3 / ms_per_step}
+        t_hbm = bytes_per_launch / (hbm_gbs * 1e9)
+        t_alu = lane_ops_per_launch / (fp32_peak * 1e12)
+        if sorted_path or t_hbm >= t_alu:
+            # the pruned kernel does not perform the full 2dK FP32 work: its
+            # binding roofline is the HBM stream of the points
+            return dict(bound="hbm", achieved=ach_gbs, peak=hbm_gbs, unit="GB/s",
+                        frac=ach_gbs / hbm_gbs, traffic=traffic,
+                        peak_source=f"MEASURED_PEAKS.json hbm_gbs ({peak_src})", **common)
+        return dict(bound="alu", achieved=ach_tops, peak=fp32_peak, unit="TFLOP/s",
+                    op="FP32 lane-op (FADD, FMUL, FFMA = 1 each)", frac=ach_tops / fp32_peak,
+                    traffic=traffic, peak_source=f"148 SMs x 128 FP32 lanes x {sm_max_mhz:.0f} MHz",
+                    hbm_frac=ach_gbs / hbm_gbs, **common)
+
+    t_assign = time_assign(ctx)
+    kname = "k_assign_sorted" if info["sorted"] else ("k_assign_chunk" if info["path"] == 0
+                                                       else "k_assign_large")
+    roofline = roofline_of(t_assign, kname, bool(info["sorted"]))
+    roofline_hbm = {"achieved": bytes_per_launch / t_assign / 1e9, "peak": hbm_gbs, "unit": "GB/s",
+                    "frac": bytes_per_launch / t_assign / 1e9 / hbm_gbs,
                     "step_frac": (bytes_per_launch / (ms_per_step / 1e3) / 1e9) / hbm_gbs,
                     "peak_source": peak_src}
+    cand = ctx.candidate_stats() if info["sorted"] else None
+    fullscan = None
+    if info["sorted"] and not args.no_fullscan_roofline:
+        # the same shard through the full-scan kernel (caller's order, no pruning)
+        cf = km.Context(Xh, w.K, device=local, comm=comm, global_offset=a, global_N=global_N,
+                        sort=False)
+        cf.start(init_idx=init, tol=0.0, max_iter=1 << 30)
+        tf = time_assign(cf)
+        fullscan = roofline_of(tf, "k_assign_chunk" if w.K <= 16 else "k_assign_large", False)
+        cf.close()
 
     # ---- end to end through the public API with host buffers ------------------------
     e2e = None
@@ -344,8 +363,11 @@ def main():
         ctx.close()
         barrier()
         t0 = time.perf_counter()
-        c2 = km.Context(Xh, w.K, device=local, comm=comm, global_offset=a, global_N=global_N)
+        c2 = km.Context(Xh, w.K, device=local, comm=comm, global_offset=a, global_N=global_N,
+                        sort=not args.no_sort)
+        t1 = time.perf_counter()
         r = c2.fit(init, 0.0, args.e2e_iters, out_labels=labels_h, traces=False)
+        t2 = time.perf_counter()
         c2.close()
         dt = time.perf_counter() - t0
         barrier()
@@ -356,7 +378,8 @@ def main():
                "d2h_bytes_per_step": int(n_local * 4 + 8 * w.K * w.d + 16),
                "step": f"one kmeans_create + kmeans_fit_ctx ({args.e2e_iters} iterations, "
                        "labels out) + kmeans_destroy call from pinned host memory",
-               "seconds_per_step": dt}
+               "seconds_per_step": dt,
+               "breakdown_s": {"create": t1 - t0, "fit": t2 - t1, "destroy": dt - (t2 - t0)}}
     else:
         ctx.close()
 
@@ -378,11 +401,13 @@ def main():
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(w, P, args.scaling),
             "roofline": roofline, "roofline_hbm": roofline_hbm,
+            "roofline_fullscan": fullscan, "candidates": cand,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "kernels_per_step": info["kernels_per_iter"],
             "clocks": clk,
             "launch": {"grid": info["grid"], "block": info["block"],
-                       "smem_bytes": info["smem_bytes"], "path": info["path"]},
+                       "smem_bytes": info["smem_bytes"], "path": info["path"],
+                       "sorted": info["sorted"]},
         }
         print(json.dumps(line), flush=True)
     if distributed:

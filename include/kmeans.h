@@ -73,7 +73,15 @@ typedef struct kmeans_opts {
                                and every compute call is collective over the group. */
     int64_t global_offset;  /* first global index of this rank's shard */
     int64_t global_N;       /* total points over all ranks; 0 = N */
+    int flags;              /* KMEANS_FLAG_* bits */
 } kmeans_opts;
+
+/* kmeans_opts.flags */
+#define KMEANS_FLAG_NO_SORT 1  /* keep the caller's point order (full-scan assign kernel).
+                                  Default (K <= 16): the shard is put in Morton order once
+                                  at create and each 2048-point chunk prunes centroids that
+                                  provably cannot be its points' argmin (exact; labels are
+                                  returned in the caller's order). */
 
 /* Fills *opts with the defaults above. */
 void kmeans_opts_init(kmeans_opts* opts);
@@ -150,6 +158,12 @@ kmeans_status kmeans_final_labels(kmeans_ctx* ctx, int32_t* labels);
  * iteration state is unchanged).  Returns without synchronising. */
 kmeans_status kmeans_profile_assign(kmeans_ctx* ctx, int n);
 
+/* Sorted path: centroid candidates per 2048-point chunk in the last assign
+ * pass -- mean, maximum, number of single-candidate chunks, number of chunks
+ * (any may be NULL).  KMEANS_ESTATE on an unsorted context.  Synchronous. */
+kmeans_status kmeans_candidate_stats(kmeans_ctx* ctx, double* mean, int* max, int64_t* single,
+                                     int64_t* chunks);
+
 /* The cudaStream_t the context runs on. */
 kmeans_status kmeans_get_stream(kmeans_ctx* ctx, void** stream);
 
@@ -164,6 +178,7 @@ typedef struct kmeans_info {
     int kernels_per_iter;   /* kernels of this library launched per iteration */
     int64_t kernel_launches;/* kernels of this library launched so far by this context */
     int nranks, rank;
+    int sorted;             /* 1 = Morton-sorted shard with per-chunk pruning */
 } kmeans_info;
 
 kmeans_status kmeans_get_info(kmeans_ctx* ctx, kmeans_info* info);

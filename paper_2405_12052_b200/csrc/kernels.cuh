@@ -82,11 +82,12 @@ __global__ void k_prep(const float* __restrict__ in, int64_t N, int d, int64_t s
 // allreduce over ranks then assembles mu^0 exactly: one x plus zeros).
 __global__ void k_init_gather(const float* __restrict__ X, int d, int K,
                               const int64_t* __restrict__ idx, int64_t offset, int64_t n_local,
-                              double* __restrict__ mu0) {
+                              const int32_t* __restrict__ invperm, double* __restrict__ mu0) {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= K * d) return;
     int k = q / d, j = q % d;
     int64_t i = idx[k] - offset;
+    if (invperm && i >= 0 && i < n_local) i = invperm[i];   // sorted layout
     mu0[q] = (i >= 0 && i < n_local)
                  ? (double)X[(i >> 6) * (d * kWarpTile) + j * kWarpTile + (i & 63)]
                  : 0.0;
@@ -421,6 +422,417 @@ k_assign_chunk(const float* __restrict__ X, int64_t n, int K,
     const double2 out = (lane & 1) ? make_double2(v0, (double)cnt) : make_double2(v0, v1);
     reinterpret_cast<double2*>(row)[lane] = (k < KP) ? out : make_double2(0.0, 0.0);
     if (lane == 0) row[64] = jj;
+}
+
+// ---------------------------------------------------------------------------
+// Spatially sorted path (default for K <= 16): preprocessing kernels.
+//
+// At kmeans_create the shard's points are put in Morton (Z-curve) order once
+// (CUB radix sort of 30/32-bit keys; stable, so deterministic), and each
+// 2048-point chunk gets its bounding box.  The order is an internal layout:
+// labels are scattered back to the caller's order, and every result of the
+// iteration is unchanged (sums are accumulated in a different fixed order).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned ord_f32(float f) {   // order-preserving float -> uint
+    unsigned u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float unord_f32(unsigned u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+// Global bounding box of the input (ordered-int min/max atomics: order-free)
+// plus the non-finite check.  box[0..d) = min, box[d..2d) = max (ordered ints).
+__global__ void k_input_bbox(const float* __restrict__ in, int64_t N, int d, int64_t si, int64_t sj,
+                             unsigned* __restrict__ box, int* __restrict__ flag) {
+    unsigned mn[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, mx[3] = {0u, 0u, 0u};
+    int bad = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) {
+        for (int j = 0; j < d; ++j) {
+            const float v = in[i * si + (int64_t)j * sj];
+            bad |= !isfinite(v);
+            const unsigned o = ord_f32(v);
+            mn[j] = min(mn[j], o);
+            mx[j] = max(mx[j], o);
+        }
+    }
+    for (int j = 0; j < d; ++j) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[j] = min(mn[j], __shfl_xor_sync(0xffffffffu, mn[j], o));
+            mx[j] = max(mx[j], __shfl_xor_sync(0xffffffffu, mx[j], o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(&box[j], mn[j]);
+            atomicMax(&box[d + j], mx[j]);
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+__device__ __forceinline__ unsigned part1by1(unsigned x) {   // 16 bits -> even bits
+    x &= 0x0000ffffu;
+    x = (x | (x << 8)) & 0x00ff00ffu;
+    x = (x | (x << 4)) & 0x0f0f0f0fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    x = (x | (x << 1)) & 0x55555555u;
+    return x;
+}
+__device__ __forceinline__ unsigned part1by2(unsigned x) {   // 10 bits -> every 3rd bit
+    x &= 0x000003ffu;
+    x = (x | (x << 16)) & 0xff0000ffu;
+    x = (x | (x << 8)) & 0x0300f00fu;
+    x = (x | (x << 4)) & 0x030c30c3u;
+    x = (x | (x << 2)) & 0x09249249u;
+    return x;
+}
+
+// Morton key of every point (quantised to the global box) and the identity
+// permutation as the sort's values.
+__global__ void k_morton(const float* __restrict__ in, int64_t N, int d, int64_t si, int64_t sj,
+                         const unsigned* __restrict__ box, unsigned* __restrict__ keys,
+                         int32_t* __restrict__ iota) {
+    const int bits = (d == 2) ? 16 : 10;
+    const float qmax = (float)((1 << bits) - 1);
+    float lo[3], sc[3];
+    for (int j = 0; j < d; ++j) {
+        lo[j] = unord_f32(box[j]);
+        const float hi = unord_f32(box[d + j]);
+        sc[j] = (hi > lo[j]) ? qmax / (hi - lo[j]) : 0.0f;
+    }
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) {
+        unsigned q[3] = {0u, 0u, 0u};
+        for (int j = 0; j < d; ++j) {
+            float t = (in[i * si + (int64_t)j * sj] - lo[j]) * sc[j];
+            t = fminf(fmaxf(t, 0.0f), qmax);
+            q[j] = (unsigned)t;
+        }
+        keys[i] = (d == 2) ? (part1by1(q[0]) | (part1by1(q[1]) << 1))
+                           : (part1by2(q[0]) | (part1by2(q[1]) << 1) | (part1by2(q[2]) << 2));
+        iota[i] = (int32_t)i;
+    }
+}
+
+// Sorted AoSoA layout: point p (sorted position) = input point perm[p];
+// invperm[perm[p]] = p.  Padding points (p >= N) are zeros.
+__global__ void k_gather_sorted(const float* __restrict__ in, int64_t N, int d, int64_t si,
+                                int64_t sj, const int32_t* __restrict__ perm,
+                                int32_t* __restrict__ invperm, float* __restrict__ out,
+                                int64_t ldx) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < ldx; p += stride) {
+        const int64_t i = (p < N) ? perm[p] : -1;
+        for (int j = 0; j < d; ++j)
+            out[(p >> 6) * (d * kWarpTile) + j * kWarpTile + (p & 63)] =
+                (i >= 0) ? in[i * si + (int64_t)j * sj] : 0.0f;
+        if (i >= 0) invperm[i] = (int32_t)p;
+    }
+}
+
+// Per-chunk bounding box of the (sorted) points: cbox[c] = {lo[D], hi[D]}.
+// One warp per chunk; only valid points (p < n) count.
+__global__ void k_chunk_bbox(const float* __restrict__ X, int64_t n, int d, int chunk_points,
+                             int n_chunks, float* __restrict__ cbox) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= n_chunks) return;
+    const int64_t p0 = (int64_t)warp * chunk_points;
+    const int64_t p1 = (n < p0 + chunk_points) ? n : p0 + chunk_points;
+    for (int j = 0; j < d; ++j) {
+        float lo = pos_inf(), hi = -pos_inf();
+        for (int64_t p = p0 + lane; p < p1; p += 32) {
+            const float v = X[(p >> 6) * (d * kWarpTile) + j * kWarpTile + (p & 63)];
+            lo = fminf(lo, v);
+            hi = fmaxf(hi, v);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane == 0) {
+            cbox[(size_t)warp * 2 * d + j] = lo;
+            cbox[(size_t)warp * 2 * d + d + j] = hi;
+        }
+    }
+}
+
+// labels_out[perm[p]] = labels_sorted[p] for p < n (back to the caller's order).
+__global__ void k_scatter_labels(const int32_t* __restrict__ lab_sorted,
+                                 const int32_t* __restrict__ perm, int64_t n,
+                                 int32_t* __restrict__ lab_out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride)
+        lab_out[perm[p]] = lab_sorted[p];
+}
+
+// ---------------------------------------------------------------------------
+// k_assign_sorted (K <= 16, sorted points): exact per-chunk pruning.
+//
+// For the chunk's box B and the staged fp32 centroids c_k, lane k computes in
+// fp64  dmin2_k = min_{x in B} ||x - c_k||^2  and  dmax2_k = max_{x in B} ||x - c_k||^2.
+// With M = min_k dmax2_k, centroid b is excluded when
+//     dmin2_b > M (1 + 1e-5) + 2^-100.
+// Then for every x in B the exact squared distances satisfy
+// E_b > E_a (1 + 1e-5) + 2^-100 for the a attaining M, and since form D is
+// within (d+2) 2^-24 relative (+ a few subnormal ulps absolute) of the exact
+// value (pinned in tests/test_oracle_pins.py), D(x, c_b) > D(x, c_a) strictly
+// in fp32: b can neither win nor tie.  So the exact argmin over the remaining
+// candidates, scanned in ascending k with strict <, equals the full scan's
+// (value, lowest index).  If M could overflow fp32 (> 1e37) nothing is pruned.
+//
+// c == 1 (one candidate): every label is known; the distances are still
+// computed (form D) for the inertia, and the sums accumulate in registers.
+// c >= 2: candidate loop with a running strict-< argmin, per-lane private fp64
+// columns indexed by candidate slot (as in k_assign_chunk).
+// ---------------------------------------------------------------------------
+template <int D>
+struct SortedSmem {
+    double2 A[16][32];
+    double2 B[16][32];
+    float ring[kStages][D * kLaneTile];
+    uint64_t bar[kStages];
+    float4 cand[16];   // negated fp32 centroid of each candidate slot
+    int candk[16];     // centroid index of each slot (ascending)
+};
+
+template <int D, int MODE>
+__global__ void __launch_bounds__(32, 10)
+k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
+                const double* __restrict__ mu_buf, const DevState* __restrict__ st,
+                int mu_sel, int ignore_done, const float* __restrict__ cbox,
+                double* __restrict__ cpart, int32_t* __restrict__ labels,
+                int* __restrict__ cand_count) {
+    if (!ignore_done && st->done) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SortedSmem<D>& S = *reinterpret_cast<SortedSmem<D>*>(smem_raw);
+    constexpr int kTileFloats = D * kLaneTile;
+    constexpr unsigned kTileBytes = kTileFloats * 4;
+    const int lane = threadIdx.x;
+    const int chunk = blockIdx.x;
+    const int64_t base = (int64_t)chunk * kChunkPoints;
+    const int64_t rem = n - base;
+    const int64_t ntile64 = (rem + kLaneTile - 1) / kLaneTile;
+    const int ntile = ntile64 < kChunkTiles ? (int)ntile64 : kChunkTiles;
+    const float* src = X + (base >> 6) * (D * kWarpTile);
+
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < kStages; ++s) mbar_init(&S.bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+        for (int s = 0; s < kStages; ++s) {
+            if (s < ntile) {
+                mbar_expect_tx(&S.bar[s], kTileBytes);
+                bulk_g2s(S.ring[s], src + s * kTileFloats, kTileBytes, &S.bar[s]);
+            }
+        }
+    }
+
+    // ---- candidates of this chunk ----
+    const double* mu = mu_buf + (size_t)((st->t - mu_sel) & 1) * K * D;
+    const bool is_k = lane < K;
+    float c32[3] = {0.f, 0.f, 0.f};
+    double dmin2 = 0.0, dmax2 = 0.0;
+    if (is_k) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            c32[j] = __double2float_rn(__ldg(&mu[lane * D + j]));
+            const double c = (double)c32[j];
+            const double lo = (double)__ldg(&cbox[(size_t)chunk * 2 * D + j]);
+            const double hi = (double)__ldg(&cbox[(size_t)chunk * 2 * D + D + j]);
+            const double dm = fmax(fmax(lo - c, c - hi), 0.0);
+            dmin2 += dm * dm;
+            const double dx = fmax(fabs(c - lo), fabs(hi - c));
+            dmax2 += dx * dx;
+        }
+    }
+    double M = is_k ? dmax2 : (double)pos_inf();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
+    const double thr = (M > 1e37) ? (double)pos_inf() : M * (1.0 + 1e-5) + 0x1p-100;
+    const bool cand = is_k && dmin2 <= thr;
+    const unsigned mask = __ballot_sync(0xffffffffu, cand);
+    const int nc = __popc(mask);
+    if (cand) {
+        const int slot = __popc(mask & ((1u << lane) - 1u));
+        S.cand[slot] = make_float4(-c32[0], -c32[1], D == 3 ? -c32[2] : 0.0f, 0.0f);
+        S.candk[slot] = lane;
+    }
+    if (lane == 0 && cand_count) cand_count[chunk] = nc;
+    __syncwarp();
+
+    struct Pts {
+        float2 xa, ya, za, xb, yb, zb;
+    };
+    auto fetch = [&](int i) {
+        const int s = i % kStages;
+        mbar_wait(&S.bar[s], (unsigned)(i / kStages) & 1u);
+        const float* rg = S.ring[s];
+        const float* rb = rg + D * kWarpTile;
+        Pts P;
+        P.xa = reinterpret_cast<const float2*>(rg)[lane];
+        P.ya = reinterpret_cast<const float2*>(rg + kWarpTile)[lane];
+        P.za = (D == 3) ? reinterpret_cast<const float2*>(rg + 2 * kWarpTile)[lane]
+                        : make_float2(0.f, 0.f);
+        P.xb = reinterpret_cast<const float2*>(rb)[lane];
+        P.yb = reinterpret_cast<const float2*>(rb + kWarpTile)[lane];
+        P.zb = (D == 3) ? reinterpret_cast<const float2*>(rb + 2 * kWarpTile)[lane]
+                        : make_float2(0.f, 0.f);
+        __syncwarp();
+        const int r = i - 1 + kStages;
+        if (lane == 0 && i >= 1 && r < ntile) {
+            const int sr = (i - 1) % kStages;
+            mbar_expect_tx(&S.bar[sr], kTileBytes);
+            bulk_g2s(S.ring[sr], src + (int64_t)r * kTileFloats, kTileBytes, &S.bar[sr]);
+        }
+        return P;
+    };
+    // form D of 2 packed points against candidate cc (negated centroid)
+    auto dist2 = [&](float2 x, float2 y, float2 z, const float4& cc) {
+        float2 e0 = __fadd2_rn(x, make_float2(cc.x, cc.x));
+        float2 e1 = __fadd2_rn(y, make_float2(cc.y, cc.y));
+        float2 sq = __fmul2_rn(e0, e0);
+        sq = __ffma2_rn(e1, e1, sq);
+        if (D == 3) {
+            float2 e2 = __fadd2_rn(z, make_float2(cc.z, cc.z));
+            sq = __ffma2_rn(e2, e2, sq);
+        }
+        return sq;
+    };
+
+    double* row = cpart + (size_t)chunk * kRowDoubles;
+    if (nc == 1) {
+        // ---- one candidate: labels known, sums in registers ----
+        const float4 cc = S.cand[0];
+        const int k0 = S.candk[0];
+        double sx = 0.0, sy = 0.0, sz = 0.0, J = 0.0;
+#pragma unroll 1
+        for (int i = 0; i < ntile; ++i) {
+            const Pts P = fetch(i);
+            const float2 da = dist2(P.xa, P.ya, P.za, cc);
+            const float2 db = dist2(P.xb, P.yb, P.zb, cc);
+            const int64_t pa = base + (int64_t)i * kLaneTile + 2 * lane, pb = pa + kWarpTile;
+            if (MODE & kModeLabels) {
+                *reinterpret_cast<int2*>(labels + pa) = make_int2(k0, k0);
+                *reinterpret_cast<int2*>(labels + pb) = make_int2(k0, k0);
+            }
+            if (MODE & kModeReduce) {
+                if (i * kLaneTile + kLaneTile <= rem) {
+                    sx += (double)P.xa.x; sy += (double)P.ya.x; sz += (double)P.za.x; J += (double)da.x;
+                    sx += (double)P.xa.y; sy += (double)P.ya.y; sz += (double)P.za.y; J += (double)da.y;
+                    sx += (double)P.xb.x; sy += (double)P.yb.x; sz += (double)P.zb.x; J += (double)db.x;
+                    sx += (double)P.xb.y; sy += (double)P.yb.y; sz += (double)P.zb.y; J += (double)db.y;
+                } else {
+                    if (pa < n) { sx += (double)P.xa.x; sy += (double)P.ya.x; sz += (double)P.za.x; J += (double)da.x; }
+                    if (pa + 1 < n) { sx += (double)P.xa.y; sy += (double)P.ya.y; sz += (double)P.za.y; J += (double)da.y; }
+                    if (pb < n) { sx += (double)P.xb.x; sy += (double)P.yb.x; sz += (double)P.zb.x; J += (double)db.x; }
+                    if (pb + 1 < n) { sx += (double)P.xb.y; sy += (double)P.yb.y; sz += (double)P.zb.y; J += (double)db.y; }
+                }
+            }
+        }
+        if (!(MODE & kModeReduce)) return;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sx += __shfl_xor_sync(0xffffffffu, sx, o);
+            sy += __shfl_xor_sync(0xffffffffu, sy, o);
+            sz += __shfl_xor_sync(0xffffffffu, sz, o);
+            J += __shfl_xor_sync(0xffffffffu, J, o);
+        }
+        // row layout [k][Sx, Sy, Sz, n]; zero for the other clusters
+        const int kk = lane >> 1;
+        double2 out = make_double2(0.0, 0.0);
+        if (kk == k0) {
+            const double cnt = (double)(rem < kChunkPoints ? rem : kChunkPoints);
+            out = (lane & 1) ? make_double2(sz, cnt) : make_double2(sx, sy);
+        }
+        reinterpret_cast<double2*>(row)[lane] = out;
+        if (lane == 0) row[64] = J;
+        return;
+    }
+
+    // ---- several candidates: running exact argmin, slot-indexed columns ----
+    if (MODE & kModeReduce) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            S.A[k][lane] = make_double2(0.0, 0.0);
+            S.B[k][lane] = make_double2(0.0, 0.0);
+        }
+    }
+    __syncwarp();
+    double J = 0.0;
+    auto accumulate = [&](int l, float px, float py, float pz) {
+        double2 a = S.A[l][lane], b = S.B[l][lane];
+        a.x += (double)px;
+        a.y += (double)py;
+        if (D == 3) b.x += (double)pz;
+        int2 c = *reinterpret_cast<int2*>(&b.y);
+        c.x += 1;
+        b.y = *reinterpret_cast<double*>(&c);
+        S.A[l][lane] = a;
+        S.B[l][lane] = b;
+    };
+#pragma unroll 1
+    for (int i = 0; i < ntile; ++i) {
+        const Pts P = fetch(i);
+        float2 ba = dist2(P.xa, P.ya, P.za, S.cand[0]);
+        float2 bb = dist2(P.xb, P.yb, P.zb, S.cand[0]);
+        int s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+#pragma unroll 1
+        for (int j = 1; j < nc; ++j) {
+            const float4 cc = S.cand[j];
+            const float2 da = dist2(P.xa, P.ya, P.za, cc);
+            const float2 db = dist2(P.xb, P.yb, P.zb, cc);
+            if (da.x < ba.x) { ba.x = da.x; s0 = j; }
+            if (da.y < ba.y) { ba.y = da.y; s1 = j; }
+            if (db.x < bb.x) { bb.x = db.x; s2 = j; }
+            if (db.y < bb.y) { bb.y = db.y; s3 = j; }
+        }
+        const int64_t pa = base + (int64_t)i * kLaneTile + 2 * lane, pb = pa + kWarpTile;
+        if (MODE & kModeLabels) {
+            *reinterpret_cast<int2*>(labels + pa) = make_int2(S.candk[s0], S.candk[s1]);
+            *reinterpret_cast<int2*>(labels + pb) = make_int2(S.candk[s2], S.candk[s3]);
+        }
+        if (MODE & kModeReduce) {
+            if (pa < n) { accumulate(s0, P.xa.x, P.ya.x, P.za.x); J += (double)ba.x; }
+            if (pa + 1 < n) { accumulate(s1, P.xa.y, P.ya.y, P.za.y); J += (double)ba.y; }
+            if (pb < n) { accumulate(s2, P.xb.x, P.yb.x, P.zb.x); J += (double)bb.x; }
+            if (pb + 1 < n) { accumulate(s3, P.xb.y, P.yb.y, P.zb.y); J += (double)bb.y; }
+        }
+    }
+    if (!(MODE & kModeReduce)) return;
+    __syncwarp();
+    // lane L sums slot (L >> 1), half (L & 1) over the 32 lanes (rotated order)
+    const int slot = lane >> 1;
+    const double2* col = (lane & 1) ? &S.B[0][0] : &S.A[0][0];
+    double v0 = 0.0, v1 = 0.0;
+    long long cnt = 0;
+    if (slot < nc) {
+#pragma unroll 8
+        for (int r = 0; r < 32; ++r) {
+            const int t = (r + lane) & 31;
+            const double2 w = col[slot * 32 + t];
+            v0 += w.x;
+            if (lane & 1) cnt += reinterpret_cast<const int2*>(&w.y)->x;
+            else v1 += w.y;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
+    // dense row: entry of cluster k comes from the lane pair owning its slot
+    const int kk = lane >> 1;                       // cluster this lane writes
+    const bool kin = (mask >> kk) & 1u;             // is cluster kk a candidate?
+    const int ks = __popc(mask & ((1u << kk) - 1u)); // its slot
+    const int srcl = 2 * ks + (lane & 1);
+    const double g0 = __shfl_sync(0xffffffffu, v0, srcl);
+    const double g1 = __shfl_sync(0xffffffffu, v1, srcl);
+    const long long gc = __shfl_sync(0xffffffffu, cnt, srcl);
+    double2 out = make_double2(0.0, 0.0);
+    if (kk < 16 && kin) out = (lane & 1) ? make_double2(g0, (double)gc) : make_double2(g0, g1);
+    reinterpret_cast<double2*>(row)[lane] = out;
+    if (lane == 0) row[64] = J;
 }
 
 // ---------------------------------------------------------------------------

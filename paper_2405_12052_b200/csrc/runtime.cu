@@ -8,6 +8,8 @@
 // polls between graph replays.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
@@ -67,6 +69,12 @@ struct kmeans_ctx {
     int G = 0, tpb = 0, smem = 0, path = 0;   // G = columns of part (blocks or groups)
     int n_chunks = 0;
     double* cpart = nullptr;      // n_chunks x kRowDoubles chunk partials (path 0)
+    bool sorted = false;          // points held in Morton order (path 0 default)
+    int32_t* perm = nullptr;      // sorted position -> caller's index (sorted only)
+    int32_t* invperm = nullptr;   // caller's index -> sorted position (sorted only)
+    float* cbox = nullptr;        // per-chunk bounding boxes (sorted only)
+    int* cand_count = nullptr;    // candidates per chunk, last assign (sorted only)
+    int32_t* labels_sorted = nullptr;  // labels in sorted order (sorted only)
     int nE = 0;
     cudaGraphExec_t graph = nullptr;
     int64_t launches = 0;
@@ -142,6 +150,20 @@ ChunkFn pick_chunk(int d, int K, int mode) {
     return pick_chunk_kp<3, 3>(K);
 }
 
+using SortedFn = void (*)(const float*, int64_t, int, const double*, const DevState*, int, int,
+                          const float*, double*, int32_t*, int*);
+
+SortedFn pick_sorted(int d, int mode) {
+    if (d == 2) {
+        if (mode == 1) return km::k_assign_sorted<2, 1>;
+        if (mode == 2) return km::k_assign_sorted<2, 2>;
+        return km::k_assign_sorted<2, 3>;
+    }
+    if (mode == 1) return km::k_assign_sorted<3, 1>;
+    if (mode == 2) return km::k_assign_sorted<3, 2>;
+    return km::k_assign_sorted<3, 3>;
+}
+
 int chunk_smem(int d, int K) {
     const int kp = small_kp(K);
     if (d == 2)
@@ -176,14 +198,22 @@ kmeans_status configure(kmeans_ctx* ctx) {
     if (ctx->K <= 16) {
         ctx->path = 0;
         ctx->tpb = 32;
-        ctx->smem = chunk_smem(ctx->d, ctx->K);
-        for (int mode = 1; mode <= 3; ++mode)
-            CK(cudaFuncSetAttribute((const void*)pick_chunk(ctx->d, ctx->K, mode),
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
+        if (ctx->sorted) {
+            ctx->smem = ctx->d == 2 ? sizeof(km::SortedSmem<2>) : sizeof(km::SortedSmem<3>);
+            for (int mode = 1; mode <= 3; ++mode)
+                CK(cudaFuncSetAttribute((const void*)pick_sorted(ctx->d, mode),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
+        } else {
+            ctx->smem = chunk_smem(ctx->d, ctx->K);
+            for (int mode = 1; mode <= 3; ++mode)
+                CK(cudaFuncSetAttribute((const void*)pick_chunk(ctx->d, ctx->K, mode),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
+        }
         ctx->n_chunks = (int)((ctx->N + km::kChunkPoints - 1) / km::kChunkPoints);
         ctx->G = (ctx->n_chunks + km::kGroupChunks - 1) / km::kGroupChunks;  // groups
     } else {
         ctx->path = 1;
+        ctx->sorted = false;   // the large-K kernel streams points in the caller's order
         int tpb = km::kLargeTPBMax;
         while (tpb > 64 && large_smem(ctx->d, ctx->K, tpb) > maxSmem - 4096) tpb -= 32;
         ctx->tpb = tpb;
@@ -209,10 +239,19 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
         CK(cudaMalloc(&ctx->labels, sizeof(int32_t) * ctx->ldx));
     }
     if (ctx->path == 0) {
-        ChunkFn f = pick_chunk(ctx->d, ctx->K, mode);
-        f<<<ctx->n_chunks, 32, ctx->smem, ctx->stream>>>(ctx->X, ctx->N, ctx->K, ctx->mu, ctx->st,
-                                                         mu_sel, ignore_done, ctx->cpart,
-                                                         ctx->labels);
+        if (ctx->sorted) {
+            if ((mode & km::kModeLabels) && !ctx->labels_sorted)
+                CK(cudaMalloc(&ctx->labels_sorted, sizeof(int32_t) * ctx->ldx));
+            SortedFn f = pick_sorted(ctx->d, mode);
+            f<<<ctx->n_chunks, 32, ctx->smem, ctx->stream>>>(
+                ctx->X, ctx->N, ctx->K, ctx->mu, ctx->st, mu_sel, ignore_done, ctx->cbox,
+                ctx->cpart, ctx->labels_sorted, ctx->cand_count);
+        } else {
+            ChunkFn f = pick_chunk(ctx->d, ctx->K, mode);
+            f<<<ctx->n_chunks, 32, ctx->smem, ctx->stream>>>(ctx->X, ctx->N, ctx->K, ctx->mu,
+                                                             ctx->st, mu_sel, ignore_done,
+                                                             ctx->cpart, ctx->labels);
+        }
         if (mode & km::kModeReduce) {
             // chunk rows -> group columns of part (fixed ascending order)
             if (ctx->d == 2)
@@ -231,6 +270,14 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
     }
     ctx->launches += 1;
     CK(cudaGetLastError());
+    if ((mode & km::kModeLabels) && ctx->sorted) {
+        // back to the caller's order
+        const int blocks = (int)std::min<int64_t>((ctx->N + 255) / 256, 148 * 8);
+        km::k_scatter_labels<<<blocks, 256, 0, ctx->stream>>>(ctx->labels_sorted, ctx->perm,
+                                                              ctx->N, ctx->labels);
+        ctx->launches += 1;
+        CK(cudaGetLastError());
+    }
     return KMEANS_OK;
 }
 
@@ -380,6 +427,72 @@ kmeans_status fetch_centroids(kmeans_ctx* ctx, const double* cent, std::vector<d
     return KMEANS_OK;
 }
 
+// Morton-order the shard once (sorted path): global box + finiteness, keys,
+// stable CUB radix sort, gather into the AoSoA layout, per-chunk boxes.
+kmeans_status sort_points(kmeans_ctx* ctx, const float* src, int64_t si, int64_t sj) {
+    const int64_t N = ctx->N;
+    const int d = ctx->d;
+    unsigned* box = nullptr;
+    unsigned *keys = nullptr, *keys2 = nullptr;
+    int32_t* iota = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    kmeans_status st = KMEANS_OK;
+    auto cleanup = [&]() {
+        cudaFree(box);
+        cudaFree(keys);
+        cudaFree(keys2);
+        cudaFree(iota);
+        cudaFree(tmp);
+    };
+    if (cudaMalloc(&ctx->perm, sizeof(int32_t) * N) != cudaSuccess ||
+        cudaMalloc(&ctx->invperm, sizeof(int32_t) * N) != cudaSuccess ||
+        cudaMalloc(&ctx->cbox, sizeof(float) * 2 * d * (size_t)ctx->n_chunks) != cudaSuccess ||
+        cudaMalloc(&ctx->cand_count, sizeof(int) * (size_t)ctx->n_chunks) != cudaSuccess ||
+        cudaMalloc(&box, sizeof(unsigned) * 6) != cudaSuccess ||
+        cudaMalloc(&keys, sizeof(unsigned) * N) != cudaSuccess ||
+        cudaMalloc(&keys2, sizeof(unsigned) * N) != cudaSuccess ||
+        cudaMalloc(&iota, sizeof(int32_t) * N) != cudaSuccess) {
+        cudaGetLastError();
+        cleanup();
+        set_error("sort buffers: allocation failed");
+        return KMEANS_ENOMEM;
+    }
+    unsigned hb2[6];
+    for (int j = 0; j < d; ++j) {
+        hb2[j] = 0xffffffffu;
+        hb2[d + j] = 0u;
+    }
+    const int blocks = (int)std::min<int64_t>((N + 255) / 256, 148 * 8);
+    cudaError_t e = cudaMemcpyAsync(box, hb2, sizeof(unsigned) * 2 * d, cudaMemcpyHostToDevice,
+                                    ctx->stream);
+    if (e == cudaSuccess) {
+        km::k_input_bbox<<<blocks, 256, 0, ctx->stream>>>(src, N, d, si, sj, box, ctx->flag);
+        km::k_morton<<<blocks, 256, 0, ctx->stream>>>(src, N, d, si, sj, box, keys, iota);
+        ctx->launches += 2;
+        e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, iota, ctx->perm, N, 0,
+                                            32, ctx->stream);
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&tmp, tmp_bytes);
+    if (e == cudaSuccess)
+        e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, iota, ctx->perm, N, 0, 32,
+                                            ctx->stream);
+    if (e == cudaSuccess) {
+        const int gb = (int)std::min<int64_t>((ctx->ldx + 255) / 256, 148 * 8);
+        km::k_gather_sorted<<<gb, 256, 0, ctx->stream>>>(src, N, d, si, sj, ctx->perm,
+                                                         ctx->invperm, ctx->X, ctx->ldx);
+        const int cb = (ctx->n_chunks * 32 + 255) / 256;
+        km::k_chunk_bbox<<<cb, 256, 0, ctx->stream>>>(ctx->X, N, d, km::kChunkPoints,
+                                                      ctx->n_chunks, ctx->cbox);
+        ctx->launches += 2;
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);  // before freeing temporaries
+    if (e != cudaSuccess) st = cuda_fail(ctx, e, "sort_points");
+    cleanup();
+    return st;
+}
+
 }  // namespace
 
 // ============================================================================
@@ -412,6 +525,7 @@ void kmeans_opts_init(kmeans_opts* o) {
     o->nccl_comm = nullptr;
     o->global_offset = 0;
     o->global_N = 0;
+    o->flags = 0;
 }
 
 void kmeans_destroy(kmeans_ctx* ctx) {
@@ -431,6 +545,11 @@ void kmeans_destroy(kmeans_ctx* ctx) {
         cudaFree(ctx->idx_dev);
         cudaFree(ctx->flag);
         cudaFree(ctx->cpart);
+        cudaFree(ctx->perm);
+        cudaFree(ctx->invperm);
+        cudaFree(ctx->cbox);
+        cudaFree(ctx->cand_count);
+        cudaFree(ctx->labels_sorted);
         if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
         cudaGetLastError();
     }
@@ -502,6 +621,7 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
         }
         ctx->own_stream = true;
     }
+    ctx->sorted = !(opts.flags & KMEANS_FLAG_NO_SORT);
     kmeans_status s = configure(ctx);
     if (s != KMEANS_OK) return fail(s);
 
@@ -557,11 +677,17 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
     }
     const int64_t si = opts.layout == KMEANS_LAYOUT_AOS ? d : 1;
     const int64_t sj = opts.layout == KMEANS_LAYOUT_AOS ? 1 : N;
-    {
+    if (!ctx->sorted) {
         int blocks = (int)std::min<int64_t>((ctx->ldx + 255) / 256, 148 * 16);
         km::k_prep<<<blocks, 256, 0, ctx->stream>>>(src, N, d, si, sj, ctx->X, ctx->ldx,
                                                     ctx->flag);
         ctx->launches += 1;
+    } else {
+        s = sort_points(ctx, src, si, sj);
+        if (s != KMEANS_OK) {
+            if (staging) cudaFree(staging);
+            return fail(s);
+        }
     }
     int hflag = 0;
     e = cudaMemcpyAsync(&hflag, ctx->flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
@@ -595,7 +721,8 @@ kmeans_status kmeans_start(kmeans_ctx* ctx, const int64_t* init_idx, const doubl
                            cudaMemcpyHostToDevice, ctx->stream));
         const int n = ctx->K * ctx->d;
         km::k_init_gather<<<(n + 255) / 256, 256, 0, ctx->stream>>>(
-            ctx->X, ctx->d, ctx->K, ctx->idx_dev, ctx->global_offset, ctx->N, ctx->mu);
+            ctx->X, ctx->d, ctx->K, ctx->idx_dev, ctx->global_offset, ctx->N, ctx->invperm,
+            ctx->mu);
         ctx->launches += 1;
         CK(cudaGetLastError());
         // CC1: assemble mu^0 from the owners (exact: one x plus zeros)
@@ -809,6 +936,33 @@ kmeans_status kmeans_profile_assign(kmeans_ctx* ctx, int n) {
     return KMEANS_OK;
 }
 
+kmeans_status kmeans_candidate_stats(kmeans_ctx* ctx, double* mean, int* max, int64_t* single,
+                                     int64_t* chunks) {
+    CHECK_CTX(ctx);
+    if (!ctx->sorted) {
+        set_error("candidate statistics exist only on the sorted path");
+        return KMEANS_ESTATE;
+    }
+    DeviceGuard g(ctx->device);
+    std::vector<int> c(ctx->n_chunks);
+    CK(cudaMemcpyAsync(c.data(), ctx->cand_count, sizeof(int) * c.size(), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    double sum = 0.0;
+    int mx = 0;
+    int64_t one = 0;
+    for (int v : c) {
+        sum += v;
+        mx = std::max(mx, v);
+        one += (v == 1);
+    }
+    if (mean) *mean = c.empty() ? 0.0 : sum / c.size();
+    if (max) *max = mx;
+    if (single) *single = one;
+    if (chunks) *chunks = (int64_t)c.size();
+    return KMEANS_OK;
+}
+
 kmeans_status kmeans_get_stream(kmeans_ctx* ctx, void** stream) {
     CHECK_CTX(ctx);
     if (!stream) return KMEANS_EINVAL;
@@ -834,6 +988,7 @@ kmeans_status kmeans_get_info(kmeans_ctx* ctx, kmeans_info* info) {
     info->kernels_per_iter = kernels_per_iter(ctx);
     info->kernel_launches = ctx->launches;
     info->nranks = ctx->nranks;
+    info->sorted = ctx->sorted ? 1 : 0;
     info->rank = ctx->rank;
     return KMEANS_OK;
 }

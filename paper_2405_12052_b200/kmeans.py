@@ -21,6 +21,7 @@ KMEANS_OK = 0
 STATUS = {0: "KMEANS_OK", -1: "KMEANS_EINVAL", -2: "KMEANS_ENONFINITE", -3: "KMEANS_ENOMEM",
           -4: "KMEANS_ECUDA", -5: "KMEANS_ENCCL", -6: "KMEANS_ESTATE"}
 LAYOUT_AOS, LAYOUT_SOA = 0, 1
+FLAG_NO_SORT = 1
 MAX_K = 1024
 
 
@@ -34,7 +35,7 @@ class KMeansError(RuntimeError):
 class Opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("layout", ctypes.c_int),
                 ("nccl_comm", ctypes.c_void_p), ("global_offset", ctypes.c_int64),
-                ("global_N", ctypes.c_int64)]
+                ("global_N", ctypes.c_int64), ("flags", ctypes.c_int)]
 
 
 class Info(ctypes.Structure):
@@ -43,7 +44,7 @@ class Info(ctypes.Structure):
                 ("d", ctypes.c_int), ("K", ctypes.c_int), ("grid", ctypes.c_int),
                 ("block", ctypes.c_int), ("smem_bytes", ctypes.c_int), ("path", ctypes.c_int),
                 ("kernels_per_iter", ctypes.c_int), ("kernel_launches", ctypes.c_int64),
-                ("nranks", ctypes.c_int), ("rank", ctypes.c_int)]
+                ("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("sorted", ctypes.c_int)]
 
 
 # Every exported symbol with (restype, argtypes); tests check the header matches.
@@ -61,6 +62,7 @@ SIGNATURES = {
     "kmeans_read_centroids": (I, [P, P]),
     "kmeans_final_labels": (I, [P, P]),
     "kmeans_profile_assign": (I, [P, I]),
+    "kmeans_candidate_stats": (I, [P, P, P, P, P]),
     "kmeans_get_stream": (I, [P, P]),
     "kmeans_get_info": (I, [P, P]),
     "kmeans_comm_unique_id": (I, [P]),
@@ -141,7 +143,7 @@ class Context:
 
     def __init__(self, points, K: int, *, d: int | None = None, layout: str = "aos",
                  device: int = -1, stream=None, comm=None, global_offset: int = 0,
-                 global_N: int = 0):
+                 global_N: int = 0, sort: bool = True):
         pts = _as_f32_points(points)
         shape = tuple(pts.shape)
         if layout == "aos":
@@ -157,6 +159,7 @@ class Context:
         o.nccl_comm = comm
         o.global_offset = global_offset
         o.global_N = global_N
+        o.flags = 0 if sort else FLAG_NO_SORT
         h = ctypes.c_void_p()
         _check(lib().kmeans_create(ctypes.byref(h), _ptr(pts), self.N, self.d, self.K,
                                    ctypes.byref(o)), "kmeans_create")
@@ -245,6 +248,15 @@ class Context:
     def profile_assign(self, n: int):
         """Enqueue n launches of the assign+reduce kernel alone (no state change)."""
         _check(lib().kmeans_profile_assign(self._h, int(n)), "kmeans_profile_assign")
+
+    def candidate_stats(self) -> dict:
+        """Sorted path: centroid candidates per chunk in the last assign pass."""
+        m, mx, one, nch = ctypes.c_double(), ctypes.c_int(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().kmeans_candidate_stats(self._h, ctypes.byref(m), ctypes.byref(mx),
+                                            ctypes.byref(one), ctypes.byref(nch)),
+               "kmeans_candidate_stats")
+        return dict(mean=m.value, max=mx.value, single_frac=one.value / max(nch.value, 1),
+                    chunks=nch.value)
 
     @property
     def stream(self) -> int:

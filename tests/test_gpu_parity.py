@@ -35,13 +35,13 @@ def cluster_abs_scale(X, labels, K):
     return s
 
 
-def check_step(X, mu, ctx=None, tag=""):
+def check_step(X, mu, ctx=None, tag="", sort=True):
     """One Lloyd step on the GPU vs the oracle at identical mu^t."""
     N, d = X.shape
     K = mu.shape[0]
     own = ctx is None
     if own:
-        ctx = km.Context(X, K)
+        ctx = km.Context(X, K, sort=sort)
     try:
         g = ctx.assign(mu)
         mu_next, E = ctx.update()
@@ -55,7 +55,10 @@ def check_step(X, mu, ctx=None, tag=""):
     assert np.array_equal(g["counts"], o["counts"]), tag
     scale = cluster_abs_scale(X, lab_o, K)
     assert np.all(np.abs(g["sums"] - o["sums"]) <= REL * scale + 1e-300), tag
-    assert abs(g["inertia"] - o["J"]) <= REL * max(o["J"], 1e-300), tag
+    if np.isinf(o["J"]):   # fp32 distances overflowed on both sides
+        assert g["inertia"] == o["J"], tag
+    else:
+        assert abs(g["inertia"] - o["J"]) <= REL * max(o["J"], 1e-300), tag
     n = np.maximum(o["counts"], 1)[:, None]
     mscale = np.maximum(np.abs(o["mu_next"]), scale / n)
     assert np.all(np.abs(mu_next - o["mu_next"]) <= REL * mscale + 1e-300), tag
@@ -78,35 +81,42 @@ def perturbed_centroids(X, K, seed):
 # --------------------------------------------------------------------------
 # per-step parity over the configs (small N) and K / ragged-N sweeps
 # --------------------------------------------------------------------------
+SORT = [pytest.param(True, id="sorted"), pytest.param(False, id="unsorted")]
+
+
+@pytest.mark.parametrize("sort", SORT)
 @pytest.mark.parametrize("name,N", [("C1", 10_000), ("C2", 200_000), ("C3", 300_001),
                                     ("NS", 250_003), ("C5", 60_000)])
-def test_step_parity_configs(name, N):
+def test_step_parity_configs(name, N, sort):
     w = datagen.WORKLOADS[name]
     X = datagen.generate(w, N=N)
     init = datagen.init_indices(w, N=N)
     mu0 = X[init].astype(np.float64)
-    check_step(X, mu0, tag=f"{name} init")
-    check_step(X, perturbed_centroids(X, w.K, 5), tag=f"{name} perturbed")
+    check_step(X, mu0, tag=f"{name} init", sort=sort)
+    check_step(X, perturbed_centroids(X, w.K, 5), tag=f"{name} perturbed", sort=sort)
 
 
+@pytest.mark.parametrize("sort", SORT)
 @pytest.mark.parametrize("d", [2, 3])
 @pytest.mark.parametrize("K", [1, 2, 3, 5, 8, 11, 13, 16, 17, 31, 64, 100, 257])
-def test_step_parity_k_sweep(d, K):
+def test_step_parity_k_sweep(d, K, sort):
     w = datagen.WORKLOADS["NS" if d == 3 else "C3"]
     N = 20_011
     X = datagen.generate(w, N=N)
-    check_step(X, perturbed_centroids(X, K, K), tag=f"d={d} K={K}")
+    check_step(X, perturbed_centroids(X, K, K), tag=f"d={d} K={K}", sort=sort)
 
 
-@pytest.mark.parametrize("N", [1, 2, 3, 7, 511, 512, 513, 1023, 1025, 4097, 65_537])
-def test_step_parity_ragged_n(N):
+@pytest.mark.parametrize("sort", SORT)
+@pytest.mark.parametrize("N", [1, 2, 3, 7, 511, 512, 513, 1023, 1025, 2047, 2049, 4097, 65_537])
+def test_step_parity_ragged_n(N, sort):
     w = datagen.WORKLOADS["NS"]
     X = datagen.generate(w, N=max(N, 16))[:N].copy()
     for K in sorted({1, min(N, 5), min(N, 16), min(N, 40)}):
-        check_step(X, perturbed_centroids(X, K, N + K), tag=f"N={N} K={K}")
+        check_step(X, perturbed_centroids(X, K, N + K), tag=f"N={N} K={K}", sort=sort)
 
 
-def test_step_parity_exact_ties_and_empty_clusters():
+@pytest.mark.parametrize("sort", SORT)
+def test_step_parity_exact_ties_and_empty_clusters(sort):
     """Integer data -> exact fp32 distances -> genuine ties (lowest k wins);
     duplicated centroids -> clusters that stay empty (keep mu^t)."""
     rng = np.random.default_rng(1)
@@ -115,14 +125,46 @@ def test_step_parity_exact_ties_and_empty_clusters():
     C[7] = C[2]
     C[9] = C[2]
     C[11] = [1000.0, 1000.0, 1000.0]
-    g, o = check_step(X, C, tag="ties")
+    g, o = check_step(X, C, tag="ties", sort=sort)
     assert g["counts"][7] == 0 and g["counts"][9] == 0 and g["counts"][11] == 0
     X2 = rng.integers(-3, 4, (40_000, 2)).astype(np.float32)
     C2 = np.array([[0, 0], [0, 0], [1, 1], [-1, 1], [1, 1], [2, -2], [0, 3], [-3, 0],
                    [3, 3], [1, 1], [0, 0], [-2, -2], [2, 2], [-1, -1], [1, -1], [3, -3],
                    [0, 1], [1, 0], [0, -1], [-1, 0]], np.float64)
-    check_step(X2, C2, tag="ties 2D K=20 (large path)")
-    check_step(X2, C2[:16], tag="ties 2D K=16 (small path)")
+    check_step(X2, C2, tag="ties 2D K=20 (large path)", sort=sort)
+    check_step(X2, C2[:16], tag="ties 2D K=16 (small path)", sort=sort)
+
+
+@pytest.mark.parametrize("sort", SORT)
+@pytest.mark.parametrize("scale", [3e19, 1e-20, 1e-30, 1.0])
+def test_step_parity_extreme_scales(scale, sort):
+    """Distances that overflow fp32 (all +inf -> every point ties -> label 0),
+    that underflow to subnormals or zero (ties again), and uniform
+    (non-clustered) data: the pruning bound must never drop a possible argmin."""
+    rng = np.random.default_rng(11)
+    X = (rng.uniform(-1, 1, (30_011, 3)) * scale).astype(np.float32)
+    C = X[rng.choice(30_011, 16, replace=False)].astype(np.float64) * 1.0000001
+    check_step(X, C, tag=f"scale {scale}", sort=sort)
+
+
+@pytest.mark.parametrize("sort", SORT)
+def test_step_parity_near_bisector_points(sort):
+    """Points placed on (and one fp32 ulp off) the bisector planes of pairs
+    of centroids: near-ties decided by the last bit of form D."""
+    rng = np.random.default_rng(12)
+    C = rng.normal(0, 5, (16, 3))
+    P = []
+    for _ in range(40_000):
+        a, b = rng.choice(16, 2, replace=False)
+        t = rng.uniform(0.3, 0.7)
+        m = C[a] * t + C[b] * (1 - t)
+        P.append(m)
+    X = np.array(P, np.float32)
+    X[1::3] = np.nextafter(X[1::3], np.float32(np.inf))
+    X[2::3] = np.nextafter(X[2::3], np.float32(-np.inf))
+    mid = ((C[:8] + C[8:]) / 2).astype(np.float32)
+    X[:8] = mid
+    check_step(X, C, tag="bisectors", sort=sort)
 
 
 def test_step_parity_soa_layout_and_device_input():
@@ -146,9 +188,9 @@ def test_step_parity_soa_layout_and_device_input():
 # --------------------------------------------------------------------------
 # full runs
 # --------------------------------------------------------------------------
-def check_fit(X, K, init, tol, max_iter, tag=""):
+def check_fit(X, K, init, tol, max_iter, tag="", sort=True):
     o = oracle.fit(X, K, init, tol, max_iter)
-    with km.Context(X, K) as c:
+    with km.Context(X, K, sort=sort) as c:
         g = c.fit(init, tol, max_iter)
     assert g["iters"] == o["iters"], f"{tag}: iters {g['iters']} vs {o['iters']}"
     assert np.array_equal(g["labels"], o["labels"]), tag
@@ -157,13 +199,14 @@ def check_fit(X, K, init, tol, max_iter, tag=""):
     return g, o
 
 
+@pytest.mark.parametrize("sort", SORT)
 @pytest.mark.parametrize("name,N", [("C1", 10_000), ("C2", 300_000), ("C3", 200_000),
                                     ("NS", 1_000_000)])
-def test_full_run_parity_one_init_per_blob(name, N):
+def test_full_run_parity_one_init_per_blob(name, N, sort):
     w = datagen.WORKLOADS[name]
     X = datagen.generate(w, N=N)
     init = datagen.one_per_blob_init(w, N=N)
-    g, o = check_fit(X, w.M, init, w.tol, w.max_iter, tag=name)
+    g, o = check_fit(X, w.M, init, w.tol, w.max_iter, tag=name, sort=sort)
     np.testing.assert_allclose(g["centroids"], w.centers(), atol=0.05)
 
 
@@ -256,14 +299,15 @@ def test_errors():
         assert r["iters"] >= 1
 
 
-def test_deterministic_bitwise():
+@pytest.mark.parametrize("sort", SORT)
+def test_deterministic_bitwise(sort):
     w = datagen.WORKLOADS["NS"]
     X = datagen.generate(w, N=400_000)
     init = datagen.init_indices(w, N=400_000)
-    with km.Context(X, 16) as c:
+    with km.Context(X, 16, sort=sort) as c:
         a = c.fit(init, 0.0, 6)
         b = c.fit(init, 0.0, 6)
-    with km.Context(X, 16) as c:
+    with km.Context(X, 16, sort=sort) as c:
         e = c.fit(init, 0.0, 6)
     for r in (b, e):
         assert np.array_equal(a["labels"], r["labels"])
@@ -275,8 +319,9 @@ def test_deterministic_bitwise():
 # --------------------------------------------------------------------------
 # sharding (T4'): P contexts on one device, partials summed in rank order
 # --------------------------------------------------------------------------
+@pytest.mark.parametrize("sort", SORT)
 @pytest.mark.parametrize("P", [2, 3, 8])
-def test_fake_sharding_matches_oracle(P):
+def test_fake_sharding_matches_oracle(P, sort):
     w = datagen.WORKLOADS["NS"]
     N = 100_003
     X = datagen.generate(w, N=N)
@@ -289,7 +334,7 @@ def test_fake_sharding_matches_oracle(P):
     for r in range(P):
         a, b = datagen.shard_range(N, P, r)
         Xs = datagen.generate(w, a, b - a, N=N)
-        with km.Context(Xs, 16) as c:
+        with km.Context(Xs, 16, sort=sort) as c:
             g = c.assign(mu)
         labels.append(g["labels"])
         counts += g["counts"]
@@ -328,16 +373,18 @@ def test_nccl_single_rank_communicator_path():
 # full-size checks in the launch configuration bench.py times
 # --------------------------------------------------------------------------
 @pytest.mark.slow
-def test_full_size_ns_step_parity():
+@pytest.mark.parametrize("sort", SORT)
+def test_full_size_ns_step_parity(sort):
     """BASELINE north-star size (N=1e8, 3D, K=16): one full step against the
     oracle on all N points (labels bit-exact, counts exact, sums / J / mu / E
     per R13), through the same Context configuration bench.py uses."""
     w = datagen.WORKLOADS["NS"]
     X = datagen.generate(w)
     mu = X[datagen.init_indices(w)].astype(np.float64)
-    with km.Context(X, w.K) as c:
+    with km.Context(X, w.K, sort=sort) as c:
         info = c.info()
         assert info["path"] == 0 and info["grid"] == (w.N + 2047) // 2048
+        assert info["sorted"] == int(sort)
         check_step(X, mu, ctx=c, tag="NS full")
 
 
