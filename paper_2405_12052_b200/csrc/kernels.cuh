@@ -586,20 +586,28 @@ __global__ void k_scatter_labels(const int32_t* __restrict__ lab_sorted,
 // c == 1 (one candidate): every label is known; the distances are still
 // computed (form D) for the inertia, and the sums accumulate in registers.
 // c >= 2: candidate loop with a running strict-< argmin, per-lane private fp64
-// columns indexed by candidate slot (as in k_assign_chunk).
+// columns for kSortedSlots candidate slots at a time (more candidates: the
+// chunk is streamed again per group of slots).  A TMA stage carries 256
+// points; small columns keep ~13 warps resident per SM so enough bytes are in
+// flight to stream at HBM speed.
 // ---------------------------------------------------------------------------
+constexpr int kSortedSlots = 4;                        // per-lane column slots
+constexpr int kSortedUnit = 2 * kLaneTile;             // 256 points per TMA stage
+constexpr int kSortedUnits = kChunkPoints / kSortedUnit;  // 8 per chunk
+constexpr int kSortedStages = 4;
+
 template <int D>
 struct SortedSmem {
-    double2 A[16][32];
-    double2 B[16][32];
-    float ring[kStages][D * kLaneTile];
-    uint64_t bar[kStages];
+    double2 A[kSortedSlots][32];
+    double2 B[kSortedSlots][32];
+    float ring[kSortedStages][D * kSortedUnit];
+    uint64_t bar[kSortedStages];
     float4 cand[16];   // negated fp32 centroid of each candidate slot
     int candk[16];     // centroid index of each slot (ascending)
 };
 
 template <int D, int MODE>
-__global__ void __launch_bounds__(32, 10)
+__global__ void __launch_bounds__(32)
 k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
                 const double* __restrict__ mu_buf, const DevState* __restrict__ st,
                 int mu_sel, int ignore_done, const float* __restrict__ cbox,
@@ -608,46 +616,59 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
     if (!ignore_done && st->done) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SortedSmem<D>& S = *reinterpret_cast<SortedSmem<D>*>(smem_raw);
-    constexpr int kTileFloats = D * kLaneTile;
-    constexpr unsigned kTileBytes = kTileFloats * 4;
+    constexpr int kUnitFloats = D * kSortedUnit;
+    constexpr unsigned kUnitBytes = kUnitFloats * 4;
+    constexpr int SS = kSortedStages;
     const int lane = threadIdx.x;
     const int chunk = blockIdx.x;
     const int64_t base = (int64_t)chunk * kChunkPoints;
     const int64_t rem = n - base;
-    const int64_t ntile64 = (rem + kLaneTile - 1) / kLaneTile;
-    const int ntile = ntile64 < kChunkTiles ? (int)ntile64 : kChunkTiles;
+    const int64_t nu64 = (rem + kSortedUnit - 1) / kSortedUnit;
+    const int nunit = nu64 < kSortedUnits ? (int)nu64 : kSortedUnits;
     const float* src = X + (base >> 6) * (D * kWarpTile);
 
+    // The stream is a sequence of unit loads q = pass * nunit + u (passes > 0
+    // only for chunks with more than kSortedSlots candidates); unit q lives in
+    // stage q % SS, phase (q / SS) & 1.  npass is known once the candidates
+    // are, so the prologue issues only pass-0 units.
+    int total = nunit;              // units in the sequence (updated with npass)
+    unsigned issued = 0;            // lane 0: next q to issue
+    auto issue_upto = [&](unsigned limit) {
+        if (lane != 0) return;
+        while (issued < limit && (int)issued < total) {
+            const int s = issued % SS;
+            const int u = (int)(issued % (unsigned)nunit);
+            mbar_expect_tx(&S.bar[s], kUnitBytes);
+            bulk_g2s(S.ring[s], src + (int64_t)u * kUnitFloats, kUnitBytes, &S.bar[s]);
+            ++issued;
+        }
+    };
     if (lane == 0) {
 #pragma unroll
-        for (int s = 0; s < kStages; ++s) mbar_init(&S.bar[s], 1);
+        for (int s = 0; s < SS; ++s) mbar_init(&S.bar[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-#pragma unroll
-        for (int s = 0; s < kStages; ++s) {
-            if (s < ntile) {
-                mbar_expect_tx(&S.bar[s], kTileBytes);
-                bulk_g2s(S.ring[s], src + s * kTileFloats, kTileBytes, &S.bar[s]);
-            }
-        }
     }
+    issue_upto(SS);
 
     // ---- candidates of this chunk ----
     const double* mu = mu_buf + (size_t)((st->t - mu_sel) & 1) * K * D;
     const bool is_k = lane < K;
+    const float bx = (lane < 2 * D) ? __ldg(&cbox[(size_t)chunk * 2 * D + lane]) : 0.0f;
     float c32[3] = {0.f, 0.f, 0.f};
-    double dmin2 = 0.0, dmax2 = 0.0;
     if (is_k) {
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
-            c32[j] = __double2float_rn(__ldg(&mu[lane * D + j]));
-            const double c = (double)c32[j];
-            const double lo = (double)__ldg(&cbox[(size_t)chunk * 2 * D + j]);
-            const double hi = (double)__ldg(&cbox[(size_t)chunk * 2 * D + D + j]);
-            const double dm = fmax(fmax(lo - c, c - hi), 0.0);
-            dmin2 += dm * dm;
-            const double dx = fmax(fabs(c - lo), fabs(hi - c));
-            dmax2 += dx * dx;
-        }
+        for (int j = 0; j < D; ++j) c32[j] = __double2float_rn(__ldg(&mu[lane * D + j]));
+    }
+    double dmin2 = 0.0, dmax2 = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        const double lo = (double)__shfl_sync(0xffffffffu, bx, j);
+        const double hi = (double)__shfl_sync(0xffffffffu, bx, D + j);
+        const double c = (double)c32[j];
+        const double dm = fmax(fmax(lo - c, c - hi), 0.0);
+        dmin2 += dm * dm;
+        const double dx = fmax(fabs(c - lo), fabs(hi - c));
+        dmax2 += dx * dx;
     }
     double M = is_k ? dmax2 : (double)pos_inf();
 #pragma unroll
@@ -667,30 +688,27 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
     struct Pts {
         float2 xa, ya, za, xb, yb, zb;
     };
-    auto fetch = [&](int i) {
-        const int s = i % kStages;
-        mbar_wait(&S.bar[s], (unsigned)(i / kStages) & 1u);
-        const float* rg = S.ring[s];
-        const float* rb = rg + D * kWarpTile;
-        Pts P;
-        P.xa = reinterpret_cast<const float2*>(rg)[lane];
-        P.ya = reinterpret_cast<const float2*>(rg + kWarpTile)[lane];
-        P.za = (D == 3) ? reinterpret_cast<const float2*>(rg + 2 * kWarpTile)[lane]
-                        : make_float2(0.f, 0.f);
-        P.xb = reinterpret_cast<const float2*>(rb)[lane];
-        P.yb = reinterpret_cast<const float2*>(rb + kWarpTile)[lane];
-        P.zb = (D == 3) ? reinterpret_cast<const float2*>(rb + 2 * kWarpTile)[lane]
-                        : make_float2(0.f, 0.f);
-        __syncwarp();
-        const int r = i - 1 + kStages;
-        if (lane == 0 && i >= 1 && r < ntile) {
-            const int sr = (i - 1) % kStages;
-            mbar_expect_tx(&S.bar[sr], kTileBytes);
-            bulk_g2s(S.ring[sr], src + (int64_t)r * kTileFloats, kTileBytes, &S.bar[sr]);
+    // unit q: wait, read both 128-point sub-tiles, refill up to unit q+SS-1
+    // (its stage was used by unit q-1, consumed by now)
+    auto fetch = [&](unsigned q, Pts (&P)[2]) {
+        const int s = q % SS;
+        mbar_wait(&S.bar[s], (q / SS) & 1u);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float* rg = S.ring[s] + h * (D * kLaneTile);
+            const float* rb = rg + D * kWarpTile;
+            P[h].xa = reinterpret_cast<const float2*>(rg)[lane];
+            P[h].ya = reinterpret_cast<const float2*>(rg + kWarpTile)[lane];
+            P[h].za = (D == 3) ? reinterpret_cast<const float2*>(rg + 2 * kWarpTile)[lane]
+                               : make_float2(0.f, 0.f);
+            P[h].xb = reinterpret_cast<const float2*>(rb)[lane];
+            P[h].yb = reinterpret_cast<const float2*>(rb + kWarpTile)[lane];
+            P[h].zb = (D == 3) ? reinterpret_cast<const float2*>(rb + 2 * kWarpTile)[lane]
+                               : make_float2(0.f, 0.f);
         }
-        return P;
+        __syncwarp();
+        issue_upto(q + SS);
     };
-    // form D of 2 packed points against candidate cc (negated centroid)
     auto dist2 = [&](float2 x, float2 y, float2 z, const float4& cc) {
         float2 e0 = __fadd2_rn(x, make_float2(cc.x, cc.x));
         float2 e1 = __fadd2_rn(y, make_float2(cc.y, cc.y));
@@ -702,38 +720,45 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
         }
         return sq;
     };
-
     double* row = cpart + (size_t)chunk * kRowDoubles;
+
     if (nc == 1) {
-        // ---- one candidate: labels known, sums in registers ----
+        // ---- one candidate: labels known, sums in registers (two chains) ----
         const float4 cc = S.cand[0];
         const int k0 = S.candk[0];
-        double sx = 0.0, sy = 0.0, sz = 0.0, J = 0.0;
+        double sx0 = 0.0, sy0 = 0.0, sz0 = 0.0, J0 = 0.0;
+        double sx1 = 0.0, sy1 = 0.0, sz1 = 0.0, J1 = 0.0;
 #pragma unroll 1
-        for (int i = 0; i < ntile; ++i) {
-            const Pts P = fetch(i);
-            const float2 da = dist2(P.xa, P.ya, P.za, cc);
-            const float2 db = dist2(P.xb, P.yb, P.zb, cc);
-            const int64_t pa = base + (int64_t)i * kLaneTile + 2 * lane, pb = pa + kWarpTile;
-            if (MODE & kModeLabels) {
-                *reinterpret_cast<int2*>(labels + pa) = make_int2(k0, k0);
-                *reinterpret_cast<int2*>(labels + pb) = make_int2(k0, k0);
-            }
-            if (MODE & kModeReduce) {
-                if (i * kLaneTile + kLaneTile <= rem) {
-                    sx += (double)P.xa.x; sy += (double)P.ya.x; sz += (double)P.za.x; J += (double)da.x;
-                    sx += (double)P.xa.y; sy += (double)P.ya.y; sz += (double)P.za.y; J += (double)da.y;
-                    sx += (double)P.xb.x; sy += (double)P.yb.x; sz += (double)P.zb.x; J += (double)db.x;
-                    sx += (double)P.xb.y; sy += (double)P.yb.y; sz += (double)P.zb.y; J += (double)db.y;
-                } else {
-                    if (pa < n) { sx += (double)P.xa.x; sy += (double)P.ya.x; sz += (double)P.za.x; J += (double)da.x; }
-                    if (pa + 1 < n) { sx += (double)P.xa.y; sy += (double)P.ya.y; sz += (double)P.za.y; J += (double)da.y; }
-                    if (pb < n) { sx += (double)P.xb.x; sy += (double)P.yb.x; sz += (double)P.zb.x; J += (double)db.x; }
-                    if (pb + 1 < n) { sx += (double)P.xb.y; sy += (double)P.yb.y; sz += (double)P.zb.y; J += (double)db.y; }
+        for (int u = 0; u < nunit; ++u) {
+            Pts P[2];
+            fetch(u, P);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
+                const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
+                const int64_t pa = base + (int64_t)u * kSortedUnit + h * kLaneTile + 2 * lane;
+                const int64_t pb = pa + kWarpTile;
+                if (MODE & kModeLabels) {
+                    *reinterpret_cast<int2*>(labels + pa) = make_int2(k0, k0);
+                    *reinterpret_cast<int2*>(labels + pb) = make_int2(k0, k0);
+                }
+                if (MODE & kModeReduce) {
+                    if ((int64_t)u * kSortedUnit + (h + 1) * kLaneTile <= rem) {
+                        sx0 += (double)P[h].xa.x; sy0 += (double)P[h].ya.x; sz0 += (double)P[h].za.x; J0 += (double)da.x;
+                        sx1 += (double)P[h].xa.y; sy1 += (double)P[h].ya.y; sz1 += (double)P[h].za.y; J1 += (double)da.y;
+                        sx0 += (double)P[h].xb.x; sy0 += (double)P[h].yb.x; sz0 += (double)P[h].zb.x; J0 += (double)db.x;
+                        sx1 += (double)P[h].xb.y; sy1 += (double)P[h].yb.y; sz1 += (double)P[h].zb.y; J1 += (double)db.y;
+                    } else {
+                        if (pa < n) { sx0 += (double)P[h].xa.x; sy0 += (double)P[h].ya.x; sz0 += (double)P[h].za.x; J0 += (double)da.x; }
+                        if (pa + 1 < n) { sx1 += (double)P[h].xa.y; sy1 += (double)P[h].ya.y; sz1 += (double)P[h].za.y; J1 += (double)da.y; }
+                        if (pb < n) { sx0 += (double)P[h].xb.x; sy0 += (double)P[h].yb.x; sz0 += (double)P[h].zb.x; J0 += (double)db.x; }
+                        if (pb + 1 < n) { sx1 += (double)P[h].xb.y; sy1 += (double)P[h].yb.y; sz1 += (double)P[h].zb.y; J1 += (double)db.y; }
+                    }
                 }
             }
         }
         if (!(MODE & kModeReduce)) return;
+        double sx = sx0 + sx1, sy = sy0 + sy1, sz = sz0 + sz1, J = J0 + J1;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             sx += __shfl_xor_sync(0xffffffffu, sx, o);
@@ -741,7 +766,6 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
             sz += __shfl_xor_sync(0xffffffffu, sz, o);
             J += __shfl_xor_sync(0xffffffffu, J, o);
         }
-        // row layout [k][Sx, Sy, Sz, n]; zero for the other clusters
         const int kk = lane >> 1;
         double2 out = make_double2(0.0, 0.0);
         if (kk == k0) {
@@ -753,15 +777,15 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
         return;
     }
 
-    // ---- several candidates: running exact argmin, slot-indexed columns ----
-    if (MODE & kModeReduce) {
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            S.A[k][lane] = make_double2(0.0, 0.0);
-            S.B[k][lane] = make_double2(0.0, 0.0);
-        }
-    }
-    __syncwarp();
+    // ---- several candidates: exact running argmin over the candidates (ascending
+    // k, strict <); per-lane private fp64 columns for kSortedSlots slots at a
+    // time -- a chunk with more candidates streams its points once per group of
+    // kSortedSlots slots (passes), each pass accumulating only its slots ----
+    // labels-only launches need a single pass (no columns)
+    const int npass = (MODE & kModeReduce) ? (nc + kSortedSlots - 1) / kSortedSlots : 1;
+    total = npass * nunit;
+    issue_upto(SS);   // pass > 0 units may now be issued if the ring has room
+    if (MODE & kModeReduce) reinterpret_cast<double2*>(row)[lane] = make_double2(0.0, 0.0);
     double J = 0.0;
     auto accumulate = [&](int l, float px, float py, float pz) {
         double2 a = S.A[l][lane], b = S.B[l][lane];
@@ -775,63 +799,86 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
         S.B[l][lane] = b;
     };
 #pragma unroll 1
-    for (int i = 0; i < ntile; ++i) {
-        const Pts P = fetch(i);
-        float2 ba = dist2(P.xa, P.ya, P.za, S.cand[0]);
-        float2 bb = dist2(P.xb, P.yb, P.zb, S.cand[0]);
-        int s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-#pragma unroll 1
-        for (int j = 1; j < nc; ++j) {
-            const float4 cc = S.cand[j];
-            const float2 da = dist2(P.xa, P.ya, P.za, cc);
-            const float2 db = dist2(P.xb, P.yb, P.zb, cc);
-            if (da.x < ba.x) { ba.x = da.x; s0 = j; }
-            if (da.y < ba.y) { ba.y = da.y; s1 = j; }
-            if (db.x < bb.x) { bb.x = db.x; s2 = j; }
-            if (db.y < bb.y) { bb.y = db.y; s3 = j; }
-        }
-        const int64_t pa = base + (int64_t)i * kLaneTile + 2 * lane, pb = pa + kWarpTile;
-        if (MODE & kModeLabels) {
-            *reinterpret_cast<int2*>(labels + pa) = make_int2(S.candk[s0], S.candk[s1]);
-            *reinterpret_cast<int2*>(labels + pb) = make_int2(S.candk[s2], S.candk[s3]);
-        }
+    for (int pass = 0; pass < npass; ++pass) {
+        const int s_lo = pass * kSortedSlots;
         if (MODE & kModeReduce) {
-            if (pa < n) { accumulate(s0, P.xa.x, P.ya.x, P.za.x); J += (double)ba.x; }
-            if (pa + 1 < n) { accumulate(s1, P.xa.y, P.ya.y, P.za.y); J += (double)ba.y; }
-            if (pb < n) { accumulate(s2, P.xb.x, P.yb.x, P.zb.x); J += (double)bb.x; }
-            if (pb + 1 < n) { accumulate(s3, P.xb.y, P.yb.y, P.zb.y); J += (double)bb.y; }
+#pragma unroll
+            for (int k = 0; k < kSortedSlots; ++k) {
+                S.A[k][lane] = make_double2(0.0, 0.0);
+                S.B[k][lane] = make_double2(0.0, 0.0);
+            }
         }
-    }
-    if (!(MODE & kModeReduce)) return;
-    __syncwarp();
-    // lane L sums slot (L >> 1), half (L & 1) over the 32 lanes (rotated order)
-    const int slot = lane >> 1;
-    const double2* col = (lane & 1) ? &S.B[0][0] : &S.A[0][0];
-    double v0 = 0.0, v1 = 0.0;
-    long long cnt = 0;
-    if (slot < nc) {
+        __syncwarp();
+#pragma unroll 1
+        for (int u = 0; u < nunit; ++u) {
+            Pts P[2];
+            fetch(pass * nunit + u, P);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float2 ba = dist2(P[h].xa, P[h].ya, P[h].za, S.cand[0]);
+                float2 bb = dist2(P[h].xb, P[h].yb, P[h].zb, S.cand[0]);
+                int s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+#pragma unroll 1
+                for (int j = 1; j < nc; ++j) {
+                    const float4 cc = S.cand[j];
+                    const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
+                    const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
+                    if (da.x < ba.x) { ba.x = da.x; s0 = j; }
+                    if (da.y < ba.y) { ba.y = da.y; s1 = j; }
+                    if (db.x < bb.x) { bb.x = db.x; s2 = j; }
+                    if (db.y < bb.y) { bb.y = db.y; s3 = j; }
+                }
+                const int64_t pa = base + (int64_t)u * kSortedUnit + h * kLaneTile + 2 * lane;
+                const int64_t pb = pa + kWarpTile;
+                if ((MODE & kModeLabels) && pass == 0) {
+                    *reinterpret_cast<int2*>(labels + pa) = make_int2(S.candk[s0], S.candk[s1]);
+                    *reinterpret_cast<int2*>(labels + pb) = make_int2(S.candk[s2], S.candk[s3]);
+                }
+                if (MODE & kModeReduce) {
+                    const unsigned w = kSortedSlots;
+                    if (pa < n) {
+                        if ((unsigned)(s0 - s_lo) < w) accumulate(s0 - s_lo, P[h].xa.x, P[h].ya.x, P[h].za.x);
+                        if (pass == 0) J += (double)ba.x;
+                    }
+                    if (pa + 1 < n) {
+                        if ((unsigned)(s1 - s_lo) < w) accumulate(s1 - s_lo, P[h].xa.y, P[h].ya.y, P[h].za.y);
+                        if (pass == 0) J += (double)ba.y;
+                    }
+                    if (pb < n) {
+                        if ((unsigned)(s2 - s_lo) < w) accumulate(s2 - s_lo, P[h].xb.x, P[h].yb.x, P[h].zb.x);
+                        if (pass == 0) J += (double)bb.x;
+                    }
+                    if (pb + 1 < n) {
+                        if ((unsigned)(s3 - s_lo) < w) accumulate(s3 - s_lo, P[h].xb.y, P[h].yb.y, P[h].zb.y);
+                        if (pass == 0) J += (double)bb.y;
+                    }
+                }
+            }
+        }
+        if (!(MODE & kModeReduce)) return;   // labels-only: one pass suffices
+        __syncwarp();
+        // lane L (< 2 * kSortedSlots) sums slot s_lo + (L >> 1), half (L & 1),
+        // over the 32 lanes in a rotated (bank-conflict-free) order
+        const int sl = lane >> 1;
+        if (sl < kSortedSlots && s_lo + sl < nc) {
+            const double2* col = (lane & 1) ? &S.B[0][0] : &S.A[0][0];
+            double v0 = 0.0, v1 = 0.0;
+            long long cnt = 0;
 #pragma unroll 8
-        for (int r = 0; r < 32; ++r) {
-            const int t = (r + lane) & 31;
-            const double2 w = col[slot * 32 + t];
-            v0 += w.x;
-            if (lane & 1) cnt += reinterpret_cast<const int2*>(&w.y)->x;
-            else v1 += w.y;
+            for (int r = 0; r < 32; ++r) {
+                const int t = (r + lane) & 31;
+                const double2 w2 = col[sl * 32 + t];
+                v0 += w2.x;
+                if (lane & 1) cnt += reinterpret_cast<const int2*>(&w2.y)->x;
+                else v1 += w2.y;
+            }
+            const int k = S.candk[s_lo + sl];
+            reinterpret_cast<double2*>(row)[2 * k + (lane & 1)] =
+                (lane & 1) ? make_double2(v0, (double)cnt) : make_double2(v0, v1);
         }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
-    // dense row: entry of cluster k comes from the lane pair owning its slot
-    const int kk = lane >> 1;                       // cluster this lane writes
-    const bool kin = (mask >> kk) & 1u;             // is cluster kk a candidate?
-    const int ks = __popc(mask & ((1u << kk) - 1u)); // its slot
-    const int srcl = 2 * ks + (lane & 1);
-    const double g0 = __shfl_sync(0xffffffffu, v0, srcl);
-    const double g1 = __shfl_sync(0xffffffffu, v1, srcl);
-    const long long gc = __shfl_sync(0xffffffffu, cnt, srcl);
-    double2 out = make_double2(0.0, 0.0);
-    if (kk < 16 && kin) out = (lane & 1) ? make_double2(g0, (double)gc) : make_double2(g0, g1);
-    reinterpret_cast<double2*>(row)[lane] = out;
     if (lane == 0) row[64] = J;
 }
 
