@@ -633,14 +633,15 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
     // are, so the prologue issues only pass-0 units.
     int total = nunit;              // units in the sequence (updated with npass)
     unsigned issued = 0;            // lane 0: next q to issue
+    int pu = 0;                     // lane 0: unit index of q = issued (wraps per pass)
     auto issue_upto = [&](unsigned limit) {
         if (lane != 0) return;
         while (issued < limit && (int)issued < total) {
             const int s = issued % SS;
-            const int u = (int)(issued % (unsigned)nunit);
             mbar_expect_tx(&S.bar[s], kUnitBytes);
-            bulk_g2s(S.ring[s], src + (int64_t)u * kUnitFloats, kUnitBytes, &S.bar[s]);
+            bulk_g2s(S.ring[s], src + (int64_t)pu * kUnitFloats, kUnitBytes, &S.bar[s]);
             ++issued;
+            if (++pu == nunit) pu = 0;
         }
     };
     if (lane == 0) {
@@ -726,8 +727,17 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
         // ---- one candidate: labels known, sums in registers (two chains) ----
         const float4 cc = S.cand[0];
         const int k0 = S.candk[0];
-        double sx0 = 0.0, sy0 = 0.0, sz0 = 0.0, J0 = 0.0;
-        double sx1 = 0.0, sy1 = 0.0, sz1 = 0.0, J1 = 0.0;
+        // four independent accumulation chains (one per point position of a
+        // sub-tile), combined in a fixed order at the end
+        double sx[4] = {0.0, 0.0, 0.0, 0.0}, sy[4] = {0.0, 0.0, 0.0, 0.0};
+        double sz[4] = {0.0, 0.0, 0.0, 0.0}, Jc[4] = {0.0, 0.0, 0.0, 0.0};
+        auto add4 = [&](const Pts& Q, float2 da, float2 db, int m) {
+            // m: bit mask of the valid points (a0, a1, b0, b1)
+            if (m & 1) { sx[0] += (double)Q.xa.x; sy[0] += (double)Q.ya.x; sz[0] += (double)Q.za.x; Jc[0] += (double)da.x; }
+            if (m & 2) { sx[1] += (double)Q.xa.y; sy[1] += (double)Q.ya.y; sz[1] += (double)Q.za.y; Jc[1] += (double)da.y; }
+            if (m & 4) { sx[2] += (double)Q.xb.x; sy[2] += (double)Q.yb.x; sz[2] += (double)Q.zb.x; Jc[2] += (double)db.x; }
+            if (m & 8) { sx[3] += (double)Q.xb.y; sy[3] += (double)Q.yb.y; sz[3] += (double)Q.zb.y; Jc[3] += (double)db.y; }
+        };
 #pragma unroll 1
         for (int u = 0; u < nunit; ++u) {
             Pts P[2];
@@ -744,33 +754,31 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
                 }
                 if (MODE & kModeReduce) {
                     if ((int64_t)u * kSortedUnit + (h + 1) * kLaneTile <= rem) {
-                        sx0 += (double)P[h].xa.x; sy0 += (double)P[h].ya.x; sz0 += (double)P[h].za.x; J0 += (double)da.x;
-                        sx1 += (double)P[h].xa.y; sy1 += (double)P[h].ya.y; sz1 += (double)P[h].za.y; J1 += (double)da.y;
-                        sx0 += (double)P[h].xb.x; sy0 += (double)P[h].yb.x; sz0 += (double)P[h].zb.x; J0 += (double)db.x;
-                        sx1 += (double)P[h].xb.y; sy1 += (double)P[h].yb.y; sz1 += (double)P[h].zb.y; J1 += (double)db.y;
+                        add4(P[h], da, db, 15);
                     } else {
-                        if (pa < n) { sx0 += (double)P[h].xa.x; sy0 += (double)P[h].ya.x; sz0 += (double)P[h].za.x; J0 += (double)da.x; }
-                        if (pa + 1 < n) { sx1 += (double)P[h].xa.y; sy1 += (double)P[h].ya.y; sz1 += (double)P[h].za.y; J1 += (double)da.y; }
-                        if (pb < n) { sx0 += (double)P[h].xb.x; sy0 += (double)P[h].yb.x; sz0 += (double)P[h].zb.x; J0 += (double)db.x; }
-                        if (pb + 1 < n) { sx1 += (double)P[h].xb.y; sy1 += (double)P[h].yb.y; sz1 += (double)P[h].zb.y; J1 += (double)db.y; }
+                        add4(P[h], da, db, (pa < n ? 1 : 0) | (pa + 1 < n ? 2 : 0) |
+                                               (pb < n ? 4 : 0) | (pb + 1 < n ? 8 : 0));
                     }
                 }
             }
         }
         if (!(MODE & kModeReduce)) return;
-        double sx = sx0 + sx1, sy = sy0 + sy1, sz = sz0 + sz1, J = J0 + J1;
+        double sxt = (sx[0] + sx[1]) + (sx[2] + sx[3]);
+        double syt = (sy[0] + sy[1]) + (sy[2] + sy[3]);
+        double szt = (sz[0] + sz[1]) + (sz[2] + sz[3]);
+        double J = (Jc[0] + Jc[1]) + (Jc[2] + Jc[3]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            sx += __shfl_xor_sync(0xffffffffu, sx, o);
-            sy += __shfl_xor_sync(0xffffffffu, sy, o);
-            sz += __shfl_xor_sync(0xffffffffu, sz, o);
+            sxt += __shfl_xor_sync(0xffffffffu, sxt, o);
+            syt += __shfl_xor_sync(0xffffffffu, syt, o);
+            szt += __shfl_xor_sync(0xffffffffu, szt, o);
             J += __shfl_xor_sync(0xffffffffu, J, o);
         }
         const int kk = lane >> 1;
         double2 out = make_double2(0.0, 0.0);
         if (kk == k0) {
             const double cnt = (double)(rem < kChunkPoints ? rem : kChunkPoints);
-            out = (lane & 1) ? make_double2(sz, cnt) : make_double2(sx, sy);
+            out = (lane & 1) ? make_double2(szt, cnt) : make_double2(sxt, syt);
         }
         reinterpret_cast<double2*>(row)[lane] = out;
         if (lane == 0) row[64] = J;
