@@ -56,8 +56,11 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: tuple = ()) -> str:
+    """Compile libkmeans.so (or a tuning variant `out` with -D `defines`)."""
+    target = out or LIB
+    if not force and out is None and not needs_build():
         return LIB
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
            "-shared", "-Xptxas", "-v" if verbose else "-O3",
@@ -68,13 +71,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
         so = sorted(glob.glob(os.path.join(lib, "libnccl.so*")))[0]
         cmd += ["-DKMEANS_WITH_NCCL", "-I", inc, "-L", lib, f"-l:{os.path.basename(so)}",
                 "-Xlinker", f"-rpath={lib}"]
-    tmp = LIB + f".tmp{os.getpid()}"
+    cmd += [f"-D{d}" for d in defines]
+    tmp = target + f".tmp{os.getpid()}"
     cmd += ["-o", tmp, *SOURCES]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

@@ -165,7 +165,16 @@ __device__ __forceinline__ void exact_argmin(const float (&d)[KP], float& m, int
 // kGroupChunks rows in ascending order, k_merge sums the groups.  No atomics.
 // ---------------------------------------------------------------------------
 constexpr int kLaneTile = 2 * kWarpTile;                 // 128 points per warp-tile
-constexpr int kChunkTiles = 16;
+#ifndef KM_CHUNK_TILES
+#define KM_CHUNK_TILES 16
+#endif
+#ifndef KM_SORTED_STAGES
+#define KM_SORTED_STAGES 4
+#endif
+#ifndef KM_SORTED_SLOTS
+#define KM_SORTED_SLOTS 4
+#endif
+constexpr int kChunkTiles = KM_CHUNK_TILES;
 constexpr int kChunkPoints = kLaneTile * kChunkTiles;    // 2048
 constexpr int kStages = 3;
 constexpr int kGroupChunks = 64;
@@ -591,10 +600,10 @@ __global__ void k_scatter_labels(const int32_t* __restrict__ lab_sorted,
 // points; small columns keep ~13 warps resident per SM so enough bytes are in
 // flight to stream at HBM speed.
 // ---------------------------------------------------------------------------
-constexpr int kSortedSlots = 4;                        // per-lane column slots
+constexpr int kSortedSlots = KM_SORTED_SLOTS;          // per-lane column slots
 constexpr int kSortedUnit = 2 * kLaneTile;             // 256 points per TMA stage
 constexpr int kSortedUnits = kChunkPoints / kSortedUnit;  // 8 per chunk
-constexpr int kSortedStages = 4;
+constexpr int kSortedStages = KM_SORTED_STAGES;
 
 template <int D>
 struct SortedSmem {

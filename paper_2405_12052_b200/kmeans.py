@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libkmeans.so")
+LIB_PATH = os.environ.get("KMEANS_LIB_OVERRIDE") or os.path.join(HERE, "libkmeans.so")
 
 KMEANS_OK = 0
 STATUS = {0: "KMEANS_OK", -1: "KMEANS_EINVAL", -2: "KMEANS_ENONFINITE", -3: "KMEANS_ENOMEM",

@@ -1,0 +1,18 @@
+"""Build tuning variants of libkmeans.so into tune/ (KMEANS_LIB_OVERRIDE selects one)."""
+import sys
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+from paper_2405_12052_b200 import build as kb
+
+VARIANTS = {
+    "base": (),
+    "c32": ("KM_CHUNK_TILES=32",),
+    "st6": ("KM_SORTED_STAGES=6",),
+    "st3": ("KM_SORTED_STAGES=3",),
+    "c32st6": ("KM_CHUNK_TILES=32", "KM_SORTED_STAGES=6"),
+    "sl2": ("KM_SORTED_SLOTS=2",),
+    "c8": ("KM_CHUNK_TILES=8",),
+}
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(VARIANTS)
+    for n in names:
+        print(kb.build(force=True, out=f"tune/libkmeans_{n}.so", defines=VARIANTS[n]))
