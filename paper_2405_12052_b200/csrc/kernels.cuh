@@ -169,7 +169,10 @@ constexpr int kLaneTile = 2 * kWarpTile;                 // 128 points per warp-
 #define KM_CHUNK_TILES 16
 #endif
 #ifndef KM_SORTED_STAGES
-#define KM_SORTED_STAGES 4
+#define KM_SORTED_STAGES 2
+#endif
+#ifndef KM_SORTED_CHUNK_TILES
+#define KM_SORTED_CHUNK_TILES 8
 #endif
 #ifndef KM_SORTED_SLOTS
 #define KM_SORTED_SLOTS 4
@@ -601,8 +604,16 @@ __global__ void k_scatter_labels(const int32_t* __restrict__ lab_sorted,
 // flight to stream at HBM speed.
 // ---------------------------------------------------------------------------
 constexpr int kSortedSlots = KM_SORTED_SLOTS;          // per-lane column slots
-constexpr int kSortedUnit = 2 * kLaneTile;             // 256 points per TMA stage
-constexpr int kSortedUnits = kChunkPoints / kSortedUnit;  // 8 per chunk
+#ifndef KM_SORTED_UNIT_SUB
+#define KM_SORTED_UNIT_SUB 2
+#endif
+constexpr int kUnitSub = KM_SORTED_UNIT_SUB;           // 128-point sub-tiles per stage
+constexpr int kSortedUnit = kUnitSub * kLaneTile;      // points per TMA stage
+// Sorted path chunk: the pruning box and the partial row cover kSChunkPoints
+// points (a one-warp block each).  Measured on NS (tools/sweep.py): 1024
+// points beats 512 (per-block overhead) and 2048 (more multi-candidate boxes).
+constexpr int kSChunkPoints = KM_SORTED_CHUNK_TILES * kLaneTile;   // 1024
+constexpr int kSortedUnits = kSChunkPoints / kSortedUnit;          // 4 per chunk
 constexpr int kSortedStages = KM_SORTED_STAGES;
 
 template <int D>
@@ -630,7 +641,7 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
     constexpr int SS = kSortedStages;
     const int lane = threadIdx.x;
     const int chunk = blockIdx.x;
-    const int64_t base = (int64_t)chunk * kChunkPoints;
+    const int64_t base = (int64_t)chunk * kSChunkPoints;
     const int64_t rem = n - base;
     const int64_t nu64 = (rem + kSortedUnit - 1) / kSortedUnit;
     const int nunit = nu64 < kSortedUnits ? (int)nu64 : kSortedUnits;
@@ -700,11 +711,11 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
     };
     // unit q: wait, read both 128-point sub-tiles, refill up to unit q+SS-1
     // (its stage was used by unit q-1, consumed by now)
-    auto fetch = [&](unsigned q, Pts (&P)[2]) {
+    auto fetch = [&](unsigned q, Pts (&P)[kUnitSub]) {
         const int s = q % SS;
         mbar_wait(&S.bar[s], (q / SS) & 1u);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < kUnitSub; ++h) {
             const float* rg = S.ring[s] + h * (D * kLaneTile);
             const float* rb = rg + D * kWarpTile;
             P[h].xa = reinterpret_cast<const float2*>(rg)[lane];
@@ -749,10 +760,10 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
         };
 #pragma unroll 1
         for (int u = 0; u < nunit; ++u) {
-            Pts P[2];
+            Pts P[kUnitSub];
             fetch(u, P);
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < kUnitSub; ++h) {
                 const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
                 const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
                 const int64_t pa = base + (int64_t)u * kSortedUnit + h * kLaneTile + 2 * lane;
@@ -786,7 +797,7 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
         const int kk = lane >> 1;
         double2 out = make_double2(0.0, 0.0);
         if (kk == k0) {
-            const double cnt = (double)(rem < kChunkPoints ? rem : kChunkPoints);
+            const double cnt = (double)(rem < kSChunkPoints ? rem : kSChunkPoints);
             out = (lane & 1) ? make_double2(szt, cnt) : make_double2(sxt, syt);
         }
         reinterpret_cast<double2*>(row)[lane] = out;
@@ -828,10 +839,10 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
         __syncwarp();
 #pragma unroll 1
         for (int u = 0; u < nunit; ++u) {
-            Pts P[2];
+            Pts P[kUnitSub];
             fetch(pass * nunit + u, P);
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < kUnitSub; ++h) {
                 float2 ba = dist2(P[h].xa, P[h].ya, P[h].za, S.cand[0]);
                 float2 bb = dist2(P[h].xb, P[h].yb, P[h].zb, S.cand[0]);
                 int s0 = 0, s1 = 0, s2 = 0, s3 = 0;

@@ -68,6 +68,7 @@ struct kmeans_ctx {
 
     int G = 0, tpb = 0, smem = 0, path = 0;   // G = columns of part (blocks or groups)
     int n_chunks = 0;
+    int chunk_points = 0;         // points per chunk row (sorted / unsorted differ)
     double* cpart = nullptr;      // n_chunks x kRowDoubles chunk partials (path 0)
     bool sorted = false;          // points held in Morton order (path 0 default)
     int32_t* perm = nullptr;      // sorted position -> caller's index (sorted only)
@@ -209,7 +210,8 @@ kmeans_status configure(kmeans_ctx* ctx) {
                 CK(cudaFuncSetAttribute((const void*)pick_chunk(ctx->d, ctx->K, mode),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
         }
-        ctx->n_chunks = (int)((ctx->N + km::kChunkPoints - 1) / km::kChunkPoints);
+        ctx->chunk_points = ctx->sorted ? km::kSChunkPoints : km::kChunkPoints;
+        ctx->n_chunks = (int)((ctx->N + ctx->chunk_points - 1) / ctx->chunk_points);
         ctx->G = (ctx->n_chunks + km::kGroupChunks - 1) / km::kGroupChunks;  // groups
     } else {
         ctx->path = 1;
@@ -482,7 +484,7 @@ kmeans_status sort_points(kmeans_ctx* ctx, const float* src, int64_t si, int64_t
         km::k_gather_sorted<<<gb, 256, 0, ctx->stream>>>(src, N, d, si, sj, ctx->perm,
                                                          ctx->invperm, ctx->X, ctx->ldx);
         const int cb = (ctx->n_chunks * 32 + 255) / 256;
-        km::k_chunk_bbox<<<cb, 256, 0, ctx->stream>>>(ctx->X, N, d, km::kChunkPoints,
+        km::k_chunk_bbox<<<cb, 256, 0, ctx->stream>>>(ctx->X, N, d, ctx->chunk_points,
                                                       ctx->n_chunks, ctx->cbox);
         ctx->launches += 2;
         e = cudaGetLastError();

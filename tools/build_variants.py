@@ -11,6 +11,17 @@ VARIANTS = {
     "c32st6": ("KM_CHUNK_TILES=32", "KM_SORTED_STAGES=6"),
     "sl2": ("KM_SORTED_SLOTS=2",),
     "c8": ("KM_CHUNK_TILES=8",),
+    "u1st3": ("KM_SORTED_UNIT_SUB=1", "KM_SORTED_STAGES=3"),
+    "u1st4": ("KM_SORTED_UNIT_SUB=1", "KM_SORTED_STAGES=4"),
+    "u1st6": ("KM_SORTED_UNIT_SUB=1", "KM_SORTED_STAGES=6"),
+    "c8st3": ("KM_CHUNK_TILES=8", "KM_SORTED_STAGES=3"),
+    "c8u1st4": ("KM_CHUNK_TILES=8", "KM_SORTED_UNIT_SUB=1", "KM_SORTED_STAGES=4"),
+    "st2": ("KM_SORTED_STAGES=2",),
+    "c4u1st4": ("KM_CHUNK_TILES=4", "KM_SORTED_UNIT_SUB=1", "KM_SORTED_STAGES=4"),
+    "c4st2": ("KM_CHUNK_TILES=4", "KM_SORTED_STAGES=2"),
+    "c8u1st3": ("KM_CHUNK_TILES=8", "KM_SORTED_UNIT_SUB=1", "KM_SORTED_STAGES=3"),
+    "c8st2": ("KM_CHUNK_TILES=8", "KM_SORTED_STAGES=2"),
+    "c2u1st2": ("KM_CHUNK_TILES=2", "KM_SORTED_UNIT_SUB=1", "KM_SORTED_STAGES=2"),
 }
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
