@@ -338,7 +338,7 @@ def main():
                     hbm_frac=ach_gbs / hbm_gbs, **common)
 
     t_assign = time_assign(ctx)
-    kname = "k_assign_sorted" if info["sorted"] else ("k_assign_chunk" if info["path"] == 0
+    kname = "k_assign_pruned" if info["sorted"] else ("k_assign_chunk" if info["path"] == 0
                                                        else "k_assign_large")
     roofline = roofline_of(t_assign, kname, bool(info["sorted"]))
     roofline_hbm = {"achieved": bytes_per_launch / t_assign / 1e9, "peak": hbm_gbs, "unit": "GB/s",

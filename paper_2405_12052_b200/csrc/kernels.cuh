@@ -483,46 +483,50 @@ __global__ void k_input_bbox(const float* __restrict__ in, int64_t N, int d, int
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
-__device__ __forceinline__ unsigned part1by1(unsigned x) {   // 16 bits -> even bits
-    x &= 0x0000ffffu;
-    x = (x | (x << 8)) & 0x00ff00ffu;
-    x = (x | (x << 4)) & 0x0f0f0f0fu;
-    x = (x | (x << 2)) & 0x33333333u;
-    x = (x | (x << 1)) & 0x55555555u;
+__device__ __forceinline__ unsigned long long part1by1_64(unsigned long long x) {   // 32 -> even bits
+    x &= 0x00000000ffffffffull;
+    x = (x | (x << 16)) & 0x0000ffff0000ffffull;
+    x = (x | (x << 8)) & 0x00ff00ff00ff00ffull;
+    x = (x | (x << 4)) & 0x0f0f0f0f0f0f0f0full;
+    x = (x | (x << 2)) & 0x3333333333333333ull;
+    x = (x | (x << 1)) & 0x5555555555555555ull;
     return x;
 }
-__device__ __forceinline__ unsigned part1by2(unsigned x) {   // 10 bits -> every 3rd bit
-    x &= 0x000003ffu;
-    x = (x | (x << 16)) & 0xff0000ffu;
-    x = (x | (x << 8)) & 0x0300f00fu;
-    x = (x | (x << 4)) & 0x030c30c3u;
-    x = (x | (x << 2)) & 0x09249249u;
+__device__ __forceinline__ unsigned long long part1by2_64(unsigned long long x) {  // 21 -> every 3rd
+    x &= 0x1fffffull;
+    x = (x | (x << 32)) & 0x1f00000000ffffull;
+    x = (x | (x << 16)) & 0x1f0000ff0000ffull;
+    x = (x | (x << 8)) & 0x100f00f00f00f00full;
+    x = (x | (x << 4)) & 0x10c30c30c30c30c3ull;
+    x = (x | (x << 2)) & 0x1249249249249249ull;
     return x;
 }
 
-// Morton key of every point (quantised to the global box) and the identity
-// permutation as the sort's values.
+// 64-bit Morton key of every point (21 bits per axis in 3D, 32 in 2D) on an
+// isotropic grid over the global box -- cubic cells keep chunk boxes compact
+// even when the box is very elongated (C5's far outliers), and the fine grid
+// keeps the dense regions resolved -- with the identity permutation as values.
 __global__ void k_morton(const float* __restrict__ in, int64_t N, int d, int64_t si, int64_t sj,
-                         const unsigned* __restrict__ box, unsigned* __restrict__ keys,
+                         const unsigned* __restrict__ box, unsigned long long* __restrict__ keys,
                          int32_t* __restrict__ iota) {
-    const int bits = (d == 2) ? 16 : 10;
-    const float qmax = (float)((1 << bits) - 1);
-    float lo[3], sc[3];
+    const double qmax = (d == 2) ? 4294967295.0 : 2097151.0;
+    double lo[3], sc[3], ext = 0.0;
     for (int j = 0; j < d; ++j) {
-        lo[j] = unord_f32(box[j]);
-        const float hi = unord_f32(box[d + j]);
-        sc[j] = (hi > lo[j]) ? qmax / (hi - lo[j]) : 0.0f;
+        lo[j] = (double)unord_f32(box[j]);
+        ext = fmax(ext, (double)unord_f32(box[d + j]) - lo[j]);
     }
+    for (int j = 0; j < d; ++j) sc[j] = (ext > 0.0) ? qmax / ext : 0.0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) {
-        unsigned q[3] = {0u, 0u, 0u};
+        unsigned long long q[3] = {0ull, 0ull, 0ull};
         for (int j = 0; j < d; ++j) {
-            float t = (in[i * si + (int64_t)j * sj] - lo[j]) * sc[j];
-            t = fminf(fmaxf(t, 0.0f), qmax);
-            q[j] = (unsigned)t;
+            double t = ((double)in[i * si + (int64_t)j * sj] - lo[j]) * sc[j];
+            t = fmin(fmax(t, 0.0), qmax);
+            q[j] = (unsigned long long)t;
         }
-        keys[i] = (d == 2) ? (part1by1(q[0]) | (part1by1(q[1]) << 1))
-                           : (part1by2(q[0]) | (part1by2(q[1]) << 1) | (part1by2(q[2]) << 2));
+        keys[i] = (d == 2) ? (part1by1_64(q[0]) | (part1by1_64(q[1]) << 1))
+                           : (part1by2_64(q[0]) | (part1by2_64(q[1]) << 1) |
+                              (part1by2_64(q[2]) << 2));
         iota[i] = (int32_t)i;
     }
 }
@@ -581,9 +585,9 @@ __global__ void k_scatter_labels(const int32_t* __restrict__ lab_sorted,
 }
 
 // ---------------------------------------------------------------------------
-// k_assign_sorted (K <= 16, sorted points): exact per-chunk pruning.
+// k_assign_pruned (sorted points): exact per-chunk pruning, any K <= 1024.
 //
-// For the chunk's box B and the staged fp32 centroids c_k, lane k computes in
+// For the chunk's box B and the staged fp32 centroids c_k, a lane computes in
 // fp64  dmin2_k = min_{x in B} ||x - c_k||^2  and  dmax2_k = max_{x in B} ||x - c_k||^2.
 // With M = min_k dmax2_k, centroid b is excluded when
 //     dmin2_b > M (1 + 1e-5) + 2^-100.
@@ -595,15 +599,24 @@ __global__ void k_scatter_labels(const int32_t* __restrict__ lab_sorted,
 // candidates, scanned in ascending k with strict <, equals the full scan's
 // (value, lowest index).  If M could overflow fp32 (> 1e37) nothing is pruned.
 //
-// c == 1 (one candidate): every label is known; the distances are still
-// computed (form D) for the inertia, and the sums accumulate in registers.
-// c >= 2: candidate loop with a running strict-< argmin, per-lane private fp64
-// columns for kSortedSlots candidate slots at a time (more candidates: the
-// chunk is streamed again per group of slots).  A TMA stage carries 256
-// points; small columns keep ~13 warps resident per SM so enough bytes are in
-// flight to stream at HBM speed.
+// Small K (<= 16): lane k evaluates centroid k.  Large K: k_prune first keeps,
+// per super-chunk of kSuperChunks chunks, the candidates of the super box (the
+// same test); the chunk then refines that list (a centroid excluded for the
+// super box is excluded for every sub-box, and the chunk's M is attained inside
+// the super list, so the refined set is exact).  More than kPCap refined
+// candidates ("big" chunks, rare): the unrefined super list is used (a superset,
+// still exact).
+//
+// One candidate: every label is known; distances are still computed (form D)
+// for the inertia; sums accumulate in registers.  Several: running strict-<
+// argmin over the candidates; the winning slot of each point is cached in
+// shared memory; per-lane private fp64 columns hold kPSlots slots per pass and
+// passes > 0 re-read the chunk's points from L2.
+//
+// Output: a sparse row per chunk: [J, count, entries...], entry = {Sx, Sy, Sz,
+// (k, n) as int2 bits}; k_merge_sparse sums the rows of each group in fixed
+// chunk order.  No float atomics.
 // ---------------------------------------------------------------------------
-constexpr int kSortedSlots = KM_SORTED_SLOTS;          // per-lane column slots
 #ifndef KM_SORTED_UNIT_SUB
 #define KM_SORTED_UNIT_SUB 2
 #endif
@@ -615,27 +628,43 @@ constexpr int kSortedUnit = kUnitSub * kLaneTile;      // points per TMA stage
 constexpr int kSChunkPoints = KM_SORTED_CHUNK_TILES * kLaneTile;   // 1024
 constexpr int kSortedUnits = kSChunkPoints / kSortedUnit;          // 4 per chunk
 constexpr int kSortedStages = KM_SORTED_STAGES;
+constexpr int kSuperChunks = 64;                        // chunks per prune super-box
+constexpr int kRowHead = 2;                             // J, count
 
-template <int D>
-struct SortedSmem {
-    double2 A[kSortedSlots][32];
-    double2 B[kSortedSlots][32];
-    float ring[kSortedStages][D * kSortedUnit];
-    uint64_t bar[kSortedStages];
-    float4 cand[16];   // negated fp32 centroid of each candidate slot
-    int candk[16];     // centroid index of each slot (ascending)
+template <bool LARGE>
+struct PCfg {
+    static constexpr int kSlots = LARGE ? 8 : KM_SORTED_SLOTS;   // column slots per pass
+    static constexpr int kCap = LARGE ? 64 : 16;                 // refined candidates kept
 };
 
-template <int D, int MODE>
+template <int D, bool LARGE>
+struct PrunedSmem {
+    double2 A[PCfg<LARGE>::kSlots][32];
+    double2 B[PCfg<LARGE>::kSlots][32];
+    float ring[kSortedStages][D * kSortedUnit];
+    uint64_t bar[kSortedStages];
+    float4 cand[PCfg<LARGE>::kCap];     // negated fp32 centroid of each candidate slot
+    int candk[PCfg<LARGE>::kCap];       // centroid index of each slot (ascending)
+    unsigned short slot[kSChunkPoints]; // winning slot of each point (multi path)
+};
+
+// {k, n} in one double's bits: k in the low word, n in the high word
+__device__ __forceinline__ double pack_kn(int k, int n) {
+    return __hiloint2double(n, k);
+}
+
+template <int D, int MODE, bool LARGE>
 __global__ void __launch_bounds__(32)
-k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
+k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
                 const double* __restrict__ mu_buf, const DevState* __restrict__ st,
                 int mu_sel, int ignore_done, const float* __restrict__ cbox,
-                double* __restrict__ cpart, int32_t* __restrict__ labels,
+                const int* __restrict__ slist, const int* __restrict__ scount,
+                double* __restrict__ rows, int row_stride, int32_t* __restrict__ labels,
                 int* __restrict__ cand_count) {
     if (!ignore_done && st->done) return;
+    using C = PCfg<LARGE>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    SortedSmem<D>& S = *reinterpret_cast<SortedSmem<D>*>(smem_raw);
+    PrunedSmem<D, LARGE>& S = *reinterpret_cast<PrunedSmem<D, LARGE>*>(smem_raw);
     constexpr int kUnitFloats = D * kSortedUnit;
     constexpr unsigned kUnitBytes = kUnitFloats * 4;
     constexpr int SS = kSortedStages;
@@ -645,23 +674,18 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
     const int64_t rem = n - base;
     const int64_t nu64 = (rem + kSortedUnit - 1) / kSortedUnit;
     const int nunit = nu64 < kSortedUnits ? (int)nu64 : kSortedUnits;
+    const int npts = rem < kSChunkPoints ? (int)rem : kSChunkPoints;
     const float* src = X + (base >> 6) * (D * kWarpTile);
 
-    // The stream is a sequence of unit loads q = pass * nunit + u (passes > 0
-    // only for chunks with more than kSortedSlots candidates); unit q lives in
-    // stage q % SS, phase (q / SS) & 1.  npass is known once the candidates
-    // are, so the prologue issues only pass-0 units.
-    int total = nunit;              // units in the sequence (updated with npass)
-    unsigned issued = 0;            // lane 0: next q to issue
-    int pu = 0;                     // lane 0: unit index of q = issued (wraps per pass)
+    // point stream: units 0..nunit-1 through the TMA ring (unit q in stage q % SS)
+    unsigned issued = 0;   // lane 0
     auto issue_upto = [&](unsigned limit) {
         if (lane != 0) return;
-        while (issued < limit && (int)issued < total) {
+        while (issued < limit && (int)issued < nunit) {
             const int s = issued % SS;
             mbar_expect_tx(&S.bar[s], kUnitBytes);
-            bulk_g2s(S.ring[s], src + (int64_t)pu * kUnitFloats, kUnitBytes, &S.bar[s]);
+            bulk_g2s(S.ring[s], src + (int64_t)issued * kUnitFloats, kUnitBytes, &S.bar[s]);
             ++issued;
-            if (++pu == nunit) pu = 0;
         }
     };
     if (lane == 0) {
@@ -673,35 +697,92 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
 
     // ---- candidates of this chunk ----
     const double* mu = mu_buf + (size_t)((st->t - mu_sel) & 1) * K * D;
-    const bool is_k = lane < K;
     const float bx = (lane < 2 * D) ? __ldg(&cbox[(size_t)chunk * 2 * D + lane]) : 0.0f;
-    float c32[3] = {0.f, 0.f, 0.f};
-    if (is_k) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) c32[j] = __double2float_rn(__ldg(&mu[lane * D + j]));
-    }
-    double dmin2 = 0.0, dmax2 = 0.0;
+    double lo[3], hi[3];
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-        const double lo = (double)__shfl_sync(0xffffffffu, bx, j);
-        const double hi = (double)__shfl_sync(0xffffffffu, bx, D + j);
-        const double c = (double)c32[j];
-        const double dm = fmax(fmax(lo - c, c - hi), 0.0);
-        dmin2 += dm * dm;
-        const double dx = fmax(fabs(c - lo), fabs(hi - c));
-        dmax2 += dx * dx;
+        lo[j] = (double)__shfl_sync(0xffffffffu, bx, j);
+        hi[j] = (double)__shfl_sync(0xffffffffu, bx, D + j);
     }
-    double M = is_k ? dmax2 : (double)pos_inf();
+    auto stage_c = [&](int k, float (&c)[3]) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
-    const double thr = (M > 1e37) ? (double)pos_inf() : M * (1.0 + 1e-5) + 0x1p-100;
-    const bool cand = is_k && dmin2 <= thr;
-    const unsigned mask = __ballot_sync(0xffffffffu, cand);
-    const int nc = __popc(mask);
-    if (cand) {
-        const int slot = __popc(mask & ((1u << lane) - 1u));
-        S.cand[slot] = make_float4(-c32[0], -c32[1], D == 3 ? -c32[2] : 0.0f, 0.0f);
-        S.candk[slot] = lane;
+        for (int j = 0; j < D; ++j) c[j] = __double2float_rn(__ldg(&mu[k * D + j]));
+    };
+    auto bounds = [&](const float (&c)[3], double& dmin2, double& dmax2) {
+        dmin2 = 0.0;
+        dmax2 = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            const double cj = (double)c[j];
+            const double dm = fmax(fmax(lo[j] - cj, cj - hi[j]), 0.0);
+            dmin2 += dm * dm;
+            const double dx = fmax(fabs(cj - lo[j]), fabs(hi[j] - cj));
+            dmax2 += dx * dx;
+        }
+    };
+    auto warp_min = [&](double v) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+        return v;
+    };
+    auto threshold = [&](double M) {
+        return (M > 1e37) ? (double)pos_inf() : M * (1.0 + 1e-5) + 0x1p-100;
+    };
+    int nc = 0;          // refined candidates
+    bool big = false;    // candidates = the unrefined super list (global)
+    const int* glist = nullptr;
+    int gcount = 0;
+    if (!LARGE) {
+        float c[3] = {0.f, 0.f, 0.f};
+        double dmin2 = 0.0, dmax2 = 0.0;
+        const bool is_k = lane < K;
+        if (is_k) {
+            stage_c(lane, c);
+            bounds(c, dmin2, dmax2);
+        }
+        const double thr = threshold(warp_min(is_k ? dmax2 : (double)pos_inf()));
+        const bool cand = is_k && dmin2 <= thr;
+        const unsigned mask = __ballot_sync(0xffffffffu, cand);
+        nc = __popc(mask);
+        if (cand) {
+            const int sl = __popc(mask & ((1u << lane) - 1u));
+            S.cand[sl] = make_float4(-c[0], -c[1], D == 3 ? -c[2] : 0.0f, 0.0f);
+            S.candk[sl] = lane;
+        }
+    } else {
+        const int sup = chunk / kSuperChunks;
+        glist = slist + (size_t)sup * K;
+        gcount = __ldg(&scount[sup]);
+        double M = (double)pos_inf();
+        for (int i = lane; i < gcount; i += 32) {
+            float c[3];
+            stage_c(__ldg(&glist[i]), c);
+            double a, b;
+            bounds(c, a, b);
+            M = fmin(M, b);
+        }
+        const double thr = threshold(warp_min(M));
+        for (int i0 = 0; i0 < gcount; i0 += 32) {
+            const int i = i0 + lane;
+            float c[3] = {0.f, 0.f, 0.f};
+            int k = 0;
+            bool cand = false;
+            if (i < gcount) {
+                k = __ldg(&glist[i]);
+                stage_c(k, c);
+                double a, b;
+                bounds(c, a, b);
+                cand = a <= thr;
+            }
+            const unsigned mask = __ballot_sync(0xffffffffu, cand);
+            const int sl = nc + __popc(mask & ((1u << lane) - 1u));
+            if (cand && sl < C::kCap) {
+                S.cand[sl] = make_float4(-c[0], -c[1], D == 3 ? -c[2] : 0.0f, 0.0f);
+                S.candk[sl] = k;
+            }
+            nc += __popc(mask);
+        }
+        big = nc > C::kCap;
     }
     if (lane == 0 && cand_count) cand_count[chunk] = nc;
     __syncwarp();
@@ -709,8 +790,6 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
     struct Pts {
         float2 xa, ya, za, xb, yb, zb;
     };
-    // unit q: wait, read both 128-point sub-tiles, refill up to unit q+SS-1
-    // (its stage was used by unit q-1, consumed by now)
     auto fetch = [&](unsigned q, Pts (&P)[kUnitSub]) {
         const int s = q % SS;
         mbar_wait(&S.bar[s], (q / SS) & 1u);
@@ -730,6 +809,20 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
         __syncwarp();
         issue_upto(q + SS);
     };
+    // the same points from global memory (passes > 0; L2-resident by then)
+    auto reload = [&](int u, Pts (&P)[kUnitSub]) {
+#pragma unroll
+        for (int h = 0; h < kUnitSub; ++h) {
+            const int64_t pa = base + (int64_t)u * kSortedUnit + h * kLaneTile + 2 * lane;
+            P[h].xa = ld_stream2(tile_coord<D>(X, pa, 0));
+            P[h].ya = ld_stream2(tile_coord<D>(X, pa, 1));
+            P[h].za = (D == 3) ? ld_stream2(tile_coord<D>(X, pa, 2)) : make_float2(0.f, 0.f);
+            P[h].xb = ld_stream2(tile_coord<D>(X, pa + kWarpTile, 0));
+            P[h].yb = ld_stream2(tile_coord<D>(X, pa + kWarpTile, 1));
+            P[h].zb = (D == 3) ? ld_stream2(tile_coord<D>(X, pa + kWarpTile, 2))
+                               : make_float2(0.f, 0.f);
+        }
+    };
     auto dist2 = [&](float2 x, float2 y, float2 z, const float4& cc) {
         float2 e0 = __fadd2_rn(x, make_float2(cc.x, cc.x));
         float2 e1 = __fadd2_rn(y, make_float2(cc.y, cc.y));
@@ -741,14 +834,24 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
         }
         return sq;
     };
-    double* row = cpart + (size_t)chunk * kRowDoubles;
+    // candidate j as a negated fp32 centroid and its index
+    auto cand_at = [&](int j, float4& cc) -> int {
+        if (!LARGE || !big) {
+            cc = S.cand[j];
+            return S.candk[j];
+        }
+        const int k = __ldg(&glist[j]);
+        float c[3];
+        stage_c(k, c);
+        cc = make_float4(-c[0], -c[1], D == 3 ? -c[2] : 0.0f, 0.0f);
+        return k;
+    };
+    double* row = rows + (size_t)chunk * row_stride;
 
     if (nc == 1) {
-        // ---- one candidate: labels known, sums in registers (two chains) ----
-        const float4 cc = S.cand[0];
-        const int k0 = S.candk[0];
-        // four independent accumulation chains (one per point position of a
-        // sub-tile), combined in a fixed order at the end
+        // ---- one candidate: labels known, sums in registers (four chains) ----
+        float4 cc;
+        const int k0 = cand_at(0, cc);
         double sx[4] = {0.0, 0.0, 0.0, 0.0}, sy[4] = {0.0, 0.0, 0.0, 0.0};
         double sz[4] = {0.0, 0.0, 0.0, 0.0}, Jc[4] = {0.0, 0.0, 0.0, 0.0};
         auto add4 = [&](const Pts& Q, float2 da, float2 db, int m) {
@@ -773,12 +876,11 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
                     *reinterpret_cast<int2*>(labels + pb) = make_int2(k0, k0);
                 }
                 if (MODE & kModeReduce) {
-                    if ((int64_t)u * kSortedUnit + (h + 1) * kLaneTile <= rem) {
+                    if ((int64_t)u * kSortedUnit + (h + 1) * kLaneTile <= rem)
                         add4(P[h], da, db, 15);
-                    } else {
+                    else
                         add4(P[h], da, db, (pa < n ? 1 : 0) | (pa + 1 < n ? 2 : 0) |
                                                (pb < n ? 4 : 0) | (pb + 1 < n ? 8 : 0));
-                    }
                 }
             }
         }
@@ -794,26 +896,17 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
             szt += __shfl_xor_sync(0xffffffffu, szt, o);
             J += __shfl_xor_sync(0xffffffffu, J, o);
         }
-        const int kk = lane >> 1;
-        double2 out = make_double2(0.0, 0.0);
-        if (kk == k0) {
-            const double cnt = (double)(rem < kSChunkPoints ? rem : kSChunkPoints);
-            out = (lane & 1) ? make_double2(szt, cnt) : make_double2(sxt, syt);
+        if (lane == 0) {
+            row[0] = J;
+            row[1] = 1.0;
+            reinterpret_cast<double2*>(row + kRowHead)[0] = make_double2(sxt, syt);
+            reinterpret_cast<double2*>(row + kRowHead)[1] = make_double2(szt, pack_kn(k0, npts));
         }
-        reinterpret_cast<double2*>(row)[lane] = out;
-        if (lane == 0) row[64] = J;
         return;
     }
 
-    // ---- several candidates: exact running argmin over the candidates (ascending
-    // k, strict <); per-lane private fp64 columns for kSortedSlots slots at a
-    // time -- a chunk with more candidates streams its points once per group of
-    // kSortedSlots slots (passes), each pass accumulating only its slots ----
-    // labels-only launches need a single pass (no columns)
-    const int npass = (MODE & kModeReduce) ? (nc + kSortedSlots - 1) / kSortedSlots : 1;
-    total = npass * nunit;
-    issue_upto(SS);   // pass > 0 units may now be issued if the ring has room
-    if (MODE & kModeReduce) reinterpret_cast<double2*>(row)[lane] = make_double2(0.0, 0.0);
+    // ---- several candidates ----
+    const int ncand = big ? gcount : nc;   // slots = indices into the candidate list
     double J = 0.0;
     auto accumulate = [&](int l, float px, float py, float pz) {
         double2 a = S.A[l][lane], b = S.B[l][lane];
@@ -826,12 +919,13 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
         S.A[l][lane] = a;
         S.B[l][lane] = b;
     };
+    const int npass = (MODE & kModeReduce) ? (ncand + C::kSlots - 1) / C::kSlots : 1;
 #pragma unroll 1
     for (int pass = 0; pass < npass; ++pass) {
-        const int s_lo = pass * kSortedSlots;
+        const int s_lo = pass * C::kSlots;
         if (MODE & kModeReduce) {
 #pragma unroll
-            for (int k = 0; k < kSortedSlots; ++k) {
+            for (int k = 0; k < C::kSlots; ++k) {
                 S.A[k][lane] = make_double2(0.0, 0.0);
                 S.B[k][lane] = make_double2(0.0, 0.0);
             }
@@ -840,55 +934,68 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
 #pragma unroll 1
         for (int u = 0; u < nunit; ++u) {
             Pts P[kUnitSub];
-            fetch(pass * nunit + u, P);
+            if (pass == 0) fetch(u, P);
+            else reload(u, P);
 #pragma unroll
             for (int h = 0; h < kUnitSub; ++h) {
-                float2 ba = dist2(P[h].xa, P[h].ya, P[h].za, S.cand[0]);
-                float2 bb = dist2(P[h].xb, P[h].yb, P[h].zb, S.cand[0]);
-                int s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+                const int off = u * kSortedUnit + h * kLaneTile + 2 * lane;   // in-chunk index
+                const int64_t pa = base + off, pb = pa + kWarpTile;
+                int s0, s1, s2, s3;
+                float2 ba, bb;
+                if (pass == 0) {
+                    float4 cc;
+                    cand_at(0, cc);
+                    ba = dist2(P[h].xa, P[h].ya, P[h].za, cc);
+                    bb = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
+                    s0 = s1 = s2 = s3 = 0;
 #pragma unroll 1
-                for (int j = 1; j < nc; ++j) {
-                    const float4 cc = S.cand[j];
-                    const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
-                    const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
-                    if (da.x < ba.x) { ba.x = da.x; s0 = j; }
-                    if (da.y < ba.y) { ba.y = da.y; s1 = j; }
-                    if (db.x < bb.x) { bb.x = db.x; s2 = j; }
-                    if (db.y < bb.y) { bb.y = db.y; s3 = j; }
-                }
-                const int64_t pa = base + (int64_t)u * kSortedUnit + h * kLaneTile + 2 * lane;
-                const int64_t pb = pa + kWarpTile;
-                if ((MODE & kModeLabels) && pass == 0) {
-                    *reinterpret_cast<int2*>(labels + pa) = make_int2(S.candk[s0], S.candk[s1]);
-                    *reinterpret_cast<int2*>(labels + pb) = make_int2(S.candk[s2], S.candk[s3]);
+                    for (int j = 1; j < ncand; ++j) {
+                        cand_at(j, cc);
+                        const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
+                        const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
+                        if (da.x < ba.x) { ba.x = da.x; s0 = j; }
+                        if (da.y < ba.y) { ba.y = da.y; s1 = j; }
+                        if (db.x < bb.x) { bb.x = db.x; s2 = j; }
+                        if (db.y < bb.y) { bb.y = db.y; s3 = j; }
+                    }
+                    if (npass > 1) {
+                        S.slot[off] = (unsigned short)s0;
+                        S.slot[off + 1] = (unsigned short)s1;
+                        S.slot[off + kWarpTile] = (unsigned short)s2;
+                        S.slot[off + kWarpTile + 1] = (unsigned short)s3;
+                    }
+                    if (MODE & kModeLabels) {
+                        float4 t;
+                        *reinterpret_cast<int2*>(labels + pa) = make_int2(cand_at(s0, t), cand_at(s1, t));
+                        *reinterpret_cast<int2*>(labels + pb) = make_int2(cand_at(s2, t), cand_at(s3, t));
+                    }
+                    if (MODE & kModeReduce) {
+                        if (pa < n) J += (double)ba.x;
+                        if (pa + 1 < n) J += (double)ba.y;
+                        if (pb < n) J += (double)bb.x;
+                        if (pb + 1 < n) J += (double)bb.y;
+                    }
+                } else {
+                    s0 = S.slot[off];
+                    s1 = S.slot[off + 1];
+                    s2 = S.slot[off + kWarpTile];
+                    s3 = S.slot[off + kWarpTile + 1];
                 }
                 if (MODE & kModeReduce) {
-                    const unsigned w = kSortedSlots;
-                    if (pa < n) {
-                        if ((unsigned)(s0 - s_lo) < w) accumulate(s0 - s_lo, P[h].xa.x, P[h].ya.x, P[h].za.x);
-                        if (pass == 0) J += (double)ba.x;
-                    }
-                    if (pa + 1 < n) {
-                        if ((unsigned)(s1 - s_lo) < w) accumulate(s1 - s_lo, P[h].xa.y, P[h].ya.y, P[h].za.y);
-                        if (pass == 0) J += (double)ba.y;
-                    }
-                    if (pb < n) {
-                        if ((unsigned)(s2 - s_lo) < w) accumulate(s2 - s_lo, P[h].xb.x, P[h].yb.x, P[h].zb.x);
-                        if (pass == 0) J += (double)bb.x;
-                    }
-                    if (pb + 1 < n) {
-                        if ((unsigned)(s3 - s_lo) < w) accumulate(s3 - s_lo, P[h].xb.y, P[h].yb.y, P[h].zb.y);
-                        if (pass == 0) J += (double)bb.y;
-                    }
+                    const unsigned w = C::kSlots;
+                    if (pa < n && (unsigned)(s0 - s_lo) < w) accumulate(s0 - s_lo, P[h].xa.x, P[h].ya.x, P[h].za.x);
+                    if (pa + 1 < n && (unsigned)(s1 - s_lo) < w) accumulate(s1 - s_lo, P[h].xa.y, P[h].ya.y, P[h].za.y);
+                    if (pb < n && (unsigned)(s2 - s_lo) < w) accumulate(s2 - s_lo, P[h].xb.x, P[h].yb.x, P[h].zb.x);
+                    if (pb + 1 < n && (unsigned)(s3 - s_lo) < w) accumulate(s3 - s_lo, P[h].xb.y, P[h].yb.y, P[h].zb.y);
                 }
             }
         }
-        if (!(MODE & kModeReduce)) return;   // labels-only: one pass suffices
+        if (!(MODE & kModeReduce)) return;   // labels only: one pass
         __syncwarp();
-        // lane L (< 2 * kSortedSlots) sums slot s_lo + (L >> 1), half (L & 1),
-        // over the 32 lanes in a rotated (bank-conflict-free) order
+        // lane L (< 2 kSlots) sums slot s_lo + (L >> 1), half (L & 1), over the
+        // 32 lanes in a rotated (bank-conflict-free) order -> row entry of the slot
         const int sl = lane >> 1;
-        if (sl < kSortedSlots && s_lo + sl < nc) {
+        if (sl < C::kSlots && s_lo + sl < ncand) {
             const double2* col = (lane & 1) ? &S.B[0][0] : &S.A[0][0];
             double v0 = 0.0, v1 = 0.0;
             long long cnt = 0;
@@ -900,14 +1007,200 @@ k_assign_sorted(const float* __restrict__ X, int64_t n, int K,
                 if (lane & 1) cnt += reinterpret_cast<const int2*>(&w2.y)->x;
                 else v1 += w2.y;
             }
-            const int k = S.candk[s_lo + sl];
-            reinterpret_cast<double2*>(row)[2 * k + (lane & 1)] =
-                (lane & 1) ? make_double2(v0, (double)cnt) : make_double2(v0, v1);
+            float4 t;
+            const int k = cand_at(s_lo + sl, t);
+            reinterpret_cast<double2*>(row + kRowHead)[2 * (s_lo + sl) + (lane & 1)] =
+                (lane & 1) ? make_double2(v0, pack_kn(k, (int)cnt)) : make_double2(v0, v1);
         }
+        __syncwarp();
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
-    if (lane == 0) row[64] = J;
+    if (lane == 0) {
+        row[0] = J;
+        row[1] = (double)ncand;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_prune (large K): candidates of each super box (kSuperChunks chunks) by the
+// same exclusion test, listed in ascending k.
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256)
+k_prune(const double* __restrict__ mu_buf, const DevState* __restrict__ st, int mu_sel,
+        int ignore_done, int K, const float* __restrict__ sbox, int* __restrict__ slist,
+        int* __restrict__ scount) {
+    if (!ignore_done && st->done) return;
+    __shared__ double wmin[8];
+    __shared__ int wcnt[8];
+    __shared__ int base_s;
+    const int s = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const double* mu = mu_buf + (size_t)((st->t - mu_sel) & 1) * K * D;
+    double lo[3], hi[3];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        lo[j] = (double)sbox[(size_t)s * 2 * D + j];
+        hi[j] = (double)sbox[(size_t)s * 2 * D + D + j];
+    }
+    auto bounds = [&](int k, double& dmin2, double& dmax2) {
+        dmin2 = 0.0;
+        dmax2 = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            const double cj = (double)__double2float_rn(mu[k * D + j]);
+            const double dm = fmax(fmax(lo[j] - cj, cj - hi[j]), 0.0);
+            dmin2 += dm * dm;
+            const double dx = fmax(fabs(cj - lo[j]), fabs(hi[j] - cj));
+            dmax2 += dx * dx;
+        }
+    };
+    double M = (double)pos_inf();
+    for (int k = tid; k < K; k += blockDim.x) {
+        double a, b;
+        bounds(k, a, b);
+        M = fmin(M, b);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
+    if (lane == 0) wmin[warp] = M;
+    if (tid == 0) base_s = 0;
+    __syncthreads();
+    M = wmin[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) M = fmin(M, wmin[w]);
+    const double thr = (M > 1e37) ? (double)pos_inf() : M * (1.0 + 1e-5) + 0x1p-100;
+    for (int k0 = 0; k0 < K; k0 += blockDim.x) {
+        const int k = k0 + tid;
+        bool cand = false;
+        if (k < K) {
+            double a, b;
+            bounds(k, a, b);
+            cand = a <= thr;
+        }
+        const unsigned mask = __ballot_sync(0xffffffffu, cand);
+        if (lane == 0) wcnt[warp] = __popc(mask);
+        __syncthreads();
+        int off = base_s;
+        for (int w = 0; w < warp; ++w) off += wcnt[w];
+        if (cand) slist[(size_t)s * K + off + __popc(mask & ((1u << lane) - 1u))] = k;
+        __syncthreads();
+        if (tid == 0) {
+            int t = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += wcnt[w];
+            base_s += t;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) scount[s] = base_s;
+}
+
+// super boxes from the chunk boxes (create time)
+__global__ void k_super_bbox(const float* __restrict__ cbox, int n_chunks, int d,
+                             float* __restrict__ sbox) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    const int c0 = s * kSuperChunks;
+    if (c0 >= n_chunks) return;
+    const int c1 = min(n_chunks, c0 + kSuperChunks);
+    for (int j = 0; j < d; ++j) {
+        float lo = pos_inf(), hi = -pos_inf();
+        for (int c = c0; c < c1; ++c) {
+            lo = fminf(lo, cbox[(size_t)c * 2 * d + j]);
+            hi = fmaxf(hi, cbox[(size_t)c * 2 * d + d + j]);
+        }
+        sbox[(size_t)s * 2 * d + j] = lo;
+        sbox[(size_t)s * 2 * d + d + j] = hi;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_merge_sparse: group g sums the sparse rows of chunks [64g, 64g + 64).
+// The headers and entries are staged in shared memory with independent
+// (parallel) loads; then each thread owns clusters k = tid, tid + 256, ... and
+// scans the staged entries in (chunk, entry) order, adding those of its k --
+// every sum is taken in ascending chunk order, with no atomics and no
+// per-chunk barrier.  Writes the group's column gpart[e][g] for k_merge.
+// ---------------------------------------------------------------------------
+constexpr int kMergeBatch = 512;   // entries staged per batch
+
+template <int D>
+__global__ void __launch_bounds__(256)
+k_merge_sparse(const double* __restrict__ rows, int row_stride, int n_chunks, int K,
+               double* __restrict__ gpart, int n_groups, const DevState* __restrict__ st,
+               int ignore_done) {
+    if (!ignore_done && st->done) return;
+    __shared__ double hj[kGroupChunks];
+    __shared__ int cnt[kGroupChunks];
+    __shared__ int off[kGroupChunks + 1];
+    __shared__ double2 E[2 * kMergeBatch];   // entry = {Sx, Sy}, {Sz, kn}
+    const int g = blockIdx.x, tid = threadIdx.x;
+    const int c0 = g * kGroupChunks;
+    const int nch = min(n_chunks, c0 + kGroupChunks) - c0;
+    if (tid < nch) {
+        const double* row = rows + (size_t)(c0 + tid) * row_stride;
+        hj[tid] = row[0];
+        cnt[tid] = (int)row[1];
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int o = 0;
+        for (int c = 0; c < nch; ++c) {
+            off[c] = o;
+            o += cnt[c];
+        }
+        off[nch] = o;
+    }
+    __syncthreads();
+    const int total = off[nch];
+    // owned clusters: k = tid + 256 i (K <= 1024 -> at most 4)
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int b0 = 0; b0 < total; b0 += kMergeBatch) {
+        const int bn = min(kMergeBatch, total - b0);
+        // stage entries [b0, b0 + bn): 2 double2 per entry
+        for (int q = tid; q < 2 * bn; q += blockDim.x) {
+            const int idx = b0 + (q >> 1);
+            int c = 0;
+            while (off[c + 1] <= idx) ++c;   // chunk of entry idx (nch <= 64)
+            const double* row = rows + (size_t)(c0 + c) * row_stride + kRowHead;
+            E[q] = reinterpret_cast<const double2*>(row)[2 * (idx - off[c]) + (q & 1)];
+        }
+        __syncthreads();
+        for (int e = 0; e < bn; ++e) {
+            const double2 v1 = E[2 * e + 1];
+            const int2 kn = *reinterpret_cast<const int2*>(&v1.y);   // {k, n}
+            if ((kn.x & 255) == tid && kn.x < K) {
+                const double2 v0 = E[2 * e];
+                const int i = kn.x >> 8;
+#pragma unroll
+                for (int ii = 0; ii < 4; ++ii) {
+                    if (ii == i) {
+                        acc[ii][0] += v0.x;
+                        acc[ii][1] += v0.y;
+                        acc[ii][2] += v1.x;
+                        acc[ii][3] += (double)kn.y;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int k = tid + 256 * i;
+        if (k < K) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) gpart[(size_t)(k * D + j) * n_groups + g] = acc[i][j];
+            gpart[(size_t)(K * D + k) * n_groups + g] = acc[i][3];
+        }
+    }
+    if (tid == 0) {
+        double J = 0.0;
+        for (int c = 0; c < nch; ++c) J += hj[c];
+        gpart[(size_t)(K * D + K) * n_groups + g] = J;
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -69,7 +69,13 @@ struct kmeans_ctx {
     int G = 0, tpb = 0, smem = 0, path = 0;   // G = columns of part (blocks or groups)
     int n_chunks = 0;
     int chunk_points = 0;         // points per chunk row (sorted / unsorted differ)
-    double* cpart = nullptr;      // n_chunks x kRowDoubles chunk partials (path 0)
+    double* cpart = nullptr;      // n_chunks x row_stride chunk rows (path 0 / sorted)
+    int row_stride = 0;           // doubles per chunk row
+    int n_super = 0;              // prune super-boxes (sorted, large K)
+    float* sbox = nullptr;        // super-box bounding boxes
+    int* slist = nullptr;         // n_super x K candidate lists
+    int* scount = nullptr;        // candidates per super-box
+    int merge_smem = 0;           // k_merge_sparse dynamic shared memory (none)
     bool sorted = false;          // points held in Morton order (path 0 default)
     int32_t* perm = nullptr;      // sorted position -> caller's index (sorted only)
     int32_t* invperm = nullptr;   // caller's index -> sorted position (sorted only)
@@ -86,8 +92,11 @@ struct kmeans_ctx {
 
 namespace {
 
-// kernels of this library per iteration: assign (+ merge_rows on path 0), merge, update
-int kernels_per_iter(const kmeans_ctx* ctx) { return ctx->path == 0 ? 4 : 3; }
+// kernels of this library per iteration: [prune], assign, [row merge], merge, update
+int kernels_per_iter(const kmeans_ctx* ctx) {
+    if (ctx->sorted) return ctx->path == 1 ? 5 : 4;
+    return ctx->path == 0 ? 4 : 3;
+}
 
 kmeans_status cuda_fail(kmeans_ctx* c, cudaError_t e, const char* what) {
     set_error("%s: %s", what, cudaGetErrorString(e));
@@ -151,18 +160,29 @@ ChunkFn pick_chunk(int d, int K, int mode) {
     return pick_chunk_kp<3, 3>(K);
 }
 
-using SortedFn = void (*)(const float*, int64_t, int, const double*, const DevState*, int, int,
-                          const float*, double*, int32_t*, int*);
+using PrunedFn = void (*)(const float*, int64_t, int, const double*, const DevState*, int, int,
+                          const float*, const int*, const int*, double*, int, int32_t*, int*);
 
-SortedFn pick_sorted(int d, int mode) {
+template <bool LARGE>
+PrunedFn pick_pruned_l(int d, int mode) {
     if (d == 2) {
-        if (mode == 1) return km::k_assign_sorted<2, 1>;
-        if (mode == 2) return km::k_assign_sorted<2, 2>;
-        return km::k_assign_sorted<2, 3>;
+        if (mode == 1) return km::k_assign_pruned<2, 1, LARGE>;
+        if (mode == 2) return km::k_assign_pruned<2, 2, LARGE>;
+        return km::k_assign_pruned<2, 3, LARGE>;
     }
-    if (mode == 1) return km::k_assign_sorted<3, 1>;
-    if (mode == 2) return km::k_assign_sorted<3, 2>;
-    return km::k_assign_sorted<3, 3>;
+    if (mode == 1) return km::k_assign_pruned<3, 1, LARGE>;
+    if (mode == 2) return km::k_assign_pruned<3, 2, LARGE>;
+    return km::k_assign_pruned<3, 3, LARGE>;
+}
+
+PrunedFn pick_pruned(int d, int K, int mode) {
+    return K <= 16 ? pick_pruned_l<false>(d, mode) : pick_pruned_l<true>(d, mode);
+}
+
+int pruned_smem(int d, int K) {
+    if (K <= 16)
+        return d == 2 ? sizeof(km::PrunedSmem<2, false>) : sizeof(km::PrunedSmem<3, false>);
+    return d == 2 ? sizeof(km::PrunedSmem<2, true>) : sizeof(km::PrunedSmem<3, true>);
 }
 
 int chunk_smem(int d, int K) {
@@ -196,26 +216,31 @@ kmeans_status configure(kmeans_ctx* ctx) {
     const int sms = prop.multiProcessorCount;
     const int maxSmem = (int)prop.sharedMemPerBlockOptin;
     ctx->nE = ctx->K * ctx->d + ctx->K + 1;
-    if (ctx->K <= 16) {
-        ctx->path = 0;
+    ctx->path = ctx->K <= 16 ? 0 : 1;
+    if (ctx->sorted) {
+        // Morton-sorted shard, per-chunk pruning (any K), sparse chunk rows
         ctx->tpb = 32;
-        if (ctx->sorted) {
-            ctx->smem = ctx->d == 2 ? sizeof(km::SortedSmem<2>) : sizeof(km::SortedSmem<3>);
-            for (int mode = 1; mode <= 3; ++mode)
-                CK(cudaFuncSetAttribute((const void*)pick_sorted(ctx->d, mode),
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
-        } else {
-            ctx->smem = chunk_smem(ctx->d, ctx->K);
-            for (int mode = 1; mode <= 3; ++mode)
-                CK(cudaFuncSetAttribute((const void*)pick_chunk(ctx->d, ctx->K, mode),
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
-        }
-        ctx->chunk_points = ctx->sorted ? km::kSChunkPoints : km::kChunkPoints;
+        ctx->smem = pruned_smem(ctx->d, ctx->K);
+        for (int mode = 1; mode <= 3; ++mode)
+            CK(cudaFuncSetAttribute((const void*)pick_pruned(ctx->d, ctx->K, mode),
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
+        ctx->chunk_points = km::kSChunkPoints;
         ctx->n_chunks = (int)((ctx->N + ctx->chunk_points - 1) / ctx->chunk_points);
+        ctx->row_stride = km::kRowHead + 4 * (ctx->K <= 16 ? 16 : ctx->K);
+        ctx->G = (ctx->n_chunks + km::kGroupChunks - 1) / km::kGroupChunks;  // groups
+        ctx->n_super = (ctx->n_chunks + km::kSuperChunks - 1) / km::kSuperChunks;
+        ctx->merge_smem = 0;
+    } else if (ctx->path == 0) {
+        ctx->tpb = 32;
+        ctx->smem = chunk_smem(ctx->d, ctx->K);
+        for (int mode = 1; mode <= 3; ++mode)
+            CK(cudaFuncSetAttribute((const void*)pick_chunk(ctx->d, ctx->K, mode),
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
+        ctx->chunk_points = km::kChunkPoints;
+        ctx->n_chunks = (int)((ctx->N + ctx->chunk_points - 1) / ctx->chunk_points);
+        ctx->row_stride = km::kRowDoubles;
         ctx->G = (ctx->n_chunks + km::kGroupChunks - 1) / km::kGroupChunks;  // groups
     } else {
-        ctx->path = 1;
-        ctx->sorted = false;   // the large-K kernel streams points in the caller's order
         int tpb = km::kLargeTPBMax;
         while (tpb > 64 && large_smem(ctx->d, ctx->K, tpb) > maxSmem - 4096) tpb -= 32;
         ctx->tpb = tpb;
@@ -240,20 +265,42 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
     if ((mode & km::kModeLabels) && !ctx->labels) {
         CK(cudaMalloc(&ctx->labels, sizeof(int32_t) * ctx->ldx));
     }
-    if (ctx->path == 0) {
-        if (ctx->sorted) {
-            if ((mode & km::kModeLabels) && !ctx->labels_sorted)
-                CK(cudaMalloc(&ctx->labels_sorted, sizeof(int32_t) * ctx->ldx));
-            SortedFn f = pick_sorted(ctx->d, mode);
-            f<<<ctx->n_chunks, 32, ctx->smem, ctx->stream>>>(
-                ctx->X, ctx->N, ctx->K, ctx->mu, ctx->st, mu_sel, ignore_done, ctx->cbox,
-                ctx->cpart, ctx->labels_sorted, ctx->cand_count);
-        } else {
-            ChunkFn f = pick_chunk(ctx->d, ctx->K, mode);
-            f<<<ctx->n_chunks, 32, ctx->smem, ctx->stream>>>(ctx->X, ctx->N, ctx->K, ctx->mu,
-                                                             ctx->st, mu_sel, ignore_done,
-                                                             ctx->cpart, ctx->labels);
+    if (ctx->sorted) {
+        if ((mode & km::kModeLabels) && !ctx->labels_sorted)
+            CK(cudaMalloc(&ctx->labels_sorted, sizeof(int32_t) * ctx->ldx));
+        if (ctx->path == 1) {
+            // super-box candidate lists (large K)
+            if (ctx->d == 2)
+                km::k_prune<2><<<ctx->n_super, 256, 0, ctx->stream>>>(
+                    ctx->mu, ctx->st, mu_sel, ignore_done, ctx->K, ctx->sbox, ctx->slist,
+                    ctx->scount);
+            else
+                km::k_prune<3><<<ctx->n_super, 256, 0, ctx->stream>>>(
+                    ctx->mu, ctx->st, mu_sel, ignore_done, ctx->K, ctx->sbox, ctx->slist,
+                    ctx->scount);
+            ctx->launches += 1;
         }
+        PrunedFn f = pick_pruned(ctx->d, ctx->K, mode);
+        f<<<ctx->n_chunks, 32, ctx->smem, ctx->stream>>>(
+            ctx->X, ctx->N, ctx->K, ctx->mu, ctx->st, mu_sel, ignore_done, ctx->cbox, ctx->slist,
+            ctx->scount, ctx->cpart, ctx->row_stride, ctx->labels_sorted, ctx->cand_count);
+        if (mode & km::kModeReduce) {
+            // sparse chunk rows -> group columns of part (fixed ascending order)
+            if (ctx->d == 2)
+                km::k_merge_sparse<2><<<ctx->G, 256, ctx->merge_smem, ctx->stream>>>(
+                    ctx->cpart, ctx->row_stride, ctx->n_chunks, ctx->K, ctx->part, ctx->G,
+                    ctx->st, ignore_done);
+            else
+                km::k_merge_sparse<3><<<ctx->G, 256, ctx->merge_smem, ctx->stream>>>(
+                    ctx->cpart, ctx->row_stride, ctx->n_chunks, ctx->K, ctx->part, ctx->G,
+                    ctx->st, ignore_done);
+            ctx->launches += 1;
+        }
+    } else if (ctx->path == 0) {
+        ChunkFn f = pick_chunk(ctx->d, ctx->K, mode);
+        f<<<ctx->n_chunks, 32, ctx->smem, ctx->stream>>>(ctx->X, ctx->N, ctx->K, ctx->mu, ctx->st,
+                                                         mu_sel, ignore_done, ctx->cpart,
+                                                         ctx->labels);
         if (mode & km::kModeReduce) {
             // chunk rows -> group columns of part (fixed ascending order)
             if (ctx->d == 2)
@@ -435,7 +482,7 @@ kmeans_status sort_points(kmeans_ctx* ctx, const float* src, int64_t si, int64_t
     const int64_t N = ctx->N;
     const int d = ctx->d;
     unsigned* box = nullptr;
-    unsigned *keys = nullptr, *keys2 = nullptr;
+    unsigned long long *keys = nullptr, *keys2 = nullptr;
     int32_t* iota = nullptr;
     void* tmp = nullptr;
     size_t tmp_bytes = 0;
@@ -452,8 +499,8 @@ kmeans_status sort_points(kmeans_ctx* ctx, const float* src, int64_t si, int64_t
         cudaMalloc(&ctx->cbox, sizeof(float) * 2 * d * (size_t)ctx->n_chunks) != cudaSuccess ||
         cudaMalloc(&ctx->cand_count, sizeof(int) * (size_t)ctx->n_chunks) != cudaSuccess ||
         cudaMalloc(&box, sizeof(unsigned) * 6) != cudaSuccess ||
-        cudaMalloc(&keys, sizeof(unsigned) * N) != cudaSuccess ||
-        cudaMalloc(&keys2, sizeof(unsigned) * N) != cudaSuccess ||
+        cudaMalloc(&keys, sizeof(unsigned long long) * N) != cudaSuccess ||
+        cudaMalloc(&keys2, sizeof(unsigned long long) * N) != cudaSuccess ||
         cudaMalloc(&iota, sizeof(int32_t) * N) != cudaSuccess) {
         cudaGetLastError();
         cleanup();
@@ -473,11 +520,11 @@ kmeans_status sort_points(kmeans_ctx* ctx, const float* src, int64_t si, int64_t
         km::k_morton<<<blocks, 256, 0, ctx->stream>>>(src, N, d, si, sj, box, keys, iota);
         ctx->launches += 2;
         e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, iota, ctx->perm, N, 0,
-                                            32, ctx->stream);
+                                            64, ctx->stream);
     }
     if (e == cudaSuccess) e = cudaMalloc(&tmp, tmp_bytes);
     if (e == cudaSuccess)
-        e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, iota, ctx->perm, N, 0, 32,
+        e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, iota, ctx->perm, N, 0, 64,
                                             ctx->stream);
     if (e == cudaSuccess) {
         const int gb = (int)std::min<int64_t>((ctx->ldx + 255) / 256, 148 * 8);
@@ -487,6 +534,11 @@ kmeans_status sort_points(kmeans_ctx* ctx, const float* src, int64_t si, int64_t
         km::k_chunk_bbox<<<cb, 256, 0, ctx->stream>>>(ctx->X, N, d, ctx->chunk_points,
                                                       ctx->n_chunks, ctx->cbox);
         ctx->launches += 2;
+        if (ctx->sbox) {
+            km::k_super_bbox<<<(ctx->n_super + 127) / 128, 128, 0, ctx->stream>>>(
+                ctx->cbox, ctx->n_chunks, d, ctx->sbox);
+            ctx->launches += 1;
+        }
         e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);  // before freeing temporaries
@@ -547,6 +599,9 @@ void kmeans_destroy(kmeans_ctx* ctx) {
         cudaFree(ctx->idx_dev);
         cudaFree(ctx->flag);
         cudaFree(ctx->cpart);
+        cudaFree(ctx->sbox);
+        cudaFree(ctx->slist);
+        cudaFree(ctx->scount);
         cudaFree(ctx->perm);
         cudaFree(ctx->invperm);
         cudaFree(ctx->cbox);
@@ -635,9 +690,13 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
         cudaMalloc(&ctx->red, sizeof(double) * ctx->nE) != cudaSuccess ||
         cudaMalloc(&ctx->st, sizeof(DevState)) != cudaSuccess ||
         cudaMalloc(&ctx->idx_dev, sizeof(int64_t) * K) != cudaSuccess ||
-        (ctx->path == 0 &&
-         cudaMalloc(&ctx->cpart, sizeof(double) * km::kRowDoubles * (size_t)ctx->n_chunks) !=
+        ((ctx->path == 0 || ctx->sorted) &&
+         cudaMalloc(&ctx->cpart, sizeof(double) * ctx->row_stride * (size_t)ctx->n_chunks) !=
              cudaSuccess) ||
+        (ctx->sorted && ctx->path == 1 &&
+         (cudaMalloc(&ctx->sbox, sizeof(float) * 2 * d * (size_t)ctx->n_super) != cudaSuccess ||
+          cudaMalloc(&ctx->slist, sizeof(int) * (size_t)K * ctx->n_super) != cudaSuccess ||
+          cudaMalloc(&ctx->scount, sizeof(int) * (size_t)ctx->n_super) != cudaSuccess)) ||
         cudaMalloc(&ctx->flag, sizeof(int)) != cudaSuccess) {
         cudaGetLastError();
         set_error("device allocation failed (%zu bytes of points)", bytesX);
@@ -646,8 +705,8 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
     if ((s = ensure_trace(ctx, 64)) != KMEANS_OK) return fail(s);
     if (cudaMemsetAsync(ctx->mu, 0, sizeof(double) * 2 * Kpad * d, ctx->stream) != cudaSuccess ||
         cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream) != cudaSuccess ||
-        (ctx->path == 0 &&
-         cudaMemsetAsync(ctx->cpart, 0, sizeof(double) * km::kRowDoubles * (size_t)ctx->n_chunks,
+        ((ctx->path == 0 || ctx->sorted) &&
+         cudaMemsetAsync(ctx->cpart, 0, sizeof(double) * ctx->row_stride * (size_t)ctx->n_chunks,
                          ctx->stream) != cudaSuccess) ||
         cudaMemsetAsync(ctx->st, 0, sizeof(DevState), ctx->stream) != cudaSuccess) {
         cuda_fail(ctx, cudaGetLastError(), "cudaMemsetAsync");
@@ -983,7 +1042,7 @@ kmeans_status kmeans_get_info(kmeans_ctx* ctx, kmeans_info* info) {
     info->ldx = ctx->ldx;
     info->d = ctx->d;
     info->K = ctx->K;
-    info->grid = ctx->path == 0 ? ctx->n_chunks : ctx->G;
+    info->grid = (ctx->path == 0 || ctx->sorted) ? ctx->n_chunks : ctx->G;
     info->block = ctx->tpb;
     info->smem_bytes = ctx->smem;
     info->path = ctx->path;

@@ -384,8 +384,7 @@ def test_full_size_ns_step_parity(sort):
     with km.Context(X, w.K, sort=sort) as c:
         info = c.info()
         assert info["path"] == 0 and info["sorted"] == int(sort)
-        if not sort:
-            assert info["grid"] == (w.N + 2047) // 2048
+        assert info["grid"] == (w.N + 1023) // 1024 if sort else (w.N + 2047) // 2048
         check_step(X, mu, ctx=c, tag="NS full")
 
 
