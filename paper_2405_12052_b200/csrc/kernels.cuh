@@ -635,6 +635,8 @@ template <bool LARGE>
 struct PCfg {
     static constexpr int kSlots = LARGE ? 8 : KM_SORTED_SLOTS;   // column slots per pass
     static constexpr int kCap = LARGE ? 64 : 16;                 // refined candidates kept
+    // winning-slot cache for passes > 0 (large K); small K recomputes the argmin
+    static constexpr int kSlotCache = LARGE ? kSChunkPoints : 2;
 };
 
 template <int D, bool LARGE>
@@ -645,7 +647,7 @@ struct PrunedSmem {
     uint64_t bar[kSortedStages];
     float4 cand[PCfg<LARGE>::kCap];     // negated fp32 centroid of each candidate slot
     int candk[PCfg<LARGE>::kCap];       // centroid index of each slot (ascending)
-    unsigned short slot[kSChunkPoints]; // winning slot of each point (multi path)
+    unsigned short slot[PCfg<LARGE>::kSlotCache];   // winning slot of each point
 };
 
 // {k, n} in one double's bits: k in the low word, n in the high word
@@ -660,7 +662,8 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
                 int mu_sel, int ignore_done, const float* __restrict__ cbox,
                 const int* __restrict__ slist, const int* __restrict__ scount,
                 double* __restrict__ rows, int row_stride, int32_t* __restrict__ labels,
-                int* __restrict__ cand_count) {
+                int* __restrict__ cand_count, int* __restrict__ heavy,
+                int* __restrict__ heavy_count) {
     if (!ignore_done && st->done) return;
     using C = PCfg<LARGE>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -785,6 +788,14 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
         big = nc > C::kCap;
     }
     if (lane == 0 && cand_count) cand_count[chunk] = nc;
+    if (LARGE && big) {
+        // more than kCap candidates: k_assign_heavy takes this chunk with a whole
+        // block.  Drain the units already in flight, then leave.
+        if (lane == 0) heavy[atomicAdd(heavy_count, 1)] = chunk;
+        const unsigned nq = __shfl_sync(0xffffffffu, issued, 0);
+        for (unsigned q = 0; q < nq; ++q) mbar_wait(&S.bar[q % SS], (q / SS) & 1u);
+        return;
+    }
     __syncwarp();
 
     struct Pts {
@@ -942,7 +953,7 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
                 const int64_t pa = base + off, pb = pa + kWarpTile;
                 int s0, s1, s2, s3;
                 float2 ba, bb;
-                if (pass == 0) {
+                if (pass == 0 || !LARGE) {
                     float4 cc;
                     cand_at(0, cc);
                     ba = dist2(P[h].xa, P[h].ya, P[h].za, cc);
@@ -958,18 +969,18 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
                         if (db.x < bb.x) { bb.x = db.x; s2 = j; }
                         if (db.y < bb.y) { bb.y = db.y; s3 = j; }
                     }
-                    if (npass > 1) {
+                    if (LARGE && npass > 1) {
                         S.slot[off] = (unsigned short)s0;
                         S.slot[off + 1] = (unsigned short)s1;
                         S.slot[off + kWarpTile] = (unsigned short)s2;
                         S.slot[off + kWarpTile + 1] = (unsigned short)s3;
                     }
-                    if (MODE & kModeLabels) {
+                    if ((MODE & kModeLabels) && pass == 0) {
                         float4 t;
                         *reinterpret_cast<int2*>(labels + pa) = make_int2(cand_at(s0, t), cand_at(s1, t));
                         *reinterpret_cast<int2*>(labels + pb) = make_int2(cand_at(s2, t), cand_at(s3, t));
                     }
-                    if (MODE & kModeReduce) {
+                    if ((MODE & kModeReduce) && pass == 0) {
                         if (pa < n) J += (double)ba.x;
                         if (pa + 1 < n) J += (double)ba.y;
                         if (pb < n) J += (double)bb.x;
@@ -1022,6 +1033,161 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// k_assign_heavy (large K): the chunks with more than kCap refined candidates
+// (boxes spanning sparse or far regions), one 8-warp block each.  Candidates =
+// the super-box list (exact superset), staged through shared memory in batches
+// of 256; each warp takes one 128-point sub-tile; exact running argmin with
+// strict < over ascending candidates.  Sums go to a per-slot shared table in a
+// fixed order (warps in turn, lanes in rounds of distinct slots, conflicting
+// lanes in lane order), then a compacted sparse row in ascending slot order.
+// ---------------------------------------------------------------------------
+constexpr int kHeavyBatch = 256;
+
+template <int D, int MODE>
+__global__ void __launch_bounds__(256)
+k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const double* __restrict__ mu_buf,
+               const DevState* __restrict__ st, int mu_sel, int ignore_done,
+               const int* __restrict__ slist, const int* __restrict__ scount,
+               const int* __restrict__ heavy, const int* __restrict__ heavy_count,
+               double* __restrict__ rows, int row_stride, int32_t* __restrict__ labels) {
+    if (!ignore_done && st->done) return;
+    static_assert(kSChunkPoints == 8 * kLaneTile, "one 128-point sub-tile per warp");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* T = reinterpret_cast<double*>(smem_raw);                 // [K][4]
+    float4* cb = reinterpret_cast<float4*>(T + 4 * (size_t)K);        // [kHeavyBatch]
+    int* kb = reinterpret_cast<int*>(cb + kHeavyBatch);               // [kHeavyBatch]
+    __shared__ double wJ[8];
+    __shared__ int wcnt[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const double* mu = mu_buf + (size_t)((st->t - mu_sel) & 1) * K * D;
+    const int nh = *heavy_count;
+    for (int h = blockIdx.x; h < nh; h += gridDim.x) {
+        const int chunk = heavy[h];
+        const int64_t base = (int64_t)chunk * kSChunkPoints;
+        const int sup = chunk / kSuperChunks;
+        const int* list = slist + (size_t)sup * K;
+        const int gc = scount[sup];
+        const int64_t pa = base + warp * kLaneTile + 2 * lane, pb = pa + kWarpTile;
+        const float2 xa = ld_stream2(tile_coord<D>(X, pa, 0));
+        const float2 ya = ld_stream2(tile_coord<D>(X, pa, 1));
+        const float2 za = (D == 3) ? ld_stream2(tile_coord<D>(X, pa, 2)) : make_float2(0.f, 0.f);
+        const float2 xb = ld_stream2(tile_coord<D>(X, pb, 0));
+        const float2 yb = ld_stream2(tile_coord<D>(X, pb, 1));
+        const float2 zb = (D == 3) ? ld_stream2(tile_coord<D>(X, pb, 2)) : make_float2(0.f, 0.f);
+        float best[4];
+        int sl[4] = {0, 0, 0, 0};
+        for (int b0 = 0; b0 < gc; b0 += kHeavyBatch) {
+            const int bn = min(kHeavyBatch, gc - b0);
+            __syncthreads();   // previous batch / chunk fully consumed
+            if (tid < bn) {
+                const int k = list[b0 + tid];
+                float c[3] = {0.f, 0.f, 0.f};
+                for (int j = 0; j < D; ++j) c[j] = __double2float_rn(mu[k * D + j]);
+                cb[tid] = make_float4(-c[0], -c[1], D == 3 ? -c[2] : 0.0f, 0.0f);
+                kb[tid] = k;
+            }
+            __syncthreads();
+            for (int j = 0; j < bn; ++j) {
+                const float4 cc = cb[j];
+                float2 e0 = __fadd2_rn(xa, make_float2(cc.x, cc.x));
+                float2 e1 = __fadd2_rn(ya, make_float2(cc.y, cc.y));
+                float2 da = __fmul2_rn(e0, e0);
+                da = __ffma2_rn(e1, e1, da);
+                float2 f0 = __fadd2_rn(xb, make_float2(cc.x, cc.x));
+                float2 f1 = __fadd2_rn(yb, make_float2(cc.y, cc.y));
+                float2 db = __fmul2_rn(f0, f0);
+                db = __ffma2_rn(f1, f1, db);
+                if (D == 3) {
+                    float2 e2 = __fadd2_rn(za, make_float2(cc.z, cc.z));
+                    da = __ffma2_rn(e2, e2, da);
+                    float2 f2 = __fadd2_rn(zb, make_float2(cc.z, cc.z));
+                    db = __ffma2_rn(f2, f2, db);
+                }
+                const int s_ = b0 + j;
+                if (s_ == 0) {
+                    best[0] = da.x; best[1] = da.y; best[2] = db.x; best[3] = db.y;
+                } else {
+                    if (da.x < best[0]) { best[0] = da.x; sl[0] = s_; }
+                    if (da.y < best[1]) { best[1] = da.y; sl[1] = s_; }
+                    if (db.x < best[2]) { best[2] = db.x; sl[2] = s_; }
+                    if (db.y < best[3]) { best[3] = db.y; sl[3] = s_; }
+                }
+            }
+        }
+        const bool v[4] = {pa < n, pa + 1 < n, pb < n, pb + 1 < n};
+        if (MODE & kModeLabels) {
+            *reinterpret_cast<int2*>(labels + pa) = make_int2(list[sl[0]], list[sl[1]]);
+            *reinterpret_cast<int2*>(labels + pb) = make_int2(list[sl[2]], list[sl[3]]);
+        }
+        if (!(MODE & kModeReduce)) continue;
+        for (int q = tid; q < 4 * gc; q += blockDim.x) T[q] = 0.0;
+        double j4 = 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (v[i]) j4 += (double)best[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) j4 += __shfl_xor_sync(0xffffffffu, j4, o);
+        if (lane == 0) wJ[warp] = j4;
+        const float px[4] = {xa.x, xa.y, xb.x, xb.y}, py[4] = {ya.x, ya.y, yb.x, yb.y};
+        const float pz[4] = {za.x, za.y, zb.x, zb.y};
+        for (int w = 0; w < 8; ++w) {
+            __syncthreads();
+            if (warp != w) continue;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                unsigned pending = __ballot_sync(0xffffffffu, v[i]);
+                while (pending) {
+                    const unsigned peers =
+                        __match_any_sync(0xffffffffu, v[i] ? sl[i] : -1 - lane) & pending;
+                    const bool mine = v[i] && ((pending >> lane) & 1u) &&
+                                      (peers & ((1u << lane) - 1u)) == 0u;
+                    if (mine) {
+                        double* t = T + 4 * sl[i];
+                        t[0] += (double)px[i];
+                        t[1] += (double)py[i];
+                        t[2] += (double)pz[i];
+                        t[3] += 1.0;
+                    }
+                    __syncwarp();
+                    pending &= ~__ballot_sync(0xffffffffu, mine);
+                }
+            }
+        }
+        __syncthreads();
+        // compact the non-empty slots (ascending) into the sparse row
+        double* row = rows + (size_t)chunk * row_stride;
+        int outc = 0;
+        for (int s0 = 0; s0 < gc; s0 += blockDim.x) {
+            const int s_ = s0 + tid;
+            const bool nz = s_ < gc && T[4 * s_ + 3] > 0.0;
+            const unsigned m = __ballot_sync(0xffffffffu, nz);
+            if (lane == 0) wcnt[warp] = __popc(m);
+            __syncthreads();
+            int o = outc;
+            for (int w = 0; w < warp; ++w) o += wcnt[w];
+            o += __popc(m & ((1u << lane) - 1u));
+            if (nz) {
+                const double* t = T + 4 * s_;
+                reinterpret_cast<double2*>(row + kRowHead)[2 * o] = make_double2(t[0], t[1]);
+                reinterpret_cast<double2*>(row + kRowHead)[2 * o + 1] =
+                    make_double2(t[2], pack_kn(list[s_], (int)t[3]));
+            }
+            int tot = 0;
+            for (int w = 0; w < 8; ++w) tot += wcnt[w];
+            outc += tot;
+            __syncthreads();
+        }
+        if (tid == 0) {
+            double J = 0.0;
+            for (int w = 0; w < 8; ++w) J += wJ[w];
+            row[0] = J;
+            row[1] = (double)outc;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // k_prune (large K): candidates of each super box (kSuperChunks chunks) by the
 // same exclusion test, listed in ascending k.
@@ -1030,8 +1196,9 @@ template <int D>
 __global__ void __launch_bounds__(256)
 k_prune(const double* __restrict__ mu_buf, const DevState* __restrict__ st, int mu_sel,
         int ignore_done, int K, const float* __restrict__ sbox, int* __restrict__ slist,
-        int* __restrict__ scount) {
+        int* __restrict__ scount, int* __restrict__ heavy_count) {
     if (!ignore_done && st->done) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *heavy_count = 0;   // the assign's heavy list
     __shared__ double wmin[8];
     __shared__ int wcnt[8];
     __shared__ int base_s;

@@ -76,6 +76,10 @@ struct kmeans_ctx {
     int* slist = nullptr;         // n_super x K candidate lists
     int* scount = nullptr;        // candidates per super-box
     int merge_smem = 0;           // k_merge_sparse dynamic shared memory (none)
+    int* heavy = nullptr;         // chunks deferred to k_assign_heavy (sorted, large K)
+    int* heavy_count = nullptr;
+    int heavy_smem = 0;
+    int heavy_grid = 0;
     bool sorted = false;          // points held in Morton order (path 0 default)
     int32_t* perm = nullptr;      // sorted position -> caller's index (sorted only)
     int32_t* invperm = nullptr;   // caller's index -> sorted position (sorted only)
@@ -94,7 +98,7 @@ namespace {
 
 // kernels of this library per iteration: [prune], assign, [row merge], merge, update
 int kernels_per_iter(const kmeans_ctx* ctx) {
-    if (ctx->sorted) return ctx->path == 1 ? 5 : 4;
+    if (ctx->sorted) return ctx->path == 1 ? 6 : 4;
     return ctx->path == 0 ? 4 : 3;
 }
 
@@ -161,7 +165,21 @@ ChunkFn pick_chunk(int d, int K, int mode) {
 }
 
 using PrunedFn = void (*)(const float*, int64_t, int, const double*, const DevState*, int, int,
-                          const float*, const int*, const int*, double*, int, int32_t*, int*);
+                          const float*, const int*, const int*, double*, int, int32_t*, int*,
+                          int*, int*);
+using HeavyFn = void (*)(const float*, int64_t, int, const double*, const DevState*, int, int,
+                         const int*, const int*, const int*, const int*, double*, int, int32_t*);
+
+HeavyFn pick_heavy(int d, int mode) {
+    if (d == 2) {
+        if (mode == 1) return km::k_assign_heavy<2, 1>;
+        if (mode == 2) return km::k_assign_heavy<2, 2>;
+        return km::k_assign_heavy<2, 3>;
+    }
+    if (mode == 1) return km::k_assign_heavy<3, 1>;
+    if (mode == 2) return km::k_assign_heavy<3, 2>;
+    return km::k_assign_heavy<3, 3>;
+}
 
 template <bool LARGE>
 PrunedFn pick_pruned_l(int d, int mode) {
@@ -230,6 +248,14 @@ kmeans_status configure(kmeans_ctx* ctx) {
         ctx->G = (ctx->n_chunks + km::kGroupChunks - 1) / km::kGroupChunks;  // groups
         ctx->n_super = (ctx->n_chunks + km::kSuperChunks - 1) / km::kSuperChunks;
         ctx->merge_smem = 0;
+        if (ctx->path == 1) {
+            ctx->heavy_smem = ctx->K * 4 * (int)sizeof(double) + km::kHeavyBatch * 20;
+            for (int mode = 1; mode <= 3; ++mode)
+                CK(cudaFuncSetAttribute((const void*)pick_heavy(ctx->d, mode),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        ctx->heavy_smem));
+            ctx->heavy_grid = 2 * sms;
+        }
     } else if (ctx->path == 0) {
         ctx->tpb = 32;
         ctx->smem = chunk_smem(ctx->d, ctx->K);
@@ -273,17 +299,26 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
             if (ctx->d == 2)
                 km::k_prune<2><<<ctx->n_super, 256, 0, ctx->stream>>>(
                     ctx->mu, ctx->st, mu_sel, ignore_done, ctx->K, ctx->sbox, ctx->slist,
-                    ctx->scount);
+                    ctx->scount, ctx->heavy_count);
             else
                 km::k_prune<3><<<ctx->n_super, 256, 0, ctx->stream>>>(
                     ctx->mu, ctx->st, mu_sel, ignore_done, ctx->K, ctx->sbox, ctx->slist,
-                    ctx->scount);
+                    ctx->scount, ctx->heavy_count);
             ctx->launches += 1;
         }
         PrunedFn f = pick_pruned(ctx->d, ctx->K, mode);
         f<<<ctx->n_chunks, 32, ctx->smem, ctx->stream>>>(
             ctx->X, ctx->N, ctx->K, ctx->mu, ctx->st, mu_sel, ignore_done, ctx->cbox, ctx->slist,
-            ctx->scount, ctx->cpart, ctx->row_stride, ctx->labels_sorted, ctx->cand_count);
+            ctx->scount, ctx->cpart, ctx->row_stride, ctx->labels_sorted, ctx->cand_count,
+            ctx->heavy, ctx->heavy_count);
+        if (ctx->path == 1) {
+            HeavyFn hf = pick_heavy(ctx->d, mode);
+            hf<<<ctx->heavy_grid, 256, ctx->heavy_smem, ctx->stream>>>(
+                ctx->X, ctx->N, ctx->K, ctx->mu, ctx->st, mu_sel, ignore_done, ctx->slist,
+                ctx->scount, ctx->heavy, ctx->heavy_count, ctx->cpart, ctx->row_stride,
+                ctx->labels_sorted);
+            ctx->launches += 1;
+        }
         if (mode & km::kModeReduce) {
             // sparse chunk rows -> group columns of part (fixed ascending order)
             if (ctx->d == 2)
@@ -602,6 +637,8 @@ void kmeans_destroy(kmeans_ctx* ctx) {
         cudaFree(ctx->sbox);
         cudaFree(ctx->slist);
         cudaFree(ctx->scount);
+        cudaFree(ctx->heavy);
+        cudaFree(ctx->heavy_count);
         cudaFree(ctx->perm);
         cudaFree(ctx->invperm);
         cudaFree(ctx->cbox);
@@ -696,7 +733,9 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
         (ctx->sorted && ctx->path == 1 &&
          (cudaMalloc(&ctx->sbox, sizeof(float) * 2 * d * (size_t)ctx->n_super) != cudaSuccess ||
           cudaMalloc(&ctx->slist, sizeof(int) * (size_t)K * ctx->n_super) != cudaSuccess ||
-          cudaMalloc(&ctx->scount, sizeof(int) * (size_t)ctx->n_super) != cudaSuccess)) ||
+          cudaMalloc(&ctx->scount, sizeof(int) * (size_t)ctx->n_super) != cudaSuccess ||
+          cudaMalloc(&ctx->heavy, sizeof(int) * (size_t)ctx->n_chunks) != cudaSuccess ||
+          cudaMalloc(&ctx->heavy_count, sizeof(int)) != cudaSuccess)) ||
         cudaMalloc(&ctx->flag, sizeof(int)) != cudaSuccess) {
         cudaGetLastError();
         set_error("device allocation failed (%zu bytes of points)", bytesX);

@@ -412,3 +412,26 @@ def test_full_size_c5_sampled_parity():
     tot = g["sums"].sum(axis=0)
     ref = X.astype(np.float64).sum(axis=0)
     assert np.all(np.abs(tot - ref) <= 1e-9 * np.abs(X).astype(np.float64).sum(axis=0))
+
+
+def test_heavy_chunks_large_k():
+    """Large K with far outliers and sparse tails: chunk boxes that span huge
+    empty regions keep more than 64 candidates and go to k_assign_heavy (one
+    block per chunk, candidates in batches); labels must stay bit-exact."""
+    rng = np.random.default_rng(21)
+    w = datagen.WORKLOADS["C5"]
+    X = datagen.generate(w, N=200_000)
+    # a sparse shell of far points between the blobs and the planted sites
+    far = rng.uniform(-3000, 3000, (3000, 3)).astype(np.float32)
+    X[rng.choice(200_000, 3000, replace=False)] = far
+    init = datagen.init_indices(w, N=200_000)
+    mu = X[init].astype(np.float64)
+    with km.Context(X, w.K) as c:
+        g, o = check_step(X, mu, ctx=c, tag="heavy")
+        st = c.candidate_stats()
+    assert st["max"] > 64, st   # the heavy path was exercised
+    # a 2-step run through the iteration graph (prune -> assign -> heavy -> merges)
+    o1 = oracle.fit(X, w.K, init, 0.0, 2)
+    with km.Context(X, w.K) as c:
+        r = c.fit(init, 0.0, 2)
+    assert np.array_equal(r["labels"], o1["labels"])
