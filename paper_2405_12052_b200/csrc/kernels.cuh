@@ -907,7 +907,14 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
             szt += __shfl_xor_sync(0xffffffffu, szt, o);
             J += __shfl_xor_sync(0xffffffffu, J, o);
         }
-        if (lane == 0) {
+        if (!LARGE) {
+            // dense row [k][Sx Sy Sz n] (k < 16), J at 64 (k_merge_rows layout)
+            const int kk = lane >> 1;
+            double2 out = make_double2(0.0, 0.0);
+            if (kk == k0) out = (lane & 1) ? make_double2(szt, (double)npts) : make_double2(sxt, syt);
+            reinterpret_cast<double2*>(row)[lane] = out;
+            if (lane == 0) row[64] = J;
+        } else if (lane == 0) {
             row[0] = J;
             row[1] = 1.0;
             reinterpret_cast<double2*>(row + kRowHead)[0] = make_double2(sxt, syt);
@@ -919,6 +926,7 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
     // ---- several candidates ----
     const int ncand = big ? gcount : nc;   // slots = indices into the candidate list
     double J = 0.0;
+    if (!LARGE && (MODE & kModeReduce)) reinterpret_cast<double2*>(row)[lane] = make_double2(0.0, 0.0);
     auto accumulate = [&](int l, float px, float py, float pz) {
         double2 a = S.A[l][lane], b = S.B[l][lane];
         a.x += (double)px;
@@ -1020,16 +1028,24 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
             }
             float4 t;
             const int k = cand_at(s_lo + sl, t);
-            reinterpret_cast<double2*>(row + kRowHead)[2 * (s_lo + sl) + (lane & 1)] =
-                (lane & 1) ? make_double2(v0, pack_kn(k, (int)cnt)) : make_double2(v0, v1);
+            if (!LARGE)
+                reinterpret_cast<double2*>(row)[2 * k + (lane & 1)] =
+                    (lane & 1) ? make_double2(v0, (double)cnt) : make_double2(v0, v1);
+            else
+                reinterpret_cast<double2*>(row + kRowHead)[2 * (s_lo + sl) + (lane & 1)] =
+                    (lane & 1) ? make_double2(v0, pack_kn(k, (int)cnt)) : make_double2(v0, v1);
         }
         __syncwarp();
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
     if (lane == 0) {
-        row[0] = J;
-        row[1] = (double)ncand;
+        if (!LARGE) {
+            row[64] = J;
+        } else {
+            row[0] = J;
+            row[1] = (double)ncand;
+        }
     }
 }
 

@@ -244,7 +244,8 @@ kmeans_status configure(kmeans_ctx* ctx) {
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
         ctx->chunk_points = km::kSChunkPoints;
         ctx->n_chunks = (int)((ctx->N + ctx->chunk_points - 1) / ctx->chunk_points);
-        ctx->row_stride = km::kRowHead + 4 * (ctx->K <= 16 ? 16 : ctx->K);
+        // small K: dense rows (k_merge_rows); large K: sparse rows (k_merge_sparse)
+        ctx->row_stride = ctx->K <= 16 ? km::kRowDoubles : km::kRowHead + 4 * ctx->K;
         ctx->G = (ctx->n_chunks + km::kGroupChunks - 1) / km::kGroupChunks;  // groups
         ctx->n_super = (ctx->n_chunks + km::kSuperChunks - 1) / km::kSuperChunks;
         ctx->merge_smem = 0;
@@ -319,7 +320,16 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
                 ctx->labels_sorted);
             ctx->launches += 1;
         }
-        if (mode & km::kModeReduce) {
+        if ((mode & km::kModeReduce) && ctx->path == 0) {
+            // dense chunk rows -> group columns of part (fixed ascending order)
+            if (ctx->d == 2)
+                km::k_merge_rows<2><<<ctx->G, 96, 0, ctx->stream>>>(
+                    ctx->cpart, ctx->n_chunks, ctx->K, ctx->part, ctx->G, ctx->st, ignore_done);
+            else
+                km::k_merge_rows<3><<<ctx->G, 96, 0, ctx->stream>>>(
+                    ctx->cpart, ctx->n_chunks, ctx->K, ctx->part, ctx->G, ctx->st, ignore_done);
+            ctx->launches += 1;
+        } else if (mode & km::kModeReduce) {
             // sparse chunk rows -> group columns of part (fixed ascending order)
             if (ctx->d == 2)
                 km::k_merge_sparse<2><<<ctx->G, 256, ctx->merge_smem, ctx->stream>>>(
