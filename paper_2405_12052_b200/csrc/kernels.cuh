@@ -658,27 +658,34 @@ __device__ __forceinline__ double pack_kn(int k, int n) {
 template <int D, int MODE, bool LARGE>
 __global__ void __launch_bounds__(32)
 k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
-                const double* __restrict__ mu_buf, const DevState* __restrict__ st,
+                const float4* __restrict__ cneg_buf, const DevState* __restrict__ st,
                 int mu_sel, int ignore_done, const float* __restrict__ cbox,
                 const int* __restrict__ slist, const int* __restrict__ scount,
                 double* __restrict__ rows, int row_stride, int32_t* __restrict__ labels,
                 int* __restrict__ cand_count, int* __restrict__ heavy,
                 int* __restrict__ heavy_count) {
-    if (!ignore_done && st->done) return;
     using C = PCfg<LARGE>;
+    // Independent loads first (their latencies overlap the stop-flag read and
+    // the TMA prologue): the box, this lane's staged centroid, the flag.
+    const int lane = threadIdx.x;
+    const int chunk = blockIdx.x;
+    const float4* cneg = cneg_buf + (size_t)mu_sel * K;   // -fl32(mu^t) (or mu^{t-1})
+    const float bx = (lane < 2 * D) ? __ldg(&cbox[(size_t)chunk * 2 * D + lane]) : 0.0f;
+    const float4 cl = (!LARGE && lane < K) ? __ldg(&cneg[lane]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int sup_count = LARGE ? __ldg(&scount[chunk / kSuperChunks]) : 0;
+    const int done_flag = ignore_done ? 0 : *(volatile const int*)&st->done;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PrunedSmem<D, LARGE>& S = *reinterpret_cast<PrunedSmem<D, LARGE>*>(smem_raw);
     constexpr int kUnitFloats = D * kSortedUnit;
     constexpr unsigned kUnitBytes = kUnitFloats * 4;
     constexpr int SS = kSortedStages;
-    const int lane = threadIdx.x;
-    const int chunk = blockIdx.x;
     const int64_t base = (int64_t)chunk * kSChunkPoints;
     const int64_t rem = n - base;
     const int64_t nu64 = (rem + kSortedUnit - 1) / kSortedUnit;
     const int nunit = nu64 < kSortedUnits ? (int)nu64 : kSortedUnits;
     const int npts = rem < kSChunkPoints ? (int)rem : kSChunkPoints;
     const float* src = X + (base >> 6) * (D * kWarpTile);
+    if (done_flag) return;   // stop rule already met (nothing issued yet)
 
     // point stream: units 0..nunit-1 through the TMA ring (unit q in stage q % SS)
     unsigned issued = 0;   // lane 0
@@ -699,17 +706,17 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
     issue_upto(SS);
 
     // ---- candidates of this chunk ----
-    const double* mu = mu_buf + (size_t)((st->t - mu_sel) & 1) * K * D;
-    const float bx = (lane < 2 * D) ? __ldg(&cbox[(size_t)chunk * 2 * D + lane]) : 0.0f;
     double lo[3], hi[3];
 #pragma unroll
     for (int j = 0; j < D; ++j) {
         lo[j] = (double)__shfl_sync(0xffffffffu, bx, j);
         hi[j] = (double)__shfl_sync(0xffffffffu, bx, D + j);
     }
-    auto stage_c = [&](int k, float (&c)[3]) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) c[j] = __double2float_rn(__ldg(&mu[k * D + j]));
+    auto stage_c = [&](int k, float (&c)[3]) {   // staged fp32 centroid k
+        const float4 v = __ldg(&cneg[k]);
+        c[0] = -v.x;
+        c[1] = -v.y;
+        c[2] = -v.z;
     };
     auto bounds = [&](const float (&c)[3], double& dmin2, double& dmax2) {
         dmin2 = 0.0;
@@ -740,7 +747,9 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
         double dmin2 = 0.0, dmax2 = 0.0;
         const bool is_k = lane < K;
         if (is_k) {
-            stage_c(lane, c);
+            c[0] = -cl.x;
+            c[1] = -cl.y;
+            c[2] = -cl.z;
             bounds(c, dmin2, dmax2);
         }
         const double thr = threshold(warp_min(is_k ? dmax2 : (double)pos_inf()));
@@ -755,7 +764,7 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
     } else {
         const int sup = chunk / kSuperChunks;
         glist = slist + (size_t)sup * K;
-        gcount = __ldg(&scount[sup]);
+        gcount = sup_count;
         double M = (double)pos_inf();
         for (int i = lane; i < gcount; i += 32) {
             float c[3];
@@ -852,9 +861,7 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
             return S.candk[j];
         }
         const int k = __ldg(&glist[j]);
-        float c[3];
-        stage_c(k, c);
-        cc = make_float4(-c[0], -c[1], D == 3 ? -c[2] : 0.0f, 0.0f);
+        cc = __ldg(&cneg[k]);
         return k;
     };
     double* row = rows + (size_t)chunk * row_stride;
@@ -1063,7 +1070,7 @@ constexpr int kHeavyBatch = 256;
 
 template <int D, int MODE>
 __global__ void __launch_bounds__(256)
-k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const double* __restrict__ mu_buf,
+k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __restrict__ cneg_buf,
                const DevState* __restrict__ st, int mu_sel, int ignore_done,
                const int* __restrict__ slist, const int* __restrict__ scount,
                const int* __restrict__ heavy, const int* __restrict__ heavy_count,
@@ -1077,7 +1084,7 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const double* __re
     __shared__ double wJ[8];
     __shared__ int wcnt[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const double* mu = mu_buf + (size_t)((st->t - mu_sel) & 1) * K * D;
+    const float4* cneg = cneg_buf + (size_t)mu_sel * K;
     const int nh = *heavy_count;
     for (int h = blockIdx.x; h < nh; h += gridDim.x) {
         const int chunk = heavy[h];
@@ -1099,9 +1106,7 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const double* __re
             __syncthreads();   // previous batch / chunk fully consumed
             if (tid < bn) {
                 const int k = list[b0 + tid];
-                float c[3] = {0.f, 0.f, 0.f};
-                for (int j = 0; j < D; ++j) c[j] = __double2float_rn(mu[k * D + j]);
-                cb[tid] = make_float4(-c[0], -c[1], D == 3 ? -c[2] : 0.0f, 0.0f);
+                cb[tid] = cneg[k];
                 kb[tid] = k;
             }
             __syncthreads();
@@ -1210,7 +1215,7 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const double* __re
 // ---------------------------------------------------------------------------
 template <int D>
 __global__ void __launch_bounds__(256)
-k_prune(const double* __restrict__ mu_buf, const DevState* __restrict__ st, int mu_sel,
+k_prune(const float4* __restrict__ cneg_buf, const DevState* __restrict__ st, int mu_sel,
         int ignore_done, int K, const float* __restrict__ sbox, int* __restrict__ slist,
         int* __restrict__ scount, int* __restrict__ heavy_count) {
     if (!ignore_done && st->done) return;
@@ -1219,7 +1224,7 @@ k_prune(const double* __restrict__ mu_buf, const DevState* __restrict__ st, int 
     __shared__ int wcnt[8];
     __shared__ int base_s;
     const int s = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const double* mu = mu_buf + (size_t)((st->t - mu_sel) & 1) * K * D;
+    const float4* cneg = cneg_buf + (size_t)mu_sel * K;
     double lo[3], hi[3];
 #pragma unroll
     for (int j = 0; j < D; ++j) {
@@ -1230,8 +1235,10 @@ k_prune(const double* __restrict__ mu_buf, const DevState* __restrict__ st, int 
         dmin2 = 0.0;
         dmax2 = 0.0;
 #pragma unroll
+        const float4 v = cneg[k];
+        const float cv[3] = {-v.x, -v.y, -v.z};
         for (int j = 0; j < D; ++j) {
-            const double cj = (double)__double2float_rn(mu[k * D + j]);
+            const double cj = (double)cv[j];
             const double dm = fmax(fmax(lo[j] - cj, cj - hi[j]), 0.0);
             dmin2 += dm * dm;
             const double dx = fmax(fabs(cj - lo[j]), fabs(hi[j] - cj));
@@ -1555,6 +1562,24 @@ k_assign_large(const float* __restrict__ X, int64_t ldx, int64_t n, int K,
 }
 
 // ---------------------------------------------------------------------------
+// k_stage: cneg[0][k] = -fl32(mu_k) (RN) from the fp64 master mu^t in buffer
+// (t & 1); slot 1 (the previous iteration's) gets the same when `both`.
+// ---------------------------------------------------------------------------
+__global__ void k_stage(const double* __restrict__ mu_buf, const DevState* __restrict__ st,
+                        int K, int d, float4* __restrict__ cneg, int both) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    const double* mu = mu_buf + (size_t)(st->t & 1) * K * d;
+    float4 v;
+    v.x = -__double2float_rn(mu[k * d + 0]);
+    v.y = -__double2float_rn(mu[k * d + 1]);
+    v.z = (d == 3) ? -__double2float_rn(mu[k * d + 2]) : 0.0f;
+    v.w = 0.0f;
+    cneg[k] = v;
+    if (both) cneg[K + k] = v;
+}
+
+// ---------------------------------------------------------------------------
 // k_merge: red[e] = sum_b part[e * G + b], one warp per entry, fixed order
 // (lane l sums b = l, l+32, ... ascending; then a butterfly).
 // ---------------------------------------------------------------------------
@@ -1580,7 +1605,8 @@ __global__ void k_merge(const double* __restrict__ part, int G, int nE,
 template <int D>
 __global__ void k_update(double* __restrict__ mu_buf, int K, const double* __restrict__ red,
                          DevState* __restrict__ st, double* __restrict__ trace_E,
-                         double* __restrict__ trace_J, int trace_cap) {
+                         double* __restrict__ trace_J, int trace_cap,
+                         float4* __restrict__ cneg) {
     if (st->done) return;
     __shared__ double red_sm[32];
     const int t = st->t;
@@ -1594,6 +1620,11 @@ __global__ void k_update(double* __restrict__ mu_buf, int K, const double* __res
         const double old = mu_old[q];
         const double nw = (nk > 0.0) ? red[q] / nk : old;   // empty cluster keeps mu^t
         mu_new[q] = nw;
+        if (cneg) {   // staged fp32 copies: [1] <- mu^t, [0] <- mu^{t+1} (pruned path)
+            const int j = q - k * D;
+            reinterpret_cast<float*>(&cneg[K + k])[j] = -__double2float_rn(old);
+            reinterpret_cast<float*>(&cneg[k])[j] = -__double2float_rn(nw);
+        }
         const double diff = nw - old;
         e_acc += diff * diff;
     }

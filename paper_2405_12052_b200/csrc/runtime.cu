@@ -56,6 +56,7 @@ struct kmeans_ctx {
 
     float* X = nullptr;          // AoSoA fp32: ldx/64 tiles of [x64 y64 (z64)]
     double* mu = nullptr;        // 2 x Kpad x d (ping-pong by t & 1)
+    float4* cneg = nullptr;      // 2 x K staged -fl32(mu): [0] current, [1] previous
     double* part = nullptr;      // nE x G per-block partials
     double* red = nullptr;       // nE merged partials
     DevState* st = nullptr;
@@ -164,10 +165,10 @@ ChunkFn pick_chunk(int d, int K, int mode) {
     return pick_chunk_kp<3, 3>(K);
 }
 
-using PrunedFn = void (*)(const float*, int64_t, int, const double*, const DevState*, int, int,
+using PrunedFn = void (*)(const float*, int64_t, int, const float4*, const DevState*, int, int,
                           const float*, const int*, const int*, double*, int, int32_t*, int*,
                           int*, int*);
-using HeavyFn = void (*)(const float*, int64_t, int, const double*, const DevState*, int, int,
+using HeavyFn = void (*)(const float*, int64_t, int, const float4*, const DevState*, int, int,
                          const int*, const int*, const int*, const int*, double*, int, int32_t*);
 
 HeavyFn pick_heavy(int d, int mode) {
@@ -299,23 +300,23 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
             // super-box candidate lists (large K)
             if (ctx->d == 2)
                 km::k_prune<2><<<ctx->n_super, 256, 0, ctx->stream>>>(
-                    ctx->mu, ctx->st, mu_sel, ignore_done, ctx->K, ctx->sbox, ctx->slist,
+                    ctx->cneg, ctx->st, mu_sel, ignore_done, ctx->K, ctx->sbox, ctx->slist,
                     ctx->scount, ctx->heavy_count);
             else
                 km::k_prune<3><<<ctx->n_super, 256, 0, ctx->stream>>>(
-                    ctx->mu, ctx->st, mu_sel, ignore_done, ctx->K, ctx->sbox, ctx->slist,
+                    ctx->cneg, ctx->st, mu_sel, ignore_done, ctx->K, ctx->sbox, ctx->slist,
                     ctx->scount, ctx->heavy_count);
             ctx->launches += 1;
         }
         PrunedFn f = pick_pruned(ctx->d, ctx->K, mode);
         f<<<ctx->n_chunks, 32, ctx->smem, ctx->stream>>>(
-            ctx->X, ctx->N, ctx->K, ctx->mu, ctx->st, mu_sel, ignore_done, ctx->cbox, ctx->slist,
+            ctx->X, ctx->N, ctx->K, ctx->cneg, ctx->st, mu_sel, ignore_done, ctx->cbox, ctx->slist,
             ctx->scount, ctx->cpart, ctx->row_stride, ctx->labels_sorted, ctx->cand_count,
             ctx->heavy, ctx->heavy_count);
         if (ctx->path == 1) {
             HeavyFn hf = pick_heavy(ctx->d, mode);
             hf<<<ctx->heavy_grid, 256, ctx->heavy_smem, ctx->stream>>>(
-                ctx->X, ctx->N, ctx->K, ctx->mu, ctx->st, mu_sel, ignore_done, ctx->slist,
+                ctx->X, ctx->N, ctx->K, ctx->cneg, ctx->st, mu_sel, ignore_done, ctx->slist,
                 ctx->scount, ctx->heavy, ctx->heavy_count, ctx->cpart, ctx->row_stride,
                 ctx->labels_sorted);
             ctx->launches += 1;
@@ -408,10 +409,12 @@ kmeans_status launch_update(kmeans_ctx* ctx) {
     const int tpb = 256;
     if (ctx->d == 2)
         km::k_update<2><<<1, tpb, 0, ctx->stream>>>(ctx->mu, ctx->K, ctx->red, ctx->st,
-                                                    ctx->trace_E, ctx->trace_J, ctx->trace_cap);
+                                                    ctx->trace_E, ctx->trace_J, ctx->trace_cap,
+                                                    ctx->sorted ? ctx->cneg : nullptr);
     else
         km::k_update<3><<<1, tpb, 0, ctx->stream>>>(ctx->mu, ctx->K, ctx->red, ctx->st,
-                                                    ctx->trace_E, ctx->trace_J, ctx->trace_cap);
+                                                    ctx->trace_E, ctx->trace_J, ctx->trace_cap,
+                                                    ctx->sorted ? ctx->cneg : nullptr);
     ctx->launches += 1;
     CK(cudaGetLastError());
     return KMEANS_OK;
@@ -464,6 +467,17 @@ kmeans_status write_state(kmeans_ctx* ctx, int t, int done, int max_iter, double
     h.tol = tol;
     CK(cudaMemcpyAsync(ctx->st, &h, sizeof(DevState), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));  // h is a stack object
+    return KMEANS_OK;
+}
+
+// cneg[0] (and [1]) <- -fl32(mu^t) for the pruned kernels; call after the
+// fp64 master and DevState::t are set.
+kmeans_status stage_centroids(kmeans_ctx* ctx) {
+    if (!ctx->sorted) return KMEANS_OK;
+    km::k_stage<<<(ctx->K + 127) / 128, 128, 0, ctx->stream>>>(ctx->mu, ctx->st, ctx->K, ctx->d,
+                                                                 ctx->cneg, 1);
+    ctx->launches += 1;
+    CK(cudaGetLastError());
     return KMEANS_OK;
 }
 
@@ -635,6 +649,7 @@ void kmeans_destroy(kmeans_ctx* ctx) {
         if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
         cudaFree(ctx->X);
         cudaFree(ctx->mu);
+        cudaFree(ctx->cneg);
         cudaFree(ctx->part);
         cudaFree(ctx->red);
         cudaFree(ctx->st);
@@ -733,6 +748,7 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
     size_t bytesX = sizeof(float) * (size_t)d * ctx->ldx;
     if (cudaMalloc(&ctx->X, bytesX) != cudaSuccess ||
         cudaMalloc(&ctx->mu, sizeof(double) * 2 * Kpad * d) != cudaSuccess ||
+        cudaMalloc(&ctx->cneg, sizeof(float4) * 2 * Kpad) != cudaSuccess ||
         cudaMalloc(&ctx->part, sizeof(double) * (size_t)ctx->nE * ctx->G) != cudaSuccess ||
         cudaMalloc(&ctx->red, sizeof(double) * ctx->nE) != cudaSuccess ||
         cudaMalloc(&ctx->st, sizeof(DevState)) != cudaSuccess ||
@@ -847,7 +863,8 @@ kmeans_status kmeans_start(kmeans_ctx* ctx, const int64_t* init_idx, const doubl
     }
     if ((s = ensure_trace(ctx, max_iter)) != KMEANS_OK) return s;
     ctx->assigned = false;
-    return write_state(ctx, 0, 0, max_iter, tol);
+    if ((s = write_state(ctx, 0, 0, max_iter, tol)) != KMEANS_OK) return s;
+    return stage_centroids(ctx);
 }
 
 kmeans_status kmeans_iterate(kmeans_ctx* ctx, int n) {
@@ -932,6 +949,7 @@ kmeans_status kmeans_assign(kmeans_ctx* ctx, const double* centroids, int32_t* l
     CK(cudaMemcpyAsync(ctx->mu, c.data(), sizeof(double) * n, cudaMemcpyHostToDevice,
                        ctx->stream));
     if ((s = write_state(ctx, 0, 0, 0x7fffffff, -1.0)) != KMEANS_OK) return s;
+    if ((s = stage_centroids(ctx)) != KMEANS_OK) return s;
     const int mode = km::kModeReduce | (labels ? km::kModeLabels : 0);
     if ((s = launch_assign(ctx, mode, 0, 1)) != KMEANS_OK) return s;
     if ((s = launch_merge(ctx, 1)) != KMEANS_OK) return s;
