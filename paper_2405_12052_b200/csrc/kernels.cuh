@@ -1059,39 +1059,109 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
 
 // ---------------------------------------------------------------------------
 // k_assign_heavy (large K): the chunks with more than kCap refined candidates
-// (boxes spanning sparse or far regions), one 8-warp block each.  Candidates =
-// the super-box list (exact superset), staged through shared memory in batches
-// of 256; each warp takes one 128-point sub-tile; exact running argmin with
-// strict < over ascending candidates.  Sums go to a per-slot shared table in a
-// fixed order (warps in turn, lanes in rounds of distinct slots, conflicting
-// lanes in lane order), then a compacted sparse row in ascending slot order.
+// (boxes spanning sparse or far regions), one 8-warp block each.  The block
+// refines the super-box list against the chunk box (exact, as in
+// k_assign_pruned), then each warp refines that list against the box of its
+// own 128-point sub-tile (the tile's minimiser of dmax2 is always in the chunk
+// list, so the tile's M and exclusions are exact too) and runs the strict-<
+// argmin over its list in ascending order.  Sums go to a per-slot shared table
+// in a fixed order (warps in turn, lanes in rounds of distinct slots,
+// conflicting lanes in lane order), then a compacted sparse row in ascending
+// slot (= ascending k) order.
 // ---------------------------------------------------------------------------
-constexpr int kHeavyBatch = 256;
-
 template <int D, int MODE>
 __global__ void __launch_bounds__(256)
 k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __restrict__ cneg_buf,
                const DevState* __restrict__ st, int mu_sel, int ignore_done,
-               const int* __restrict__ slist, const int* __restrict__ scount,
-               const int* __restrict__ heavy, const int* __restrict__ heavy_count,
-               double* __restrict__ rows, int row_stride, int32_t* __restrict__ labels) {
+               const float* __restrict__ cbox, const int* __restrict__ slist,
+               const int* __restrict__ scount, const int* __restrict__ heavy,
+               const int* __restrict__ heavy_count, double* __restrict__ rows, int row_stride,
+               int32_t* __restrict__ labels) {
     if (!ignore_done && st->done) return;
     static_assert(kSChunkPoints == 8 * kLaneTile, "one 128-point sub-tile per warp");
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* T = reinterpret_cast<double*>(smem_raw);                 // [K][4]
-    float4* cb = reinterpret_cast<float4*>(T + 4 * (size_t)K);        // [kHeavyBatch]
-    int* kb = reinterpret_cast<int*>(cb + kHeavyBatch);               // [kHeavyBatch]
-    __shared__ double wJ[8];
+    double* T = reinterpret_cast<double*>(smem_raw);                    // [K][4]
+    float4* cl = reinterpret_cast<float4*>(T + 4 * (size_t)K);           // [K] chunk candidates
+    int* kl = reinterpret_cast<int*>(cl + K);                            // [K]
+    unsigned short* wl = reinterpret_cast<unsigned short*>(kl + K);      // [8][K] tile lists
+    __shared__ double wJ[8], wM[8];
     __shared__ int wcnt[8];
+    __shared__ float box[6];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const float4* cneg = cneg_buf + (size_t)mu_sel * K;
     const int nh = *heavy_count;
+    auto bounds = [&](const float4& v, const double (&lo)[3], const double (&hi)[3], double& dmin2,
+                      double& dmax2) {
+        const float c[3] = {-v.x, -v.y, -v.z};
+        dmin2 = 0.0;
+        dmax2 = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            const double cj = (double)c[j];
+            const double dm = fmax(fmax(lo[j] - cj, cj - hi[j]), 0.0);
+            dmin2 += dm * dm;
+            const double dx = fmax(fabs(cj - lo[j]), fabs(hi[j] - cj));
+            dmax2 += dx * dx;
+        }
+    };
+    auto thr_of = [](double M) {
+        return (M > 1e37) ? (double)pos_inf() : M * (1.0 + 1e-5) + 0x1p-100;
+    };
     for (int h = blockIdx.x; h < nh; h += gridDim.x) {
         const int chunk = heavy[h];
         const int64_t base = (int64_t)chunk * kSChunkPoints;
         const int sup = chunk / kSuperChunks;
         const int* list = slist + (size_t)sup * K;
         const int gc = scount[sup];
+        __syncthreads();   // the previous chunk is done with every shared buffer
+        if (tid < 2 * D) box[tid] = cbox[(size_t)chunk * 2 * D + tid];
+        __syncthreads();
+        double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+        for (int j = 0; j < D; ++j) {
+            lo[j] = (double)box[j];
+            hi[j] = (double)box[D + j];
+        }
+        // ---- chunk-level refinement of the super list ----
+        double M = (double)pos_inf();
+        for (int i = tid; i < gc; i += blockDim.x) {
+            double a, b;
+            bounds(cneg[list[i]], lo, hi, a, b);
+            M = fmin(M, b);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
+        if (lane == 0) wM[warp] = M;
+        __syncthreads();
+        M = wM[0];
+        for (int w = 1; w < 8; ++w) M = fmin(M, wM[w]);
+        const double thr = thr_of(M);
+        int nc = 0;
+        for (int i0 = 0; i0 < gc; i0 += blockDim.x) {
+            const int i = i0 + tid;
+            bool cand = false;
+            int k = 0;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (i < gc) {
+                k = list[i];
+                v = cneg[k];
+                double a, b;
+                bounds(v, lo, hi, a, b);
+                cand = a <= thr;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, cand);
+            if (lane == 0) wcnt[warp] = __popc(m);
+            __syncthreads();
+            int o = nc;
+            for (int w = 0; w < warp; ++w) o += wcnt[w];
+            o += __popc(m & ((1u << lane) - 1u));
+            if (cand) {
+                cl[o] = v;
+                kl[o] = k;
+            }
+            for (int w = 0; w < 8; ++w) nc += wcnt[w];
+            __syncthreads();
+        }
+        // ---- this warp's sub-tile: points, box, tile-level refinement ----
         const int64_t pa = base + warp * kLaneTile + 2 * lane, pb = pa + kWarpTile;
         const float2 xa = ld_stream2(tile_coord<D>(X, pa, 0));
         const float2 ya = ld_stream2(tile_coord<D>(X, pa, 1));
@@ -1099,51 +1169,108 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
         const float2 xb = ld_stream2(tile_coord<D>(X, pb, 0));
         const float2 yb = ld_stream2(tile_coord<D>(X, pb, 1));
         const float2 zb = (D == 3) ? ld_stream2(tile_coord<D>(X, pb, 2)) : make_float2(0.f, 0.f);
-        float best[4];
-        int sl[4] = {0, 0, 0, 0};
-        for (int b0 = 0; b0 < gc; b0 += kHeavyBatch) {
-            const int bn = min(kHeavyBatch, gc - b0);
-            __syncthreads();   // previous batch / chunk fully consumed
-            if (tid < bn) {
-                const int k = list[b0 + tid];
-                cb[tid] = cneg[k];
-                kb[tid] = k;
-            }
-            __syncthreads();
-            for (int j = 0; j < bn; ++j) {
-                const float4 cc = cb[j];
-                float2 e0 = __fadd2_rn(xa, make_float2(cc.x, cc.x));
-                float2 e1 = __fadd2_rn(ya, make_float2(cc.y, cc.y));
-                float2 da = __fmul2_rn(e0, e0);
-                da = __ffma2_rn(e1, e1, da);
-                float2 f0 = __fadd2_rn(xb, make_float2(cc.x, cc.x));
-                float2 f1 = __fadd2_rn(yb, make_float2(cc.y, cc.y));
-                float2 db = __fmul2_rn(f0, f0);
-                db = __ffma2_rn(f1, f1, db);
-                if (D == 3) {
-                    float2 e2 = __fadd2_rn(za, make_float2(cc.z, cc.z));
-                    da = __ffma2_rn(e2, e2, da);
-                    float2 f2 = __fadd2_rn(zb, make_float2(cc.z, cc.z));
-                    db = __ffma2_rn(f2, f2, db);
-                }
-                const int s_ = b0 + j;
-                if (s_ == 0) {
-                    best[0] = da.x; best[1] = da.y; best[2] = db.x; best[3] = db.y;
-                } else {
-                    if (da.x < best[0]) { best[0] = da.x; sl[0] = s_; }
-                    if (da.y < best[1]) { best[1] = da.y; sl[1] = s_; }
-                    if (db.x < best[2]) { best[2] = db.x; sl[2] = s_; }
-                    if (db.y < best[3]) { best[3] = db.y; sl[3] = s_; }
-                }
-            }
-        }
         const bool v[4] = {pa < n, pa + 1 < n, pb < n, pb + 1 < n};
+        const float px[4] = {xa.x, xa.y, xb.x, xb.y}, py[4] = {ya.x, ya.y, yb.x, yb.y};
+        const float pz[4] = {za.x, za.y, zb.x, zb.y};
+        double tlo[3] = {0, 0, 0}, thi[3] = {0, 0, 0};
+        for (int j = 0; j < D; ++j) {
+            const float* pj = j == 0 ? px : (j == 1 ? py : pz);
+            float l_ = pos_inf(), h_ = -pos_inf();
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (v[i]) {
+                    l_ = fminf(l_, pj[i]);
+                    h_ = fmaxf(h_, pj[i]);
+                }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                l_ = fminf(l_, __shfl_xor_sync(0xffffffffu, l_, o));
+                h_ = fmaxf(h_, __shfl_xor_sync(0xffffffffu, h_, o));
+            }
+            tlo[j] = (double)l_;
+            thi[j] = (double)h_;
+        }
+        const bool any_valid = tlo[0] <= thi[0];   // false for an all-padding tile
+        unsigned short* my = wl + (size_t)warp * K;
+        int nt = 0;
+        if (any_valid) {
+            double tM = (double)pos_inf();
+            for (int i = lane; i < nc; i += 32) {
+                double a, b;
+                bounds(cl[i], tlo, thi, a, b);
+                tM = fmin(tM, b);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) tM = fmin(tM, __shfl_xor_sync(0xffffffffu, tM, o));
+            const double tthr = thr_of(tM);
+            for (int i0 = 0; i0 < nc; i0 += 32) {
+                const int i = i0 + lane;
+                bool cand = false;
+                if (i < nc) {
+                    double a, b;
+                    bounds(cl[i], tlo, thi, a, b);
+                    cand = a <= tthr;
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, cand);
+                if (cand) my[nt + __popc(m & ((1u << lane) - 1u))] = (unsigned short)i;
+                nt += __popc(m);
+            }
+        } else {
+            if (lane == 0) my[0] = 0;
+            nt = 1;
+        }
+        __syncwarp();
+        // ---- exact argmin over the tile list (ascending chunk slots) ----
+        float best[4];
+        int sl[4];
+        {
+            const int i0 = my[0];
+            const float4 cc = cl[i0];
+            float2 e0 = __fadd2_rn(xa, make_float2(cc.x, cc.x));
+            float2 e1 = __fadd2_rn(ya, make_float2(cc.y, cc.y));
+            float2 da = __fmul2_rn(e0, e0);
+            da = __ffma2_rn(e1, e1, da);
+            float2 f0 = __fadd2_rn(xb, make_float2(cc.x, cc.x));
+            float2 f1 = __fadd2_rn(yb, make_float2(cc.y, cc.y));
+            float2 db = __fmul2_rn(f0, f0);
+            db = __ffma2_rn(f1, f1, db);
+            if (D == 3) {
+                float2 e2 = __fadd2_rn(za, make_float2(cc.z, cc.z));
+                da = __ffma2_rn(e2, e2, da);
+                float2 f2 = __fadd2_rn(zb, make_float2(cc.z, cc.z));
+                db = __ffma2_rn(f2, f2, db);
+            }
+            best[0] = da.x; best[1] = da.y; best[2] = db.x; best[3] = db.y;
+            sl[0] = sl[1] = sl[2] = sl[3] = i0;
+        }
+        for (int t = 1; t < nt; ++t) {
+            const int i = my[t];
+            const float4 cc = cl[i];
+            float2 e0 = __fadd2_rn(xa, make_float2(cc.x, cc.x));
+            float2 e1 = __fadd2_rn(ya, make_float2(cc.y, cc.y));
+            float2 da = __fmul2_rn(e0, e0);
+            da = __ffma2_rn(e1, e1, da);
+            float2 f0 = __fadd2_rn(xb, make_float2(cc.x, cc.x));
+            float2 f1 = __fadd2_rn(yb, make_float2(cc.y, cc.y));
+            float2 db = __fmul2_rn(f0, f0);
+            db = __ffma2_rn(f1, f1, db);
+            if (D == 3) {
+                float2 e2 = __fadd2_rn(za, make_float2(cc.z, cc.z));
+                da = __ffma2_rn(e2, e2, da);
+                float2 f2 = __fadd2_rn(zb, make_float2(cc.z, cc.z));
+                db = __ffma2_rn(f2, f2, db);
+            }
+            if (da.x < best[0]) { best[0] = da.x; sl[0] = i; }
+            if (da.y < best[1]) { best[1] = da.y; sl[1] = i; }
+            if (db.x < best[2]) { best[2] = db.x; sl[2] = i; }
+            if (db.y < best[3]) { best[3] = db.y; sl[3] = i; }
+        }
         if (MODE & kModeLabels) {
-            *reinterpret_cast<int2*>(labels + pa) = make_int2(list[sl[0]], list[sl[1]]);
-            *reinterpret_cast<int2*>(labels + pb) = make_int2(list[sl[2]], list[sl[3]]);
+            *reinterpret_cast<int2*>(labels + pa) = make_int2(kl[sl[0]], kl[sl[1]]);
+            *reinterpret_cast<int2*>(labels + pb) = make_int2(kl[sl[2]], kl[sl[3]]);
         }
         if (!(MODE & kModeReduce)) continue;
-        for (int q = tid; q < 4 * gc; q += blockDim.x) T[q] = 0.0;
+        for (int q = tid; q < 4 * nc; q += blockDim.x) T[q] = 0.0;
         double j4 = 0.0;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -1151,8 +1278,6 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) j4 += __shfl_xor_sync(0xffffffffu, j4, o);
         if (lane == 0) wJ[warp] = j4;
-        const float px[4] = {xa.x, xa.y, xb.x, xb.y}, py[4] = {ya.x, ya.y, yb.x, yb.y};
-        const float pz[4] = {za.x, za.y, zb.x, zb.y};
         for (int w = 0; w < 8; ++w) {
             __syncthreads();
             if (warp != w) continue;
@@ -1180,9 +1305,9 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
         // compact the non-empty slots (ascending) into the sparse row
         double* row = rows + (size_t)chunk * row_stride;
         int outc = 0;
-        for (int s0 = 0; s0 < gc; s0 += blockDim.x) {
+        for (int s0 = 0; s0 < nc; s0 += blockDim.x) {
             const int s_ = s0 + tid;
-            const bool nz = s_ < gc && T[4 * s_ + 3] > 0.0;
+            const bool nz = s_ < nc && T[4 * s_ + 3] > 0.0;
             const unsigned m = __ballot_sync(0xffffffffu, nz);
             if (lane == 0) wcnt[warp] = __popc(m);
             __syncthreads();
@@ -1193,7 +1318,7 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
                 const double* t = T + 4 * s_;
                 reinterpret_cast<double2*>(row + kRowHead)[2 * o] = make_double2(t[0], t[1]);
                 reinterpret_cast<double2*>(row + kRowHead)[2 * o + 1] =
-                    make_double2(t[2], pack_kn(list[s_], (int)t[3]));
+                    make_double2(t[2], pack_kn(kl[s_], (int)t[3]));
             }
             int tot = 0;
             for (int w = 0; w < 8; ++w) tot += wcnt[w];
@@ -1331,13 +1456,19 @@ k_merge_sparse(const double* __restrict__ rows, int row_stride, int n_chunks, in
         cnt[tid] = (int)row[1];
     }
     __syncthreads();
-    if (tid == 0) {
-        int o = 0;
-        for (int c = 0; c < nch; ++c) {
-            off[c] = o;
-            o += cnt[c];
+    if (tid < 32) {   // exclusive scan of the counts (warp 0, two per lane)
+        const int a = (2 * tid < nch) ? cnt[2 * tid] : 0;
+        const int b = (2 * tid + 1 < nch) ? cnt[2 * tid + 1] : 0;
+        int x = a + b;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (tid >= o) x += y;
         }
-        off[nch] = o;
+        const int excl = x - a - b;
+        if (2 * tid < nch) off[2 * tid] = excl;
+        if (2 * tid + 1 < nch) off[2 * tid + 1] = excl + a;
+        if (tid == 31) off[nch] = x;
     }
     __syncthreads();
     const int total = off[nch];
@@ -1349,14 +1480,29 @@ k_merge_sparse(const double* __restrict__ rows, int row_stride, int n_chunks, in
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
     for (int b0 = 0; b0 < total; b0 += kMergeBatch) {
         const int bn = min(kMergeBatch, total - b0);
-        // stage entries [b0, b0 + bn): 2 double2 per entry
-        for (int q = tid; q < 2 * bn; q += blockDim.x) {
-            const int idx = b0 + (q >> 1);
-            int c = 0;
-            while (off[c + 1] <= idx) ++c;   // chunk of entry idx (nch <= 64)
-            const double* row = rows + (size_t)(c0 + c) * row_stride + kRowHead;
-            E[q] = reinterpret_cast<const double2*>(row)[2 * (idx - off[c]) + (q & 1)];
+        // stage entries [b0, b0 + bn) (2 double2 each): every thread issues its
+        // (up to 4) independent loads before any store
+        double2 tmp[4];
+        int dst[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int q = tid + r * (int)blockDim.x;
+            dst[r] = -1;
+            if (q < 2 * bn) {
+                const int idx = b0 + (q >> 1);
+                int lo_ = 0, hi_ = nch;   // chunk c with off[c] <= idx < off[c + 1]
+                while (hi_ - lo_ > 1) {
+                    const int mid = (lo_ + hi_) >> 1;
+                    if (off[mid] <= idx) lo_ = mid; else hi_ = mid;
+                }
+                const double* row = rows + (size_t)(c0 + lo_) * row_stride + kRowHead;
+                tmp[r] = reinterpret_cast<const double2*>(row)[2 * (idx - off[lo_]) + (q & 1)];
+                dst[r] = q;
+            }
         }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+            if (dst[r] >= 0) E[dst[r]] = tmp[r];
         __syncthreads();
         for (int e = 0; e < bn; ++e) {
             const double2 v1 = E[2 * e + 1];

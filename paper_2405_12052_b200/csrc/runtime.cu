@@ -169,7 +169,8 @@ using PrunedFn = void (*)(const float*, int64_t, int, const float4*, const DevSt
                           const float*, const int*, const int*, double*, int, int32_t*, int*,
                           int*, int*);
 using HeavyFn = void (*)(const float*, int64_t, int, const float4*, const DevState*, int, int,
-                         const int*, const int*, const int*, const int*, double*, int, int32_t*);
+                         const float*, const int*, const int*, const int*, const int*, double*, int,
+                         int32_t*);
 
 HeavyFn pick_heavy(int d, int mode) {
     if (d == 2) {
@@ -251,12 +252,16 @@ kmeans_status configure(kmeans_ctx* ctx) {
         ctx->n_super = (ctx->n_chunks + km::kSuperChunks - 1) / km::kSuperChunks;
         ctx->merge_smem = 0;
         if (ctx->path == 1) {
-            ctx->heavy_smem = ctx->K * 4 * (int)sizeof(double) + km::kHeavyBatch * 20;
+            // T [K][4] doubles, chunk list K x (float4 + int), 8 tile lists K x u16
+            ctx->heavy_smem = ctx->K * (32 + 16 + 4 + 16);
             for (int mode = 1; mode <= 3; ++mode)
                 CK(cudaFuncSetAttribute((const void*)pick_heavy(ctx->d, mode),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         ctx->heavy_smem));
-            ctx->heavy_grid = 2 * sms;
+            int hocc = 0;   // one resident block per heavy chunk when possible
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &hocc, (const void*)pick_heavy(ctx->d, 1), 256, ctx->heavy_smem));
+            ctx->heavy_grid = sms * std::max(hocc, 1);
         }
     } else if (ctx->path == 0) {
         ctx->tpb = 32;
@@ -316,8 +321,8 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
         if (ctx->path == 1) {
             HeavyFn hf = pick_heavy(ctx->d, mode);
             hf<<<ctx->heavy_grid, 256, ctx->heavy_smem, ctx->stream>>>(
-                ctx->X, ctx->N, ctx->K, ctx->cneg, ctx->st, mu_sel, ignore_done, ctx->slist,
-                ctx->scount, ctx->heavy, ctx->heavy_count, ctx->cpart, ctx->row_stride,
+                ctx->X, ctx->N, ctx->K, ctx->cneg, ctx->st, mu_sel, ignore_done, ctx->cbox,
+                ctx->slist, ctx->scount, ctx->heavy, ctx->heavy_count, ctx->cpart, ctx->row_stride,
                 ctx->labels_sorted);
             ctx->launches += 1;
         }
@@ -406,7 +411,8 @@ kmeans_status allreduce(kmeans_ctx* ctx, double* buf, size_t count) {
 }
 
 kmeans_status launch_update(kmeans_ctx* ctx) {
-    const int tpb = 256;
+    // one block; enough threads that each handles <= ~4 of the K d entries
+    const int tpb = std::min(1024, std::max(256, ((ctx->K * ctx->d + 3) / 4 + 31) / 32 * 32));
     if (ctx->d == 2)
         km::k_update<2><<<1, tpb, 0, ctx->stream>>>(ctx->mu, ctx->K, ctx->red, ctx->st,
                                                     ctx->trace_E, ctx->trace_J, ctx->trace_cap,
