@@ -1428,12 +1428,12 @@ __global__ void k_super_bbox(const float* __restrict__ cbox, int n_chunks, int d
 }
 
 // ---------------------------------------------------------------------------
-// k_merge_sparse: group g sums the sparse rows of chunks [64g, 64g + 64).
-// The headers and entries are staged in shared memory with independent
-// (parallel) loads; then each thread owns clusters k = tid, tid + 256, ... and
-// scans the staged entries in (chunk, entry) order, adding those of its k --
-// every sum is taken in ascending chunk order, with no atomics and no
-// per-chunk barrier.  Writes the group's column gpart[e][g] for k_merge.
+// k_merge_sparse: group g sums the sparse rows of chunks [64g, 64g + 64) into
+// a dense shared table T[K][4].  Entries are staged in shared memory with
+// independent loads; then the chunks are added in ascending order, one thread
+// per entry (the entries of one row have distinct k), a barrier between
+// chunks -- every sum is taken in chunk order, no atomics.  Writes the group's
+// column gpart[e][g] for k_merge.
 // ---------------------------------------------------------------------------
 constexpr int kMergeBatch = 512;   // entries staged per batch
 
@@ -1443,6 +1443,8 @@ k_merge_sparse(const double* __restrict__ rows, int row_stride, int n_chunks, in
                double* __restrict__ gpart, int n_groups, const DevState* __restrict__ st,
                int ignore_done) {
     if (!ignore_done && st->done) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* T = reinterpret_cast<double*>(smem_raw);   // [K][4]: Sx Sy Sz n
     __shared__ double hj[kGroupChunks];
     __shared__ int cnt[kGroupChunks];
     __shared__ int off[kGroupChunks + 1];
@@ -1450,6 +1452,7 @@ k_merge_sparse(const double* __restrict__ rows, int row_stride, int n_chunks, in
     const int g = blockIdx.x, tid = threadIdx.x;
     const int c0 = g * kGroupChunks;
     const int nch = min(n_chunks, c0 + kGroupChunks) - c0;
+    for (int q = tid; q < 4 * K; q += blockDim.x) T[q] = 0.0;
     if (tid < nch) {
         const double* row = rows + (size_t)(c0 + tid) * row_stride;
         hj[tid] = row[0];
@@ -1472,12 +1475,7 @@ k_merge_sparse(const double* __restrict__ rows, int row_stride, int n_chunks, in
     }
     __syncthreads();
     const int total = off[nch];
-    // owned clusters: k = tid + 256 i (K <= 1024 -> at most 4)
-    double acc[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    int c = 0;   // first chunk with entries in the current batch
     for (int b0 = 0; b0 < total; b0 += kMergeBatch) {
         const int bn = min(kMergeBatch, total - b0);
         // stage entries [b0, b0 + bn) (2 double2 each): every thread issues its
@@ -1490,7 +1488,7 @@ k_merge_sparse(const double* __restrict__ rows, int row_stride, int n_chunks, in
             dst[r] = -1;
             if (q < 2 * bn) {
                 const int idx = b0 + (q >> 1);
-                int lo_ = 0, hi_ = nch;   // chunk c with off[c] <= idx < off[c + 1]
+                int lo_ = 0, hi_ = nch;   // chunk with off[c] <= idx < off[c + 1]
                 while (hi_ - lo_ > 1) {
                     const int mid = (lo_ + hi_) >> 1;
                     if (off[mid] <= idx) lo_ = mid; else hi_ = mid;
@@ -1504,37 +1502,31 @@ k_merge_sparse(const double* __restrict__ rows, int row_stride, int n_chunks, in
         for (int r = 0; r < 4; ++r)
             if (dst[r] >= 0) E[dst[r]] = tmp[r];
         __syncthreads();
-        for (int e = 0; e < bn; ++e) {
-            const double2 v1 = E[2 * e + 1];
-            const int2 kn = *reinterpret_cast<const int2*>(&v1.y);   // {k, n}
-            if ((kn.x & 255) == tid && kn.x < K) {
-                const double2 v0 = E[2 * e];
-                const int i = kn.x >> 8;
-#pragma unroll
-                for (int ii = 0; ii < 4; ++ii) {
-                    if (ii == i) {
-                        acc[ii][0] += v0.x;
-                        acc[ii][1] += v0.y;
-                        acc[ii][2] += v1.x;
-                        acc[ii][3] += (double)kn.y;
-                    }
-                }
+        // chunks in ascending order; the batch may end inside a chunk
+        for (; c < nch && off[c] < b0 + bn; ++c) {
+            const int e_end = min(off[c + 1], b0 + bn);
+            for (int e = max(off[c], b0) + tid; e < e_end; e += blockDim.x) {
+                const double2 v0 = E[2 * (e - b0)];
+                const double2 v1 = E[2 * (e - b0) + 1];
+                const int2 kn = *reinterpret_cast<const int2*>(&v1.y);   // {k, n}
+                double* t = T + 4 * kn.x;
+                t[0] += v0.x;
+                t[1] += v0.y;
+                t[2] += v1.x;
+                t[3] += (double)kn.y;
             }
+            __syncthreads();
+            if (off[c + 1] > b0 + bn) break;   // rest of chunk c is in the next batch
         }
-        __syncthreads();
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int k = tid + 256 * i;
-        if (k < K) {
-#pragma unroll
-            for (int j = 0; j < D; ++j) gpart[(size_t)(k * D + j) * n_groups + g] = acc[i][j];
-            gpart[(size_t)(K * D + k) * n_groups + g] = acc[i][3];
-        }
+    __syncthreads();
+    for (int k = tid; k < K; k += blockDim.x) {
+        for (int j = 0; j < D; ++j) gpart[(size_t)(k * D + j) * n_groups + g] = T[4 * k + j];
+        gpart[(size_t)(K * D + k) * n_groups + g] = T[4 * k + 3];
     }
     if (tid == 0) {
         double J = 0.0;
-        for (int c = 0; c < nch; ++c) J += hj[c];
+        for (int cc = 0; cc < nch; ++cc) J += hj[cc];
         gpart[(size_t)(K * D + K) * n_groups + g] = J;
     }
 }

@@ -76,7 +76,7 @@ struct kmeans_ctx {
     float* sbox = nullptr;        // super-box bounding boxes
     int* slist = nullptr;         // n_super x K candidate lists
     int* scount = nullptr;        // candidates per super-box
-    int merge_smem = 0;           // k_merge_sparse dynamic shared memory (none)
+    int merge_smem = 0;           // k_merge_sparse dynamic shared memory (K x 4 doubles)
     int* heavy = nullptr;         // chunks deferred to k_assign_heavy (sorted, large K)
     int* heavy_count = nullptr;
     int heavy_smem = 0;
@@ -250,7 +250,11 @@ kmeans_status configure(kmeans_ctx* ctx) {
         ctx->row_stride = ctx->K <= 16 ? km::kRowDoubles : km::kRowHead + 4 * ctx->K;
         ctx->G = (ctx->n_chunks + km::kGroupChunks - 1) / km::kGroupChunks;  // groups
         ctx->n_super = (ctx->n_chunks + km::kSuperChunks - 1) / km::kSuperChunks;
-        ctx->merge_smem = 0;
+        ctx->merge_smem = 4 * ctx->K * (int)sizeof(double);   // k_merge_sparse table
+        CK(cudaFuncSetAttribute((const void*)km::k_merge_sparse<2>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->merge_smem));
+        CK(cudaFuncSetAttribute((const void*)km::k_merge_sparse<3>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->merge_smem));
         if (ctx->path == 1) {
             // T [K][4] doubles, chunk list K x (float4 + int), 8 tile lists K x u16
             ctx->heavy_smem = ctx->K * (32 + 16 + 4 + 16);
