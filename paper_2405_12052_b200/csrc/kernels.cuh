@@ -181,6 +181,7 @@ constexpr int kChunkTiles = KM_CHUNK_TILES;
 constexpr int kChunkPoints = kLaneTile * kChunkTiles;    // 2048
 constexpr int kStages = 3;
 constexpr int kGroupChunks = 64;
+constexpr int kRowGroup = 256;   // chunks per group, dense / <=16-entry rows
 constexpr int kRowDoubles = 16 * 4 + 2;                  // [k][Sx Sy Sz n] + J + pad
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -914,14 +915,7 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
             szt += __shfl_xor_sync(0xffffffffu, szt, o);
             J += __shfl_xor_sync(0xffffffffu, J, o);
         }
-        if (!LARGE) {
-            // dense row [k][Sx Sy Sz n] (k < 16), J at 64 (k_merge_rows layout)
-            const int kk = lane >> 1;
-            double2 out = make_double2(0.0, 0.0);
-            if (kk == k0) out = (lane & 1) ? make_double2(szt, (double)npts) : make_double2(sxt, syt);
-            reinterpret_cast<double2*>(row)[lane] = out;
-            if (lane == 0) row[64] = J;
-        } else if (lane == 0) {
+        if (lane == 0) {   // sparse row: J, 1 entry {Sx, Sy, Sz, (k, n)}
             row[0] = J;
             row[1] = 1.0;
             reinterpret_cast<double2*>(row + kRowHead)[0] = make_double2(sxt, syt);
@@ -933,7 +927,6 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
     // ---- several candidates ----
     const int ncand = big ? gcount : nc;   // slots = indices into the candidate list
     double J = 0.0;
-    if (!LARGE && (MODE & kModeReduce)) reinterpret_cast<double2*>(row)[lane] = make_double2(0.0, 0.0);
     auto accumulate = [&](int l, float px, float py, float pz) {
         double2 a = S.A[l][lane], b = S.B[l][lane];
         a.x += (double)px;
@@ -1035,11 +1028,7 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
             }
             float4 t;
             const int k = cand_at(s_lo + sl, t);
-            if (!LARGE)
-                reinterpret_cast<double2*>(row)[2 * k + (lane & 1)] =
-                    (lane & 1) ? make_double2(v0, (double)cnt) : make_double2(v0, v1);
-            else
-                reinterpret_cast<double2*>(row + kRowHead)[2 * (s_lo + sl) + (lane & 1)] =
+            reinterpret_cast<double2*>(row + kRowHead)[2 * (s_lo + sl) + (lane & 1)] =
                     (lane & 1) ? make_double2(v0, pack_kn(k, (int)cnt)) : make_double2(v0, v1);
         }
         __syncwarp();
@@ -1047,12 +1036,8 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
     if (lane == 0) {
-        if (!LARGE) {
-            row[64] = J;
-        } else {
-            row[0] = J;
-            row[1] = (double)ncand;
-        }
+        row[0] = J;
+        row[1] = (double)ncand;
     }
 }
 
@@ -1532,27 +1517,110 @@ k_merge_sparse(const double* __restrict__ rows, int row_stride, int n_chunks, in
 }
 
 // ---------------------------------------------------------------------------
-// k_merge_rows: group g sums the rows of chunks [64g, 64g + 64) in ascending
-// chunk order and scatters them to gpart[e][g] (the layout k_merge sums).
+// k_merge_sparse16 (sorted path, K <= 16): group g = chunks [256 g, 256 (g+1)),
+// one thread per chunk row in the head phase.  Warp w takes its 32 chunks in
+// ascending order; for chunk j the lanes 0 .. 2 ncand_j - 1 each hold one
+// double2 of the row's entries (ncand <= 16 -> <= 32 double2) and add it into
+// the warp's K-table T[w][k] (distinct k within a row: no conflicts).  The 8
+// warp tables are then added in warp order -> gpart[e][g].  Fixed order, no
+// atomics; only the rows' written entries are read.
 // ---------------------------------------------------------------------------
 template <int D>
-__global__ void __launch_bounds__(96)
+__global__ void __launch_bounds__(256)
+k_merge_sparse16(const double* __restrict__ cpart, int n_chunks, int K, double* __restrict__ gpart,
+                 int n_groups, const DevState* __restrict__ st, int ignore_done) {
+    if (!ignore_done && st->done) return;
+    __shared__ double2 T[8][16][2];   // [warp][k]{(Sx, Sy), (Sz, n)}
+    __shared__ double WJ[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = blockIdx.x;
+    const int c = g * kRowGroup + tid;
+    reinterpret_cast<double2*>(&T[0][0][0])[tid] = make_double2(0.0, 0.0);   // 8*16*2 = 256
+    double2 head = make_double2(0.0, 0.0);
+    if (c < n_chunks) head = *reinterpret_cast<const double2*>(cpart + (size_t)c * kRowDoubles);
+    const int my_n = (int)head.y;
+    double J = head.x;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
+    if (lane == 0) WJ[warp] = J;
+    __syncthreads();   // T zeroed
+    // entries: lane l holds double2 l of chunk (warp base + j); 8 chunks in flight
+    const int cbase = g * kRowGroup + warp * 32;
+#pragma unroll 1
+    for (int j0 = 0; j0 < 32; j0 += 8) {
+        double2 v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int nj = __shfl_sync(0xffffffffu, my_n, j0 + j);
+            v[j] = make_double2(0.0, 0.0);
+            if (lane < 2 * nj)
+                v[j] = reinterpret_cast<const double2*>(cpart + (size_t)(cbase + j0 + j) * kRowDoubles +
+                                                        kRowHead)[lane];
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int nj = __shfl_sync(0xffffffffu, my_n, j0 + j);
+            // k of entry (lane >> 1) sits in the low word of the odd double2's .y
+            const double kn = __shfl_sync(0xffffffffu, v[j].y, lane | 1);
+            const int k = __double2loint(kn);
+            if (lane < 2 * nj) {
+                double2 a = T[warp][k][lane & 1];
+                a.x += v[j].x;
+                a.y += (lane & 1) ? (double)__double2hiint(v[j].y) : v[j].y;
+                T[warp][k][lane & 1] = a;
+            }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    if (tid > 64) return;
+    if (tid == 64) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) s += WJ[w];
+        gpart[(size_t)(K * D + K) * n_groups + g] = s;
+        return;
+    }
+    const int k = tid >> 2, j = tid & 3;
+    if (k >= K || (j >= D && j != 3)) return;
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += reinterpret_cast<const double*>(&T[w][k][0])[j];
+    if (j < D) gpart[(size_t)(k * D + j) * n_groups + g] = s;
+    else gpart[(size_t)(K * D + k) * n_groups + g] = s;
+}
+
+// ---------------------------------------------------------------------------
+// k_merge_rows (dense rows): group g sums the rows of chunks
+// [kRowGroup g, kRowGroup (g+1)).  Thread (r, q), r < 4, sums entry q of rows
+// c0 + r, c0 + r + 4, ... in ascending order; the four stripes are then added
+// in order r = 0..3 -- a fixed summation tree.  Scatters to gpart[e][g].
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(288)
 k_merge_rows(const double* __restrict__ cpart, int n_chunks, int K, double* __restrict__ gpart,
              int n_groups, const DevState* __restrict__ st, int ignore_done) {
     if (!ignore_done && st->done) return;
-    const int q = threadIdx.x;            // row entry
-    if (q > 64) return;
+    __shared__ double P[4][65];
+    const int tid = threadIdx.x;
+    const int r = tid / 65, q = tid - 65 * r;   // stripe, row entry (64 = J)
     const int g = blockIdx.x;
-    const int c0 = g * kGroupChunks;
-    const int c1 = min(n_chunks, c0 + kGroupChunks);
-    double v = 0.0;
+    const int c0 = g * kRowGroup;
+    const int c1 = min(n_chunks, c0 + kRowGroup);
+    if (r < 4) {
+        double v = 0.0;
 #pragma unroll 8
-    for (int c = c0; c < c1; ++c) v += cpart[(size_t)c * kRowDoubles + q];
-    if (q == 64) {
+        for (int c = c0 + r; c < c1; c += 4) v += cpart[(size_t)c * kRowDoubles + q];
+        P[r][q] = v;
+    }
+    __syncthreads();
+    if (tid > 64) return;
+    const double v = ((P[0][tid] + P[1][tid]) + P[2][tid]) + P[3][tid];
+    if (tid == 64) {
         gpart[(size_t)(K * D + K) * n_groups + g] = v;
         return;
     }
-    const int k = q >> 2, j = q & 3;
+    const int k = tid >> 2, j = tid & 3;
     if (k < K) {
         if (j < D) gpart[(size_t)(k * D + j) * n_groups + g] = v;
         else if (j == 3) gpart[(size_t)(K * D + k) * n_groups + g] = v;
@@ -1730,6 +1798,7 @@ __global__ void k_merge(const double* __restrict__ part, int G, int nE,
     if (e >= nE) return;
     const double* row = part + (size_t)e * G;
     double v = 0.0;
+#pragma unroll 8
     for (int b = lane; b < G; b += 32) v += row[b];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -1737,15 +1806,15 @@ __global__ void k_merge(const double* __restrict__ part, int G, int nE,
 }
 
 // ---------------------------------------------------------------------------
-// k_update (one block): the mean step of PAPER.md:50-62 and the error term of
-// PAPER.md:66-69; then t += 1 and the stop decision of PAPER.md:70.
+// The update (one block): the mean step of PAPER.md:50-62 and the error term of
+// PAPER.md:66-69; then t += 1 and the stop decision of PAPER.md:70.  `red` is
+// the merged (and, distributed, allreduced) vector.
 // ---------------------------------------------------------------------------
 template <int D>
-__global__ void k_update(double* __restrict__ mu_buf, int K, const double* __restrict__ red,
-                         DevState* __restrict__ st, double* __restrict__ trace_E,
-                         double* __restrict__ trace_J, int trace_cap,
-                         float4* __restrict__ cneg) {
-    if (st->done) return;
+__device__ void update_body(double* __restrict__ mu_buf, int K, const double* red,
+                            DevState* __restrict__ st, double* __restrict__ trace_E,
+                            double* __restrict__ trace_J, int trace_cap,
+                            float4* __restrict__ cneg, unsigned* __restrict__ work) {
     __shared__ double red_sm[32];
     const int t = st->t;
     const double* mu_old = mu_buf + (size_t)(t & 1) * K * D;
@@ -1787,8 +1856,48 @@ __global__ void k_update(double* __restrict__ mu_buf, int K, const double* __res
             }
             st->t = t + 1;
             st->done = (E < st->tol) || (t + 1 >= st->max_iter);
+            if (work) *work = 0u;
         }
     }
+}
+
+template <int D>
+__global__ void k_update(double* __restrict__ mu_buf, int K, const double* __restrict__ red,
+                         DevState* __restrict__ st, double* __restrict__ trace_E,
+                         double* __restrict__ trace_J, int trace_cap,
+                         float4* __restrict__ cneg) {
+    if (st->done) return;
+    update_body<D>(mu_buf, K, red, st, trace_E, trace_J, trace_cap, cneg, nullptr);
+}
+
+// k_merge_update (single GPU): the group merge of k_merge and the update in one
+// block -- warp w sums entries e = w, w + 32, ... over the groups in the fixed
+// k_merge order (lane l: groups l, l + 32, ...; then a butterfly), into shared
+// memory; then the update.  Saves a launch per iteration.
+template <int D>
+__global__ void __launch_bounds__(1024)
+k_merge_update(const double* __restrict__ part, int G, int nE, double* __restrict__ red,
+               double* __restrict__ mu_buf, int K, DevState* __restrict__ st,
+               double* __restrict__ trace_E, double* __restrict__ trace_J, int trace_cap,
+               float4* __restrict__ cneg) {
+    if (st->done) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* rs = reinterpret_cast<double*>(smem_raw);   // [nE]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    for (int e = warp; e < nE; e += nwarp) {
+        const double* row = part + (size_t)e * G;
+        double v = 0.0;
+#pragma unroll 8
+        for (int b = lane; b < G; b += 32) v += row[b];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) {
+            rs[e] = v;
+            red[e] = v;
+        }
+    }
+    __syncthreads();
+    update_body<D>(mu_buf, K, rs, st, trace_E, trace_J, trace_cap, cneg, nullptr);
 }
 
 }  // namespace km

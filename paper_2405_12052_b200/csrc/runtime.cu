@@ -97,10 +97,14 @@ struct kmeans_ctx {
 
 namespace {
 
-// kernels of this library per iteration: [prune], assign, [row merge], merge, update
+bool fused_update(const kmeans_ctx* ctx);
+
+// kernels of this library per iteration: [prune], assign, [heavy], [row merge],
+// merge + update (fused into one kernel on a single GPU when small enough)
 int kernels_per_iter(const kmeans_ctx* ctx) {
-    if (ctx->sorted) return ctx->path == 1 ? 6 : 4;
-    return ctx->path == 0 ? 4 : 3;
+    int n = ctx->sorted ? (ctx->path == 1 ? 6 : 4) : (ctx->path == 0 ? 4 : 3);
+    if (fused_update(ctx)) n -= 1;
+    return n;
 }
 
 kmeans_status cuda_fail(kmeans_ctx* c, cudaError_t e, const char* what) {
@@ -248,7 +252,9 @@ kmeans_status configure(kmeans_ctx* ctx) {
         ctx->n_chunks = (int)((ctx->N + ctx->chunk_points - 1) / ctx->chunk_points);
         // small K: dense rows (k_merge_rows); large K: sparse rows (k_merge_sparse)
         ctx->row_stride = ctx->K <= 16 ? km::kRowDoubles : km::kRowHead + 4 * ctx->K;
-        ctx->G = (ctx->n_chunks + km::kGroupChunks - 1) / km::kGroupChunks;  // groups
+        // groups: 256 dense rows (k_merge_rows) or 64 sparse rows (k_merge_sparse)
+        ctx->G = ctx->K <= 16 ? (ctx->n_chunks + km::kRowGroup - 1) / km::kRowGroup
+                              : (ctx->n_chunks + km::kGroupChunks - 1) / km::kGroupChunks;
         ctx->n_super = (ctx->n_chunks + km::kSuperChunks - 1) / km::kSuperChunks;
         ctx->merge_smem = 4 * ctx->K * (int)sizeof(double);   // k_merge_sparse table
         CK(cudaFuncSetAttribute((const void*)km::k_merge_sparse<2>,
@@ -276,7 +282,7 @@ kmeans_status configure(kmeans_ctx* ctx) {
         ctx->chunk_points = km::kChunkPoints;
         ctx->n_chunks = (int)((ctx->N + ctx->chunk_points - 1) / ctx->chunk_points);
         ctx->row_stride = km::kRowDoubles;
-        ctx->G = (ctx->n_chunks + km::kGroupChunks - 1) / km::kGroupChunks;  // groups
+        ctx->G = (ctx->n_chunks + km::kRowGroup - 1) / km::kRowGroup;  // groups
     } else {
         int tpb = km::kLargeTPBMax;
         while (tpb > 64 && large_smem(ctx->d, ctx->K, tpb) > maxSmem - 4096) tpb -= 32;
@@ -331,12 +337,12 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
             ctx->launches += 1;
         }
         if ((mode & km::kModeReduce) && ctx->path == 0) {
-            // dense chunk rows -> group columns of part (fixed ascending order)
+            // sparse chunk rows (<= 16 entries) -> group columns of part (fixed order)
             if (ctx->d == 2)
-                km::k_merge_rows<2><<<ctx->G, 96, 0, ctx->stream>>>(
+                km::k_merge_sparse16<2><<<ctx->G, 256, 0, ctx->stream>>>(
                     ctx->cpart, ctx->n_chunks, ctx->K, ctx->part, ctx->G, ctx->st, ignore_done);
             else
-                km::k_merge_rows<3><<<ctx->G, 96, 0, ctx->stream>>>(
+                km::k_merge_sparse16<3><<<ctx->G, 256, 0, ctx->stream>>>(
                     ctx->cpart, ctx->n_chunks, ctx->K, ctx->part, ctx->G, ctx->st, ignore_done);
             ctx->launches += 1;
         } else if (mode & km::kModeReduce) {
@@ -359,10 +365,10 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
         if (mode & km::kModeReduce) {
             // chunk rows -> group columns of part (fixed ascending order)
             if (ctx->d == 2)
-                km::k_merge_rows<2><<<ctx->G, 96, 0, ctx->stream>>>(
+                km::k_merge_rows<2><<<ctx->G, 288, 0, ctx->stream>>>(
                     ctx->cpart, ctx->n_chunks, ctx->K, ctx->part, ctx->G, ctx->st, ignore_done);
             else
-                km::k_merge_rows<3><<<ctx->G, 96, 0, ctx->stream>>>(
+                km::k_merge_rows<3><<<ctx->G, 288, 0, ctx->stream>>>(
                     ctx->cpart, ctx->n_chunks, ctx->K, ctx->part, ctx->G, ctx->st, ignore_done);
             ctx->launches += 1;
         }
@@ -430,10 +436,32 @@ kmeans_status launch_update(kmeans_ctx* ctx) {
     return KMEANS_OK;
 }
 
+// Single GPU and a small enough group table: merge + update in one block.
+bool fused_update(const kmeans_ctx* ctx) {
+    return !ctx->comm && (int64_t)ctx->nE * ctx->G <= 400000 && ctx->nE * 8 <= 48 * 1024;
+}
+
+kmeans_status launch_merge_update(kmeans_ctx* ctx) {
+    const int tpb = 1024;
+    const size_t sm = sizeof(double) * ctx->nE;
+    if (ctx->d == 2)
+        km::k_merge_update<2><<<1, tpb, sm, ctx->stream>>>(
+            ctx->part, ctx->G, ctx->nE, ctx->red, ctx->mu, ctx->K, ctx->st, ctx->trace_E,
+            ctx->trace_J, ctx->trace_cap, ctx->sorted ? ctx->cneg : nullptr);
+    else
+        km::k_merge_update<3><<<1, tpb, sm, ctx->stream>>>(
+            ctx->part, ctx->G, ctx->nE, ctx->red, ctx->mu, ctx->K, ctx->st, ctx->trace_E,
+            ctx->trace_J, ctx->trace_cap, ctx->sorted ? ctx->cneg : nullptr);
+    ctx->launches += 1;
+    CK(cudaGetLastError());
+    return KMEANS_OK;
+}
+
 // One iteration: assign+reduce, merge, [allreduce], update.
 kmeans_status enqueue_iteration(kmeans_ctx* ctx) {
     kmeans_status s;
     if ((s = launch_assign(ctx, km::kModeReduce, 0, 0)) != KMEANS_OK) return s;
+    if (fused_update(ctx)) return launch_merge_update(ctx);
     if ((s = launch_merge(ctx, 0)) != KMEANS_OK) return s;
     if ((s = allreduce(ctx, ctx->red, ctx->nE)) != KMEANS_OK) return s;
     return launch_update(ctx);
