@@ -293,18 +293,12 @@ def main():
     ms_per_step = ms / args.steps
 
     # ---- dominant kernel alone (roofline): assign + fused reduction ------------
-    def time_assign(c):
-        st_ = torch.cuda.ExternalStream(c.stream)
+    def time_assign(c, stage=1):
+        # stage 1: the assign kernels alone (kmeans_profile_stage): `reps`
+        # launches captured in one CUDA graph, CUDA events on the library's
+        # stream around the graph launch -> device ms per launch
         reps = max(20, min(args.steps, 200))
-        c.profile_assign(3)
-        torch.cuda.synchronize()
-        a0 = torch.cuda.Event(enable_timing=True)
-        a1 = torch.cuda.Event(enable_timing=True)
-        a0.record(st_)
-        c.profile_assign(reps)
-        a1.record(st_)
-        a1.synchronize()
-        return a0.elapsed_time(a1) / reps / 1e3        # s per launch
+        return c.profile_stage(reps, stage, timed=True) / 1e3   # s per launch
 
     n_local = b - a
     hbm_gbs, sm_max_mhz, peak_src = peaks()
@@ -338,8 +332,14 @@ def main():
                     hbm_frac=ach_gbs / hbm_gbs, **common)
 
     t_assign = time_assign(ctx)
-    kname = "k_assign_pruned" if info["sorted"] else ("k_assign_chunk" if info["path"] == 0
-                                                       else "k_assign_large")
+    if info["sorted"]:
+        kname = "k_assign_pruned" if info["path"] == 0 else "k_prune+k_assign_pruned+k_assign_heavy"
+    else:
+        kname = "k_assign_chunk" if info["path"] == 0 else "k_assign_large"
+    # per-stage device time (each stage alone, back-to-back launches)
+    stage_ms = {"assign": t_assign * 1e3, "row_merge": time_assign(ctx, 2) * 1e3}
+    stage_ms["merge_update_and_gaps"] = ms_per_step - stage_ms["assign"] - stage_ms["row_merge"]
+    stage_ms["k_merge_alone"] = time_assign(ctx, 3) * 1e3   # the P>1 path's group merge
     roofline = roofline_of(t_assign, kname, bool(info["sorted"]))
     roofline_hbm = {"achieved": bytes_per_launch / t_assign / 1e9, "peak": hbm_gbs, "unit": "GB/s",
                     "frac": bytes_per_launch / t_assign / 1e9 / hbm_gbs,
@@ -400,7 +400,7 @@ def main():
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(w, P, args.scaling),
-            "roofline": roofline, "roofline_hbm": roofline_hbm,
+            "roofline": roofline, "roofline_hbm": roofline_hbm, "stage_ms": stage_ms,
             "roofline_fullscan": fullscan, "candidates": cand,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "kernels_per_step": info["kernels_per_iter"],

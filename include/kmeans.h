@@ -153,10 +153,26 @@ kmeans_status kmeans_read_centroids(kmeans_ctx* ctx, double* centroids);
  * i.e. the labels of the last completed iteration (t >= 1).  Synchronous. */
 kmeans_status kmeans_final_labels(kmeans_ctx* ctx, int32_t* labels);
 
-/* Profiling aid (bench.py's roofline): enqueues n launches of the
- * assign+reduce kernel alone at the current mu^t (no merge / update, the
- * iteration state is unchanged).  Returns without synchronising. */
+/* Profiling aid (bench.py's roofline): enqueues n passes of the assignment
+ * step with its fused per-chunk reduction at the current mu^t -- the assign
+ * kernels plus the chunk-row merge, no group merge / update; the iteration
+ * state is unchanged.  Returns without synchronising.  Same as
+ * kmeans_profile_stage(ctx, n, 0). */
 kmeans_status kmeans_profile_assign(kmeans_ctx* ctx, int n);
+
+/* Profiling aid: n launches of one stage of the iteration, state unchanged:
+ *   stage 0  assign kernels + chunk-row merge (= kmeans_profile_assign)
+ *   stage 1  the assign kernels alone ([prune], assign+reduce, [heavy]) --
+ *            the dominant kernel bench.py reports the roofline of
+ *   stage 2  the chunk-row merge alone (k_merge_sparse16 / k_merge_rows /
+ *            k_merge_sparse; nothing on the unsorted large-K path)
+ *   stage 3  the group merge (k_merge) alone
+ * ms_per_launch NULL: enqueues the launches and returns without synchronising.
+ * ms_per_launch non-NULL: captures the n launches in a CUDA graph, runs it
+ * once untimed and once between two CUDA events on the context's stream, and
+ * writes the device time per launch (synchronous; excludes host launch cost).
+ * KMEANS_EINVAL if n < 0 or stage is not 0..3. */
+kmeans_status kmeans_profile_stage(kmeans_ctx* ctx, int n, int stage, float* ms_per_launch);
 
 /* Sorted path: centroid candidates per 2048-point chunk in the last assign
  * pass -- mean, maximum, number of single-candidate chunks, number of chunks

@@ -181,7 +181,12 @@ constexpr int kChunkTiles = KM_CHUNK_TILES;
 constexpr int kChunkPoints = kLaneTile * kChunkTiles;    // 2048
 constexpr int kStages = 3;
 constexpr int kGroupChunks = 64;
-constexpr int kRowGroup = 256;   // chunks per group, dense / <=16-entry rows
+#ifndef KM_ROW_GROUP
+#define KM_ROW_GROUP 256
+#endif
+constexpr int kRowGroup = KM_ROW_GROUP;   // chunks per group, sorted small-K rows (k_merge_sparse16)
+constexpr int kMergeWarps = kRowGroup / 32;
+constexpr int kDenseGroup = 256;   // chunks per group, dense rows (k_merge_rows)
 constexpr int kRowDoubles = 16 * 4 + 2;                  // [k][Sx Sy Sz n] + J + pad
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -1517,82 +1522,172 @@ k_merge_sparse(const double* __restrict__ rows, int row_stride, int n_chunks, in
 }
 
 // ---------------------------------------------------------------------------
-// k_merge_sparse16 (sorted path, K <= 16): group g = chunks [256 g, 256 (g+1)),
-// one thread per chunk row in the head phase.  Warp w takes its 32 chunks in
-// ascending order; for chunk j the lanes 0 .. 2 ncand_j - 1 each hold one
-// double2 of the row's entries (ncand <= 16 -> <= 32 double2) and add it into
-// the warp's K-table T[w][k] (distinct k within a row: no conflicts).  The 8
-// warp tables are then added in warp order -> gpart[e][g].  Fixed order, no
-// atomics; only the rows' written entries are read.
+// block_merge_groups: rs[e] = red[e] = sum over the G group columns of part
+// [e][G], in the order of k_merge (lane l: groups l, l + 32, ... ascending,
+// then a butterfly over the lanes) -- bit-identical to k_merge.  Warp w takes
+// entries w, w + nwarp, ... four at a time so that 16 loads are in flight per
+// lane.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void block_merge_groups(const double* part, int G, int nE,
+                                                   double* rs, double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    for (int e0 = warp; e0 < nE; e0 += 4 * nwarp) {
+        double v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+        for (int b = lane; b < G; b += 32) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int e = e0 + r * nwarp;
+                if (e < nE) v[r] += part[(size_t)e * G + b];
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v[r] += __shfl_xor_sync(0xffffffffu, v[r], o);
+            const int e = e0 + r * nwarp;
+            if (lane == 0 && e < nE) {
+                rs[e] = v[r];
+                red[e] = v[r];
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_merge_sparse16 (sorted path, K <= 16): group g = chunks [1024 g, 1024 (g+1)),
+// thread = chunk.  Each lane holds its row's head and up to kMergeRegs entries
+// in registers (two loaded speculatively with the head, the rest in one more
+// round when some lane needs them); then for every k present in the warp
+// (ascending) the 32 lanes' contributions are added by a fixed butterfly, and
+// the 32 warp results in warp order -> gpart[e][g].  Entries beyond kMergeRegs
+// (rare) are added afterwards, rows in lane order.  Fixed order, no atomics.
+// ---------------------------------------------------------------------------
+constexpr int kMergeRegs = 6;
+
 template <int D>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kRowGroup)
 k_merge_sparse16(const double* __restrict__ cpart, int n_chunks, int K, double* __restrict__ gpart,
                  int n_groups, const DevState* __restrict__ st, int ignore_done) {
-    if (!ignore_done && st->done) return;
-    __shared__ double2 T[8][16][2];   // [warp][k]{(Sx, Sy), (Sz, n)}
-    __shared__ double WJ[8];
+    __shared__ double T[kMergeWarps][16][4];   // [warp][k]{Sx, Sy, Sz, n}
+    __shared__ double WJ[kMergeWarps];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = blockIdx.x;
     const int c = g * kRowGroup + tid;
-    reinterpret_cast<double2*>(&T[0][0][0])[tid] = make_double2(0.0, 0.0);   // 8*16*2 = 256
+    const double* row = cpart + (size_t)c * kRowDoubles;
+    const double2* ent = reinterpret_cast<const double2*>(row + kRowHead);
+    // round 1 (independent loads): done flag, head, entry slots 0 and 1
+    const int done = ignore_done ? 0 : st->done;
     double2 head = make_double2(0.0, 0.0);
-    if (c < n_chunks) head = *reinterpret_cast<const double2*>(cpart + (size_t)c * kRowDoubles);
-    const int my_n = (int)head.y;
+    double2 ea[kMergeRegs], eb[kMergeRegs];
+#pragma unroll
+    for (int i = 0; i < kMergeRegs; ++i) ea[i] = eb[i] = make_double2(0.0, 0.0);
+    if (c < n_chunks) {
+        head = *reinterpret_cast<const double2*>(row);
+        ea[0] = ent[0];
+        eb[0] = ent[1];
+        ea[1] = ent[2];
+        eb[1] = ent[3];
+    }
+    if (done) return;
+    for (int i = tid; i < kMergeWarps * 32; i += blockDim.x)   // kMergeWarps * 64 doubles
+        reinterpret_cast<double2*>(&T[0][0][0])[i] = make_double2(0.0, 0.0);
+    const int n = (int)head.y;
+    // round 2 (only warps with a longer row): entries 2 .. kMergeRegs - 1
+    if (__any_sync(0xffffffffu, n > 2)) {
+#pragma unroll
+        for (int i = 2; i < kMergeRegs; ++i)
+            if (i < n) {
+                ea[i] = ent[2 * i];
+                eb[i] = ent[2 * i + 1];
+            }
+    }
+    int kk[kMergeRegs];
+    unsigned kset = 0u;
+#pragma unroll
+    for (int i = 0; i < kMergeRegs; ++i) {
+        kk[i] = (i < n) ? __double2loint(eb[i].y) : -1;
+        if (i < n) kset |= 1u << kk[i];
+    }
     double J = head.x;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
     if (lane == 0) WJ[warp] = J;
+    unsigned m = __reduce_or_sync(0xffffffffu, kset);
     __syncthreads();   // T zeroed
-    // entries: lane l holds double2 l of chunk (warp base + j); 8 chunks in flight
-    const int cbase = g * kRowGroup + warp * 32;
-#pragma unroll 1
-    for (int j0 = 0; j0 < 32; j0 += 8) {
-        double2 v[8];
+    while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        double sx = 0.0, sy = 0.0, sz = 0.0, cn = 0.0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int nj = __shfl_sync(0xffffffffu, my_n, j0 + j);
-            v[j] = make_double2(0.0, 0.0);
-            if (lane < 2 * nj)
-                v[j] = reinterpret_cast<const double2*>(cpart + (size_t)(cbase + j0 + j) * kRowDoubles +
-                                                        kRowHead)[lane];
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int nj = __shfl_sync(0xffffffffu, my_n, j0 + j);
-            // k of entry (lane >> 1) sits in the low word of the odd double2's .y
-            const double kn = __shfl_sync(0xffffffffu, v[j].y, lane | 1);
-            const int k = __double2loint(kn);
-            if (lane < 2 * nj) {
-                double2 a = T[warp][k][lane & 1];
-                a.x += v[j].x;
-                a.y += (lane & 1) ? (double)__double2hiint(v[j].y) : v[j].y;
-                T[warp][k][lane & 1] = a;
+        for (int i = 0; i < kMergeRegs; ++i)
+            if (kk[i] == k) {
+                sx = ea[i].x;
+                sy = ea[i].y;
+                sz = eb[i].x;
+                cn = (double)__double2hiint(eb[i].y);
             }
-            __syncwarp();
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sx += __shfl_xor_sync(0xffffffffu, sx, o);
+            sy += __shfl_xor_sync(0xffffffffu, sy, o);
+            if (D == 3) sz += __shfl_xor_sync(0xffffffffu, sz, o);
+            cn += __shfl_xor_sync(0xffffffffu, cn, o);
+        }
+        if (lane == 0) {
+            T[warp][k][0] = sx;
+            T[warp][k][1] = sy;
+            T[warp][k][2] = sz;
+            T[warp][k][3] = cn;
         }
     }
+    // entries kMergeRegs.. of the (rare) longer rows: rows in lane order, the
+    // warp loading one row's extra entries at a time (distinct k within a row)
+    unsigned more = __ballot_sync(0xffffffffu, n > kMergeRegs);
+    const double2* wrow = reinterpret_cast<const double2*>(
+        cpart + (size_t)(g * kRowGroup + warp * 32) * kRowDoubles + kRowHead) + 2 * kMergeRegs;
+    constexpr int kRowD2 = kRowDoubles / 2;
+    // software-pipelined: the next long row's entries load while this one is added
+    int j = more ? __ffs(more) - 1 : 0;
+    int nx = __shfl_sync(0xffffffffu, n, j) - kMergeRegs;
+    double2 v = make_double2(0.0, 0.0);
+    if (more && lane < 2 * nx) v = wrow[(size_t)j * kRowD2 + lane];   // nx <= 16 - kMergeRegs
+    while (more) {
+        more &= more - 1;
+        const int jn = more ? __ffs(more) - 1 : 0;
+        const int nxn = __shfl_sync(0xffffffffu, n, jn) - kMergeRegs;
+        double2 vn = make_double2(0.0, 0.0);
+        if (more && lane < 2 * nxn) vn = wrow[(size_t)jn * kRowD2 + lane];
+        const double kn = __shfl_sync(0xffffffffu, v.y, lane | 1);
+        if (lane < 2 * nx) {
+            double* t = &T[warp][__double2loint(kn)][2 * (lane & 1)];
+            t[0] += v.x;
+            t[1] += (lane & 1) ? (double)__double2hiint(v.y) : v.y;
+        }
+        __syncwarp();
+        v = vn;
+        nx = nxn;
+    }
     __syncthreads();
-    if (tid > 64) return;
     if (tid == 64) {
         double s = 0.0;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) s += WJ[w];
+        for (int w = 0; w < kMergeWarps; ++w) s += WJ[w];
         gpart[(size_t)(K * D + K) * n_groups + g] = s;
-        return;
-    }
-    const int k = tid >> 2, j = tid & 3;
-    if (k >= K || (j >= D && j != 3)) return;
-    double s = 0.0;
+    } else if (tid < 64) {
+        const int k = tid >> 2, q = tid & 3;
+        if (k < K && (q < D || q == 3)) {
+            double s = 0.0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) s += reinterpret_cast<const double*>(&T[w][k][0])[j];
-    if (j < D) gpart[(size_t)(k * D + j) * n_groups + g] = s;
-    else gpart[(size_t)(K * D + k) * n_groups + g] = s;
+            for (int w = 0; w < kMergeWarps; ++w) s += T[w][k][q];
+            if (q < D) gpart[(size_t)(k * D + q) * n_groups + g] = s;
+            else gpart[(size_t)(K * D + k) * n_groups + g] = s;
+        }
+    }
 }
 
-// ---------------------------------------------------------------------------
 // k_merge_rows (dense rows): group g sums the rows of chunks
-// [kRowGroup g, kRowGroup (g+1)).  Thread (r, q), r < 4, sums entry q of rows
+// [kDenseGroup g, kDenseGroup (g+1)).  Thread (r, q), r < 4, sums entry q of rows
 // c0 + r, c0 + r + 4, ... in ascending order; the four stripes are then added
 // in order r = 0..3 -- a fixed summation tree.  Scatters to gpart[e][g].
 // ---------------------------------------------------------------------------
@@ -1605,8 +1700,8 @@ k_merge_rows(const double* __restrict__ cpart, int n_chunks, int K, double* __re
     const int tid = threadIdx.x;
     const int r = tid / 65, q = tid - 65 * r;   // stripe, row entry (64 = J)
     const int g = blockIdx.x;
-    const int c0 = g * kRowGroup;
-    const int c1 = min(n_chunks, c0 + kRowGroup);
+    const int c0 = g * kDenseGroup;
+    const int c1 = min(n_chunks, c0 + kDenseGroup);
     if (r < 4) {
         double v = 0.0;
 #pragma unroll 8
@@ -1814,7 +1909,7 @@ template <int D>
 __device__ void update_body(double* __restrict__ mu_buf, int K, const double* red,
                             DevState* __restrict__ st, double* __restrict__ trace_E,
                             double* __restrict__ trace_J, int trace_cap,
-                            float4* __restrict__ cneg, unsigned* __restrict__ work) {
+                            float4* __restrict__ cneg) {
     __shared__ double red_sm[32];
     const int t = st->t;
     const double* mu_old = mu_buf + (size_t)(t & 1) * K * D;
@@ -1856,7 +1951,6 @@ __device__ void update_body(double* __restrict__ mu_buf, int K, const double* re
             }
             st->t = t + 1;
             st->done = (E < st->tol) || (t + 1 >= st->max_iter);
-            if (work) *work = 0u;
         }
     }
 }
@@ -1867,7 +1961,7 @@ __global__ void k_update(double* __restrict__ mu_buf, int K, const double* __res
                          double* __restrict__ trace_J, int trace_cap,
                          float4* __restrict__ cneg) {
     if (st->done) return;
-    update_body<D>(mu_buf, K, red, st, trace_E, trace_J, trace_cap, cneg, nullptr);
+    update_body<D>(mu_buf, K, red, st, trace_E, trace_J, trace_cap, cneg);
 }
 
 // k_merge_update (single GPU): the group merge of k_merge and the update in one
@@ -1883,21 +1977,9 @@ k_merge_update(const double* __restrict__ part, int G, int nE, double* __restric
     if (st->done) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* rs = reinterpret_cast<double*>(smem_raw);   // [nE]
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-    for (int e = warp; e < nE; e += nwarp) {
-        const double* row = part + (size_t)e * G;
-        double v = 0.0;
-#pragma unroll 8
-        for (int b = lane; b < G; b += 32) v += row[b];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) {
-            rs[e] = v;
-            red[e] = v;
-        }
-    }
+    block_merge_groups(part, G, nE, rs, red);
     __syncthreads();
-    update_body<D>(mu_buf, K, rs, st, trace_E, trace_J, trace_cap, cneg, nullptr);
+    update_body<D>(mu_buf, K, rs, st, trace_E, trace_J, trace_cap, cneg);
 }
 
 }  // namespace km

@@ -88,7 +88,8 @@ struct kmeans_ctx {
     int* cand_count = nullptr;    // candidates per chunk, last assign (sorted only)
     int32_t* labels_sorted = nullptr;  // labels in sorted order (sorted only)
     int nE = 0;
-    cudaGraphExec_t graph = nullptr;
+    cudaGraphExec_t graph = nullptr;    // one iteration
+    cudaGraphExec_t graph_u = nullptr;  // kGraphUnroll iterations (fewer graph launches)
     int64_t launches = 0;
     kmeans_status sticky = KMEANS_OK;
     bool assigned = false;
@@ -252,7 +253,7 @@ kmeans_status configure(kmeans_ctx* ctx) {
         ctx->n_chunks = (int)((ctx->N + ctx->chunk_points - 1) / ctx->chunk_points);
         // small K: dense rows (k_merge_rows); large K: sparse rows (k_merge_sparse)
         ctx->row_stride = ctx->K <= 16 ? km::kRowDoubles : km::kRowHead + 4 * ctx->K;
-        // groups: 256 dense rows (k_merge_rows) or 64 sparse rows (k_merge_sparse)
+        // groups: 1024 rows (k_merge_sparse16) or 64 rows (k_merge_sparse, large K)
         ctx->G = ctx->K <= 16 ? (ctx->n_chunks + km::kRowGroup - 1) / km::kRowGroup
                               : (ctx->n_chunks + km::kGroupChunks - 1) / km::kGroupChunks;
         ctx->n_super = (ctx->n_chunks + km::kSuperChunks - 1) / km::kSuperChunks;
@@ -282,7 +283,7 @@ kmeans_status configure(kmeans_ctx* ctx) {
         ctx->chunk_points = km::kChunkPoints;
         ctx->n_chunks = (int)((ctx->N + ctx->chunk_points - 1) / ctx->chunk_points);
         ctx->row_stride = km::kRowDoubles;
-        ctx->G = (ctx->n_chunks + km::kRowGroup - 1) / km::kRowGroup;  // groups
+        ctx->G = (ctx->n_chunks + km::kDenseGroup - 1) / km::kDenseGroup;  // groups
     } else {
         int tpb = km::kLargeTPBMax;
         while (tpb > 64 && large_smem(ctx->d, ctx->K, tpb) > maxSmem - 4096) tpb -= 32;
@@ -304,14 +305,18 @@ kmeans_status configure(kmeans_ctx* ctx) {
     return KMEANS_OK;
 }
 
-kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_done) {
+// stages: 1 = the assign kernels ([prune], assign, [heavy]), 2 = the chunk-row
+// merge; 3 = both (the iteration).  Split only for kmeans_profile_stage.
+kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_done,
+                            int stages = 3) {
+    const bool A = stages & 1, Mg = (stages & 2) && (mode & km::kModeReduce);
     if ((mode & km::kModeLabels) && !ctx->labels) {
         CK(cudaMalloc(&ctx->labels, sizeof(int32_t) * ctx->ldx));
     }
     if (ctx->sorted) {
         if ((mode & km::kModeLabels) && !ctx->labels_sorted)
             CK(cudaMalloc(&ctx->labels_sorted, sizeof(int32_t) * ctx->ldx));
-        if (ctx->path == 1) {
+        if (A && ctx->path == 1) {
             // super-box candidate lists (large K)
             if (ctx->d == 2)
                 km::k_prune<2><<<ctx->n_super, 256, 0, ctx->stream>>>(
@@ -324,11 +329,12 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
             ctx->launches += 1;
         }
         PrunedFn f = pick_pruned(ctx->d, ctx->K, mode);
-        f<<<ctx->n_chunks, 32, ctx->smem, ctx->stream>>>(
+        if (A) f<<<ctx->n_chunks, 32, ctx->smem, ctx->stream>>>(
             ctx->X, ctx->N, ctx->K, ctx->cneg, ctx->st, mu_sel, ignore_done, ctx->cbox, ctx->slist,
             ctx->scount, ctx->cpart, ctx->row_stride, ctx->labels_sorted, ctx->cand_count,
             ctx->heavy, ctx->heavy_count);
-        if (ctx->path == 1) {
+        if (A) ctx->launches += 1;
+        if (A && ctx->path == 1) {
             HeavyFn hf = pick_heavy(ctx->d, mode);
             hf<<<ctx->heavy_grid, 256, ctx->heavy_smem, ctx->stream>>>(
                 ctx->X, ctx->N, ctx->K, ctx->cneg, ctx->st, mu_sel, ignore_done, ctx->cbox,
@@ -336,16 +342,16 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
                 ctx->labels_sorted);
             ctx->launches += 1;
         }
-        if ((mode & km::kModeReduce) && ctx->path == 0) {
+        if (Mg && ctx->path == 0) {
             // sparse chunk rows (<= 16 entries) -> group columns of part (fixed order)
             if (ctx->d == 2)
-                km::k_merge_sparse16<2><<<ctx->G, 256, 0, ctx->stream>>>(
+                km::k_merge_sparse16<2><<<ctx->G, km::kRowGroup, 0, ctx->stream>>>(
                     ctx->cpart, ctx->n_chunks, ctx->K, ctx->part, ctx->G, ctx->st, ignore_done);
             else
-                km::k_merge_sparse16<3><<<ctx->G, 256, 0, ctx->stream>>>(
+                km::k_merge_sparse16<3><<<ctx->G, km::kRowGroup, 0, ctx->stream>>>(
                     ctx->cpart, ctx->n_chunks, ctx->K, ctx->part, ctx->G, ctx->st, ignore_done);
             ctx->launches += 1;
-        } else if (mode & km::kModeReduce) {
+        } else if (Mg) {
             // sparse chunk rows -> group columns of part (fixed ascending order)
             if (ctx->d == 2)
                 km::k_merge_sparse<2><<<ctx->G, 256, ctx->merge_smem, ctx->stream>>>(
@@ -359,10 +365,11 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
         }
     } else if (ctx->path == 0) {
         ChunkFn f = pick_chunk(ctx->d, ctx->K, mode);
-        f<<<ctx->n_chunks, 32, ctx->smem, ctx->stream>>>(ctx->X, ctx->N, ctx->K, ctx->mu, ctx->st,
+        if (A) f<<<ctx->n_chunks, 32, ctx->smem, ctx->stream>>>(ctx->X, ctx->N, ctx->K, ctx->mu, ctx->st,
                                                          mu_sel, ignore_done, ctx->cpart,
                                                          ctx->labels);
-        if (mode & km::kModeReduce) {
+        if (A) ctx->launches += 1;
+        if (Mg) {
             // chunk rows -> group columns of part (fixed ascending order)
             if (ctx->d == 2)
                 km::k_merge_rows<2><<<ctx->G, 288, 0, ctx->stream>>>(
@@ -374,13 +381,13 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
         }
     } else {
         LargeFn f = pick_large(ctx->d, mode);
-        f<<<ctx->G, ctx->tpb, ctx->smem, ctx->stream>>>(ctx->X, ctx->ldx, ctx->N, ctx->K, ctx->mu,
+        if (A) ctx->launches += 1;
+        if (A) f<<<ctx->G, ctx->tpb, ctx->smem, ctx->stream>>>(ctx->X, ctx->ldx, ctx->N, ctx->K, ctx->mu,
                                                         ctx->st, mu_sel, ignore_done, ctx->part,
                                                         ctx->labels);
     }
-    ctx->launches += 1;
     CK(cudaGetLastError());
-    if ((mode & km::kModeLabels) && ctx->sorted) {
+    if (A && (mode & km::kModeLabels) && ctx->sorted) {
         // back to the caller's order
         const int blocks = (int)std::min<int64_t>((ctx->N + 255) / 256, 148 * 8);
         km::k_scatter_labels<<<blocks, 256, 0, ctx->stream>>>(ctx->labels_sorted, ctx->perm,
@@ -467,12 +474,14 @@ kmeans_status enqueue_iteration(kmeans_ctx* ctx) {
     return launch_update(ctx);
 }
 
-kmeans_status ensure_graph(kmeans_ctx* ctx) {
-    if (ctx->graph) return KMEANS_OK;
+constexpr int kGraphUnroll = 8;
+
+kmeans_status capture_iterations(kmeans_ctx* ctx, int n, cudaGraphExec_t* out) {
     cudaGraph_t g = nullptr;
     CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     const int64_t before = ctx->launches;
-    kmeans_status s = enqueue_iteration(ctx);
+    kmeans_status s = KMEANS_OK;
+    for (int i = 0; i < n && s == KMEANS_OK; ++i) s = enqueue_iteration(ctx);
     cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
     ctx->launches = before;  // capture is not a launch
     if (s != KMEANS_OK) {
@@ -480,9 +489,19 @@ kmeans_status ensure_graph(kmeans_ctx* ctx) {
         return s;
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamEndCapture");
-    e = cudaGraphInstantiate(&ctx->graph, g, 0);
+    e = cudaGraphInstantiate(out, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaGraphInstantiate");
+    return KMEANS_OK;
+}
+
+// The iteration as CUDA graphs: one iteration, and kGraphUnroll iterations
+// back to back (the device stop flag makes iterations after convergence no-ops).
+kmeans_status ensure_graph(kmeans_ctx* ctx) {
+    kmeans_status s;
+    if (!ctx->graph && (s = capture_iterations(ctx, 1, &ctx->graph)) != KMEANS_OK) return s;
+    if (!ctx->graph_u && (s = capture_iterations(ctx, kGraphUnroll, &ctx->graph_u)) != KMEANS_OK)
+        return s;
     return KMEANS_OK;
 }
 
@@ -525,6 +544,8 @@ kmeans_status ensure_trace(kmeans_ctx* ctx, int cap) {
     if (ctx->graph) {
         cudaGraphExecDestroy(ctx->graph);  // captured the old trace pointers
         ctx->graph = nullptr;
+        if (ctx->graph_u) cudaGraphExecDestroy(ctx->graph_u);
+        ctx->graph_u = nullptr;
     }
     cudaFree(ctx->trace_E);
     cudaFree(ctx->trace_J);
@@ -685,6 +706,7 @@ void kmeans_destroy(kmeans_ctx* ctx) {
         DeviceGuard g(ctx->device);
         if (ctx->stream) cudaStreamSynchronize(ctx->stream);
         if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
+        if (ctx->graph_u) cudaGraphExecDestroy(ctx->graph_u);
         cudaFree(ctx->X);
         cudaFree(ctx->mu);
         cudaFree(ctx->cneg);
@@ -914,10 +936,11 @@ kmeans_status kmeans_iterate(kmeans_ctx* ctx, int n) {
     DeviceGuard g(ctx->device);
     kmeans_status s = ensure_graph(ctx);
     if (s != KMEANS_OK) return s;
-    for (int i = 0; i < n; ++i) {
-        CK(cudaGraphLaunch(ctx->graph, ctx->stream));
-        ctx->launches += kernels_per_iter(ctx);
-    }
+    int i = 0;
+    for (; i + kGraphUnroll <= n; i += kGraphUnroll)
+        CK(cudaGraphLaunch(ctx->graph_u, ctx->stream));
+    for (; i < n; ++i) CK(cudaGraphLaunch(ctx->graph, ctx->stream));
+    ctx->launches += (int64_t)n * kernels_per_iter(ctx);
     return KMEANS_OK;
 }
 
@@ -1088,6 +1111,8 @@ kmeans_status kmeans_fit(const float* points, int64_t N, int d, int K, const int
     return s;
 }
 
+static kmeans_status enqueue_stage(kmeans_ctx* ctx, int n, int stage);
+
 kmeans_status kmeans_profile_assign(kmeans_ctx* ctx, int n) {
     CHECK_CTX(ctx);
     if (n < 0) {
@@ -1095,10 +1120,66 @@ kmeans_status kmeans_profile_assign(kmeans_ctx* ctx, int n) {
         return KMEANS_EINVAL;
     }
     DeviceGuard g(ctx->device);
+    return enqueue_stage(ctx, n, 0);
+}
+
+static kmeans_status enqueue_stage(kmeans_ctx* ctx, int n, int stage) {
     for (int i = 0; i < n; ++i) {
-        kmeans_status s = launch_assign(ctx, km::kModeReduce, 0, 1);
+        kmeans_status s;
+        if (stage == 0 || stage == 1)
+            s = launch_assign(ctx, km::kModeReduce, 0, 1, stage == 0 ? 3 : 1);
+        else if (stage == 2)
+            s = launch_assign(ctx, km::kModeReduce, 0, 1, 2);
+        else
+            s = launch_merge(ctx, 1);
         if (s != KMEANS_OK) return s;
     }
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_profile_stage(kmeans_ctx* ctx, int n, int stage, float* ms_per_launch) {
+    CHECK_CTX(ctx);
+    if (n < 0 || stage < 0 || stage > 3) {
+        set_error("n < 0 or stage not in {0, 1, 2, 3}");
+        return KMEANS_EINVAL;
+    }
+    DeviceGuard g(ctx->device);
+    if (!ms_per_launch) return enqueue_stage(ctx, n, stage);
+    // timed: the n launches captured in one graph (no host launch cost in the
+    // measurement), run once untimed, then once between two events
+    if (n == 0) {
+        *ms_per_launch = 0.f;
+        return KMEANS_OK;
+    }
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    const int64_t launches0 = ctx->launches;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    kmeans_status s = enqueue_stage(ctx, n, stage);
+    cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
+    if (s != KMEANS_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return s;
+    }
+    CK(ce);
+    ctx->launches = launches0 + 2 * (ctx->launches - launches0);   // two graph runs
+    ce = cudaGraphInstantiate(&exec, graph, 0);
+    if (ce == cudaSuccess) ce = cudaEventCreate(&e0);
+    if (ce == cudaSuccess) ce = cudaEventCreate(&e1);
+    if (ce == cudaSuccess) ce = cudaGraphLaunch(exec, ctx->stream);
+    if (ce == cudaSuccess) ce = cudaEventRecord(e0, ctx->stream);
+    if (ce == cudaSuccess) ce = cudaGraphLaunch(exec, ctx->stream);
+    if (ce == cudaSuccess) ce = cudaEventRecord(e1, ctx->stream);
+    if (ce == cudaSuccess) ce = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    if (ce == cudaSuccess) ce = cudaEventElapsedTime(&ms, e0, e1);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (exec) cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    CK(ce);
+    *ms_per_launch = ms / n;
     return KMEANS_OK;
 }
 

@@ -62,6 +62,7 @@ SIGNATURES = {
     "kmeans_read_centroids": (I, [P, P]),
     "kmeans_final_labels": (I, [P, P]),
     "kmeans_profile_assign": (I, [P, I]),
+    "kmeans_profile_stage": (I, [P, I, I, P]),
     "kmeans_candidate_stats": (I, [P, P, P, P, P]),
     "kmeans_get_stream": (I, [P, P]),
     "kmeans_get_info": (I, [P, P]),
@@ -246,8 +247,21 @@ class Context:
         return out
 
     def profile_assign(self, n: int):
-        """Enqueue n launches of the assign+reduce kernel alone (no state change)."""
+        """Enqueue n assignment passes (assign kernels + chunk-row merge; no state change)."""
         _check(lib().kmeans_profile_assign(self._h, int(n)), "kmeans_profile_assign")
+
+    def profile_stage(self, n: int, stage: int, timed: bool = False):
+        """n launches of one iteration stage (see kmeans_profile_stage).  timed:
+        run them as one CUDA graph between two events and return ms per launch;
+        else enqueue them and return None."""
+        if not timed:
+            _check(lib().kmeans_profile_stage(self._h, int(n), int(stage), None),
+                   "kmeans_profile_stage")
+            return None
+        ms = ctypes.c_float()
+        _check(lib().kmeans_profile_stage(self._h, int(n), int(stage), ctypes.byref(ms)),
+               "kmeans_profile_stage")
+        return ms.value
 
     def candidate_stats(self) -> dict:
         """Sorted path: centroid candidates per chunk in the last assign pass."""

@@ -93,6 +93,7 @@ def test_invalid_arguments_rejected_before_device_work(km):
     # NULL context
     assert L.kmeans_iterate(None, 1) == -1
     assert L.kmeans_update(None, None, None) == -1
+    assert L.kmeans_profile_stage(None, 1, 1, None) == -1
     L.kmeans_destroy(None)  # NULL-safe
     assert L.kmeans_last_error()  # a message was recorded
 

@@ -300,6 +300,32 @@ def test_errors():
 
 
 @pytest.mark.parametrize("sort", SORT)
+@pytest.mark.parametrize("K", [8, 40])
+def test_profile_stages_leave_state(sort, K):
+    """kmeans_profile_stage (bench.py's per-stage timing) does not move the
+    iteration: after timed launches of every stage the fit continues exactly."""
+    w = datagen.WORKLOADS["C2"]
+    X = datagen.generate(w, N=200_000)
+    init = datagen.init_indices(w, N=200_000)[:8]
+    init = np.concatenate([init, np.arange(1000, 1000 + K - 8)]) if K > 8 else init
+    with km.Context(X, K, sort=sort) as c:
+        ref = c.fit(init, 0.0, 5)
+        c.start(init_idx=init, tol=0.0, max_iter=5)
+        c.iterate(2)
+        for stage in range(4):
+            ms = c.profile_stage(5, stage, timed=True)
+            assert ms >= 0.0
+        c.profile_stage(2, 1)
+        c.iterate(3)
+        st = c.poll()
+        assert st["iters"] == 5
+        assert np.array_equal(c.read_centroids(), ref["centroids"])
+        with pytest.raises(km.KMeansError) as e:
+            c.profile_stage(1, 4)
+        assert e.value.name == "KMEANS_EINVAL"
+
+
+@pytest.mark.parametrize("sort", SORT)
 def test_deterministic_bitwise(sort):
     w = datagen.WORKLOADS["NS"]
     X = datagen.generate(w, N=400_000)

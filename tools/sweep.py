@@ -47,14 +47,10 @@ def main():
         ctx.iterate(a.iters)
         ctx.poll()
         st = torch.cuda.ExternalStream(ctx.stream)
-        ctx.profile_assign(3)
+        t = ctx.profile_stage(a.reps, 1, timed=True)        # assign kernels alone
+        t_rm = ctx.profile_stage(a.reps, 2, timed=True)     # chunk-row merge alone
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        ctx.profile_assign(a.reps)
-        e1.record(st)
-        e1.synchronize()
-        t = e0.elapsed_time(e1) / a.reps
         e0.record(st)
         ctx.iterate(a.reps)
         e1.record(st)
@@ -63,7 +59,7 @@ def main():
         info = ctx.info()
         cand = ctx.candidate_stats() if info["sorted"] else {}
         gbs = 4 * w.d * w.N / (t / 1e3) / 1e9
-        print(json.dumps({"lib": os.path.basename(lib), "assign_ms": round(t, 4),
+        print(json.dumps({"lib": os.path.basename(lib), "assign_ms": round(t, 4), "row_merge_ms": round(t_rm, 4),
                           "iter_ms": round(ti, 4), "hbm_frac": round(gbs / peak, 4),
                           "grid": info["grid"], "smem": info["smem_bytes"],
                           "cand_mean": round(cand.get("mean", 0), 3)}), flush=True)
