@@ -213,8 +213,14 @@ kmeans_status kmeans_comm_init(void** comm, int nranks, const unsigned char id[1
 kmeans_status kmeans_comm_destroy(void* comm);
 
 /* NULL-safe; frees all device memory of the context (not the caller's stream
- * or communicator). */
+ * or communicator).  Freed blocks go to a library-owned cache per device that
+ * the next kmeans_create reuses (no cudaMalloc / cudaFree of the point arrays
+ * on every create / destroy); a failing cudaMalloc empties the cache first. */
 void kmeans_destroy(kmeans_ctx* ctx);
+
+/* Returns the blocks the library cache of CUDA device `device` holds (memory
+ * of destroyed contexts) to the driver.  KMEANS_EINVAL for a bad device. */
+kmeans_status kmeans_release_memory(int device);
 
 const char* kmeans_status_string(kmeans_status s);
 const char* kmeans_last_error(void);

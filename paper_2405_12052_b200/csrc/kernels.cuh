@@ -82,15 +82,38 @@ __global__ void k_prep(const float* __restrict__ in, int64_t N, int d, int64_t s
 // allreduce over ranks then assembles mu^0 exactly: one x plus zeros).
 __global__ void k_init_gather(const float* __restrict__ X, int d, int K,
                               const int64_t* __restrict__ idx, int64_t offset, int64_t n_local,
-                              const int32_t* __restrict__ invperm, double* __restrict__ mu0) {
+                              const int32_t* __restrict__ pos, double* __restrict__ mu0) {
     int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= K * d) return;
     int k = q / d, j = q % d;
     int64_t i = idx[k] - offset;
-    if (invperm && i >= 0 && i < n_local) i = invperm[i];   // sorted layout
+    if (pos) i = pos[k];   // sorted layout: position found by k_find_pos (-1: not local)
     mu0[q] = (i >= 0 && i < n_local)
                  ? (double)X[(i >> 6) * (d * kWarpTile) + j * kWarpTile + (i & 63)]
                  : 0.0;
+}
+
+// Sorted layout: the sorted positions of the local initial indices.  pairs =
+// (local index, k) sorted by index (host-built, npairs <= K <= 1024, staged in
+// shared memory); every sorted position p looks its perm[p] up by binary
+// search and, on a hit, writes pos[k] = p.  (Replaces a full inverse
+// permutation: one coalesced pass over perm per kmeans_start.)
+__global__ void k_find_pos(const int32_t* __restrict__ perm, int64_t n, const int2* __restrict__ pairs,
+                           int npairs, int32_t* __restrict__ pos) {
+    __shared__ int2 sp[1024];
+    for (int t = threadIdx.x; t < npairs; t += blockDim.x) sp[t] = pairs[t];
+    __syncthreads();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
+        const int i = perm[p];
+        int lo = 0, hi = npairs;   // first pair with index >= i
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (sp[mid].x < i) lo = mid + 1;
+            else hi = mid;
+        }
+        if (lo < npairs && sp[lo].x == i) pos[sp[lo].y] = (int32_t)p;
+    }
 }
 
 // Per-block partial layout: part[e * G + b], e in [0, K*D + K + 1):
@@ -508,14 +531,14 @@ __device__ __forceinline__ unsigned long long part1by2_64(unsigned long long x) 
     return x;
 }
 
-// 64-bit Morton key of every point (21 bits per axis in 3D, 32 in 2D) on an
+// 64-bit Morton key of every point (qbits <= 21 bits per axis in 3D, <= 32 in 2D) on an
 // isotropic grid over the global box -- cubic cells keep chunk boxes compact
 // even when the box is very elongated (C5's far outliers), and the fine grid
 // keeps the dense regions resolved -- with the identity permutation as values.
 __global__ void k_morton(const float* __restrict__ in, int64_t N, int d, int64_t si, int64_t sj,
-                         const unsigned* __restrict__ box, unsigned long long* __restrict__ keys,
-                         int32_t* __restrict__ iota) {
-    const double qmax = (d == 2) ? 4294967295.0 : 2097151.0;
+                         const unsigned* __restrict__ box, int qbits,
+                         unsigned long long* __restrict__ keys, int32_t* __restrict__ iota) {
+    const double qmax = (double)((1ull << qbits) - 1ull);   // qbits <= 32 (2D), <= 21 (3D)
     double lo[3], sc[3], ext = 0.0;
     for (int j = 0; j < d; ++j) {
         lo[j] = (double)unord_f32(box[j]);
@@ -537,19 +560,35 @@ __global__ void k_morton(const float* __restrict__ in, int64_t N, int d, int64_t
     }
 }
 
-// Sorted AoSoA layout: point p (sorted position) = input point perm[p];
-// invperm[perm[p]] = p.  Padding points (p >= N) are zeros.
+// Sorted AoSoA layout: point p (sorted position) = input point perm[p].
+// Padding points (p >= N) are zeros.
 __global__ void k_gather_sorted(const float* __restrict__ in, int64_t N, int d, int64_t si,
                                 int64_t sj, const int32_t* __restrict__ perm,
-                                int32_t* __restrict__ invperm, float* __restrict__ out,
-                                int64_t ldx) {
+                                float* __restrict__ out, int64_t ldx) {
+    // U points per thread per pass, all their (random) loads in flight at once
+    constexpr int U = 8;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < ldx; p += stride) {
-        const int64_t i = (p < N) ? perm[p] : -1;
-        for (int j = 0; j < d; ++j)
-            out[(p >> 6) * (d * kWarpTile) + j * kWarpTile + (p & 63)] =
-                (i >= 0) ? in[i * si + (int64_t)j * sj] : 0.0f;
-        if (i >= 0) invperm[i] = (int32_t)p;
+    for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < ldx; p0 += U * stride) {
+        int64_t i[U];
+        float v[U][3];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t p = p0 + u * stride;
+            i[u] = (p < N) ? perm[p] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+                v[u][j] = (i[u] >= 0 && j < d) ? __ldg(in + i[u] * si + (int64_t)j * sj) : 0.0f;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t p = p0 + u * stride;
+            if (p >= ldx) break;
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+                if (j < d) out[(p >> 6) * (d * kWarpTile) + j * kWarpTile + (p & 63)] = v[u][j];
+        }
     }
 }
 

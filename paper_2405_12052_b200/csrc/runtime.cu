@@ -11,11 +11,15 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -27,6 +31,64 @@
 #include "kernels.cuh"
 
 using km::DevState;
+
+// ---------------------------------------------------------------------------
+// Device memory: a per-device cache of freed blocks in front of cudaMalloc
+// (like a caching allocator).  Blocks are returned to the cache only when idle
+// (every free site has synchronised the context's stream first), so a later
+// create reuses them without paying cudaMalloc / cudaFree of gigabytes again.
+// A failed cudaMalloc flushes the cache and retries; kmeans_release_memory
+// gives the cached blocks back to the driver.
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int kMaxDevices = 64;
+std::mutex g_mem_mu;
+std::multimap<size_t, void*> g_cache[kMaxDevices];   // size -> idle block
+std::unordered_map<void*, std::pair<int, size_t>> g_live;   // block -> (device, size)
+
+size_t round_block(size_t bytes) {
+    const size_t g = bytes >= (1u << 20) ? (2u << 20) : 512;
+    return (bytes + g - 1) / g * g;
+}
+
+void flush_cache_locked(int dev) {
+    for (auto& kv : g_cache[dev]) cudaFree(kv.second);
+    g_cache[dev].clear();
+}
+
+cudaError_t cached_malloc(int dev, void** p, size_t bytes) {
+    *p = nullptr;
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    const size_t sz = round_block(bytes ? bytes : 1);
+    std::lock_guard<std::mutex> lk(g_mem_mu);
+    auto& c = g_cache[dev];
+    auto it = c.lower_bound(sz);
+    if (it != c.end() && it->first <= sz + sz / 4 + (8u << 20)) {   // close fit only
+        *p = it->second;
+        g_live[*p] = {dev, it->first};
+        c.erase(it);
+        return cudaSuccess;
+    }
+    cudaError_t e = cudaMalloc(p, sz);
+    if (e != cudaSuccess) {   // give the cache back and retry once
+        cudaGetLastError();
+        flush_cache_locked(dev);
+        e = cudaMalloc(p, sz);
+    }
+    if (e == cudaSuccess) g_live[*p] = {dev, sz};
+    return e;
+}
+
+void cached_free(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_mem_mu);
+    auto it = g_live.find(p);
+    if (it == g_live.end()) return;
+    g_cache[it->second.first].emplace(it->second.second, p);
+    g_live.erase(it);
+}
+}  // namespace
+
 
 namespace {
 
@@ -83,7 +145,8 @@ struct kmeans_ctx {
     int heavy_grid = 0;
     bool sorted = false;          // points held in Morton order (path 0 default)
     int32_t* perm = nullptr;      // sorted position -> caller's index (sorted only)
-    int32_t* invperm = nullptr;   // caller's index -> sorted position (sorted only)
+    int2* init_pairs = nullptr;   // (local index, k) of the initial indices (sorted only)
+    int32_t* init_pos = nullptr;  // their sorted positions (k_find_pos)
     float* cbox = nullptr;        // per-chunk bounding boxes (sorted only)
     int* cand_count = nullptr;    // candidates per chunk, last assign (sorted only)
     int32_t* labels_sorted = nullptr;  // labels in sorted order (sorted only)
@@ -97,6 +160,34 @@ struct kmeans_ctx {
 };
 
 namespace {
+
+// KMEANS_TRACE=1: kmeans_create prints a per-phase timeline to stderr
+// (synchronising the stream at every mark -- a tuning aid, off by default).
+struct CreateTrace {
+    bool on = false;
+    std::chrono::steady_clock::time_point t0;
+    CreateTrace() {
+        const char* e = getenv("KMEANS_TRACE");
+        on = e && *e && *e != '0';
+        t0 = std::chrono::steady_clock::now();
+    }
+    void mark(cudaStream_t s, const char* what) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const double ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        fprintf(stderr, "[kmeans_create] %8.2f ms  %s\n", ms, what);
+    }
+};
+
+// Device allocation for a context (through the block cache).  Freed blocks
+// must be idle: callers synchronise ctx->stream before pool_free.
+template <class T>
+cudaError_t pool_alloc(kmeans_ctx* ctx, T** p, size_t bytes) {
+    return cached_malloc(ctx->device, reinterpret_cast<void**>(p), bytes);
+}
+
+void pool_free(kmeans_ctx*, void* p) { cached_free(p); }
 
 bool fused_update(const kmeans_ctx* ctx);
 
@@ -236,10 +327,10 @@ int large_smem(int d, int K, int tpb) {
 }
 
 kmeans_status configure(kmeans_ctx* ctx) {
-    cudaDeviceProp prop;
-    CK(cudaGetDeviceProperties(&prop, ctx->device));
-    const int sms = prop.multiProcessorCount;
-    const int maxSmem = (int)prop.sharedMemPerBlockOptin;
+    // (cudaDeviceGetAttribute: cudaGetDeviceProperties costs milliseconds)
+    int sms = 0, maxSmem = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    CK(cudaDeviceGetAttribute(&maxSmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
     ctx->nE = ctx->K * ctx->d + ctx->K + 1;
     ctx->path = ctx->K <= 16 ? 0 : 1;
     if (ctx->sorted) {
@@ -311,11 +402,11 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
                             int stages = 3) {
     const bool A = stages & 1, Mg = (stages & 2) && (mode & km::kModeReduce);
     if ((mode & km::kModeLabels) && !ctx->labels) {
-        CK(cudaMalloc(&ctx->labels, sizeof(int32_t) * ctx->ldx));
+        CK(pool_alloc(ctx, &ctx->labels, sizeof(int32_t) * ctx->ldx));
     }
     if (ctx->sorted) {
         if ((mode & km::kModeLabels) && !ctx->labels_sorted)
-            CK(cudaMalloc(&ctx->labels_sorted, sizeof(int32_t) * ctx->ldx));
+            CK(pool_alloc(ctx, &ctx->labels_sorted, sizeof(int32_t) * ctx->ldx));
         if (A && ctx->path == 1) {
             // super-box candidate lists (large K)
             if (ctx->d == 2)
@@ -547,12 +638,12 @@ kmeans_status ensure_trace(kmeans_ctx* ctx, int cap) {
         if (ctx->graph_u) cudaGraphExecDestroy(ctx->graph_u);
         ctx->graph_u = nullptr;
     }
-    cudaFree(ctx->trace_E);
-    cudaFree(ctx->trace_J);
+    pool_free(ctx, ctx->trace_E);
+    pool_free(ctx, ctx->trace_J);
     ctx->trace_E = ctx->trace_J = nullptr;
     ctx->trace_cap = 0;
-    if (cudaMalloc(&ctx->trace_E, sizeof(double) * cap) != cudaSuccess ||
-        cudaMalloc(&ctx->trace_J, sizeof(double) * cap) != cudaSuccess) {
+    if (pool_alloc(ctx, &ctx->trace_E, sizeof(double) * cap) != cudaSuccess ||
+        pool_alloc(ctx, &ctx->trace_J, sizeof(double) * cap) != cudaSuccess) {
         cudaGetLastError();
         set_error("trace allocation failed");
         return KMEANS_ENOMEM;
@@ -596,7 +687,8 @@ kmeans_status fetch_centroids(kmeans_ctx* ctx, const double* cent, std::vector<d
 
 // Morton-order the shard once (sorted path): global box + finiteness, keys,
 // stable CUB radix sort, gather into the AoSoA layout, per-chunk boxes.
-kmeans_status sort_points(kmeans_ctx* ctx, const float* src, int64_t si, int64_t sj) {
+kmeans_status sort_points(kmeans_ctx* ctx, const float* src, int64_t si, int64_t sj,
+                          CreateTrace& tr) {
     const int64_t N = ctx->N;
     const int d = ctx->d;
     unsigned* box = nullptr;
@@ -606,20 +698,22 @@ kmeans_status sort_points(kmeans_ctx* ctx, const float* src, int64_t si, int64_t
     size_t tmp_bytes = 0;
     kmeans_status st = KMEANS_OK;
     auto cleanup = [&]() {
-        cudaFree(box);
-        cudaFree(keys);
-        cudaFree(keys2);
-        cudaFree(iota);
-        cudaFree(tmp);
+        cudaStreamSynchronize(ctx->stream);   // temporaries idle before they are cached
+        pool_free(ctx, box);
+        pool_free(ctx, keys);
+        pool_free(ctx, keys2);
+        pool_free(ctx, iota);
+        pool_free(ctx, tmp);
     };
-    if (cudaMalloc(&ctx->perm, sizeof(int32_t) * N) != cudaSuccess ||
-        cudaMalloc(&ctx->invperm, sizeof(int32_t) * N) != cudaSuccess ||
-        cudaMalloc(&ctx->cbox, sizeof(float) * 2 * d * (size_t)ctx->n_chunks) != cudaSuccess ||
-        cudaMalloc(&ctx->cand_count, sizeof(int) * (size_t)ctx->n_chunks) != cudaSuccess ||
-        cudaMalloc(&box, sizeof(unsigned) * 6) != cudaSuccess ||
-        cudaMalloc(&keys, sizeof(unsigned long long) * N) != cudaSuccess ||
-        cudaMalloc(&keys2, sizeof(unsigned long long) * N) != cudaSuccess ||
-        cudaMalloc(&iota, sizeof(int32_t) * N) != cudaSuccess) {
+    if (pool_alloc(ctx, &ctx->perm, sizeof(int32_t) * N) != cudaSuccess ||
+        pool_alloc(ctx, &ctx->init_pairs, sizeof(int2) * ctx->K) != cudaSuccess ||
+        pool_alloc(ctx, &ctx->init_pos, sizeof(int32_t) * ctx->K) != cudaSuccess ||
+        pool_alloc(ctx, &ctx->cbox, sizeof(float) * 2 * d * (size_t)ctx->n_chunks) != cudaSuccess ||
+        pool_alloc(ctx, &ctx->cand_count, sizeof(int) * (size_t)ctx->n_chunks) != cudaSuccess ||
+        pool_alloc(ctx, &box, sizeof(unsigned) * 6) != cudaSuccess ||
+        pool_alloc(ctx, &keys, sizeof(unsigned long long) * N) != cudaSuccess ||
+        pool_alloc(ctx, &keys2, sizeof(unsigned long long) * N) != cudaSuccess ||
+        pool_alloc(ctx, &iota, sizeof(int32_t) * N) != cudaSuccess) {
         cudaGetLastError();
         cleanup();
         set_error("sort buffers: allocation failed");
@@ -630,24 +724,33 @@ kmeans_status sort_points(kmeans_ctx* ctx, const float* src, int64_t si, int64_t
         hb2[j] = 0xffffffffu;
         hb2[d + j] = 0u;
     }
+    // Morton resolution: 2^qbits cells per axis with qbits = ceil(log2 N / d) + 6
+    // (>= 64 cells per point per axis on average; sharper order buys nothing for
+    // 1024-point chunks), capped by the 64-bit key; the sort only visits d*qbits bits.
+    int lg = 1;
+    while (lg < 40 && (int64_t(1) << lg) < N) ++lg;
+    const int qbits = std::min(d == 2 ? 32 : 21, (lg + d - 1) / d + 6);
     const int blocks = (int)std::min<int64_t>((N + 255) / 256, 148 * 8);
     cudaError_t e = cudaMemcpyAsync(box, hb2, sizeof(unsigned) * 2 * d, cudaMemcpyHostToDevice,
                                     ctx->stream);
     if (e == cudaSuccess) {
         km::k_input_bbox<<<blocks, 256, 0, ctx->stream>>>(src, N, d, si, sj, box, ctx->flag);
-        km::k_morton<<<blocks, 256, 0, ctx->stream>>>(src, N, d, si, sj, box, keys, iota);
+        km::k_morton<<<blocks, 256, 0, ctx->stream>>>(src, N, d, si, sj, box, qbits, keys, iota);
         ctx->launches += 2;
+        tr.mark(ctx->stream, "bbox + morton keys");
         e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, iota, ctx->perm, N, 0,
-                                            64, ctx->stream);
+                                            d * qbits, ctx->stream);
     }
-    if (e == cudaSuccess) e = cudaMalloc(&tmp, tmp_bytes);
+    if (e == cudaSuccess) e = pool_alloc(ctx, &tmp, tmp_bytes);
     if (e == cudaSuccess)
-        e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, iota, ctx->perm, N, 0, 64,
-                                            ctx->stream);
+        e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, iota, ctx->perm, N, 0,
+                                            d * qbits, ctx->stream);
+    tr.mark(ctx->stream, "radix sort");
     if (e == cudaSuccess) {
         const int gb = (int)std::min<int64_t>((ctx->ldx + 255) / 256, 148 * 8);
         km::k_gather_sorted<<<gb, 256, 0, ctx->stream>>>(src, N, d, si, sj, ctx->perm,
-                                                         ctx->invperm, ctx->X, ctx->ldx);
+                                                         ctx->X, ctx->ldx);
+        tr.mark(ctx->stream, "gather");
         const int cb = (ctx->n_chunks * 32 + 255) / 256;
         km::k_chunk_bbox<<<cb, 256, 0, ctx->stream>>>(ctx->X, N, d, ctx->chunk_points,
                                                       ctx->n_chunks, ctx->cbox);
@@ -673,6 +776,20 @@ kmeans_status sort_points(kmeans_ctx* ctx, const float* src, int64_t si, int64_t
 extern "C" {
 
 int kmeans_abi_version(void) { return KMEANS_ABI_VERSION; }
+
+kmeans_status kmeans_release_memory(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n ||
+        device >= kMaxDevices) {
+        cudaGetLastError();
+        set_error("kmeans_release_memory: bad device %d", device);
+        return KMEANS_EINVAL;
+    }
+    DeviceGuard g(device);
+    std::lock_guard<std::mutex> lk(g_mem_mu);
+    flush_cache_locked(device);
+    return KMEANS_OK;
+}
 
 const char* kmeans_last_error(void) { return g_last_error.c_str(); }
 
@@ -707,28 +824,29 @@ void kmeans_destroy(kmeans_ctx* ctx) {
         if (ctx->stream) cudaStreamSynchronize(ctx->stream);
         if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
         if (ctx->graph_u) cudaGraphExecDestroy(ctx->graph_u);
-        cudaFree(ctx->X);
-        cudaFree(ctx->mu);
-        cudaFree(ctx->cneg);
-        cudaFree(ctx->part);
-        cudaFree(ctx->red);
-        cudaFree(ctx->st);
-        cudaFree(ctx->trace_E);
-        cudaFree(ctx->trace_J);
-        cudaFree(ctx->labels);
-        cudaFree(ctx->idx_dev);
-        cudaFree(ctx->flag);
-        cudaFree(ctx->cpart);
-        cudaFree(ctx->sbox);
-        cudaFree(ctx->slist);
-        cudaFree(ctx->scount);
-        cudaFree(ctx->heavy);
-        cudaFree(ctx->heavy_count);
-        cudaFree(ctx->perm);
-        cudaFree(ctx->invperm);
-        cudaFree(ctx->cbox);
-        cudaFree(ctx->cand_count);
-        cudaFree(ctx->labels_sorted);
+        pool_free(ctx, ctx->X);
+        pool_free(ctx, ctx->mu);
+        pool_free(ctx, ctx->cneg);
+        pool_free(ctx, ctx->part);
+        pool_free(ctx, ctx->red);
+        pool_free(ctx, ctx->st);
+        pool_free(ctx, ctx->trace_E);
+        pool_free(ctx, ctx->trace_J);
+        pool_free(ctx, ctx->labels);
+        pool_free(ctx, ctx->idx_dev);
+        pool_free(ctx, ctx->flag);
+        pool_free(ctx, ctx->cpart);
+        pool_free(ctx, ctx->sbox);
+        pool_free(ctx, ctx->slist);
+        pool_free(ctx, ctx->scount);
+        pool_free(ctx, ctx->heavy);
+        pool_free(ctx, ctx->heavy_count);
+        pool_free(ctx, ctx->perm);
+        pool_free(ctx, ctx->init_pairs);
+        pool_free(ctx, ctx->init_pos);
+        pool_free(ctx, ctx->cbox);
+        pool_free(ctx, ctx->cand_count);
+        pool_free(ctx, ctx->labels_sorted);
         if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
         cudaGetLastError();
     }
@@ -737,6 +855,7 @@ void kmeans_destroy(kmeans_ctx* ctx) {
 
 kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, int d, int K,
                             const kmeans_opts* opts_in) {
+    CreateTrace tr;
     if (!out) {
         set_error("out is NULL");
         return KMEANS_EINVAL;
@@ -803,30 +922,32 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
     ctx->sorted = !(opts.flags & KMEANS_FLAG_NO_SORT);
     kmeans_status s = configure(ctx);
     if (s != KMEANS_OK) return fail(s);
+    tr.mark(ctx->stream, "stream + configure");
 
     const int Kpad = K + 16;
     size_t bytesX = sizeof(float) * (size_t)d * ctx->ldx;
-    if (cudaMalloc(&ctx->X, bytesX) != cudaSuccess ||
-        cudaMalloc(&ctx->mu, sizeof(double) * 2 * Kpad * d) != cudaSuccess ||
-        cudaMalloc(&ctx->cneg, sizeof(float4) * 2 * Kpad) != cudaSuccess ||
-        cudaMalloc(&ctx->part, sizeof(double) * (size_t)ctx->nE * ctx->G) != cudaSuccess ||
-        cudaMalloc(&ctx->red, sizeof(double) * ctx->nE) != cudaSuccess ||
-        cudaMalloc(&ctx->st, sizeof(DevState)) != cudaSuccess ||
-        cudaMalloc(&ctx->idx_dev, sizeof(int64_t) * K) != cudaSuccess ||
+    if (pool_alloc(ctx, &ctx->X, bytesX) != cudaSuccess ||
+        pool_alloc(ctx, &ctx->mu, sizeof(double) * 2 * Kpad * d) != cudaSuccess ||
+        pool_alloc(ctx, &ctx->cneg, sizeof(float4) * 2 * Kpad) != cudaSuccess ||
+        pool_alloc(ctx, &ctx->part, sizeof(double) * (size_t)ctx->nE * ctx->G) != cudaSuccess ||
+        pool_alloc(ctx, &ctx->red, sizeof(double) * ctx->nE) != cudaSuccess ||
+        pool_alloc(ctx, &ctx->st, sizeof(DevState)) != cudaSuccess ||
+        pool_alloc(ctx, &ctx->idx_dev, sizeof(int64_t) * K) != cudaSuccess ||
         ((ctx->path == 0 || ctx->sorted) &&
-         cudaMalloc(&ctx->cpart, sizeof(double) * ctx->row_stride * (size_t)ctx->n_chunks) !=
+         pool_alloc(ctx, &ctx->cpart, sizeof(double) * ctx->row_stride * (size_t)ctx->n_chunks) !=
              cudaSuccess) ||
         (ctx->sorted && ctx->path == 1 &&
-         (cudaMalloc(&ctx->sbox, sizeof(float) * 2 * d * (size_t)ctx->n_super) != cudaSuccess ||
-          cudaMalloc(&ctx->slist, sizeof(int) * (size_t)K * ctx->n_super) != cudaSuccess ||
-          cudaMalloc(&ctx->scount, sizeof(int) * (size_t)ctx->n_super) != cudaSuccess ||
-          cudaMalloc(&ctx->heavy, sizeof(int) * (size_t)ctx->n_chunks) != cudaSuccess ||
-          cudaMalloc(&ctx->heavy_count, sizeof(int)) != cudaSuccess)) ||
-        cudaMalloc(&ctx->flag, sizeof(int)) != cudaSuccess) {
+         (pool_alloc(ctx, &ctx->sbox, sizeof(float) * 2 * d * (size_t)ctx->n_super) != cudaSuccess ||
+          pool_alloc(ctx, &ctx->slist, sizeof(int) * (size_t)K * ctx->n_super) != cudaSuccess ||
+          pool_alloc(ctx, &ctx->scount, sizeof(int) * (size_t)ctx->n_super) != cudaSuccess ||
+          pool_alloc(ctx, &ctx->heavy, sizeof(int) * (size_t)ctx->n_chunks) != cudaSuccess ||
+          pool_alloc(ctx, &ctx->heavy_count, sizeof(int)) != cudaSuccess)) ||
+        pool_alloc(ctx, &ctx->flag, sizeof(int)) != cudaSuccess) {
         cudaGetLastError();
         set_error("device allocation failed (%zu bytes of points)", bytesX);
         return fail(KMEANS_ENOMEM);
     }
+    tr.mark(ctx->stream, "pool allocations");
     if ((s = ensure_trace(ctx, 64)) != KMEANS_OK) return fail(s);
     if (cudaMemsetAsync(ctx->mu, 0, sizeof(double) * 2 * Kpad * d, ctx->stream) != cudaSuccess ||
         cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream) != cudaSuccess ||
@@ -847,7 +968,7 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
     const float* src = points;
     float* staging = nullptr;
     if (!on_device) {
-        if (cudaMalloc(&staging, sizeof(float) * (size_t)N * d) != cudaSuccess) {
+        if (pool_alloc(ctx, &staging, sizeof(float) * (size_t)N * d) != cudaSuccess) {
             cudaGetLastError();
             set_error("staging allocation failed");
             return fail(KMEANS_ENOMEM);
@@ -855,12 +976,13 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
         e = cudaMemcpyAsync(staging, points, sizeof(float) * (size_t)N * d,
                             cudaMemcpyHostToDevice, ctx->stream);
         if (e != cudaSuccess) {
-            cudaFree(staging);
+            pool_free(ctx, staging);
             cuda_fail(ctx, e, "H2D points");
             return fail(KMEANS_ECUDA);
         }
         src = staging;
     }
+    tr.mark(ctx->stream, on_device ? "memsets" : "memsets + H2D");
     const int64_t si = opts.layout == KMEANS_LAYOUT_AOS ? d : 1;
     const int64_t sj = opts.layout == KMEANS_LAYOUT_AOS ? 1 : N;
     if (!ctx->sorted) {
@@ -869,20 +991,22 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
                                                     ctx->flag);
         ctx->launches += 1;
     } else {
-        s = sort_points(ctx, src, si, sj);
+        s = sort_points(ctx, src, si, sj, tr);
         if (s != KMEANS_OK) {
-            if (staging) cudaFree(staging);
+            cudaStreamSynchronize(ctx->stream);
+            if (staging) pool_free(ctx, staging);
             return fail(s);
         }
     }
     int hflag = 0;
     e = cudaMemcpyAsync(&hflag, ctx->flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-    if (staging) cudaFree(staging);
+    if (staging) pool_free(ctx, staging);
     if (e != cudaSuccess) {
         cuda_fail(ctx, e, "k_prep");
         return fail(KMEANS_ECUDA);
     }
+    tr.mark(ctx->stream, "done");
     if (hflag) {
         set_error("points contain NaN or Inf");
         return fail(KMEANS_ENONFINITE);
@@ -906,9 +1030,28 @@ kmeans_status kmeans_start(kmeans_ctx* ctx, const int64_t* init_idx, const doubl
         CK(cudaMemcpyAsync(ctx->idx_dev, idx.data(), sizeof(int64_t) * ctx->K,
                            cudaMemcpyHostToDevice, ctx->stream));
         const int n = ctx->K * ctx->d;
+        std::vector<int2> pairs;
+        if (ctx->sorted) {
+            // sorted positions of the local initial indices (one pass over perm)
+            for (int k = 0; k < ctx->K; ++k) {
+                const int64_t i = idx[k] - ctx->global_offset;
+                if (i >= 0 && i < ctx->N) pairs.push_back(make_int2((int)i, k));
+            }
+            std::sort(pairs.begin(), pairs.end(),
+                      [](const int2& a, const int2& b) { return a.x < b.x; });
+            CK(cudaMemsetAsync(ctx->init_pos, 0xff, sizeof(int32_t) * ctx->K, ctx->stream));
+            if (!pairs.empty()) {
+                CK(cudaMemcpyAsync(ctx->init_pairs, pairs.data(), sizeof(int2) * pairs.size(),
+                                   cudaMemcpyHostToDevice, ctx->stream));
+                const int blocks = (int)std::min<int64_t>((ctx->N + 255) / 256, 148 * 8);
+                km::k_find_pos<<<blocks, 256, 0, ctx->stream>>>(ctx->perm, ctx->N, ctx->init_pairs,
+                                                                 (int)pairs.size(), ctx->init_pos);
+                ctx->launches += 1;
+            }
+        }
         km::k_init_gather<<<(n + 255) / 256, 256, 0, ctx->stream>>>(
-            ctx->X, ctx->d, ctx->K, ctx->idx_dev, ctx->global_offset, ctx->N, ctx->invperm,
-            ctx->mu);
+            ctx->X, ctx->d, ctx->K, ctx->idx_dev, ctx->global_offset, ctx->N,
+            ctx->sorted ? ctx->init_pos : nullptr, ctx->mu);
         ctx->launches += 1;
         CK(cudaGetLastError());
         // CC1: assemble mu^0 from the owners (exact: one x plus zeros)

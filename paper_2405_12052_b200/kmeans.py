@@ -73,6 +73,7 @@ SIGNATURES = {
     "kmeans_status_string": (ctypes.c_char_p, [I]),
     "kmeans_last_error": (ctypes.c_char_p, []),
     "kmeans_abi_version": (I, []),
+    "kmeans_release_memory": (I, [I]),
 }
 
 _lib = None
@@ -317,3 +318,8 @@ def comm_init(nranks: int, uid: bytes, rank: int, device: int) -> int:
 
 def comm_destroy(comm: int):
     _check(lib().kmeans_comm_destroy(ctypes.c_void_p(comm)), "kmeans_comm_destroy")
+
+
+def release_memory(device: int = 0):
+    """Give the library pool's unused device memory back to the driver."""
+    _check(lib().kmeans_release_memory(int(device)), "kmeans_release_memory")
