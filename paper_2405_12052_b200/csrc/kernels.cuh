@@ -1094,9 +1094,9 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
 // own 128-point sub-tile (the tile's minimiser of dmax2 is always in the chunk
 // list, so the tile's M and exclusions are exact too) and runs the strict-<
 // argmin over its list in ascending order.  Sums go to a per-slot shared table
-// in a fixed order (warps in turn, lanes in rounds of distinct slots,
-// conflicting lanes in lane order), then a compacted sparse row in ascending
-// slot (= ascending k) order.
+// in a fixed order (per warp and point set, lanes sharing a slot summed in lane
+// order by their lowest lane; those group sums added warp by warp), then a
+// compacted sparse row in ascending slot (= ascending k) order.
 // ---------------------------------------------------------------------------
 template <int D, int MODE>
 __global__ void __launch_bounds__(256)
@@ -1307,27 +1307,51 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) j4 += __shfl_xor_sync(0xffffffffu, j4, o);
         if (lane == 0) wJ[warp] = j4;
+        // warp pre-aggregation, all warps at once: for each point set i, the
+        // lanes sharing a slot form a group whose lowest lane (the leader) sums
+        // the group's points in ascending lane order (shuffles over the
+        // non-leader lanes, warp-uniform loop)
+        double gx[4], gy[4], gz[4];
+        int gn[4];
+        bool lead[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const unsigned peers = __match_any_sync(0xffffffffu, v[i] ? sl[i] : -1 - lane);
+            lead[i] = v[i] && (peers & ((1u << lane) - 1u)) == 0u;
+            gx[i] = (double)px[i];
+            gy[i] = (double)py[i];
+            gz[i] = (double)pz[i];
+            gn[i] = 1;
+            unsigned rest = __ballot_sync(0xffffffffu, v[i] && !lead[i]);
+            while (rest) {
+                const int r = __ffs(rest) - 1;
+                rest &= rest - 1;
+                const double ox = __shfl_sync(0xffffffffu, gx[i], r);
+                const double oy = __shfl_sync(0xffffffffu, gy[i], r);
+                const double oz = __shfl_sync(0xffffffffu, gz[i], r);
+                if (lead[i] && ((peers >> r) & 1u)) {
+                    gx[i] += ox;
+                    gy[i] += oy;
+                    gz[i] += oz;
+                    gn[i] += 1;
+                }
+            }
+        }
+        // warps in turn add their group sums into the slot table (distinct
+        // slots within one point set: no conflicts)
         for (int w = 0; w < 8; ++w) {
             __syncthreads();
             if (warp != w) continue;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                unsigned pending = __ballot_sync(0xffffffffu, v[i]);
-                while (pending) {
-                    const unsigned peers =
-                        __match_any_sync(0xffffffffu, v[i] ? sl[i] : -1 - lane) & pending;
-                    const bool mine = v[i] && ((pending >> lane) & 1u) &&
-                                      (peers & ((1u << lane) - 1u)) == 0u;
-                    if (mine) {
-                        double* t = T + 4 * sl[i];
-                        t[0] += (double)px[i];
-                        t[1] += (double)py[i];
-                        t[2] += (double)pz[i];
-                        t[3] += 1.0;
-                    }
-                    __syncwarp();
-                    pending &= ~__ballot_sync(0xffffffffu, mine);
+                if (lead[i]) {
+                    double* t = T + 4 * sl[i];
+                    t[0] += gx[i];
+                    t[1] += gy[i];
+                    t[2] += gz[i];
+                    t[3] += (double)gn[i];
                 }
+                __syncwarp();
             }
         }
         __syncthreads();
