@@ -263,7 +263,7 @@ def main():
     init = datagen.init_indices(gen_w, N=global_N, K=w.K)
 
     ctx = km.Context(Xh, w.K, device=local, comm=comm, global_offset=a, global_N=global_N,
-                     sort=not args.no_sort)
+                     sort=False if args.no_sort else None)
     info = ctx.info()
     stream = torch.cuda.ExternalStream(ctx.stream)
     ctx.start(init_idx=init, tol=0.0, max_iter=1 << 30)
@@ -364,7 +364,7 @@ def main():
         barrier()
         t0 = time.perf_counter()
         c2 = km.Context(Xh, w.K, device=local, comm=comm, global_offset=a, global_N=global_N,
-                        sort=not args.no_sort)
+                        sort=False if args.no_sort else None)
         t1 = time.perf_counter()
         r = c2.fit(init, 0.0, args.e2e_iters, out_labels=labels_h, traces=False)
         t2 = time.perf_counter()

@@ -77,11 +77,14 @@ typedef struct kmeans_opts {
 } kmeans_opts;
 
 /* kmeans_opts.flags */
-#define KMEANS_FLAG_NO_SORT 1  /* keep the caller's point order (full-scan assign kernel).
-                                  Default (K <= 16): the shard is put in Morton order once
-                                  at create and each 2048-point chunk prunes centroids that
-                                  provably cannot be its points' argmin (exact; labels are
-                                  returned in the caller's order). */
+#define KMEANS_FLAG_NO_SORT 1     /* keep the caller's point order: full-scan assign kernels */
+#define KMEANS_FLAG_FORCE_SORT 2  /* always use the sorted (pruned) path */
+/* Default (neither flag): the sorted path -- the shard is put in Morton order
+ * once at create and each 1024-point chunk prunes the centroids that provably
+ * cannot be its points' argmin (exact; labels are returned in the caller's
+ * order) -- when K > 16 or N*K*d >= 3.84e8 (N >= 8e6 at K = 16, d = 3);
+ * below that the full scan is faster (the pruned kernel has a fixed per-chunk
+ * latency, measured in DESIGN.md section 5).  Both flags: KMEANS_EINVAL. */
 
 /* Fills *opts with the defaults above. */
 void kmeans_opts_init(kmeans_opts* opts);

@@ -919,7 +919,13 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
         }
         ctx->own_stream = true;
     }
-    ctx->sorted = !(opts.flags & KMEANS_FLAG_NO_SORT);
+    if ((opts.flags & KMEANS_FLAG_NO_SORT) && (opts.flags & KMEANS_FLAG_FORCE_SORT)) {
+        set_error("KMEANS_FLAG_NO_SORT and KMEANS_FLAG_FORCE_SORT together");
+        return fail(KMEANS_EINVAL);
+    }
+    if (opts.flags & KMEANS_FLAG_NO_SORT) ctx->sorted = false;
+    else if (opts.flags & KMEANS_FLAG_FORCE_SORT) ctx->sorted = true;
+    else ctx->sorted = K > 16 || (double)N * K * d >= 3.84e8;   // see kmeans.h
     kmeans_status s = configure(ctx);
     if (s != KMEANS_OK) return fail(s);
     tr.mark(ctx->stream, "stream + configure");

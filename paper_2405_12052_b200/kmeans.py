@@ -22,6 +22,7 @@ STATUS = {0: "KMEANS_OK", -1: "KMEANS_EINVAL", -2: "KMEANS_ENONFINITE", -3: "KME
           -4: "KMEANS_ECUDA", -5: "KMEANS_ENCCL", -6: "KMEANS_ESTATE"}
 LAYOUT_AOS, LAYOUT_SOA = 0, 1
 FLAG_NO_SORT = 1
+FLAG_FORCE_SORT = 2
 MAX_K = 1024
 
 
@@ -145,7 +146,7 @@ class Context:
 
     def __init__(self, points, K: int, *, d: int | None = None, layout: str = "aos",
                  device: int = -1, stream=None, comm=None, global_offset: int = 0,
-                 global_N: int = 0, sort: bool = True):
+                 global_N: int = 0, sort: bool | None = None):
         pts = _as_f32_points(points)
         shape = tuple(pts.shape)
         if layout == "aos":
@@ -161,7 +162,8 @@ class Context:
         o.nccl_comm = comm
         o.global_offset = global_offset
         o.global_N = global_N
-        o.flags = 0 if sort else FLAG_NO_SORT
+        # sort: None = the library's choice, True = sorted (pruned) path, False = full scan
+        o.flags = 0 if sort is None else (FLAG_FORCE_SORT if sort else FLAG_NO_SORT)
         h = ctypes.c_void_p()
         _check(lib().kmeans_create(ctypes.byref(h), _ptr(pts), self.N, self.d, self.K,
                                    ctypes.byref(o)), "kmeans_create")

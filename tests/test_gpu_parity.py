@@ -299,6 +299,29 @@ def test_errors():
         assert r["iters"] >= 1
 
 
+def test_auto_path_selection():
+    """Default flags: the full scan below N*K*d = 3.84e8 with K <= 16, the
+    sorted (pruned) path above it or for K > 16; both flags -> EINVAL."""
+    X = datagen.generate(datagen.WORKLOADS["C2"], N=50_000)
+    with km.Context(X, 16) as c:
+        assert c.info()["sorted"] == 0
+    with km.Context(X, 40) as c:
+        assert c.info()["sorted"] == 1
+    with km.Context(X, 16, sort=True) as c:
+        assert c.info()["sorted"] == 1
+    with km.Context(X, 40, sort=False) as c:
+        assert c.info()["sorted"] == 0
+    L = km.lib()
+    o = km.Opts()
+    L.kmeans_opts_init(km.ctypes.byref(o))
+    o.flags = km.FLAG_NO_SORT | km.FLAG_FORCE_SORT
+    h = km.ctypes.c_void_p()
+    Xc = np.ascontiguousarray(X)
+    rc = L.kmeans_create(km.ctypes.byref(h), km.ctypes.c_void_p(Xc.ctypes.data), Xc.shape[0], 3, 8,
+                         km.ctypes.byref(o))
+    assert rc == -1 and not h.value   # KMEANS_EINVAL
+
+
 @pytest.mark.parametrize("sort", SORT)
 @pytest.mark.parametrize("K", [8, 40])
 def test_profile_stages_leave_state(sort, K):

@@ -47,7 +47,7 @@ def main():
         torch.cuda.synchronize()
         r["torch_d2h_labels"] = time.perf_counter() - t
         t = time.perf_counter()
-        c = km.Context(Xh, w.K, sort=not a.no_sort)
+        c = km.Context(Xh, w.K, sort=False if a.no_sort else (True if getattr(a, "force_sort", False) else None))
         r["create_host"] = time.perf_counter() - t
         t = time.perf_counter()
         c.fit(init, 0.0, a.iters, labels=False, traces=False)
@@ -59,7 +59,7 @@ def main():
         c.close()
         r["destroy"] = time.perf_counter() - t
         t = time.perf_counter()
-        c = km.Context(Xd, w.K, sort=not a.no_sort)
+        c = km.Context(Xd, w.K, sort=False if a.no_sort else (True if getattr(a, "force_sort", False) else None))
         r["create_device"] = time.perf_counter() - t
         c.close()
         print(json.dumps({k: round(v * 1e3, 2) for k, v in r.items()}), flush=True)

@@ -27,9 +27,14 @@ def main():
     ap.add_argument("--reps", type=int, default=100)
     ap.add_argument("--iters", type=int, default=10, help="Lloyd iterations before timing")
     ap.add_argument("--no-sort", action="store_true")
+    ap.add_argument("--force-sort", action="store_true")
     ap.add_argument("--K", type=int, default=0, help="override K (init = first K seeded indices)")
+    ap.add_argument("--N", type=int, default=0, help="override N (a prefix-shaped draw of the workload)")
     a = ap.parse_args()
     w = datagen.WORKLOADS[a.workload]
+    if a.N:
+        import dataclasses
+        w = dataclasses.replace(w, N=a.N)
     X = torch.empty((w.N, w.d), dtype=torch.float32, pin_memory=True)
     datagen.generate(w, out=X.numpy())
     init = datagen.init_indices(w)
@@ -42,13 +47,14 @@ def main():
     for lib in a.libs:
         km._lib = None
         km.LIB_PATH = os.path.abspath(lib)
-        ctx = km.Context(X, w.K, sort=not a.no_sort)
+        ctx = km.Context(X, w.K, sort=False if a.no_sort else (True if getattr(a, "force_sort", False) else None))
         ctx.start(init_idx=init, tol=0.0, max_iter=1 << 30)
         ctx.iterate(a.iters)
         ctx.poll()
         st = torch.cuda.ExternalStream(ctx.stream)
         t = ctx.profile_stage(a.reps, 1, timed=True)        # assign kernels alone
         t_rm = ctx.profile_stage(a.reps, 2, timed=True)     # chunk-row merge alone
+        # (unsorted small-K path: stage 2 = k_merge_rows)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
@@ -59,7 +65,7 @@ def main():
         info = ctx.info()
         cand = ctx.candidate_stats() if info["sorted"] else {}
         gbs = 4 * w.d * w.N / (t / 1e3) / 1e9
-        print(json.dumps({"lib": os.path.basename(lib), "assign_ms": round(t, 4), "row_merge_ms": round(t_rm, 4),
+        print(json.dumps({"lib": os.path.basename(lib), "N": w.N, "sorted": info["sorted"], "assign_ms": round(t, 4), "row_merge_ms": round(t_rm, 4),
                           "iter_ms": round(ti, 4), "hbm_frac": round(gbs / peak, 4),
                           "grid": info["grid"], "smem": info["smem_bytes"],
                           "cand_mean": round(cand.get("mean", 0), 3)}), flush=True)
