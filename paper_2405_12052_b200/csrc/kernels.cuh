@@ -37,6 +37,19 @@ struct DevState {
     double J;
 };
 
+// Programmatic dependent launch (PDL): a kernel launched with programmatic
+// stream serialization may start before its predecessor finishes; it must not
+// read the predecessor's results before pdl_wait() (griddepcontrol.wait: the
+// predecessor grid has completed and its writes are visible), and pdl_trigger()
+// lets its own successor launch early.  Both are no-ops without the attribute.
+#ifndef KM_PDL_ASSIGN_TRIGGER
+#define KM_PDL_ASSIGN_TRIGGER 0   // measured: an early trigger in the assign kernel costs ~7 us
+#endif
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 constexpr int kLargeTPBMax = 256;  // threads per block (max), large-K path
 
 __device__ __forceinline__ float pos_inf() { return __int_as_float(0x7f800000); }
@@ -710,15 +723,13 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
                 int* __restrict__ cand_count, int* __restrict__ heavy,
                 int* __restrict__ heavy_count) {
     using C = PCfg<LARGE>;
-    // Independent loads first (their latencies overlap the stop-flag read and
-    // the TMA prologue): the box, this lane's staged centroid, the flag.
+    // Prologue before pdl_wait() touches only what no predecessor writes: the
+    // chunk box and the points (the TMA ring is filled here, so with PDL the
+    // first units stream in while the previous update finishes).
     const int lane = threadIdx.x;
     const int chunk = blockIdx.x;
     const float4* cneg = cneg_buf + (size_t)mu_sel * K;   // -fl32(mu^t) (or mu^{t-1})
     const float bx = (lane < 2 * D) ? __ldg(&cbox[(size_t)chunk * 2 * D + lane]) : 0.0f;
-    const float4 cl = (!LARGE && lane < K) ? __ldg(&cneg[lane]) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const int sup_count = LARGE ? __ldg(&scount[chunk / kSuperChunks]) : 0;
-    const int done_flag = ignore_done ? 0 : *(volatile const int*)&st->done;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PrunedSmem<D, LARGE>& S = *reinterpret_cast<PrunedSmem<D, LARGE>*>(smem_raw);
     constexpr int kUnitFloats = D * kSortedUnit;
@@ -730,7 +741,6 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
     const int nunit = nu64 < kSortedUnits ? (int)nu64 : kSortedUnits;
     const int npts = rem < kSChunkPoints ? (int)rem : kSChunkPoints;
     const float* src = X + (base >> 6) * (D * kWarpTile);
-    if (done_flag) return;   // stop rule already met (nothing issued yet)
 
     // point stream: units 0..nunit-1 through the TMA ring (unit q in stage q % SS)
     unsigned issued = 0;   // lane 0
@@ -749,6 +759,17 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     issue_upto(SS);
+#if KM_PDL_ASSIGN_TRIGGER
+    pdl_trigger();
+#endif
+    pdl_wait();   // the centroids, the stop flag and (large K) the super lists are ready
+    const float4 cl = (!LARGE && lane < K) ? __ldg(&cneg[lane]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int sup_count = LARGE ? __ldg(&scount[chunk / kSuperChunks]) : 0;
+    const int done_flag = ignore_done ? 0 : *(volatile const int*)&st->done;
+    if (done_flag) {   // stop rule already met: drain the issued copies, then leave
+        for (unsigned q = 0; q < (unsigned)min(SS, nunit); ++q) mbar_wait(&S.bar[q % SS], 0u);
+        return;
+    }
 
     // ---- candidates of this chunk ----
     double lo[3], hi[3];
@@ -1639,6 +1660,8 @@ k_merge_sparse16(const double* __restrict__ cpart, int n_chunks, int K, double* 
     const int c = g * kRowGroup + tid;
     const double* row = cpart + (size_t)c * kRowDoubles;
     const double2* ent = reinterpret_cast<const double2*>(row + kRowHead);
+    pdl_trigger();
+    pdl_wait();   // the rows are written
     // round 1 (independent loads): done flag, head, entry slots 0 and 1
     const int done = ignore_done ? 0 : st->done;
     double2 head = make_double2(0.0, 0.0);
@@ -2037,6 +2060,8 @@ k_merge_update(const double* __restrict__ part, int G, int nE, double* __restric
                double* __restrict__ mu_buf, int K, DevState* __restrict__ st,
                double* __restrict__ trace_E, double* __restrict__ trace_J, int trace_cap,
                float4* __restrict__ cneg) {
+    pdl_trigger();
+    pdl_wait();   // the group columns are written
     if (st->done) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* rs = reinterpret_cast<double*>(smem_raw);   // [nE]

@@ -180,6 +180,29 @@ struct CreateTrace {
     }
 };
 
+#ifndef KM_PDL
+#define KM_PDL 1   // programmatic dependent launch between the iteration's kernels
+#endif
+
+// Launch with programmatic stream serialization (PDL) when `pdl`: the kernel
+// may start while its stream predecessor drains (it synchronises with
+// griddepcontrol.wait before reading the predecessor's results).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     bool pdl, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = (pdl && KM_PDL) ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 // Device allocation for a context (through the block cache).  Freed blocks
 // must be idle: callers synchronise ctx->stream before pool_free.
 template <class T>
@@ -420,10 +443,12 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
             ctx->launches += 1;
         }
         PrunedFn f = pick_pruned(ctx->d, ctx->K, mode);
-        if (A) f<<<ctx->n_chunks, 32, ctx->smem, ctx->stream>>>(
-            ctx->X, ctx->N, ctx->K, ctx->cneg, ctx->st, mu_sel, ignore_done, ctx->cbox, ctx->slist,
-            ctx->scount, ctx->cpart, ctx->row_stride, ctx->labels_sorted, ctx->cand_count,
-            ctx->heavy, ctx->heavy_count);
+        if (A)
+            CK(launch_k(f, ctx->n_chunks, 32, ctx->smem, ctx->stream, ctx->path == 0, ctx->X,
+                        ctx->N, ctx->K, (const float4*)ctx->cneg, (const DevState*)ctx->st, mu_sel,
+                        ignore_done, (const float*)ctx->cbox, (const int*)ctx->slist,
+                        (const int*)ctx->scount, ctx->cpart, ctx->row_stride, ctx->labels_sorted,
+                        ctx->cand_count, ctx->heavy, ctx->heavy_count));
         if (A) ctx->launches += 1;
         if (A && ctx->path == 1) {
             HeavyFn hf = pick_heavy(ctx->d, mode);
@@ -435,12 +460,10 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
         }
         if (Mg && ctx->path == 0) {
             // sparse chunk rows (<= 16 entries) -> group columns of part (fixed order)
-            if (ctx->d == 2)
-                km::k_merge_sparse16<2><<<ctx->G, km::kRowGroup, 0, ctx->stream>>>(
-                    ctx->cpart, ctx->n_chunks, ctx->K, ctx->part, ctx->G, ctx->st, ignore_done);
-            else
-                km::k_merge_sparse16<3><<<ctx->G, km::kRowGroup, 0, ctx->stream>>>(
-                    ctx->cpart, ctx->n_chunks, ctx->K, ctx->part, ctx->G, ctx->st, ignore_done);
+            CK(launch_k(ctx->d == 2 ? km::k_merge_sparse16<2> : km::k_merge_sparse16<3>, ctx->G,
+                        km::kRowGroup, 0, ctx->stream, true, (const double*)ctx->cpart,
+                        ctx->n_chunks, ctx->K, ctx->part, ctx->G, (const DevState*)ctx->st,
+                        ignore_done));
             ctx->launches += 1;
         } else if (Mg) {
             // sparse chunk rows -> group columns of part (fixed ascending order)
@@ -542,14 +565,12 @@ bool fused_update(const kmeans_ctx* ctx) {
 kmeans_status launch_merge_update(kmeans_ctx* ctx) {
     const int tpb = 1024;
     const size_t sm = sizeof(double) * ctx->nE;
-    if (ctx->d == 2)
-        km::k_merge_update<2><<<1, tpb, sm, ctx->stream>>>(
-            ctx->part, ctx->G, ctx->nE, ctx->red, ctx->mu, ctx->K, ctx->st, ctx->trace_E,
-            ctx->trace_J, ctx->trace_cap, ctx->sorted ? ctx->cneg : nullptr);
-    else
-        km::k_merge_update<3><<<1, tpb, sm, ctx->stream>>>(
-            ctx->part, ctx->G, ctx->nE, ctx->red, ctx->mu, ctx->K, ctx->st, ctx->trace_E,
-            ctx->trace_J, ctx->trace_cap, ctx->sorted ? ctx->cneg : nullptr);
+    // PDL after the sorted small-K row merge (k_merge_sparse16 triggers it)
+    const bool pdl = ctx->sorted && ctx->path == 0;
+    CK(launch_k(ctx->d == 2 ? km::k_merge_update<2> : km::k_merge_update<3>, 1, tpb, sm,
+                ctx->stream, pdl, (const double*)ctx->part, ctx->G, ctx->nE, ctx->red, ctx->mu,
+                ctx->K, ctx->st, ctx->trace_E, ctx->trace_J, ctx->trace_cap,
+                ctx->sorted ? ctx->cneg : (float4*)nullptr));
     ctx->launches += 1;
     CK(cudaGetLastError());
     return KMEANS_OK;

@@ -25,6 +25,9 @@ VARIANTS = {
     "rg256": ("KM_ROW_GROUP=256",),
     "rg512": ("KM_ROW_GROUP=512",),
     "rg1024": ("KM_ROW_GROUP=1024",),
+    "pdl0": ("KM_PDL=0",),
+    "pdl1": ("KM_PDL=1",),
+    "pdl1t": ("KM_PDL=1", "KM_PDL_ASSIGN_TRIGGER=1"),
 }
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
