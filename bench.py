@@ -325,6 +325,7 @@ def main():
             # binding roofline is the HBM stream of the points
             return dict(bound="hbm", achieved=ach_gbs, peak=hbm_gbs, unit="GB/s",
                         frac=ach_gbs / hbm_gbs, traffic=traffic,
+                        frac_of_8tbs_spec=ach_gbs / 8000.0,
                         peak_source=f"MEASURED_PEAKS.json hbm_gbs ({peak_src})", **common)
         return dict(bound="alu", achieved=ach_tops, peak=fp32_peak, unit="TFLOP/s",
                     op="FP32 lane-op (FADD, FMUL, FFMA = 1 each)", frac=ach_tops / fp32_peak,

@@ -79,6 +79,10 @@ typedef struct kmeans_opts {
 /* kmeans_opts.flags */
 #define KMEANS_FLAG_NO_SORT 1     /* keep the caller's point order: full-scan assign kernels */
 #define KMEANS_FLAG_FORCE_SORT 2  /* always use the sorted (pruned) path */
+#define KMEANS_FLAG_NO_FUSED 4    /* full-scan path: never use the one-launch
+                                     multi-iteration kernel (k_fused_iterate) that
+                                     kmeans_iterate / kmeans_fit_ctx use for small
+                                     single-GPU shards (<= 4 x 8 x SMs chunks of 2048) */
 /* Default (neither flag): the sorted path -- the shard is put in Morton order
  * once at create and each 1024-point chunk prunes the centroids that provably
  * cannot be its points' argmin (exact; labels are returned in the caller's
@@ -198,6 +202,8 @@ typedef struct kmeans_info {
     int64_t kernel_launches;/* kernels of this library launched so far by this context */
     int nranks, rank;
     int sorted;             /* 1 = Morton-sorted shard with per-chunk pruning */
+    int fused;              /* 1 = kmeans_iterate runs k_fused_iterate (grid = fused_grid) */
+    int fused_grid;         /* its cooperative grid (blocks of 256 threads) */
 } kmeans_info;
 
 kmeans_status kmeans_get_info(kmeans_ctx* ctx, kmeans_info* info);

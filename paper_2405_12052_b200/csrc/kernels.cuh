@@ -20,6 +20,7 @@
 // No global float atomics anywhere; every reduction has a fixed order, so results
 // are bit-reproducible run to run for a fixed grid.
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -282,30 +283,29 @@ __device__ __forceinline__ void form_d_pair(const float (&nc)[KP][D], float2 x, 
     }
 }
 
-template <int D, int KP, int MODE>
-__global__ void __launch_bounds__(32, 10)
-k_assign_chunk(const float* __restrict__ X, int64_t n, int K,
-               const double* __restrict__ mu_buf, const DevState* __restrict__ st,
-               int mu_sel, int ignore_done, double* __restrict__ cpart,
-               int32_t* __restrict__ labels) {
-    if (!ignore_done && st->done) return;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    ChunkSmem<D, KP>& S = *reinterpret_cast<ChunkSmem<D, KP>*>(smem_raw);
+__device__ __forceinline__ void mbar_inval(uint64_t* bar) {
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Start chunk `chunk`'s point stream: (re)initialise the stage barriers and
+// issue the first kStages tiles (lane 0).  `reinit`: the barriers were used by
+// an earlier chunk of this warp (all their copies consumed).
+template <int D, int KP>
+__device__ __forceinline__ void chunk_prologue(ChunkSmem<D, KP>& S, const float* __restrict__ X,
+                                               int64_t n, int chunk, int lane, bool reinit) {
     constexpr int kTileFloats = D * kLaneTile;
     constexpr unsigned kTileBytes = kTileFloats * 4;
-    const int lane = threadIdx.x;
-    const int chunk = blockIdx.x;
     const int64_t base = (int64_t)chunk * kChunkPoints;
     const int64_t rem = n - base;
     const int64_t ntile64 = (rem + kLaneTile - 1) / kLaneTile;
     const int ntile = ntile64 < kChunkTiles ? (int)ntile64 : kChunkTiles;
-    const int nfull = rem >= kChunkPoints ? kChunkTiles : (int)(rem / kLaneTile);
     const float* src = X + (base >> 6) * (D * kWarpTile);   // first AoSoA tile of the chunk
-
-    // kick off the point stream first (its latency overlaps the staging below)
     if (lane == 0) {
 #pragma unroll
-        for (int s = 0; s < kStages; ++s) mbar_init(&S.bar[s], 1);
+        for (int s = 0; s < kStages; ++s) {
+            if (reinit) mbar_inval(&S.bar[s]);
+            mbar_init(&S.bar[s], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 #pragma unroll
         for (int s = 0; s < kStages; ++s) {
@@ -315,28 +315,25 @@ k_assign_chunk(const float* __restrict__ X, int64_t n, int K,
             }
         }
     }
+}
 
-    const int t_it = st->t;
-    const double* mu = mu_buf + (size_t)((t_it - mu_sel) & 1) * K * D;
-    // Stage: c_k = fl32(mu_k^t) (RN), negated so that x + (-c) == x - c; each
-    // lane converts <= 2 entries, the warp shares them through smem.
-    for (int q = lane; q < KP * D; q += 32)
-        S.cst[q] = (q < K * D) ? -__double2float_rn(__ldg(&mu[q])) : -pos_inf();
-    if (MODE & kModeReduce) {
-#pragma unroll
-        for (int k = 0; k < KP; ++k) {
-            S.A[k][lane] = make_double2(0.0, 0.0);
-            S.B[k][lane] = make_double2(0.0, 0.0);
-        }
-    }
-    __syncwarp();
-    float nc[KP][D];
-#pragma unroll
-    for (int k = 0; k < KP; ++k) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) nc[k][j] = S.cst[k * D + j];
-    }
-    double J = 0.0;
+// One chunk of the full scan (after chunk_prologue): reassignment (PAPER.md:
+// 45-49, form D, exact argmin) of its points, 4 per lane per warp-tile, and
+// the fused numerator / denominator of the mean added to the
+// lane's private fp64 columns S.A / S.B and to J, points in the fixed order
+// a0, a1, b0, b1 of each tile, tiles ascending.
+template <int D, int KP, int MODE>
+__device__ __forceinline__ void chunk_body(ChunkSmem<D, KP>& S, const float* __restrict__ X,
+                                           int64_t n, int chunk, const float (&nc)[KP][D],
+                                           double& J, int32_t* __restrict__ labels, int lane) {
+    constexpr int kTileFloats = D * kLaneTile;
+    constexpr unsigned kTileBytes = kTileFloats * 4;
+    const int64_t base = (int64_t)chunk * kChunkPoints;
+    const int64_t rem = n - base;
+    const int64_t ntile64 = (rem + kLaneTile - 1) / kLaneTile;
+    const int ntile = ntile64 < kChunkTiles ? (int)ntile64 : kChunkTiles;
+    const int nfull = rem >= kChunkPoints ? kChunkTiles : (int)(rem / kLaneTile);
+    const float* src = X + (base >> 6) * (D * kWarpTile);
 
     auto accumulate = [&](int l, float px, float py, float pz) {
         double2 a = S.A[l][lane], b = S.B[l][lane];
@@ -394,8 +391,6 @@ k_assign_chunk(const float* __restrict__ X, int64_t n, int K,
             *reinterpret_cast<int2*>(labels + pa + kWarpTile) = make_int2(l[2], l[3]);
         }
     };
-    // Fused numerator / denominator of the mean, points in the
-    // fixed order a0, a1, b0, b1.
     auto reduce_full = [&](const Pts& P, const float (&m)[4], const int (&l)[4]) {
         if (!(MODE & kModeReduce)) return;
         accumulate(l[0], P.xa.x, P.ya.x, P.za.x);
@@ -448,12 +443,12 @@ k_assign_chunk(const float* __restrict__ X, int64_t n, int K,
             reduce_checked(i, P, m, l);
         }
     }
-    if (!(MODE & kModeReduce)) return;
+}
 
-    // ---- chunk partial: row[4k + j] = sum over lanes, fixed rotation order ----
-    __syncwarp();
-    // lane L owns double2 entry (k = L >> 1, half = L & 1); the 8 lanes of one
-    // LDS.128 phase read distinct columns -> conflict-free.
+// Lane L's entry of the warp row: the sum over the 32 lanes' private columns of
+// (k = L >> 1, half = L & 1), in a rotated (bank-conflict-free) fixed order.
+template <int KP, class SM>
+__device__ __forceinline__ double2 columns_to_row(const SM& S, int lane) {
     const int k = lane >> 1;
     const double2* col = (lane & 1) ? &S.B[0][0] : &S.A[0][0];
     double v0 = 0.0, v1 = 0.0;
@@ -468,13 +463,60 @@ k_assign_chunk(const float* __restrict__ X, int64_t n, int K,
             else v1 += w.y;
         }
     }
+    return (k < KP) ? ((lane & 1) ? make_double2(v0, (double)cnt) : make_double2(v0, v1))
+                    : make_double2(0.0, 0.0);
+}
+
+template <int KP, class SM>
+__device__ __forceinline__ void zero_columns(SM& S, int lane) {
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+        S.A[k][lane] = make_double2(0.0, 0.0);
+        S.B[k][lane] = make_double2(0.0, 0.0);
+    }
+}
+
+template <int D, int KP, int MODE>
+__global__ void __launch_bounds__(32, 10)
+k_assign_chunk(const float* __restrict__ X, int64_t n, int K,
+               const double* __restrict__ mu_buf, const DevState* __restrict__ st,
+               int mu_sel, int ignore_done, double* __restrict__ cpart,
+               int32_t* __restrict__ labels) {
+    if (!ignore_done && st->done) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ChunkSmem<D, KP>& S = *reinterpret_cast<ChunkSmem<D, KP>*>(smem_raw);
+    const int lane = threadIdx.x;
+    const int chunk = blockIdx.x;
+    // kick off the point stream first (its latency overlaps the staging below)
+    chunk_prologue<D, KP>(S, X, n, chunk, lane, false);
+
+    const int t_it = st->t;
+    const double* mu = mu_buf + (size_t)((t_it - mu_sel) & 1) * K * D;
+    // Stage: c_k = fl32(mu_k^t) (RN), negated so that x + (-c) == x - c; each
+    // lane converts <= 2 entries, the warp shares them through smem.
+    for (int q = lane; q < KP * D; q += 32)
+        S.cst[q] = (q < K * D) ? -__double2float_rn(__ldg(&mu[q])) : -pos_inf();
+    if (MODE & kModeReduce) zero_columns<KP>(S, lane);
+    __syncwarp();
+    float nc[KP][D];
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) nc[k][j] = S.cst[k * D + j];
+    }
+    double J = 0.0;
+    chunk_body<D, KP, MODE>(S, X, n, chunk, nc, J, labels, lane);
+    if (!(MODE & kModeReduce)) return;
+
+    // ---- chunk partial: row[4k + j] = sum over lanes, fixed rotation order ----
+    __syncwarp();
+    const double2 out = columns_to_row<KP>(S, lane);
     double jj = J;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) jj += __shfl_xor_sync(0xffffffffu, jj, o);
     double* row = cpart + (size_t)chunk * kRowDoubles;
     // row layout [k][Sx, Sy, Sz, n] (k < KP), then J at 64
-    const double2 out = (lane & 1) ? make_double2(v0, (double)cnt) : make_double2(v0, v1);
-    reinterpret_cast<double2*>(row)[lane] = (k < KP) ? out : make_double2(0.0, 0.0);
+    reinterpret_cast<double2*>(row)[lane] = out;
     if (lane == 0) row[64] = jj;
 }
 
@@ -1622,7 +1664,7 @@ __device__ __forceinline__ void block_merge_groups(const double* part, int G, in
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
                 const int e = e0 + r * nwarp;
-                if (e < nE) v[r] += part[(size_t)e * G + b];
+                if (e < nE) v[r] += __ldcg(part + (size_t)e * G + b);   // L2: may be written by other blocks of this kernel
             }
         }
 #pragma unroll
@@ -1632,7 +1674,7 @@ __device__ __forceinline__ void block_merge_groups(const double* part, int G, in
             const int e = e0 + r * nwarp;
             if (lane == 0 && e < nE) {
                 rs[e] = v[r];
-                red[e] = v[r];
+                if (red) red[e] = v[r];
             }
         }
     }
@@ -2068,6 +2110,180 @@ k_merge_update(const double* __restrict__ part, int G, int nE, double* __restric
     block_merge_groups(part, G, nE, rs, red);
     __syncthreads();
     update_body<D>(mu_buf, K, rs, st, trace_E, trace_J, trace_cap, cneg);
+}
+
+// ---------------------------------------------------------------------------
+// k_fused_iterate (full-scan path, K <= 16, one GPU): up to n_iter whole Lloyd
+// iterations in ONE cooperative launch -- for the small shards where an
+// iteration is a few microseconds of work and launch latency dominates.
+//
+// Per iteration: warp w of the grid takes the 128-point warp-tiles w, w + W,
+// ... (loads prefetched two tiles ahead; the data is L2-resident after the
+// first iteration) and runs the same form-D distances, exact argmin and fused
+// accumulation as k_assign_chunk into its lane columns,
+// warps -> block row (fixed order) -> brow[t & 1][e][b]; one grid barrier;
+// then EVERY block merges the G block rows in the k_merge order and applies
+// the update (mu = S / n, empty keeps mu^t, E summed
+// k-major in the oracle's order, stop rule) to its shared copy of mu -- the
+// same bits in every block, so all blocks stop together and the next
+// iteration needs no second barrier (brow is double-buffered by iteration
+// parity).  Block 0 publishes mu^{t+1}, E, J, the traces and the state.
+// ---------------------------------------------------------------------------
+constexpr int kFusedWarps = 8;
+
+template <int KP>
+struct FusedSmem {
+    double2 A[KP][32];   // {Sx, Sy} per (k, lane)
+    double2 B[KP][32];   // {Sz, n|pad} per (k, lane)
+};
+
+template <int D, int KP>
+__global__ void __launch_bounds__(kFusedWarps * 32, 1)
+k_fused_iterate(const float* __restrict__ X, int64_t n, int K, int n_chunks,
+                double* __restrict__ mu_buf, DevState* __restrict__ st,
+                double* __restrict__ trace_E, double* __restrict__ trace_J, int trace_cap,
+                double* __restrict__ brow, double* __restrict__ red, int n_iter) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x, b = blockIdx.x;
+    FusedSmem<KP>& S = reinterpret_cast<FusedSmem<KP>*>(smem_raw)[warp];
+    double* wrow = reinterpret_cast<double*>(smem_raw + sizeof(FusedSmem<KP>) * kFusedWarps);
+    double* mu_s = wrow + kFusedWarps * 66;   // [K*D] mu^t
+    double* mu_n = mu_s + KP * D;             // [K*D] mu^{t+1}
+    double* rs = mu_n + KP * D;               // [nE] merged vector
+    __shared__ double sh_E;
+    const int nE = K * D + K + 1;
+    const int64_t ntiles = (n + kLaneTile - 1) / kLaneTile;   // 128-point warp-tiles
+    const int64_t tw = (int64_t)G * kFusedWarps;              // warps in the grid
+    const int64_t gw = (int64_t)b * kFusedWarps + warp;
+    int t = st->t;
+    bool done = st->done != 0;
+    const int max_iter = st->max_iter;
+    const double tol = st->tol;
+    for (int q = tid; q < K * D; q += blockDim.x) mu_s[q] = mu_buf[(size_t)(t & 1) * K * D + q];
+    __syncthreads();
+
+    struct Pts {
+        float2 xa, ya, za, xb, yb, zb;
+    };
+    auto load = [&](int64_t tile, Pts& P) {   // this lane's 4 points of a warp-tile
+        const int64_t pa = tile * kLaneTile + 2 * lane, pb = pa + kWarpTile;
+        P.xa = __ldg(reinterpret_cast<const float2*>(tile_coord<D>(X, pa, 0)));
+        P.ya = __ldg(reinterpret_cast<const float2*>(tile_coord<D>(X, pa, 1)));
+        P.za = (D == 3) ? __ldg(reinterpret_cast<const float2*>(tile_coord<D>(X, pa, 2)))
+                        : make_float2(0.f, 0.f);
+        P.xb = __ldg(reinterpret_cast<const float2*>(tile_coord<D>(X, pb, 0)));
+        P.yb = __ldg(reinterpret_cast<const float2*>(tile_coord<D>(X, pb, 1)));
+        P.zb = (D == 3) ? __ldg(reinterpret_cast<const float2*>(tile_coord<D>(X, pb, 2)))
+                        : make_float2(0.f, 0.f);
+    };
+    auto accumulate = [&](int l, float px, float py, float pz) {
+        double2 a = S.A[l][lane], c = S.B[l][lane];
+        a.x += (double)px;
+        a.y += (double)py;
+        if (D == 3) c.x += (double)pz;
+        int2 cn = *reinterpret_cast<int2*>(&c.y);
+        cn.x += 1;
+        c.y = *reinterpret_cast<double*>(&cn);
+        S.A[l][lane] = a;
+        S.B[l][lane] = c;
+    };
+
+    for (int it = 0; it < n_iter && !done; ++it) {
+        // stage c_k = fl32(mu_k^t) (RN), negated; padded slots -inf (never win)
+        float nc[KP][D];
+#pragma unroll
+        for (int k = 0; k < KP; ++k)
+#pragma unroll
+            for (int j = 0; j < D; ++j)
+                nc[k][j] = (k < K) ? -__double2float_rn(mu_s[k * D + j]) : -pos_inf();
+        zero_columns<KP>(S, lane);
+        __syncwarp();
+        double J = 0.0;
+        // this warp's tiles gw, gw + tw, ... ascending; two tiles prefetched
+        Pts P0, P1;
+        if (gw < ntiles) load(gw, P0);
+        if (gw + tw < ntiles) load(gw + tw, P1);
+        for (int64_t tile = gw; tile < ntiles; tile += tw) {
+            const Pts P = P0;
+            P0 = P1;
+            if (tile + 2 * tw < ntiles) load(tile + 2 * tw, P1);
+            float da0[KP], da1[KP], db0[KP], db1[KP], m[4];
+            int l[4];
+            form_d_pair<D, KP>(nc, P.xa, P.ya, P.za, da0, da1);
+            form_d_pair<D, KP>(nc, P.xb, P.yb, P.zb, db0, db1);
+            exact_argmin<KP>(da0, m[0], l[0]);
+            exact_argmin<KP>(da1, m[1], l[1]);
+            exact_argmin<KP>(db0, m[2], l[2]);
+            exact_argmin<KP>(db1, m[3], l[3]);
+            const int64_t pa = tile * kLaneTile + 2 * lane, pb = pa + kWarpTile;
+            if (pa < n) { accumulate(l[0], P.xa.x, P.ya.x, P.za.x); J += (double)m[0]; }
+            if (pa + 1 < n) { accumulate(l[1], P.xa.y, P.ya.y, P.za.y); J += (double)m[1]; }
+            if (pb < n) { accumulate(l[2], P.xb.x, P.yb.x, P.zb.x); J += (double)m[2]; }
+            if (pb + 1 < n) { accumulate(l[3], P.xb.y, P.yb.y, P.zb.y); J += (double)m[3]; }
+        }
+        __syncwarp();
+        const double2 out = columns_to_row<KP>(S, lane);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
+        reinterpret_cast<double2*>(wrow + warp * 66)[lane] = out;
+        if (lane == 0) wrow[warp * 66 + 64] = J;
+        __syncthreads();
+        // block row -> brow[t & 1][e][b] (warps in order)
+        double* bp = brow + (size_t)(t & 1) * nE * G;
+        if (tid < 65) {
+            const int k = tid >> 2, q = tid & 3;
+            int e = -1;
+            if (tid == 64) e = K * D + K;
+            else if (k < K && q < D) e = k * D + q;
+            else if (k < K && q == 3) e = K * D + k;
+            if (e >= 0) {
+                double v = 0.0;
+#pragma unroll
+                for (int w = 0; w < kFusedWarps; ++w) v += wrow[w * 66 + tid];
+                bp[(size_t)e * G + b] = v;
+            }
+        }
+        grid.sync();
+        // every block: the merged vector (k_merge order) and the update
+        block_merge_groups(bp, G, nE, rs, b == 0 ? red : nullptr);
+        __syncthreads();
+        for (int q = tid; q < K * D; q += blockDim.x) {
+            const double nk = rs[K * D + q / D];
+            mu_n[q] = (nk > 0.0) ? rs[q] / nk : mu_s[q];   // empty cluster keeps mu^t
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double E = 0.0;   // k-major, j inner: the oracle's order
+            for (int q = 0; q < K * D; ++q) {
+                const double dlt = mu_n[q] - mu_s[q];
+                E += dlt * dlt;
+            }
+            sh_E = E;
+        }
+        __syncthreads();
+        const double E = sh_E, Jt = rs[K * D + K];
+        if (b == 0) {
+            for (int q = tid; q < K * D; q += blockDim.x)
+                mu_buf[(size_t)((t + 1) & 1) * K * D + q] = mu_n[q];
+            if (tid == 0) {
+                if (t < trace_cap) {
+                    trace_E[t] = E;
+                    trace_J[t] = Jt;
+                }
+                st->E = E;
+                st->J = Jt;
+                st->t = t + 1;
+                st->done = (E < tol) || (t + 1 >= max_iter);
+            }
+        }
+        for (int q = tid; q < K * D; q += blockDim.x) mu_s[q] = mu_n[q];
+        t += 1;
+        done = (E < tol) || (t >= max_iter);
+        __syncthreads();
+    }
 }
 
 }  // namespace km

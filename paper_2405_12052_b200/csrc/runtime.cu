@@ -153,6 +153,11 @@ struct kmeans_ctx {
     int nE = 0;
     cudaGraphExec_t graph = nullptr;    // one iteration
     cudaGraphExec_t graph_u = nullptr;  // kGraphUnroll iterations (fewer graph launches)
+    int flags = 0;            // kmeans_opts.flags
+    bool fused = false;       // small full-scan shard: k_fused_iterate (one launch, many iterations)
+    int fused_grid = 0;
+    int fused_smem = 0;
+    double* brow = nullptr;   // k_fused_iterate block rows [2][nE][fused_grid]
     int64_t launches = 0;
     kmeans_status sticky = KMEANS_OK;
     bool assigned = false;
@@ -217,6 +222,7 @@ bool fused_update(const kmeans_ctx* ctx);
 // kernels of this library per iteration: [prune], assign, [heavy], [row merge],
 // merge + update (fused into one kernel on a single GPU when small enough)
 int kernels_per_iter(const kmeans_ctx* ctx) {
+    if (ctx->fused) return 1;   // one launch covers many iterations
     int n = ctx->sorted ? (ctx->path == 1 ? 6 : 4) : (ctx->path == 0 ? 4 : 3);
     if (fused_update(ctx)) n -= 1;
     return n;
@@ -265,6 +271,26 @@ using LargeFn = void (*)(const float*, int64_t, int64_t, int, const double*, con
                          int, int, double*, int32_t*);
 
 int small_kp(int K) { return K <= 4 ? 4 : (K <= 8 ? 8 : 16); }
+
+using FusedFn = void (*)(const float*, int64_t, int, int, double*, DevState*, double*, double*,
+                         int, double*, double*, int);
+
+FusedFn pick_fused(int d, int K) {
+    const int kp = small_kp(K);
+    if (d == 2) return kp == 4 ? km::k_fused_iterate<2, 4>
+                               : (kp == 8 ? km::k_fused_iterate<2, 8> : km::k_fused_iterate<2, 16>);
+    return kp == 4 ? km::k_fused_iterate<3, 4>
+                   : (kp == 8 ? km::k_fused_iterate<3, 8> : km::k_fused_iterate<3, 16>);
+}
+
+int fused_smem(int d, int K) {
+    const int kp = small_kp(K);
+    const int nE = K * d + K + 1;
+    const size_t cs = kp == 4 ? sizeof(km::FusedSmem<4>)
+                              : (kp == 8 ? sizeof(km::FusedSmem<8>) : sizeof(km::FusedSmem<16>));
+    return (int)(cs * km::kFusedWarps +
+                 sizeof(double) * (km::kFusedWarps * 66 + 2 * kp * d + nE));
+}
 
 template <int D, int MODE>
 ChunkFn pick_chunk_kp(int K) {
@@ -398,6 +424,27 @@ kmeans_status configure(kmeans_ctx* ctx) {
         ctx->n_chunks = (int)((ctx->N + ctx->chunk_points - 1) / ctx->chunk_points);
         ctx->row_stride = km::kRowDoubles;
         ctx->G = (ctx->n_chunks + km::kDenseGroup - 1) / km::kDenseGroup;  // groups
+        // small single-GPU shard: whole iterations in one cooperative launch
+        if (!ctx->comm && !(ctx->flags & KMEANS_FLAG_NO_FUSED) &&
+            ctx->n_chunks <= 4 * sms * km::kFusedWarps) {
+            ctx->fused_smem = fused_smem(ctx->d, ctx->K);
+            FusedFn ff = pick_fused(ctx->d, ctx->K);
+            int occ = 0;
+            if (ctx->fused_smem <= maxSmem &&
+                cudaFuncSetAttribute((const void*)ff, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     ctx->fused_smem) == cudaSuccess &&
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)ff,
+                                                              km::kFusedWarps * 32,
+                                                              ctx->fused_smem) == cudaSuccess &&
+                occ >= 1) {
+                // ~4 warp-tiles (512 points) per warp, <= 1 block per SM (co-resident)
+                const int64_t tiles = (ctx->N + 127) / 128;
+                const int64_t need = (tiles + 4 * km::kFusedWarps - 1) / (4 * km::kFusedWarps);
+                ctx->fused_grid = (int)std::min<int64_t>(std::max<int64_t>(need, 1), sms);
+                ctx->fused = true;
+            }
+            cudaGetLastError();
+        }
     } else {
         int tpb = km::kLargeTPBMax;
         while (tpb > 64 && large_smem(ctx->d, ctx->K, tpb) > maxSmem - 4096) tpb -= 32;
@@ -868,6 +915,7 @@ void kmeans_destroy(kmeans_ctx* ctx) {
         pool_free(ctx, ctx->cbox);
         pool_free(ctx, ctx->cand_count);
         pool_free(ctx, ctx->labels_sorted);
+        pool_free(ctx, ctx->brow);
         if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
         cudaGetLastError();
     }
@@ -944,6 +992,7 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
         set_error("KMEANS_FLAG_NO_SORT and KMEANS_FLAG_FORCE_SORT together");
         return fail(KMEANS_EINVAL);
     }
+    ctx->flags = opts.flags;
     if (opts.flags & KMEANS_FLAG_NO_SORT) ctx->sorted = false;
     else if (opts.flags & KMEANS_FLAG_FORCE_SORT) ctx->sorted = true;
     else ctx->sorted = K > 16 || (double)N * K * d >= 3.84e8;   // see kmeans.h
@@ -969,7 +1018,9 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
           pool_alloc(ctx, &ctx->scount, sizeof(int) * (size_t)ctx->n_super) != cudaSuccess ||
           pool_alloc(ctx, &ctx->heavy, sizeof(int) * (size_t)ctx->n_chunks) != cudaSuccess ||
           pool_alloc(ctx, &ctx->heavy_count, sizeof(int)) != cudaSuccess)) ||
-        pool_alloc(ctx, &ctx->flag, sizeof(int)) != cudaSuccess) {
+        pool_alloc(ctx, &ctx->flag, sizeof(int)) != cudaSuccess ||
+        (ctx->fused && pool_alloc(ctx, &ctx->brow, sizeof(double) * 2 * (size_t)ctx->nE *
+                                                       ctx->fused_grid) != cudaSuccess)) {
         cudaGetLastError();
         set_error("device allocation failed (%zu bytes of points)", bytesX);
         return fail(KMEANS_ENOMEM);
@@ -1106,6 +1157,20 @@ kmeans_status kmeans_iterate(kmeans_ctx* ctx, int n) {
     DeviceGuard g(ctx->device);
     kmeans_status s = ensure_graph(ctx);
     if (s != KMEANS_OK) return s;
+    if (ctx->fused) {   // n iterations (or until the stop rule) in one cooperative launch
+        if (n == 0) return KMEANS_OK;
+        FusedFn ff = pick_fused(ctx->d, ctx->K);
+        int n_iter = n;
+        void* args[] = {(void*)&ctx->X,     (void*)&ctx->N,         (void*)&ctx->K,
+                        (void*)&ctx->n_chunks, (void*)&ctx->mu,     (void*)&ctx->st,
+                        (void*)&ctx->trace_E, (void*)&ctx->trace_J, (void*)&ctx->trace_cap,
+                        (void*)&ctx->brow,  (void*)&ctx->red,       (void*)&n_iter};
+        CK(cudaLaunchCooperativeKernel((const void*)ff, dim3(ctx->fused_grid),
+                                       dim3(km::kFusedWarps * 32), args, ctx->fused_smem,
+                                       ctx->stream));
+        ctx->launches += 1;
+        return KMEANS_OK;
+    }
     int i = 0;
     for (; i + kGraphUnroll <= n; i += kGraphUnroll)
         CK(cudaGraphLaunch(ctx->graph_u, ctx->stream));
@@ -1406,6 +1471,8 @@ kmeans_status kmeans_get_info(kmeans_ctx* ctx, kmeans_info* info) {
     info->kernel_launches = ctx->launches;
     info->nranks = ctx->nranks;
     info->sorted = ctx->sorted ? 1 : 0;
+    info->fused = ctx->fused ? 1 : 0;
+    info->fused_grid = ctx->fused_grid;
     info->rank = ctx->rank;
     return KMEANS_OK;
 }

@@ -106,6 +106,33 @@ WORKLOADS = {
 }
 
 
+def paper_grid() -> list[Workload]:
+    """The paper's experiment grid as synthetic workloads:
+    Table 1 (serial, PAPER.md:77-91): 2D N = 5e5 and 3D N = 1e6 at K = 4, 8, 11;
+    Tables 2/4 (PAPER.md:103-114, 149-160): 2D N = 1e5, 2e5, 5e5 at K = 8;
+    Tables 3/5: 3D N = 1e5 ... 1e6 at K = 4.
+    The paper's mixtures are unpublished ("Bivariate Gaussian Distributions of
+    some mean and covariance"): here 8 blobs on a 4 x 2 grid (2D)
+    and 4 blobs on a 2 x 2 x 1 grid (3D), sigma = 1, spacing 10 sigma; the
+    dataset of a given (d, N) is the same for every K (seed by d and N)."""
+    out = []
+
+    def wl(d, N, K):
+        grid = (4, 2) if d == 2 else (2, 2, 1)
+        seed = 1100 + 10 * d + int(round(math.log10(N) * 10))
+        return Workload(f"P{d}D-N{N}-K{K}", N, d, K, grid, seed, seed + 1000,
+                        tol=1e-6, max_iter=1000)
+    for K in (4, 8, 11):
+        out.append(wl(2, 500_000, K))
+    for K in (4, 8, 11):
+        out.append(wl(3, 1_000_000, K))
+    for N in (100_000, 200_000):
+        out.append(wl(2, N, 8))
+    for N in (100_000, 200_000, 400_000, 800_000):
+        out.append(wl(3, N, 4))
+    return out
+
+
 def planted_indices(w: Workload, N: int | None = None) -> np.ndarray:
     """Indices of the planted duplicate points (C5): site g occupies
     [g * (N // G), g * (N // G) + r)."""

@@ -29,6 +29,13 @@ def broadcast_unique_id(rank: int, group=None) -> bytes:
 
 
 def init_comm(rank: int, world: int, device: int, group=None) -> int:
-    """Create the library's NCCL communicator for this rank (collective)."""
+    """Create the library's NCCL communicator for this rank (collective).
+
+    NCCL_ALGO / NCCL_PROTO are pinned (unless the caller set them) so the
+    allreduce's summation order -- and so every centroid bit -- is the same
+    from run to run."""
+    import os
+    os.environ.setdefault("NCCL_ALGO", "Ring")
+    os.environ.setdefault("NCCL_PROTO", "Simple")
     uid = broadcast_unique_id(rank, group)
     return km.comm_init(world, uid, rank, device)

@@ -23,6 +23,7 @@ STATUS = {0: "KMEANS_OK", -1: "KMEANS_EINVAL", -2: "KMEANS_ENONFINITE", -3: "KME
 LAYOUT_AOS, LAYOUT_SOA = 0, 1
 FLAG_NO_SORT = 1
 FLAG_FORCE_SORT = 2
+FLAG_NO_FUSED = 4
 MAX_K = 1024
 
 
@@ -45,7 +46,8 @@ class Info(ctypes.Structure):
                 ("d", ctypes.c_int), ("K", ctypes.c_int), ("grid", ctypes.c_int),
                 ("block", ctypes.c_int), ("smem_bytes", ctypes.c_int), ("path", ctypes.c_int),
                 ("kernels_per_iter", ctypes.c_int), ("kernel_launches", ctypes.c_int64),
-                ("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("sorted", ctypes.c_int)]
+                ("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("sorted", ctypes.c_int),
+                ("fused", ctypes.c_int), ("fused_grid", ctypes.c_int)]
 
 
 # Every exported symbol with (restype, argtypes); tests check the header matches.
@@ -146,7 +148,7 @@ class Context:
 
     def __init__(self, points, K: int, *, d: int | None = None, layout: str = "aos",
                  device: int = -1, stream=None, comm=None, global_offset: int = 0,
-                 global_N: int = 0, sort: bool | None = None):
+                 global_N: int = 0, sort: bool | None = None, fused: bool = True):
         pts = _as_f32_points(points)
         shape = tuple(pts.shape)
         if layout == "aos":
@@ -164,6 +166,8 @@ class Context:
         o.global_N = global_N
         # sort: None = the library's choice, True = sorted (pruned) path, False = full scan
         o.flags = 0 if sort is None else (FLAG_FORCE_SORT if sort else FLAG_NO_SORT)
+        if not fused:   # full-scan path: one graph launch per iteration instead of k_fused_iterate
+            o.flags |= FLAG_NO_FUSED
         h = ctypes.c_void_p()
         _check(lib().kmeans_create(ctypes.byref(h), _ptr(pts), self.N, self.d, self.K,
                                    ctypes.byref(o)), "kmeans_create")

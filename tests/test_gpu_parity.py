@@ -188,9 +188,9 @@ def test_step_parity_soa_layout_and_device_input():
 # --------------------------------------------------------------------------
 # full runs
 # --------------------------------------------------------------------------
-def check_fit(X, K, init, tol, max_iter, tag="", sort=True):
+def check_fit(X, K, init, tol, max_iter, tag="", sort=True, fused=True):
     o = oracle.fit(X, K, init, tol, max_iter)
-    with km.Context(X, K, sort=sort) as c:
+    with km.Context(X, K, sort=sort, fused=fused) as c:
         g = c.fit(init, tol, max_iter)
     assert g["iters"] == o["iters"], f"{tag}: iters {g['iters']} vs {o['iters']}"
     assert np.array_equal(g["labels"], o["labels"]), tag
@@ -208,6 +208,48 @@ def test_full_run_parity_one_init_per_blob(name, N, sort):
     init = datagen.one_per_blob_init(w, N=N)
     g, o = check_fit(X, w.M, init, w.tol, w.max_iter, tag=name, sort=sort)
     np.testing.assert_allclose(g["centroids"], w.centers(), atol=0.05)
+
+
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("name,N,K", [("C1", 10_000, 4), ("C2", 1_000_000, 8), ("C2", 77_777, 3),
+                                      ("NS", 3_000_000, 16), ("C3", 2_100_000, 13)])
+def test_fused_iteration_kernel(name, N, K, fused):
+    """Full-scan path on one GPU: k_fused_iterate (many iterations per
+    cooperative launch, one grid barrier each) and the per-iteration graph give
+    the oracle's run -- iterations, labels, centroids, traces."""
+    w = datagen.WORKLOADS[name]
+    X = datagen.generate(w, N=N)
+    init = datagen.init_indices(w, N=N, K=K)
+    g, o = check_fit(X, K, init, 1e-6, 60, tag=f"{name} fused={fused}", sort=False, fused=fused)
+    with km.Context(X, K, sort=False, fused=fused) as c:
+        assert c.info()["fused"] == int(fused)
+        r = c.fit(init, 1e-6, 60)
+        np.testing.assert_allclose(r["E_trace"], o["E_trace"], rtol=1e-6, atol=1e-12)
+        np.testing.assert_allclose(r["J_trace"], o["J_trace"], rtol=1e-9)
+        # split launches: iterate 3 + 2 == a 5-iteration run, bit for bit
+        ref = c.fit(init, 0.0, 5)
+        c.start(init_idx=init, tol=0.0, max_iter=5)
+        c.iterate(3)
+        c.iterate(2)
+        c.iterate(4)   # past max_iter: no-op
+        st = c.poll()
+        assert st["iters"] == 5 and st["done"]
+        assert np.array_equal(c.read_centroids(), ref["centroids"])
+        assert np.array_equal(c.final_labels(), ref["labels"])
+
+
+@pytest.mark.parametrize("cell", ["P2D-N100000-K8", "P3D-N100000-K4", "P2D-N200000-K8",
+                                  "P2D-N500000-K11"])
+def test_paper_grid_full_runs(cell):
+    """cells of the paper's experiment grid (PAPER.md Tables
+    1-5, datagen.paper_grid) run to convergence from the paper's seeded random
+    initial points (tol 1e-6): same iteration count, labels and
+    centroids as the oracle (K = 11 on 8 blobs is a local optimum, reached
+    identically)."""
+    w = {x.name: x for x in datagen.paper_grid()}[cell]
+    X = datagen.generate(w)
+    init = datagen.init_indices(w)
+    check_fit(X, w.K, init, w.tol, w.max_iter, tag=cell, sort=None)
 
 
 def test_full_run_parity_c1_seeded_init():
