@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--no-sort", action="store_true",
                     help="keep the caller's point order (full-scan assign kernel)")
     ap.add_argument("--no-fullscan-roofline", action="store_true")
+    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
+                    help="P > 1: the per-iteration allreduce as one kernel over peer memory "
+                         "(kmeans_p2p_open, default) or ncclAllReduce in the graph")
     return ap.parse_args()
 
 
@@ -262,8 +265,14 @@ def main():
     datagen.generate(gen_w, a, b - a, N=global_N, out=Xh.numpy())
     init = datagen.init_indices(gen_w, N=global_N, K=w.K)
 
-    ctx = km.Context(Xh, w.K, device=local, comm=comm, global_offset=a, global_N=global_N,
-                     sort=False if args.no_sort else None)
+    def make_ctx(points, sort):
+        c = km.Context(points, w.K, device=local, comm=comm, global_offset=a, global_N=global_N,
+                       sort=sort)
+        if distributed and args.exchange == "p2p":
+            kdist.enable_p2p(c)   # collective: all-gathers the IPC handles
+        return c
+
+    ctx = make_ctx(Xh, False if args.no_sort else None)
     info = ctx.info()
     stream = torch.cuda.ExternalStream(ctx.stream)
     ctx.start(init_idx=init, tol=0.0, max_iter=1 << 30)
@@ -350,8 +359,7 @@ def main():
     fullscan = None
     if info["sorted"] and not args.no_fullscan_roofline:
         # the same shard through the full-scan kernel (caller's order, no pruning)
-        cf = km.Context(Xh, w.K, device=local, comm=comm, global_offset=a, global_N=global_N,
-                        sort=False)
+        cf = make_ctx(Xh, False)
         cf.start(init_idx=init, tol=0.0, max_iter=1 << 30)
         tf = time_assign(cf)
         fullscan = roofline_of(tf, "k_assign_chunk" if w.K <= 16 else "k_assign_large", False)
@@ -364,8 +372,7 @@ def main():
         ctx.close()
         barrier()
         t0 = time.perf_counter()
-        c2 = km.Context(Xh, w.K, device=local, comm=comm, global_offset=a, global_N=global_N,
-                        sort=False if args.no_sort else None)
+        c2 = make_ctx(Xh, False if args.no_sort else None)
         t1 = time.perf_counter()
         r = c2.fit(init, 0.0, args.e2e_iters, out_labels=labels_h, traces=False)
         t2 = time.perf_counter()
@@ -400,7 +407,8 @@ def main():
             "n_gpus": P, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": workload_config(w, P, args.scaling),
+            "config": dict(workload_config(w, P, args.scaling),
+                           **({"exchange": args.exchange} if P > 1 else {})),
             "roofline": roofline, "roofline_hbm": roofline_hbm, "stage_ms": stage_ms,
             "roofline_fullscan": fullscan, "candidates": cand,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),

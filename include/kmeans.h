@@ -221,6 +221,35 @@ kmeans_status kmeans_comm_init(void** comm, int nranks, const unsigned char id[1
 
 kmeans_status kmeans_comm_destroy(void* comm);
 
+/* P2P exchange (multi-GPU).  On a context with an NCCL
+ * communicator, the per-iteration allreduce of the K(d+1)+1 partials
+ * ("local cluster means ... transferred to a global variable")
+ * can run as one kernel over peer memory instead of ncclAllReduce: each rank
+ * owns an exchange buffer in its HBM, every rank maps every peer's buffer
+ * (CUDA IPC, NVLink), pushes its vector into all of them, publishes an epoch
+ * flag, waits for all peers' flags and sums the P vectors in rank order (the
+ * same bits on every rank), fused with the update (k_p2p_update).
+ *   1. kmeans_p2p_handle: allocates this rank's buffer (once) and writes its
+ *      64-byte cudaIpcMemHandle_t; the caller all-gathers the handles.
+ *   2. kmeans_p2p_open: `handles` = nranks x 64 bytes in rank order; maps the
+ *      peers' buffers; from then on the iteration, kmeans_start's mu^0
+ *      assembly and kmeans_assign use the exchange.  Collective: every rank
+ *      must open before any rank iterates.
+ * KMEANS_EINVAL without a communicator, or on a second open; KMEANS_ECUDA if
+ * IPC mapping fails (e.g. no peer access). */
+kmeans_status kmeans_p2p_handle(kmeans_ctx* ctx, unsigned char handle[64]);
+kmeans_status kmeans_p2p_open(kmeans_ctx* ctx, const unsigned char* handles);
+
+/* Self-test of the exchange protocol on ONE GPU: P emulated ranks as P blocks
+ * of one cooperative launch (ranks that wait on one another must not be
+ * separate launches on one GPU), each with its own exchange buffer; in round
+ * i rank r contributes vals[i][r][0..n) (host, rounds x P x n doubles) and
+ * out[i][r][0..n) (host) receives what rank r computed -- the rank-ordered sum
+ * over q of vals[i][q].  Synchronous.  KMEANS_EINVAL for P not in [1, 64],
+ * n < 1, rounds < 1 or NULL pointers. */
+kmeans_status kmeans_p2p_selftest(int device, int P, int n, int rounds, const double* vals,
+                                  double* out);
+
 /* NULL-safe; frees all device memory of the context (not the caller's stream
  * or communicator).  Freed blocks go to a library-owned cache per device that
  * the next kmeans_create reuses (no cudaMalloc / cudaFree of the point arrays

@@ -32,7 +32,7 @@ struct DevState {
     int t;
     int done;
     int max_iter;
-    int pad0;
+    int gen;        // kmeans_start generation (P2P exchange epochs)
     double tol;
     double E;
     double J;
@@ -2282,6 +2282,107 @@ k_fused_iterate(const float* __restrict__ X, int64_t n, int K, int n_chunks,
         for (int q = tid; q < K * D; q += blockDim.x) mu_s[q] = mu_n[q];
         t += 1;
         done = (E < tol) || (t >= max_iter);
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// P2P exchange (multi-GPU): the allreduce of the K(d+1)+1
+// partials as one kernel over peer memory instead of a collective library call.
+// Every rank owns an exchange buffer in its own HBM, mapped into every peer
+// (CUDA IPC over NVLink): xb[slot][P][cap] doubles and xf[slot][P] epochs.
+// Rank r stores its vector into xb[slot][r] of EVERY rank (remote stores),
+// fences at system scope, then publishes `epoch` in xf[slot][r] of every rank
+// (st.release.sys); it waits until its own xf[slot][q] == epoch for all q
+// (ld.acquire.sys) and sums xb[slot][0..P-1] in rank order -- the same bits on
+// every rank.  Slots alternate with the exchange parity, so a rank can only
+// overwrite a slot after every peer has published the next exchange, i.e.
+// finished reading that slot.  Epochs are unique per exchange (generation,
+// iteration) so stale flags never match.
+// ---------------------------------------------------------------------------
+constexpr int kXSlots = 4;   // 0/1: iteration exchanges (parity of t), 2/3: host-driven ones
+
+struct P2PView {
+    double* const* xb;       // [P] exchange buffers (index rank = own)
+    uint64_t* const* xf;     // [P] epoch flags
+    int P, rank, cap;
+};
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Block-wide: out[i] = sum over ranks q (ascending) of rank q's local[i], i < n.
+// `out` may alias `local` (local is fully sent before out is written).
+__device__ void p2p_exchange(const P2PView& v, const double* local, int n, int slot, uint64_t epoch,
+                             double* out) {
+    const int tid = threadIdx.x;
+    for (int i = tid; i < n; i += blockDim.x) {
+        const double x = local[i];
+        for (int q = 0; q < v.P; ++q) v.xb[q][((size_t)slot * v.P + v.rank) * v.cap + i] = x;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (tid < v.P) st_release_sys(&v.xf[tid][slot * v.P + v.rank], epoch);
+    if (tid < v.P) {
+        const uint64_t* f = &v.xf[v.rank][slot * v.P + tid];
+        while (ld_acquire_sys(f) != epoch) __nanosleep(64);
+    }
+    __threadfence_system();
+    __syncthreads();
+    const double* mine = v.xb[v.rank] + (size_t)slot * v.P * v.cap;
+    for (int i = tid; i < n; i += blockDim.x) {
+        double s = 0.0;
+        for (int q = 0; q < v.P; ++q) s += __ldcv(mine + (size_t)q * v.cap + i);
+        out[i] = s;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ uint64_t iter_epoch(const DevState* st) {
+    return ((uint64_t)(unsigned)(st->gen & 0x7fffffff) << 32) | (uint64_t)(unsigned)(st->t + 1);
+}
+
+// Host-driven exchange (mu^0 assembly, kmeans_assign): buf <- sum over ranks.
+__global__ void k_p2p_allreduce(P2PView v, double* buf, int n, int slot, uint64_t epoch) {
+    p2p_exchange(v, buf, n, slot, epoch, buf);
+}
+
+// The iteration's exchange fused with the update: red <- sum over ranks of the
+// local merged vector, then the update of k_update (one block).
+template <int D>
+__global__ void k_p2p_update(P2PView v, double* __restrict__ red, int nE, double* __restrict__ mu_buf,
+                             int K, DevState* __restrict__ st, double* __restrict__ trace_E,
+                             double* __restrict__ trace_J, int trace_cap, float4* __restrict__ cneg) {
+    if (st->done) return;
+    p2p_exchange(v, red, nE, st->t & 1, iter_epoch(st), red);
+    __threadfence();
+    __syncthreads();
+    update_body<D>(mu_buf, K, red, st, trace_E, trace_J, trace_cap, cneg);
+}
+
+// One-GPU emulation of P ranks for the tests (PROFILING guide: ranks that wait
+// on one another must not be separate launches on one GPU): ONE cooperative
+// launch, block r = rank r, each with its own exchange buffer in this GPU's
+// memory.  Round i: rank r contributes vals[i][r][0..n) and writes what it
+// received to out[i][r][0..n).
+__global__ void k_p2p_emulate(double* const* xb, uint64_t* const* xf, int P, int cap, int n,
+                              int rounds, const double* __restrict__ vals, double* __restrict__ out,
+                              double* __restrict__ scratch) {
+    P2PView v{xb, xf, P, (int)blockIdx.x, cap};
+    double* loc = scratch + (size_t)blockIdx.x * cap;
+    for (int i = 0; i < rounds; ++i) {
+        for (int e = threadIdx.x; e < n; e += blockDim.x)
+            loc[e] = vals[((size_t)i * P + blockIdx.x) * n + e];
+        __syncthreads();
+        p2p_exchange(v, loc, n, i & 1, (1ull << 40) + (uint64_t)i + 1, loc);
+        for (int e = threadIdx.x; e < n; e += blockDim.x)
+            out[((size_t)i * P + blockIdx.x) * n + e] = loc[e];
         __syncthreads();
     }
 }

@@ -154,6 +154,14 @@ struct kmeans_ctx {
     cudaGraphExec_t graph = nullptr;    // one iteration
     cudaGraphExec_t graph_u = nullptr;  // kGraphUnroll iterations (fewer graph launches)
     int flags = 0;            // kmeans_opts.flags
+    // P2P exchange (kmeans_p2p_handle / kmeans_p2p_open): replaces the NCCL allreduce
+    bool p2p = false;
+    int gen = 0;              // kmeans_start generation (iteration exchange epochs)
+    uint64_t xcount = 0;      // host-driven exchanges so far
+    int xcap = 0;             // doubles per exchange slot
+    void* xown = nullptr;     // own exchange buffer (cudaMalloc, IPC-exported)
+    std::vector<void*> xopened;   // peers' buffers opened by IPC (closed at destroy)
+    void** xtab = nullptr;    // device [2P]: xb pointers then xf pointers
     bool fused = false;       // small full-scan shard: k_fused_iterate (one launch, many iterations)
     int fused_grid = 0;
     int fused_smem = 0;
@@ -568,7 +576,25 @@ kmeans_status launch_merge(kmeans_ctx* ctx, int ignore_done) {
     return KMEANS_OK;
 }
 
+km::P2PView p2p_view(const kmeans_ctx* ctx) {
+    km::P2PView v;
+    v.xb = reinterpret_cast<double* const*>(ctx->xtab);
+    v.xf = reinterpret_cast<uint64_t* const*>(ctx->xtab + ctx->nranks);
+    v.P = ctx->nranks;
+    v.rank = ctx->rank;
+    v.cap = ctx->xcap;
+    return v;
+}
+
 kmeans_status allreduce(kmeans_ctx* ctx, double* buf, size_t count) {
+    if (ctx->p2p) {   // host-driven exchange over peer memory (slots 2/3)
+        const uint64_t n = ++ctx->xcount;
+        km::k_p2p_allreduce<<<1, 256, 0, ctx->stream>>>(p2p_view(ctx), buf, (int)count,
+                                                       2 + (int)(n & 1), (1ull << 63) | n);
+        ctx->launches += 1;
+        CK(cudaGetLastError());
+        return KMEANS_OK;
+    }
     if (!ctx->comm) return KMEANS_OK;
 #ifdef KMEANS_WITH_NCCL
     ncclResult_t r = ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)ctx->comm,
@@ -628,6 +654,21 @@ kmeans_status enqueue_iteration(kmeans_ctx* ctx) {
     kmeans_status s;
     if ((s = launch_assign(ctx, km::kModeReduce, 0, 0)) != KMEANS_OK) return s;
     if (fused_update(ctx)) return launch_merge_update(ctx);
+    if (ctx->p2p) {   // local merge, then the exchange over peer memory fused with the update
+        if ((s = launch_merge(ctx, 0)) != KMEANS_OK) return s;
+        const int tpb = 256;
+        if (ctx->d == 2)
+            km::k_p2p_update<2><<<1, tpb, 0, ctx->stream>>>(
+                p2p_view(ctx), ctx->red, ctx->nE, ctx->mu, ctx->K, ctx->st, ctx->trace_E,
+                ctx->trace_J, ctx->trace_cap, ctx->sorted ? ctx->cneg : nullptr);
+        else
+            km::k_p2p_update<3><<<1, tpb, 0, ctx->stream>>>(
+                p2p_view(ctx), ctx->red, ctx->nE, ctx->mu, ctx->K, ctx->st, ctx->trace_E,
+                ctx->trace_J, ctx->trace_cap, ctx->sorted ? ctx->cneg : nullptr);
+        ctx->launches += 1;
+        CK(cudaGetLastError());
+        return KMEANS_OK;
+    }
     if ((s = launch_merge(ctx, 0)) != KMEANS_OK) return s;
     if ((s = allreduce(ctx, ctx->red, ctx->nE)) != KMEANS_OK) return s;
     return launch_update(ctx);
@@ -681,6 +722,7 @@ kmeans_status write_state(kmeans_ctx* ctx, int t, int done, int max_iter, double
     h.done = done;
     h.max_iter = max_iter;
     h.tol = tol;
+    h.gen = ctx->gen;
     CK(cudaMemcpyAsync(ctx->st, &h, sizeof(DevState), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));  // h is a stack object
     return KMEANS_OK;
@@ -845,6 +887,114 @@ extern "C" {
 
 int kmeans_abi_version(void) { return KMEANS_ABI_VERSION; }
 
+kmeans_status kmeans_p2p_handle(kmeans_ctx* ctx, unsigned char handle[64]) {
+    CHECK_CTX(ctx);
+    if (!handle || !ctx->comm || ctx->p2p) {
+        set_error("kmeans_p2p_handle: needs a handle buffer and an NCCL context not yet opened");
+        return KMEANS_EINVAL;
+    }
+    DeviceGuard g(ctx->device);
+    const int P = ctx->nranks;
+    if (!ctx->xown) {
+        ctx->xcap = ctx->nE;
+        const size_t bytes = sizeof(double) * km::kXSlots * P * (size_t)ctx->xcap +
+                             sizeof(uint64_t) * km::kXSlots * P;
+        CK(cudaMalloc(&ctx->xown, bytes));   // own allocation: IPC-exportable
+        CK(cudaMemset(ctx->xown, 0, bytes));
+        CK(cudaDeviceSynchronize());
+    }
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, ctx->xown));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    memcpy(handle, &h, 64);
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_p2p_open(kmeans_ctx* ctx, const unsigned char* handles) {
+    CHECK_CTX(ctx);
+    if (!handles || !ctx->xown || ctx->p2p) {
+        set_error("kmeans_p2p_open: call kmeans_p2p_handle first (once)");
+        return KMEANS_EINVAL;
+    }
+    DeviceGuard g(ctx->device);
+    const int P = ctx->nranks;
+    std::vector<void*> tab(2 * (size_t)P);
+    for (int q = 0; q < P; ++q) {
+        void* base = nullptr;
+        if (q == ctx->rank) {
+            base = ctx->xown;
+        } else {
+            cudaIpcMemHandle_t h;
+            memcpy(&h, handles + 64 * (size_t)q, 64);
+            CK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+            ctx->xopened.push_back(base);
+        }
+        tab[q] = base;
+        tab[P + q] = static_cast<double*>(base) + (size_t)km::kXSlots * P * ctx->xcap;
+    }
+    if (!ctx->xtab) CK(pool_alloc(ctx, &ctx->xtab, sizeof(void*) * 2 * P));
+    CK(cudaMemcpyAsync(ctx->xtab, tab.data(), sizeof(void*) * 2 * P, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->p2p = true;
+    if (ctx->graph) cudaGraphExecDestroy(ctx->graph);   // the iteration changes
+    if (ctx->graph_u) cudaGraphExecDestroy(ctx->graph_u);
+    ctx->graph = ctx->graph_u = nullptr;
+    return KMEANS_OK;
+}
+
+kmeans_status kmeans_p2p_selftest(int device, int P, int n, int rounds, const double* vals,
+                                  double* out) {
+    if (P < 1 || P > 64 || n < 1 || rounds < 1 || !vals || !out) {
+        set_error("kmeans_p2p_selftest: bad argument");
+        return KMEANS_EINVAL;
+    }
+    DeviceGuard g(device);
+    kmeans_ctx* ctx = nullptr;   // for CK
+    int coop = 0;
+    CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+    const int cap = n;
+    const size_t per = sizeof(double) * km::kXSlots * P * (size_t)cap +
+                       sizeof(uint64_t) * km::kXSlots * P;
+    char* arena = nullptr;
+    double *dv = nullptr, *dout = nullptr, *scratch = nullptr;
+    void** tab = nullptr;
+    const size_t nv = (size_t)rounds * P * n;
+    cudaError_t e = cudaMalloc(&arena, per * P);
+    if (e == cudaSuccess) e = cudaMemset(arena, 0, per * P);
+    if (e == cudaSuccess) e = cudaMalloc(&dv, sizeof(double) * nv);
+    if (e == cudaSuccess) e = cudaMalloc(&dout, sizeof(double) * nv);
+    if (e == cudaSuccess) e = cudaMalloc(&scratch, sizeof(double) * P * (size_t)cap);
+    if (e == cudaSuccess) e = cudaMalloc(&tab, sizeof(void*) * 2 * P);
+    std::vector<void*> h(2 * (size_t)P);
+    for (int q = 0; q < P; ++q) {
+        h[q] = arena + per * q;
+        h[P + q] = static_cast<double*>(h[q]) + (size_t)km::kXSlots * P * cap;
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(tab, h.data(), sizeof(void*) * 2 * P, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(dv, vals, sizeof(double) * nv, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        double* const* xb = reinterpret_cast<double* const*>(tab);
+        uint64_t* const* xf = reinterpret_cast<uint64_t* const*>(tab + P);
+        int cap_ = cap, P_ = P, n_ = n, r_ = rounds;
+        void* args[] = {(void*)&xb, (void*)&xf, (void*)&P_, (void*)&cap_, (void*)&n_, (void*)&r_,
+                        (void*)&dv, (void*)&dout, (void*)&scratch};
+        // all P "ranks" co-resident (they wait on one another): a cooperative launch
+        e = coop ? cudaLaunchCooperativeKernel((const void*)km::k_p2p_emulate, dim3(P), dim3(128),
+                                               args, 0, 0)
+                 : cudaErrorNotSupported;
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(out, dout, sizeof(double) * nv, cudaMemcpyDeviceToHost);
+    cudaFree(arena);
+    cudaFree(dv);
+    cudaFree(dout);
+    cudaFree(scratch);
+    cudaFree(tab);
+    CK(e);
+    return KMEANS_OK;
+}
+
 kmeans_status kmeans_release_memory(int device) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n ||
@@ -916,6 +1066,9 @@ void kmeans_destroy(kmeans_ctx* ctx) {
         pool_free(ctx, ctx->cand_count);
         pool_free(ctx, ctx->labels_sorted);
         pool_free(ctx, ctx->brow);
+        for (void* p : ctx->xopened) cudaIpcCloseMemHandle(p);
+        if (ctx->xown) cudaFree(ctx->xown);
+        pool_free(ctx, ctx->xtab);
         if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
         cudaGetLastError();
     }
@@ -1144,6 +1297,7 @@ kmeans_status kmeans_start(kmeans_ctx* ctx, const int64_t* init_idx, const doubl
     }
     if ((s = ensure_trace(ctx, max_iter)) != KMEANS_OK) return s;
     ctx->assigned = false;
+    ctx->gen += 1;   // new epochs for the iteration exchanges of this run
     if ((s = write_state(ctx, 0, 0, max_iter, tol)) != KMEANS_OK) return s;
     return stage_centroids(ctx);
 }

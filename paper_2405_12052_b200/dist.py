@@ -39,3 +39,14 @@ def init_comm(rank: int, world: int, device: int, group=None) -> int:
     os.environ.setdefault("NCCL_PROTO", "Simple")
     uid = broadcast_unique_id(rank, group)
     return km.comm_init(world, uid, rank, device)
+
+
+def enable_p2p(ctx, group=None):
+    """Switch a communicator context to the P2P exchange (kmeans_p2p_handle /
+    kmeans_p2p_open): the IPC handles are all-gathered over torch.distributed."""
+    import torch.distributed as dist
+    h = ctx.p2p_handle()
+    world = dist.get_world_size(group)
+    handles = [None] * world
+    dist.all_gather_object(handles, h, group=group)
+    ctx.p2p_open(handles)

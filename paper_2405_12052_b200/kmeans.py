@@ -77,6 +77,9 @@ SIGNATURES = {
     "kmeans_last_error": (ctypes.c_char_p, []),
     "kmeans_abi_version": (I, []),
     "kmeans_release_memory": (I, [I]),
+    "kmeans_p2p_handle": (I, [P, P]),
+    "kmeans_p2p_open": (I, [P, P]),
+    "kmeans_p2p_selftest": (I, [I, I, I, I, P, P]),
 }
 
 _lib = None
@@ -270,6 +273,18 @@ class Context:
                "kmeans_profile_stage")
         return ms.value
 
+    def p2p_handle(self) -> bytes:
+        """This rank's exchange-buffer IPC handle (kmeans_p2p_handle, 64 bytes)."""
+        buf = (ctypes.c_ubyte * 64)()
+        _check(lib().kmeans_p2p_handle(self._h, buf), "kmeans_p2p_handle")
+        return bytes(buf)
+
+    def p2p_open(self, handles):
+        """Map every rank's exchange buffer (kmeans_p2p_open); handles in rank order."""
+        blob = b"".join(handles)
+        buf = (ctypes.c_ubyte * len(blob)).from_buffer_copy(blob)
+        _check(lib().kmeans_p2p_open(self._h, buf), "kmeans_p2p_open")
+
     def candidate_stats(self) -> dict:
         """Sorted path: centroid candidates per chunk in the last assign pass."""
         m, mx, one, nch = ctypes.c_double(), ctypes.c_int(), ctypes.c_int64(), ctypes.c_int64()
@@ -329,3 +344,14 @@ def comm_destroy(comm: int):
 def release_memory(device: int = 0):
     """Give the library pool's unused device memory back to the driver."""
     _check(lib().kmeans_release_memory(int(device)), "kmeans_release_memory")
+
+
+def p2p_selftest(vals, device: int = 0):
+    """kmeans_p2p_selftest: vals (rounds, P, n) float64 -> what each emulated
+    rank computed, same shape."""
+    v = np.ascontiguousarray(vals, dtype=np.float64)
+    rounds, P, n = v.shape
+    out = np.empty_like(v)
+    _check(lib().kmeans_p2p_selftest(int(device), int(P), int(n), int(rounds), _ptr(v), _ptr(out)),
+           "kmeans_p2p_selftest")
+    return out

@@ -23,7 +23,7 @@ def km():
 def header_functions():
     src = open(os.path.join(ROOT, "include", "kmeans.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    names = re.findall(r"\b(kmeans_[a-z_]+)\s*\(", src)
+    names = re.findall(r"\b(kmeans_[a-z0-9_]+)\s*\(", src)
     return sorted(set(names))
 
 

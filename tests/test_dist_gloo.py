@@ -91,6 +91,19 @@ def _worker(rank, world, port, q):
             all(np.array_equal(x, y) for x, y in zip(m[0], allmu[0][0])) and m[1] == allmu[0][1]
             for m in allmu)
         out["shards"] = (a, b)
+        # P2P exchange setup (kdist.enable_p2p): every rank maps the handles of
+        # all ranks in rank order
+        class FakeCtx:
+            opened = None
+
+            def p2p_handle(self):
+                return bytes([rank + 1]) * 64
+
+            def p2p_open(self, handles):
+                self.opened = list(handles)
+        fc = FakeCtx()
+        kdist.enable_p2p(fc)
+        out["p2p_handles_ok"] = fc.opened == [bytes([q + 1]) * 64 for q in range(world)]
         q.put((rank, out))
         dist.destroy_process_group()
     except Exception as e:  # pragma: no cover - surfaced by the assertion below
@@ -115,6 +128,7 @@ def test_distributed_decomposition_gloo(world):
         assert res[r]["mu0_exact"]
         assert res[r]["step_ok"]
         assert res[r]["replicated"]
+        assert res[r]["p2p_handles_ok"]
     # shards cover [0, N) contiguously
     spans = sorted(res[r]["shards"] for r in range(world))
     assert spans[0][0] == 0 and spans[-1][1] == 40_001

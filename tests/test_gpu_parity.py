@@ -460,6 +460,51 @@ def test_nccl_single_rank_communicator_path():
     assert np.array_equal(rd["centroids"], rs["centroids"])
 
 
+@pytest.mark.parametrize("P,n,rounds", [(1, 5, 3), (2, 65, 6), (3, 1, 4), (8, 4097, 5),
+                                         (16, 33, 9), (64, 200, 3)])
+def test_p2p_exchange_protocol_emulated(P, n, rounds):
+    """The P2P exchange with P emulated ranks as the blocks
+    of one cooperative launch: every rank receives, bit for bit, the rank-order
+    sum of all ranks' vectors, every round (slot reuse, epochs)."""
+    rng = np.random.default_rng(P * 1000 + n)
+    vals = rng.standard_normal((rounds, P, n)) * 10.0 ** rng.integers(-3, 8, (rounds, P, n))
+    out = km.p2p_selftest(vals)
+    for i in range(rounds):
+        expect = np.zeros(n)
+        for q in range(P):   # rank order, fp64
+            expect = expect + vals[i, q]
+        for r in range(P):
+            assert np.array_equal(out[i, r], expect), (i, r)
+
+
+@pytest.mark.parametrize("sort", SORT)
+def test_p2p_single_rank_iteration(sort):
+    """The iteration with the exchange over peer memory (k_p2p_update, 1-rank
+    communicator: the rank maps only itself) equals the single-GPU run."""
+    w = datagen.WORKLOADS["C2"]
+    N = 200_000
+    X = datagen.generate(w, N=N)
+    init = datagen.one_per_blob_init(w, N=N)
+    uid = km.comm_unique_id()
+    comm = km.comm_init(1, uid, 0, 0)
+    try:
+        with km.Context(X, w.M, comm=comm, global_offset=0, global_N=N, sort=sort) as c:
+            c.p2p_open([c.p2p_handle()])
+            rd = c.fit(init, w.tol, w.max_iter)
+            a = c.assign(rd["centroids"])
+            with pytest.raises(km.KMeansError):
+                c.p2p_open([c.p2p_handle()])   # only once
+    finally:
+        km.comm_destroy(comm)
+    with km.Context(X, w.M, sort=sort) as c:
+        rs = c.fit(init, w.tol, w.max_iter)
+        b = c.assign(rs["centroids"])
+    assert rd["iters"] == rs["iters"]
+    assert np.array_equal(rd["labels"], rs["labels"])
+    assert np.array_equal(rd["centroids"], rs["centroids"])
+    assert np.array_equal(a["counts"], b["counts"]) and np.array_equal(a["sums"], b["sums"])
+
+
 # --------------------------------------------------------------------------
 # full-size checks in the launch configuration bench.py times
 # --------------------------------------------------------------------------
