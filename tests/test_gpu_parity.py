@@ -525,6 +525,49 @@ def test_full_size_ns_step_parity(sort):
 
 
 @pytest.mark.slow
+def test_full_size_c3_step_parity():
+    """C3 at P = 1 (N=1e8, 2D, K=16): one full step against the oracle on all
+    N points, in the launch configuration bench.py --workload C3 uses."""
+    w = datagen.WORKLOADS["C3"]
+    X = datagen.generate(w)
+    mu = X[datagen.init_indices(w)].astype(np.float64)
+    with km.Context(X, w.K) as c:
+        assert c.info()["sorted"] == 1
+        check_step(X, mu, ctx=c, tag="C3 full")
+
+
+@pytest.mark.slow
+def test_full_size_c4_rank_shard_sampled_parity():
+    """C4 (N=1e9, 3D, K=16, P=8): the shard of rank 5 (1.25e8 points, global
+    offset 6.25e8) as bench.py --gpus 8 generates it; labels of a sample
+    against the oracle one by one; counts and per-cluster sums of the whole
+    shard against a float64 bincount over the GPU labels and the shard's
+    coordinate sums."""
+    w = datagen.WORKLOADS["C4"]
+    P, r = 8, 5
+    a, b = datagen.shard_range(w.N, P, r)
+    Xs = datagen.generate(w, a, b - a)
+    init = datagen.init_indices(w)
+    rows = np.stack([datagen.generate(w, int(i), 1)[0] for i in init])   # global init points
+    mu = rows.astype(np.float64)
+    with km.Context(Xs, w.K) as c:   # (global offsets need a communicator; assign takes mu)
+        assert c.info()["sorted"] == 1
+        g = c.assign(mu)
+    rng = np.random.default_rng(5)
+    sample = np.sort(rng.choice(b - a, 300_000, replace=False))
+    o = oracle.partials(Xs[sample], mu)
+    assert np.array_equal(g["labels"][sample], o["labels"])
+    assert g["counts"].sum() == b - a
+    tot = g["sums"].sum(axis=0)
+    ref = Xs.astype(np.float64).sum(axis=0)
+    assert np.all(np.abs(tot - ref) <= 1e-9 * np.abs(Xs).astype(np.float64).sum(axis=0))
+    # per-cluster sums of the full shard against a float64 bincount of the GPU labels
+    for j in range(w.d):
+        ref_j = np.bincount(g["labels"], weights=Xs[:, j].astype(np.float64), minlength=w.K)
+        assert np.all(np.abs(g["sums"][:, j] - ref_j) <= 1e-9 * np.abs(ref_j) + 1e-6)
+
+
+@pytest.mark.slow
 def test_full_size_c5_sampled_parity():
     """C5 (N=5e7, 3D, K=1024, forced empty clusters): labels of a sample
     against the oracle one by one; properties at full size (counts sum to N,
