@@ -59,6 +59,10 @@ def parse():
     ap.add_argument("--no-sort", action="store_true",
                     help="keep the caller's point order (full-scan assign kernel)")
     ap.add_argument("--no-fullscan-roofline", action="store_true")
+    ap.add_argument("--gen", choices=["host", "device"], default="host",
+                    help="where the synthetic shard is generated: datagen on the host, or "
+                         "kmeans_generate in HBM (SURVEY.md NEXT-2; the e2e leg still copies "
+                         "it to pinned host memory first, outside its timing)")
     ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
                     help="P > 1: the per-iteration allreduce as one kernel over peer memory "
                          "(kmeans_p2p_open, default) or ncclAllReduce in the graph")
@@ -262,7 +266,13 @@ def main():
     a, b = datagen.shard_range(global_N, P, rank)
     gen_w = w if args.scaling == "strong" else dataclasses.replace(w, N=global_N)
     Xh = torch.empty((b - a, w.d), dtype=torch.float32, pin_memory=True)
-    datagen.generate(gen_w, a, b - a, N=global_N, out=Xh.numpy())
+    Xd = None
+    if args.gen == "device":
+        Xd = torch.empty((b - a, w.d), dtype=torch.float32, device="cuda")
+        km.generate(datagen.mixture_spec(gen_w, global_N), a, b - a, Xd, device=local)
+        Xh.copy_(Xd)
+    else:
+        datagen.generate(gen_w, a, b - a, N=global_N, out=Xh.numpy())
     init = datagen.init_indices(gen_w, N=global_N, K=w.K)
 
     def make_ctx(points, sort):
@@ -272,7 +282,8 @@ def main():
             kdist.enable_p2p(c)   # collective: all-gathers the IPC handles
         return c
 
-    ctx = make_ctx(Xh, False if args.no_sort else None)
+    ctx = make_ctx(Xh if Xd is None else Xd, False if args.no_sort else None)
+    del Xd   # the context holds its own (sorted) copy
     info = ctx.info()
     stream = torch.cuda.ExternalStream(ctx.stream)
     ctx.start(init_idx=init, tol=0.0, max_iter=1 << 30)
@@ -407,7 +418,7 @@ def main():
             "n_gpus": P, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": dict(workload_config(w, P, args.scaling),
+            "config": dict(workload_config(w, P, args.scaling), gen=args.gen,
                            **({"exchange": args.exchange} if P > 1 else {})),
             "roofline": roofline, "roofline_hbm": roofline_hbm, "stage_ms": stage_ms,
             "roofline_fullscan": fullscan, "candidates": cand,

@@ -221,6 +221,31 @@ kmeans_status kmeans_comm_init(void** comm, int nranks, const unsigned char id[1
 
 kmeans_status kmeans_comm_destroy(void* comm);
 
+/* On-device synthetic input: the seeded Gaussian mixture
+ * of DESIGN.md "Inputs", generated directly in HBM by the same
+ * counter-based recipe as the host generator (datagen.py), so a rank can make
+ * its shard [start, start + count) of an N-point dataset without host memory
+ * or PCIe.  Box-Muller runs in fp64 with the device libm, whose log1p / cos /
+ * sin may differ from the host's by an ulp: a value can move by one fp32 ulp
+ * (rarely; bounded in the tests). */
+typedef struct kmeans_mixture {
+    uint64_t seed;          /* data seed (datagen Workload.data_seed) */
+    int d;                  /* 2 or 3 */
+    int M;                  /* blobs, >= 1 */
+    const double* centers;  /* M x d, host */
+    double sigma;           /* blob standard deviation */
+    int n_sites;            /* planted outlier sites G (0 = none) */
+    int site_dups;          /* duplicates per site r: points g (N / G) + q, q < r */
+    const double* sites;    /* G x d, host (NULL if G = 0) */
+    int64_t N;              /* points in the whole dataset */
+} kmeans_mixture;
+
+/* Writes points [start, start + count) as AoS fp32 (count x d) to `out`
+ * (device memory) on `stream` (cudaStream_t, NULL = default stream) of CUDA
+ * device `device`; synchronous.  KMEANS_EINVAL for a bad spec or range. */
+kmeans_status kmeans_generate(const kmeans_mixture* mix, int64_t start, int64_t count, float* out,
+                              int device, void* stream);
+
 /* P2P exchange (multi-GPU).  On a context with an NCCL
  * communicator, the per-iteration allreduce of the K(d+1)+1 partials
  * ("local cluster means ... transferred to a global variable")

@@ -211,6 +211,15 @@ constexpr int kLaneTile = 2 * kWarpTile;                 // 128 points per warp-
 #ifndef KM_SORTED_CHUNK_TILES
 #define KM_SORTED_CHUNK_TILES 8
 #endif
+#ifndef KM_TWO_CAND
+#define KM_TWO_CAND 1   // register path for two-candidate chunks (K <= 16)
+#endif
+#ifndef KM_LARGE_SLOTS
+#define KM_LARGE_SLOTS 8
+#endif
+#ifndef KM_LARGE_CAP
+#define KM_LARGE_CAP 64
+#endif
 #ifndef KM_SORTED_SLOTS
 #define KM_SORTED_SLOTS 4
 #endif
@@ -733,8 +742,8 @@ constexpr int kRowHead = 2;                             // J, count
 
 template <bool LARGE>
 struct PCfg {
-    static constexpr int kSlots = LARGE ? 8 : KM_SORTED_SLOTS;   // column slots per pass
-    static constexpr int kCap = LARGE ? 64 : 16;                 // refined candidates kept
+    static constexpr int kSlots = LARGE ? KM_LARGE_SLOTS : KM_SORTED_SLOTS;   // column slots per pass
+    static constexpr int kCap = LARGE ? KM_LARGE_CAP : 16;   // refined candidates kept
     // winning-slot cache for passes > 0 (large K); small K recomputes the argmin
     static constexpr int kSlotCache = LARGE ? kSChunkPoints : 2;
 };
@@ -1030,6 +1039,84 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
         }
         return;
     }
+
+#if KM_TWO_CAND
+    if (!LARGE && nc == 2) {
+        // ---- two candidates (nearly every multi-candidate chunk at NS): the
+        // strict-< argmin of the pair (lowest k on ties: the list ascends in k),
+        // sums of both candidates in registers (selects; adding +0.0 leaves a
+        // sum unchanged), two chains (a- and b-points) ----
+        float4 c0, c1;
+        const int k0 = cand_at(0, c0), k1 = cand_at(1, c1);
+        double s0[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+        double s1[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+        double Jc[2] = {0.0, 0.0};
+        int n1[2] = {0, 0}, nv[2] = {0, 0};
+        auto add = [&](int ch, float px, float py, float pz, float d0, float d1) {
+            const bool w1 = d1 < d0;
+            const double x = (double)px, y = (double)py, z = (double)pz;
+            s0[ch][0] += w1 ? 0.0 : x;
+            s0[ch][1] += w1 ? 0.0 : y;
+            s1[ch][0] += w1 ? x : 0.0;
+            s1[ch][1] += w1 ? y : 0.0;
+            if (D == 3) {
+                s0[ch][2] += w1 ? 0.0 : z;
+                s1[ch][2] += w1 ? z : 0.0;
+            }
+            Jc[ch] += (double)(w1 ? d1 : d0);
+            n1[ch] += w1 ? 1 : 0;
+            nv[ch] += 1;
+        };
+#pragma unroll 1
+        for (int u = 0; u < nunit; ++u) {
+            Pts P[kUnitSub];
+            fetch(u, P);
+#pragma unroll
+            for (int h = 0; h < kUnitSub; ++h) {
+                const float2 a0 = dist2(P[h].xa, P[h].ya, P[h].za, c0);
+                const float2 a1 = dist2(P[h].xa, P[h].ya, P[h].za, c1);
+                const float2 b0 = dist2(P[h].xb, P[h].yb, P[h].zb, c0);
+                const float2 b1 = dist2(P[h].xb, P[h].yb, P[h].zb, c1);
+                const int64_t pa = base + (int64_t)u * kSortedUnit + h * kLaneTile + 2 * lane;
+                const int64_t pb = pa + kWarpTile;
+                if (MODE & kModeLabels) {
+                    *reinterpret_cast<int2*>(labels + pa) =
+                        make_int2(a1.x < a0.x ? k1 : k0, a1.y < a0.y ? k1 : k0);
+                    *reinterpret_cast<int2*>(labels + pb) =
+                        make_int2(b1.x < b0.x ? k1 : k0, b1.y < b0.y ? k1 : k0);
+                }
+                if (MODE & kModeReduce) {
+                    if (pa < n) add(0, P[h].xa.x, P[h].ya.x, P[h].za.x, a0.x, a1.x);
+                    if (pa + 1 < n) add(0, P[h].xa.y, P[h].ya.y, P[h].za.y, a0.y, a1.y);
+                    if (pb < n) add(1, P[h].xb.x, P[h].yb.x, P[h].zb.x, b0.x, b1.x);
+                    if (pb + 1 < n) add(1, P[h].xb.y, P[h].yb.y, P[h].zb.y, b0.y, b1.y);
+                }
+            }
+        }
+        if (!(MODE & kModeReduce)) return;
+        double v[7] = {s0[0][0] + s0[1][0], s0[0][1] + s0[1][1], s0[0][2] + s0[1][2],
+                       s1[0][0] + s1[1][0], s1[0][1] + s1[1][1], s1[0][2] + s1[1][2],
+                       Jc[0] + Jc[1]};
+        int c1n = n1[0] + n1[1], cvn = nv[0] + nv[1];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+            for (int q = 0; q < 7; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+            c1n += __shfl_xor_sync(0xffffffffu, c1n, o);
+            cvn += __shfl_xor_sync(0xffffffffu, cvn, o);
+        }
+        if (lane == 0) {   // sparse row: J, 2 entries (ascending k)
+            row[0] = v[6];
+            row[1] = 2.0;
+            double2* e = reinterpret_cast<double2*>(row + kRowHead);
+            e[0] = make_double2(v[0], v[1]);
+            e[1] = make_double2(v[2], pack_kn(k0, cvn - c1n));
+            e[2] = make_double2(v[3], v[4]);
+            e[3] = make_double2(v[5], pack_kn(k1, c1n));
+        }
+        return;
+    }
+#endif
 
     // ---- several candidates ----
     const int ncand = big ? gcount : nc;   // slots = indices into the candidate list
@@ -2384,6 +2471,68 @@ __global__ void k_p2p_emulate(double* const* xb, uint64_t* const* xf, int P, int
         for (int e = threadIdx.x; e < n; e += blockDim.x)
             out[((size_t)i * P + blockIdx.x) * n + e] = loc[e];
         __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_generate: the synthetic Gaussian-mixture points of
+// DESIGN.md "Inputs" ("mixture of Bivariate Gaussian
+// Distributions"), generated in HBM by the same counter-based recipe as
+// paper_2405_12052_b200/datagen.py (an independent implementation of it):
+//   u(i, s) = mix64(mix64(seed) + (8 i + s + 1) * golden) >> 11, times 2^-53
+//   blob    = min(floor(u(i,0) M), M - 1)
+//   n0, n1  = Box-Muller(u(i,1), u(i,2)); n2 = Box-Muller cos part of (u(i,3), u(i,4))
+//   x_ij    = fp32(center[blob][j] + sigma n_j)            (fp64, one rounding)
+// planted duplicates (C5): point g (N / G) + q, q < r, is site g.  Points
+// [start, start + count) of the dataset, AoS.  The fp64 log1p / cos / sin may
+// differ from the host libm by an ulp, which moves an fp32 result by one ulp
+// in rare cases (bounded in the tests).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t mix64_dev(uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+}
+
+__global__ void k_generate(uint64_t key, int d, int M, const double* __restrict__ centers,
+                           double sigma, int G, int r, const double* __restrict__ sites,
+                           int64_t N, int64_t start, int64_t count, float* __restrict__ out) {
+    constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += stride) {
+        const int64_t i = start + t;
+        auto U = [&](int s_) {
+            const uint64_t z = mix64_dev(key + ((uint64_t)i * 8ull + (uint64_t)s_ + 1ull) * kGolden);
+            return (double)(z >> 11) * (1.0 / 9007199254740992.0);
+        };
+        int blob = (int)(U(0) * (double)M);
+        blob = blob < M - 1 ? blob : M - 1;
+        const double u1 = U(1), u2 = U(2);
+        const double rr = sqrt(__dmul_rn(-2.0, log1p(-u1)));
+        const double th = __dmul_rn(2.0 * 3.141592653589793, u2);
+        double col[3];
+        col[0] = __dmul_rn(rr, cos(th));
+        col[1] = __dmul_rn(rr, sin(th));
+        if (d > 2) {
+            const double u3 = U(3), u4 = U(4);
+            col[2] = __dmul_rn(sqrt(__dmul_rn(-2.0, log1p(-u3))),
+                               cos(__dmul_rn(2.0 * 3.141592653589793, u4)));
+        }
+        int site = -1;
+        if (G > 0) {
+            const int64_t st_ = N / G;
+            const int64_t g = i / st_, q = i - g * st_;
+            if (g < G && q < r) site = (int)g;
+        }
+        for (int j = 0; j < d; ++j) {
+            // mul then add, each rounded (no FMA contraction), as on the host
+            const double v = (site >= 0) ? sites[site * d + j]
+                                         : __dadd_rn(centers[blob * d + j], __dmul_rn(sigma, col[j]));
+            out[t * d + j] = (float)v;
+        }
     }
 }
 

@@ -995,6 +995,43 @@ kmeans_status kmeans_p2p_selftest(int device, int P, int n, int rounds, const do
     return KMEANS_OK;
 }
 
+kmeans_status kmeans_generate(const kmeans_mixture* mix, int64_t start, int64_t count, float* out,
+                              int device, void* stream) {
+    if (!mix || !out || (mix->d != 2 && mix->d != 3) || mix->M < 1 || !mix->centers ||
+        mix->n_sites < 0 || (mix->n_sites > 0 && (!mix->sites || mix->site_dups < 0)) ||
+        mix->N < 1 || start < 0 || count < 0 || start + count > mix->N) {
+        set_error("kmeans_generate: invalid argument");
+        return KMEANS_EINVAL;
+    }
+    if (count == 0) return KMEANS_OK;
+    DeviceGuard g(device);
+    kmeans_ctx* ctx = nullptr;   // for CK
+    cudaStream_t s = (cudaStream_t)stream;
+    const int d = mix->d;
+    double *dc = nullptr, *ds = nullptr;
+    CK(cudaMallocAsync(&dc, sizeof(double) * mix->M * d, s));
+    if (mix->n_sites > 0) CK(cudaMallocAsync(&ds, sizeof(double) * mix->n_sites * d, s));
+    CK(cudaMemcpyAsync(dc, mix->centers, sizeof(double) * mix->M * d, cudaMemcpyHostToDevice, s));
+    if (ds)
+        CK(cudaMemcpyAsync(ds, mix->sites, sizeof(double) * mix->n_sites * d,
+                           cudaMemcpyHostToDevice, s));
+    // key = mix64(seed) on the host (the same finaliser as the kernel)
+    uint64_t z = mix->seed;
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    const int blocks = (int)std::min<int64_t>((count + 255) / 256, 148 * 16);
+    km::k_generate<<<blocks, 256, 0, s>>>(z, d, mix->M, dc, mix->sigma, mix->n_sites,
+                                          mix->site_dups, ds, mix->N, start, count, out);
+    CK(cudaGetLastError());
+    CK(cudaFreeAsync(dc, s));
+    if (ds) CK(cudaFreeAsync(ds, s));
+    CK(cudaStreamSynchronize(s));   // the host spec arrays are copied by now
+    return KMEANS_OK;
+}
+
 kmeans_status kmeans_release_memory(int device) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n ||

@@ -133,6 +133,15 @@ def paper_grid() -> list[Workload]:
     return out
 
 
+def mixture_spec(w: Workload, N: int | None = None) -> dict:
+    """The parameters of this recipe for the on-device generator
+    (kmeans_generate): seed, blob centres, sigma, planted sites."""
+    N = w.N if N is None else N
+    return {"seed": w.data_seed, "d": w.d, "M": w.M, "centers": w.centers(), "sigma": w.sigma,
+            "n_sites": w.planted_sites, "site_dups": w.planted_dups,
+            "sites": planted_site_coords(w) if w.planted_sites else None, "N": N}
+
+
 def planted_indices(w: Workload, N: int | None = None) -> np.ndarray:
     """Indices of the planted duplicate points (C5): site g occupies
     [g * (N // G), g * (N // G) + r)."""

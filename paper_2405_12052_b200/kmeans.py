@@ -50,6 +50,13 @@ class Info(ctypes.Structure):
                 ("fused", ctypes.c_int), ("fused_grid", ctypes.c_int)]
 
 
+class Mixture(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("d", ctypes.c_int), ("M", ctypes.c_int),
+                ("centers", ctypes.c_void_p), ("sigma", ctypes.c_double),
+                ("n_sites", ctypes.c_int), ("site_dups", ctypes.c_int),
+                ("sites", ctypes.c_void_p), ("N", ctypes.c_int64)]
+
+
 # Every exported symbol with (restype, argtypes); tests check the header matches.
 P, I, I64, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
 SIGNATURES = {
@@ -77,6 +84,7 @@ SIGNATURES = {
     "kmeans_last_error": (ctypes.c_char_p, []),
     "kmeans_abi_version": (I, []),
     "kmeans_release_memory": (I, [I]),
+    "kmeans_generate": (I, [P, I64, I64, P, I, P]),
     "kmeans_p2p_handle": (I, [P, P]),
     "kmeans_p2p_open": (I, [P, P]),
     "kmeans_p2p_selftest": (I, [I, I, I, I, P, P]),
@@ -354,4 +362,17 @@ def p2p_selftest(vals, device: int = 0):
     out = np.empty_like(v)
     _check(lib().kmeans_p2p_selftest(int(device), int(P), int(n), int(rounds), _ptr(v), _ptr(out)),
            "kmeans_p2p_selftest")
+    return out
+
+
+def generate(spec: dict, start: int, count: int, out, device: int = 0, stream=None):
+    """kmeans_generate: points [start, start + count) of the mixture `spec`
+    (datagen.mixture_spec) into the device tensor `out` (count x d, float32)."""
+    centers = np.ascontiguousarray(spec["centers"], np.float64)
+    sites = np.ascontiguousarray(spec["sites"], np.float64) if spec["n_sites"] else None
+    m = Mixture(spec["seed"], spec["d"], spec["M"], centers.ctypes.data, spec["sigma"],
+                spec["n_sites"], spec["site_dups"], None if sites is None else sites.ctypes.data,
+                spec["N"])
+    _check(lib().kmeans_generate(ctypes.byref(m), int(start), int(count), _ptr(out), int(device),
+                                 stream), "kmeans_generate")
     return out

@@ -460,6 +460,33 @@ def test_nccl_single_rank_communicator_path():
     assert np.array_equal(rd["centroids"], rs["centroids"])
 
 
+@pytest.mark.parametrize("name,N,start,count", [("C1", 10_000, 0, 10_000),
+                                                ("C5", 2_000_000, 0, 2_000_000),
+                                                ("C4", 1_000_000_000, 625_000_000, 3_000_001),
+                                                ("C3", 100_000_000, 77_777_777, 1_000_000)])
+def test_device_generator_matches_host_recipe(name, N, start, count):
+    """kmeans_generate reproduces datagen.generate: blob
+    choice and planted sites exactly; coordinates bit-identical except where
+    the device libm's fp64 log1p / cos / sin differ from the host's by an ulp,
+    which may move an fp32 value by one ulp (a tiny fraction, bounded here)."""
+    import torch
+    w = datagen.WORKLOADS[name]
+    host = datagen.generate(w, start, count, N=N)
+    dev = torch.empty((count, w.d), dtype=torch.float32, device="cuda")
+    km.generate(datagen.mixture_spec(w, N), start, count, dev)
+    got = dev.cpu().numpy()
+    diff = got != host
+    frac = diff.mean()
+    assert frac <= 1e-5, frac
+    if diff.any():
+        ulp = np.abs(got.view(np.int32).astype(np.int64) - host.view(np.int32).astype(np.int64))
+        assert ulp[diff].max() == 1
+    if w.planted_sites:
+        p = datagen.planted_indices(w, N)
+        p = p[(p >= start) & (p < start + count)] - start
+        assert np.array_equal(got[p], host[p])
+
+
 @pytest.mark.parametrize("P,n,rounds", [(1, 5, 3), (2, 65, 6), (3, 1, 4), (8, 4097, 5),
                                          (16, 33, 9), (64, 200, 3)])
 def test_p2p_exchange_protocol_emulated(P, n, rounds):

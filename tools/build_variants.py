@@ -25,6 +25,12 @@ VARIANTS = {
     "rg256": ("KM_ROW_GROUP=256",),
     "rg512": ("KM_ROW_GROUP=512",),
     "rg1024": ("KM_ROW_GROUP=1024",),
+    "tc0": ("KM_TWO_CAND=0",),
+    "tc1": ("KM_TWO_CAND=1",),
+    "ls4": ("KM_LARGE_SLOTS=4",),
+    "ls16": ("KM_LARGE_SLOTS=16",),
+    "lc32": ("KM_LARGE_CAP=32",),
+    "lc128": ("KM_LARGE_CAP=128",),
     "pdl0": ("KM_PDL=0",),
     "pdl1": ("KM_PDL=1",),
     "pdl1t": ("KM_PDL=1", "KM_PDL_ASSIGN_TRIGGER=1"),
