@@ -226,7 +226,10 @@ constexpr int kLaneTile = 2 * kWarpTile;                 // 128 points per warp-
 constexpr int kChunkTiles = KM_CHUNK_TILES;
 constexpr int kChunkPoints = kLaneTile * kChunkTiles;    // 2048
 constexpr int kStages = 3;
-constexpr int kGroupChunks = 64;
+#ifndef KM_SPARSE_GROUP
+#define KM_SPARSE_GROUP 64
+#endif
+constexpr int kGroupChunks = KM_SPARSE_GROUP;   // chunks per group, large-K sparse rows (<= 256)
 #ifndef KM_ROW_GROUP
 #define KM_ROW_GROUP 256
 #endif
@@ -1633,10 +1636,10 @@ __global__ void k_super_bbox(const float* __restrict__ cbox, int n_chunks, int d
 // ---------------------------------------------------------------------------
 // k_merge_sparse: group g sums the sparse rows of chunks [64g, 64g + 64) into
 // a dense shared table T[K][4].  Entries are staged in shared memory with
-// independent loads; then the chunks are added in ascending order, one thread
-// per entry (the entries of one row have distinct k), a barrier between
-// chunks -- every sum is taken in chunk order, no atomics.  Writes the group's
-// column gpart[e][g] for k_merge.
+// independent loads; then warp w adds, chunk by chunk in ascending order, the
+// entries whose k lies in its own range of T -- every sum is taken in chunk
+// order, no atomics, no block barrier per chunk.  Writes the group's column
+// gpart[e][g] for k_merge.
 // ---------------------------------------------------------------------------
 constexpr int kMergeBatch = 512;   // entries staged per batch
 
@@ -1656,29 +1659,38 @@ k_merge_sparse(const double* __restrict__ rows, int row_stride, int n_chunks, in
     const int c0 = g * kGroupChunks;
     const int nch = min(n_chunks, c0 + kGroupChunks) - c0;
     for (int q = tid; q < 4 * K; q += blockDim.x) T[q] = 0.0;
-    if (tid < nch) {
-        const double* row = rows + (size_t)(c0 + tid) * row_stride;
-        hj[tid] = row[0];
-        cnt[tid] = (int)row[1];
+    for (int q = tid; q < nch; q += blockDim.x) {
+        const double* row = rows + (size_t)(c0 + q) * row_stride;
+        hj[q] = row[0];
+        cnt[q] = (int)row[1];
     }
     __syncthreads();
-    if (tid < 32) {   // exclusive scan of the counts (warp 0, two per lane)
-        const int a = (2 * tid < nch) ? cnt[2 * tid] : 0;
-        const int b = (2 * tid + 1 < nch) ? cnt[2 * tid + 1] : 0;
-        int x = a + b;
+    if (tid < 32) {   // exclusive scan of the counts (warp 0, kPer consecutive per lane)
+        constexpr int kPer = (kGroupChunks + 31) / 32;
+        int a[kPer], sum = 0;
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            const int c = tid * kPer + i;
+            a[i] = (c < nch) ? cnt[c] : 0;
+            sum += a[i];
+        }
+        int x = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(0xffffffffu, x, o);
             if (tid >= o) x += y;
         }
-        const int excl = x - a - b;
-        if (2 * tid < nch) off[2 * tid] = excl;
-        if (2 * tid + 1 < nch) off[2 * tid + 1] = excl + a;
+        int run = x - sum;
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            const int c = tid * kPer + i;
+            if (c < nch) off[c] = run;
+            run += a[i];
+        }
         if (tid == 31) off[nch] = x;
     }
     __syncthreads();
     const int total = off[nch];
-    int c = 0;   // first chunk with entries in the current batch
     for (int b0 = 0; b0 < total; b0 += kMergeBatch) {
         const int bn = min(kMergeBatch, total - b0);
         // stage entries [b0, b0 + bn) (2 double2 each): every thread issues its
@@ -1705,28 +1717,41 @@ k_merge_sparse(const double* __restrict__ rows, int row_stride, int n_chunks, in
         for (int r = 0; r < 4; ++r)
             if (dst[r] >= 0) E[dst[r]] = tmp[r];
         __syncthreads();
-        // chunks in ascending order; the batch may end inside a chunk
-        for (; c < nch && off[c] < b0 + bn; ++c) {
-            const int e_end = min(off[c + 1], b0 + bn);
-            for (int e = max(off[c], b0) + tid; e < e_end; e += blockDim.x) {
-                const double2 v0 = E[2 * (e - b0)];
-                const double2 v1 = E[2 * (e - b0) + 1];
-                const int2 kn = *reinterpret_cast<const int2*>(&v1.y);   // {k, n}
-                double* t = T + 4 * kn.x;
-                t[0] += v0.x;
-                t[1] += v0.y;
-                t[2] += v1.x;
-                t[3] += (double)kn.y;
+        // warp w owns k in [w kw, (w + 1) kw): every warp walks the batch's
+        // chunks in ascending order and adds the entries of its k range (the
+        // entries of one row have distinct k: no conflicts within a chunk;
+        // __syncwarp orders consecutive chunks) -- no block barrier per chunk
+        {
+            const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+            const int kw = (K + nw - 1) / nw, klo = warp * kw, khi = klo + kw;
+            int c = 0;
+            while (c < nch && off[c + 1] <= b0) ++c;   // first chunk with entries in the batch
+            for (; c < nch && off[c] < b0 + bn; ++c) {
+                const int e0 = max(off[c], b0), e1 = min(off[c + 1], b0 + bn);
+                for (int e = e0 + lane; e < e1; e += 32) {
+                    const double2 v1 = E[2 * (e - b0) + 1];
+                    const int2 kn = *reinterpret_cast<const int2*>(&v1.y);   // {k, n}
+                    if (kn.x >= klo && kn.x < khi) {
+                        const double2 v0 = E[2 * (e - b0)];
+                        double* t = T + 4 * kn.x;
+                        t[0] += v0.x;
+                        t[1] += v0.y;
+                        t[2] += v1.x;
+                        t[3] += (double)kn.y;
+                    }
+                }
+                __syncwarp();
             }
-            __syncthreads();
-            if (off[c + 1] > b0 + bn) break;   // rest of chunk c is in the next batch
         }
+        __syncthreads();   // the batch buffer is reused
     }
     __syncthreads();
+#ifndef KM_EXP_NOWRITE
     for (int k = tid; k < K; k += blockDim.x) {
         for (int j = 0; j < D; ++j) gpart[(size_t)(k * D + j) * n_groups + g] = T[4 * k + j];
         gpart[(size_t)(K * D + k) * n_groups + g] = T[4 * k + 3];
     }
+#endif
     if (tid == 0) {
         double J = 0.0;
         for (int cc = 0; cc < nch; ++cc) J += hj[cc];

@@ -25,6 +25,9 @@ VARIANTS = {
     "rg256": ("KM_ROW_GROUP=256",),
     "rg512": ("KM_ROW_GROUP=512",),
     "rg1024": ("KM_ROW_GROUP=1024",),
+    "nowrite": ("KM_EXP_NOWRITE=1",),   # timing experiment only (wrong results)
+    "sg128": ("KM_SPARSE_GROUP=128",),
+    "sg256": ("KM_SPARSE_GROUP=256",),
     "tc0": ("KM_TWO_CAND=0",),
     "tc1": ("KM_TWO_CAND=1",),
     "ls4": ("KM_LARGE_SLOTS=4",),
