@@ -760,6 +760,31 @@ struct PrunedSmem {
     float4 cand[PCfg<LARGE>::kCap];     // negated fp32 centroid of each candidate slot
     int candk[PCfg<LARGE>::kCap];       // centroid index of each slot (ascending)
     unsigned short slot[PCfg<LARGE>::kSlotCache];   // winning slot of each point
+    __device__ __forceinline__ float* ring_at(int s) { return ring[s]; }
+    __device__ __forceinline__ double2* col_a(int k) { return A[k]; }
+    __device__ __forceinline__ double2* col_b(int k) { return B[k]; }
+};
+
+// Small K: the slot columns (only the rare >= 3-candidate chunks use them) share
+// the ring's memory -- such a chunk drains the ring first and then reads its
+// points from global memory -- so a CTA needs ~6.4 KB and more CTAs (more bytes
+// in flight) fit on an SM.
+template <int D>
+struct PrunedSmem<D, false> {
+    static_assert(2 * PCfg<false>::kSlots * 32 * sizeof(double2) <=
+                      kSortedStages * D * kSortedUnit * sizeof(float),
+                  "slot columns must fit in the ring");
+    union {
+        float ring[kSortedStages][D * kSortedUnit];
+        double2 AB[2][PCfg<false>::kSlots][32];
+    } u;
+    uint64_t bar[kSortedStages];
+    float4 cand[PCfg<false>::kCap];
+    int candk[PCfg<false>::kCap];
+    unsigned short slot[PCfg<false>::kSlotCache];
+    __device__ __forceinline__ float* ring_at(int s) { return u.ring[s]; }
+    __device__ __forceinline__ double2* col_a(int k) { return u.AB[0][k]; }
+    __device__ __forceinline__ double2* col_b(int k) { return u.AB[1][k]; }
 };
 
 // {k, n} in one double's bits: k in the low word, n in the high word
@@ -767,8 +792,14 @@ __device__ __forceinline__ double pack_kn(int k, int n) {
     return __hiloint2double(n, k);
 }
 
+// Small K: resident CTAs per SM the register budget is cut for (more CTAs =
+// more bytes in flight; measured: 28 best in 3D, 32 -- the per-SM block limit --
+// in 2D; a 64-register 3D kernel loses more to its two-candidate path)
+#ifndef KM_PRUNED_MINB
+#define KM_PRUNED_MINB (D == 2 ? 32 : 28)
+#endif
 template <int D, int MODE, bool LARGE>
-__global__ void __launch_bounds__(32)
+__global__ void __launch_bounds__(32, LARGE ? 1 : KM_PRUNED_MINB)
 k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
                 const float4* __restrict__ cneg_buf, const DevState* __restrict__ st,
                 int mu_sel, int ignore_done, const float* __restrict__ cbox,
@@ -803,7 +834,7 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
         while (issued < limit && (int)issued < nunit) {
             const int s = issued % SS;
             mbar_expect_tx(&S.bar[s], kUnitBytes);
-            bulk_g2s(S.ring[s], src + (int64_t)issued * kUnitFloats, kUnitBytes, &S.bar[s]);
+            bulk_g2s(S.ring_at(s), src + (int64_t)issued * kUnitFloats, kUnitBytes, &S.bar[s]);
             ++issued;
         }
     };
@@ -935,7 +966,7 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
         mbar_wait(&S.bar[s], (q / SS) & 1u);
 #pragma unroll
         for (int h = 0; h < kUnitSub; ++h) {
-            const float* rg = S.ring[s] + h * (D * kLaneTile);
+            const float* rg = S.ring_at(s) + h * (D * kLaneTile);
             const float* rb = rg + D * kWarpTile;
             P[h].xa = reinterpret_cast<const float2*>(rg)[lane];
             P[h].ya = reinterpret_cast<const float2*>(rg + kWarpTile)[lane];
@@ -1125,16 +1156,23 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
     const int ncand = big ? gcount : nc;   // slots = indices into the candidate list
     double J = 0.0;
     auto accumulate = [&](int l, float px, float py, float pz) {
-        double2 a = S.A[l][lane], b = S.B[l][lane];
+        double2 a = S.col_a(l)[lane], b = S.col_b(l)[lane];
         a.x += (double)px;
         a.y += (double)py;
         if (D == 3) b.x += (double)pz;
         int2 c = *reinterpret_cast<int2*>(&b.y);
         c.x += 1;
         b.y = *reinterpret_cast<double*>(&c);
-        S.A[l][lane] = a;
-        S.B[l][lane] = b;
+        S.col_a(l)[lane] = a;
+        S.col_b(l)[lane] = b;
     };
+    if (!LARGE) {
+        // the slot columns live in the ring: drain the copies in flight first;
+        // every pass then reads the points from global memory
+        const unsigned nq = __shfl_sync(0xffffffffu, issued, 0);
+        for (unsigned q = 0; q < nq; ++q) mbar_wait(&S.bar[q % SS], (q / SS) & 1u);
+        __syncwarp();
+    }
     const int npass = (MODE & kModeReduce) ? (ncand + C::kSlots - 1) / C::kSlots : 1;
 #pragma unroll 1
     for (int pass = 0; pass < npass; ++pass) {
@@ -1142,15 +1180,15 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
         if (MODE & kModeReduce) {
 #pragma unroll
             for (int k = 0; k < C::kSlots; ++k) {
-                S.A[k][lane] = make_double2(0.0, 0.0);
-                S.B[k][lane] = make_double2(0.0, 0.0);
+                S.col_a(k)[lane] = make_double2(0.0, 0.0);
+                S.col_b(k)[lane] = make_double2(0.0, 0.0);
             }
         }
         __syncwarp();
 #pragma unroll 1
         for (int u = 0; u < nunit; ++u) {
             Pts P[kUnitSub];
-            if (pass == 0) fetch(u, P);
+            if (pass == 0 && LARGE) fetch(u, P);
             else reload(u, P);
 #pragma unroll
             for (int h = 0; h < kUnitSub; ++h) {
@@ -1212,7 +1250,7 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
         // 32 lanes in a rotated (bank-conflict-free) order -> row entry of the slot
         const int sl = lane >> 1;
         if (sl < C::kSlots && s_lo + sl < ncand) {
-            const double2* col = (lane & 1) ? &S.B[0][0] : &S.A[0][0];
+            const double2* col = (lane & 1) ? S.col_b(0) : S.col_a(0);
             double v0 = 0.0, v1 = 0.0;
             long long cnt = 0;
 #pragma unroll 8

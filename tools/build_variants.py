@@ -28,6 +28,12 @@ VARIANTS = {
     "nowrite": ("KM_EXP_NOWRITE=1",),   # timing experiment only (wrong results)
     "sg128": ("KM_SPARSE_GROUP=128",),
     "sg256": ("KM_SPARSE_GROUP=256",),
+    "mb1": ("KM_PRUNED_MINB=1",),
+    "mb20": ("KM_PRUNED_MINB=20",),
+    "mb26": ("KM_PRUNED_MINB=26",),
+    "mb24": ("KM_PRUNED_MINB=24",),
+    "mb28": ("KM_PRUNED_MINB=28",),
+    "mb32": ("KM_PRUNED_MINB=32",),
     "tc0": ("KM_TWO_CAND=0",),
     "tc1": ("KM_TWO_CAND=1",),
     "ls4": ("KM_LARGE_SLOTS=4",),
