@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--e2e-iters", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU time of the oracle baseline sample")
     ap.add_argument("--ref-seconds", type=float, default=60.0,
@@ -352,15 +353,23 @@ def main():
                     traffic=traffic, peak_source=f"148 SMs x 128 FP32 lanes x {sm_max_mhz:.0f} MHz",
                     hbm_frac=ach_gbs / hbm_gbs, **common)
 
-    t_assign = time_assign(ctx)
-    if info["sorted"]:
-        kname = "k_assign_pruned" if info["path"] == 0 else "k_prune+k_assign_pruned+k_assign_heavy"
+    if info["fused"]:
+        # small full-scan shard: the whole iteration is ONE kernel (k_fused_iterate,
+        # many iterations per cooperative launch) -- its time per iteration is the step
+        t_assign = ms_per_step / 1e3
+        kname = "k_fused_iterate"
+        stage_ms = {"fused_iteration": ms_per_step}
     else:
-        kname = "k_assign_chunk" if info["path"] == 0 else "k_assign_large"
-    # per-stage device time (each stage alone, back-to-back launches)
-    stage_ms = {"assign": t_assign * 1e3, "row_merge": time_assign(ctx, 2) * 1e3}
-    stage_ms["merge_update_and_gaps"] = ms_per_step - stage_ms["assign"] - stage_ms["row_merge"]
-    stage_ms["k_merge_alone"] = time_assign(ctx, 3) * 1e3   # the P>1 path's group merge
+        t_assign = time_assign(ctx)
+        if info["sorted"]:
+            kname = ("k_assign_pruned" if info["path"] == 0
+                     else "k_prune+k_assign_pruned+k_assign_heavy")
+        else:
+            kname = "k_assign_chunk" if info["path"] == 0 else "k_assign_large"
+        # per-stage device time (each stage alone, back-to-back launches)
+        stage_ms = {"assign": t_assign * 1e3, "row_merge": time_assign(ctx, 2) * 1e3}
+        stage_ms["merge_update_and_gaps"] = ms_per_step - stage_ms["assign"] - stage_ms["row_merge"]
+        stage_ms["k_merge_alone"] = time_assign(ctx, 3) * 1e3   # the P>1 path's group merge
     roofline = roofline_of(t_assign, kname, bool(info["sorted"]))
     roofline_hbm = {"achieved": bytes_per_launch / t_assign / 1e9, "peak": hbm_gbs, "unit": "GB/s",
                     "frac": bytes_per_launch / t_assign / 1e9 / hbm_gbs,
@@ -381,24 +390,32 @@ def main():
     if not args.no_e2e:
         labels_h = torch.empty(n_local, dtype=torch.int32, pin_memory=True)
         ctx.close()
-        barrier()
-        t0 = time.perf_counter()
-        c2 = make_ctx(Xh, False if args.no_sort else None)
-        t1 = time.perf_counter()
-        r = c2.fit(init, 0.0, args.e2e_iters, out_labels=labels_h, traces=False)
-        t2 = time.perf_counter()
-        c2.close()
-        dt = time.perf_counter() - t0
-        barrier()
-        dt = max_over_ranks(dt)
-        assert r["iters"] == args.e2e_iters
+
+        def e2e_step():
+            barrier()
+            t0 = time.perf_counter()
+            c2 = make_ctx(Xh, False if args.no_sort else None)
+            t1 = time.perf_counter()
+            r = c2.fit(init, 0.0, args.e2e_iters, out_labels=labels_h, traces=False)
+            t2 = time.perf_counter()
+            c2.close()
+            t3 = time.perf_counter()
+            barrier()
+            assert r["iters"] == args.e2e_iters
+            return max_over_ranks(t3 - t0), (t1 - t0, t2 - t1, t3 - t2)
+
+        e2e_step()   # warm-up step (first-use costs: allocations, module loading)
+        steps = [e2e_step() for _ in range(args.e2e_steps)]
+        dt = sum(x[0] for x in steps) / len(steps)
+        parts = [sum(x[1][i] for x in steps) / len(steps) for i in range(3)]
         e2e = {"value": global_N * args.e2e_iters / dt, "unit": "points·iter/s",
                "h2d_bytes_per_step": int(Xh.numel() * 4 + 8 * w.K),
                "d2h_bytes_per_step": int(n_local * 4 + 8 * w.K * w.d + 16),
                "step": f"one kmeans_create + kmeans_fit_ctx ({args.e2e_iters} iterations, "
                        "labels out) + kmeans_destroy call from pinned host memory",
+               "steps_timed": args.e2e_steps, "warmup_steps": 1,
                "seconds_per_step": dt,
-               "breakdown_s": {"create": t1 - t0, "fit": t2 - t1, "destroy": dt - (t2 - t0)}}
+               "breakdown_s": {"create": parts[0], "fit": parts[1], "destroy": parts[2]}}
     else:
         ctx.close()
 
