@@ -1,22 +1,31 @@
 // kernels.cuh -- sm_100a kernels of one Lloyd iteration (arXiv 2405.12052).
 //
-// Step map:
-//   k_prep          AoS/SoA fp32 input -> padded SoA fp32, non-finite check (create only)
+// Step map (DESIGN.md section 1 / section 5):
+//   k_prep / k_input_bbox / k_morton / k_gather_sorted / k_chunk_bbox
+//                   create: input -> padded AoSoA fp32 tiles (Morton-sorted by
+//                   default), non-finite check, per-chunk / super-box boxes
 //   k_init_gather   mu^0_k = (double) x[init_idx[k]]
-//   k_assign_chunk  K <= 16: one-warp blocks over fixed 2048-point chunks fed by
-//                   TMA bulk copies; centroids in registers, form-D distances with
-//                   packed f32x2 FADD2/FMUL2/FFMA2, exact argmin (lowest index on
-//                   ties), per-lane private fp64 smem columns, per-chunk partial
-//                   rows merged per 64-chunk group by the last arriving chunk
+//   k_assign_pruned sorted shard (default): one warp per 1024-point chunk fed by
+//                   TMA bulk copies; an exact box bound keeps only the centroids
+//                   that can be a point's argmin; form-D distances (packed
+//                   f32x2), strict-< argmin (lowest index on ties), fused fp64
+//                   sums / counts / inertia -> one sparse row per chunk
 //                                                                        PAPER.md:45-52
-//   k_assign_large  16 < K <= 1024: centroids in smem, per-warp fp64 accumulators
-//                   updated in lane order (conflicting lanes serialised by
-//                   __match_any_sync rounds), per-block partials
-//   k_merge         per-GPU sum of the per-block partials in a fixed order
-//                   (the OpenMP "global variable" merge of PAPER.md:97, without
-//                   the critical section)
-//   k_update        mu^{t+1} = S/n (empty cluster keeps mu^t), E, J, stop flag
-//                                                                        PAPER.md:50-70
+//   k_prune / k_assign_heavy   K > 16: super-box candidate lists; chunks with
+//                   more than 64 candidates, one 8-warp block each
+//   k_assign_chunk  full scan (small shards, KMEANS_FLAG_NO_SORT), K <= 16:
+//                   one warp per 2048-point chunk, centroids in registers,
+//                   exact argmin via FMNMX3 + select, per-lane fp64 columns
+//   k_assign_large  full scan, 16 < K <= 1024: centroids in smem
+//   k_fused_iterate small full-scan shards on one GPU: many whole iterations in
+//                   one cooperative launch (one grid barrier per iteration)
+//   k_merge_sparse16 / k_merge_rows / k_merge_sparse   chunk rows -> groups
+//   k_merge         groups -> one vector, fixed order (the OpenMP "global
+//                   variable" merge of PAPER.md:97, without the critical section)
+//   k_merge_update / k_update / k_p2p_update   mu^{t+1} = S/n (empty cluster
+//                   keeps mu^t), E, J, stop flag (k_p2p_update: after the sum
+//                   over ranks through peer memory)
+//   k_generate      the synthetic mixture on the device
 // No global float atomics anywhere; every reduction has a fixed order, so results
 // are bit-reproducible run to run for a fixed grid.
 #pragma once
@@ -536,8 +545,8 @@ k_assign_chunk(const float* __restrict__ X, int64_t n, int K,
 // Spatially sorted path (default for K <= 16): preprocessing kernels.
 //
 // At kmeans_create the shard's points are put in Morton (Z-curve) order once
-// (CUB radix sort of 30/32-bit keys; stable, so deterministic), and each
-// 2048-point chunk gets its bounding box.  The order is an internal layout:
+// (CUB radix sort of up to 64-bit keys; stable, so deterministic), and each
+// 1024-point chunk gets its bounding box.  The order is an internal layout:
 // labels are scattered back to the caller's order, and every result of the
 // iteration is unchanged (sums are accumulated in a different fixed order).
 // ---------------------------------------------------------------------------

@@ -399,9 +399,9 @@ kmeans_status configure(kmeans_ctx* ctx) {
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
         ctx->chunk_points = km::kSChunkPoints;
         ctx->n_chunks = (int)((ctx->N + ctx->chunk_points - 1) / ctx->chunk_points);
-        // small K: dense rows (k_merge_rows); large K: sparse rows (k_merge_sparse)
+        // sparse rows: <= 16 entries (k_merge_sparse16) or up to K (k_merge_sparse)
         ctx->row_stride = ctx->K <= 16 ? km::kRowDoubles : km::kRowHead + 4 * ctx->K;
-        // groups: 1024 rows (k_merge_sparse16) or 64 rows (k_merge_sparse, large K)
+        // groups: kRowGroup rows (k_merge_sparse16) or kGroupChunks rows (k_merge_sparse)
         ctx->G = ctx->K <= 16 ? (ctx->n_chunks + km::kRowGroup - 1) / km::kRowGroup
                               : (ctx->n_chunks + km::kGroupChunks - 1) / km::kGroupChunks;
         ctx->n_super = (ctx->n_chunks + km::kSuperChunks - 1) / km::kSuperChunks;
