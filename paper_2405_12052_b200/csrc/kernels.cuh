@@ -208,7 +208,7 @@ __device__ __forceinline__ void exact_argmin(const float (&d)[KP], float& m, int
 // Per lane: 4 points per warp-tile (2 float2 groups), packed f32x2 form-D math,
 // centroids (negated fp32) in registers, exact argmin, private fp64 column.
 // Partials: one coalesced row per chunk; k_merge_rows sums each group of
-// kGroupChunks rows in ascending order, k_merge sums the groups.  No atomics.
+// kDenseGroup rows in ascending order, k_merge sums the groups.  No atomics.
 // ---------------------------------------------------------------------------
 constexpr int kLaneTile = 2 * kWarpTile;                 // 128 points per warp-tile
 #ifndef KM_CHUNK_TILES
