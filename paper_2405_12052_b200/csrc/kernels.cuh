@@ -611,9 +611,10 @@ __device__ __forceinline__ unsigned long long part1by2_64(unsigned long long x) 
 // isotropic grid over the global box -- cubic cells keep chunk boxes compact
 // even when the box is very elongated (C5's far outliers), and the fine grid
 // keeps the dense regions resolved -- with the identity permutation as values.
+template <typename KeyT>   // uint32 (d * qbits <= 32) or uint64 keys
 __global__ void k_morton(const float* __restrict__ in, int64_t N, int d, int64_t si, int64_t sj,
                          const unsigned* __restrict__ box, int qbits,
-                         unsigned long long* __restrict__ keys, int32_t* __restrict__ iota) {
+                         KeyT* __restrict__ keys, int32_t* __restrict__ iota) {
     const double qmax = (double)((1ull << qbits) - 1ull);   // qbits <= 32 (2D), <= 21 (3D)
     double lo[3], sc[3], ext = 0.0;
     for (int j = 0; j < d; ++j) {
@@ -629,9 +630,9 @@ __global__ void k_morton(const float* __restrict__ in, int64_t N, int d, int64_t
             t = fmin(fmax(t, 0.0), qmax);
             q[j] = (unsigned long long)t;
         }
-        keys[i] = (d == 2) ? (part1by1_64(q[0]) | (part1by1_64(q[1]) << 1))
-                           : (part1by2_64(q[0]) | (part1by2_64(q[1]) << 1) |
-                              (part1by2_64(q[2]) << 2));
+        keys[i] = (KeyT)((d == 2) ? (part1by1_64(q[0]) | (part1by1_64(q[1]) << 1))
+                                  : (part1by2_64(q[0]) | (part1by2_64(q[1]) << 1) |
+                                     (part1by2_64(q[2]) << 2)));
         iota[i] = (int32_t)i;
     }
 }

@@ -193,6 +193,12 @@ struct CreateTrace {
     }
 };
 
+#ifndef KM_MORTON32
+#define KM_MORTON32 0   // 32-bit Morton keys (see sort_points): 2 ms faster create at
+                        // NS, but 10 bits per axis over a box stretched by far outliers
+                        // (C5's planted sites) destroy the chunks' locality (C5: 360
+                        // candidates per chunk, 7.7 ms per iteration) -- off
+#endif
 #ifndef KM_PDL
 #define KM_PDL 1   // programmatic dependent launch between the iteration's kernels
 #endif
@@ -802,7 +808,7 @@ kmeans_status sort_points(kmeans_ctx* ctx, const float* src, int64_t si, int64_t
     const int64_t N = ctx->N;
     const int d = ctx->d;
     unsigned* box = nullptr;
-    unsigned long long *keys = nullptr, *keys2 = nullptr;
+    void *keys = nullptr, *keys2 = nullptr;
     int32_t* iota = nullptr;
     void* tmp = nullptr;
     size_t tmp_bytes = 0;
@@ -815,14 +821,25 @@ kmeans_status sort_points(kmeans_ctx* ctx, const float* src, int64_t si, int64_t
         pool_free(ctx, iota);
         pool_free(ctx, tmp);
     };
+    // Morton resolution: 2^qbits cells per axis with qbits = ceil(log2 N / d) + 6
+    // (>= 64 cells per point per axis on average; sharper order buys nothing for
+    // 1024-point chunks), capped by the key: 64-bit keys (21 / 32 bits per axis),
+    // or with KM_MORTON32 32-bit keys (10 / 16 bits per axis, 4 radix passes over
+    // 8-byte pairs); the sort only visits d * qbits bits.
+    int lg = 1;
+    while (lg < 40 && (int64_t(1) << lg) < N) ++lg;
+    const bool k32 = KM_MORTON32 != 0;
+    const int qcap = k32 ? 32 / d : (d == 2 ? 32 : 21);
+    const int qbits = std::min(qcap, (lg + d - 1) / d + 6);
+    const size_t ksz = k32 ? sizeof(uint32_t) : sizeof(unsigned long long);
     if (pool_alloc(ctx, &ctx->perm, sizeof(int32_t) * N) != cudaSuccess ||
         pool_alloc(ctx, &ctx->init_pairs, sizeof(int2) * ctx->K) != cudaSuccess ||
         pool_alloc(ctx, &ctx->init_pos, sizeof(int32_t) * ctx->K) != cudaSuccess ||
         pool_alloc(ctx, &ctx->cbox, sizeof(float) * 2 * d * (size_t)ctx->n_chunks) != cudaSuccess ||
         pool_alloc(ctx, &ctx->cand_count, sizeof(int) * (size_t)ctx->n_chunks) != cudaSuccess ||
         pool_alloc(ctx, &box, sizeof(unsigned) * 6) != cudaSuccess ||
-        pool_alloc(ctx, &keys, sizeof(unsigned long long) * N) != cudaSuccess ||
-        pool_alloc(ctx, &keys2, sizeof(unsigned long long) * N) != cudaSuccess ||
+        pool_alloc(ctx, (char**)&keys, ksz * N) != cudaSuccess ||
+        pool_alloc(ctx, (char**)&keys2, ksz * N) != cudaSuccess ||
         pool_alloc(ctx, &iota, sizeof(int32_t) * N) != cudaSuccess) {
         cudaGetLastError();
         cleanup();
@@ -834,27 +851,27 @@ kmeans_status sort_points(kmeans_ctx* ctx, const float* src, int64_t si, int64_t
         hb2[j] = 0xffffffffu;
         hb2[d + j] = 0u;
     }
-    // Morton resolution: 2^qbits cells per axis with qbits = ceil(log2 N / d) + 6
-    // (>= 64 cells per point per axis on average; sharper order buys nothing for
-    // 1024-point chunks), capped by the 64-bit key; the sort only visits d*qbits bits.
-    int lg = 1;
-    while (lg < 40 && (int64_t(1) << lg) < N) ++lg;
-    const int qbits = std::min(d == 2 ? 32 : 21, (lg + d - 1) / d + 6);
     const int blocks = (int)std::min<int64_t>((N + 255) / 256, 148 * 8);
     cudaError_t e = cudaMemcpyAsync(box, hb2, sizeof(unsigned) * 2 * d, cudaMemcpyHostToDevice,
                                     ctx->stream);
+    auto radix = [&](auto* k1, auto* k2) {
+        km::k_morton<<<blocks, 256, 0, ctx->stream>>>(src, N, d, si, sj, box, qbits, k1, iota);
+        ctx->launches += 1;
+        tr.mark(ctx->stream, "bbox + morton keys");
+        cudaError_t r = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k1, k2, iota,
+                                                        ctx->perm, N, 0, d * qbits, ctx->stream);
+        if (r == cudaSuccess) r = pool_alloc(ctx, &tmp, tmp_bytes);
+        if (r == cudaSuccess)
+            r = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k1, k2, iota, ctx->perm, N, 0,
+                                                d * qbits, ctx->stream);
+        return r;
+    };
     if (e == cudaSuccess) {
         km::k_input_bbox<<<blocks, 256, 0, ctx->stream>>>(src, N, d, si, sj, box, ctx->flag);
-        km::k_morton<<<blocks, 256, 0, ctx->stream>>>(src, N, d, si, sj, box, qbits, keys, iota);
-        ctx->launches += 2;
-        tr.mark(ctx->stream, "bbox + morton keys");
-        e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, iota, ctx->perm, N, 0,
-                                            d * qbits, ctx->stream);
+        ctx->launches += 1;
+        e = k32 ? radix((uint32_t*)keys, (uint32_t*)keys2)
+                : radix((unsigned long long*)keys, (unsigned long long*)keys2);
     }
-    if (e == cudaSuccess) e = pool_alloc(ctx, &tmp, tmp_bytes);
-    if (e == cudaSuccess)
-        e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, iota, ctx->perm, N, 0,
-                                            d * qbits, ctx->stream);
     tr.mark(ctx->stream, "radix sort");
     if (e == cudaSuccess) {
         const int gb = (int)std::min<int64_t>((ctx->ldx + 255) / 256, 148 * 8);

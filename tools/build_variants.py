@@ -29,6 +29,8 @@ VARIANTS = {
     "nowrite": ("KM_EXP_NOWRITE=1",),   # timing experiment only (wrong results)
     "sg128": ("KM_SPARSE_GROUP=128",),
     "sg256": ("KM_SPARSE_GROUP=256",),
+    "m32": ("KM_MORTON32=1",),
+    "m64": ("KM_MORTON32=0",),
     "mb1": ("KM_PRUNED_MINB=1",),
     "mb20": ("KM_PRUNED_MINB=20",),
     "mb26": ("KM_PRUNED_MINB=26",),
