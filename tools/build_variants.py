@@ -31,6 +31,9 @@ VARIANTS = {
     "sg256": ("KM_SPARSE_GROUP=256",),
     "m32": ("KM_MORTON32=1",),
     "m64": ("KM_MORTON32=0",),
+    "cm10": ("KM_CHUNK_MINB=10",),
+    "cm12": ("KM_CHUNK_MINB=12",),
+    "cm16": ("KM_CHUNK_MINB=16",),
     "mb1": ("KM_PRUNED_MINB=1",),
     "mb20": ("KM_PRUNED_MINB=20",),
     "mb26": ("KM_PRUNED_MINB=26",),
