@@ -2544,11 +2544,20 @@ __global__ void k_p2p_allreduce(P2PView v, double* buf, int n, int slot, uint64_
 
 // The iteration's exchange fused with the update: red <- sum over ranks of the
 // local merged vector, then the update of k_update (one block).
+// part != nullptr: the group merge (k_merge's order) is done here first, by the
+// same block -- one kernel for merge + exchange + update when G x nE is small.
 template <int D>
 __global__ void k_p2p_update(P2PView v, double* __restrict__ red, int nE, double* __restrict__ mu_buf,
                              int K, DevState* __restrict__ st, double* __restrict__ trace_E,
-                             double* __restrict__ trace_J, int trace_cap, float4* __restrict__ cneg) {
+                             double* __restrict__ trace_J, int trace_cap, float4* __restrict__ cneg,
+                             const double* __restrict__ part, int G) {
     if (st->done) return;
+    if (part) {
+        extern __shared__ __align__(16) unsigned char smem_raw[];
+        block_merge_groups(part, G, nE, reinterpret_cast<double*>(smem_raw), red);
+        __threadfence_block();
+        __syncthreads();
+    }
     p2p_exchange(v, red, nE, st->t & 1, iter_epoch(st), red);
     __threadfence();
     __syncthreads();

@@ -232,13 +232,14 @@ cudaError_t pool_alloc(kmeans_ctx* ctx, T** p, size_t bytes) {
 void pool_free(kmeans_ctx*, void* p) { cached_free(p); }
 
 bool fused_update(const kmeans_ctx* ctx);
+bool p2p_one_kernel(const kmeans_ctx* ctx);
 
 // kernels of this library per iteration: [prune], assign, [heavy], [row merge],
 // merge + update (fused into one kernel on a single GPU when small enough)
 int kernels_per_iter(const kmeans_ctx* ctx) {
     if (ctx->fused) return 1;   // one launch covers many iterations
     int n = ctx->sorted ? (ctx->path == 1 ? 6 : 4) : (ctx->path == 0 ? 4 : 3);
-    if (fused_update(ctx)) n -= 1;
+    if (fused_update(ctx) || p2p_one_kernel(ctx)) n -= 1;
     return n;
 }
 
@@ -641,6 +642,11 @@ bool fused_update(const kmeans_ctx* ctx) {
     return !ctx->comm && (int64_t)ctx->nE * ctx->G <= 400000 && ctx->nE * 8 <= 48 * 1024;
 }
 
+// P2P exchange and a small group table: merge + exchange + update in one block.
+bool p2p_one_kernel(const kmeans_ctx* ctx) {
+    return ctx->p2p && (int64_t)ctx->nE * ctx->G <= 400000 && ctx->nE * 8 <= 48 * 1024;
+}
+
 kmeans_status launch_merge_update(kmeans_ctx* ctx) {
     const int tpb = 1024;
     const size_t sm = sizeof(double) * ctx->nE;
@@ -660,17 +666,21 @@ kmeans_status enqueue_iteration(kmeans_ctx* ctx) {
     kmeans_status s;
     if ((s = launch_assign(ctx, km::kModeReduce, 0, 0)) != KMEANS_OK) return s;
     if (fused_update(ctx)) return launch_merge_update(ctx);
-    if (ctx->p2p) {   // local merge, then the exchange over peer memory fused with the update
-        if ((s = launch_merge(ctx, 0)) != KMEANS_OK) return s;
-        const int tpb = 256;
+    if (ctx->p2p) {   // [local group merge,] the exchange over peer memory, the update
+        // small group table: the merge runs in the same block (one kernel)
+        const bool one = p2p_one_kernel(ctx);
+        if (!one && (s = launch_merge(ctx, 0)) != KMEANS_OK) return s;
+        const int tpb = one ? 1024 : 256;
+        const size_t sm = one ? sizeof(double) * ctx->nE : 0;
+        const double* part = one ? ctx->part : nullptr;
         if (ctx->d == 2)
-            km::k_p2p_update<2><<<1, tpb, 0, ctx->stream>>>(
+            km::k_p2p_update<2><<<1, tpb, sm, ctx->stream>>>(
                 p2p_view(ctx), ctx->red, ctx->nE, ctx->mu, ctx->K, ctx->st, ctx->trace_E,
-                ctx->trace_J, ctx->trace_cap, ctx->sorted ? ctx->cneg : nullptr);
+                ctx->trace_J, ctx->trace_cap, ctx->sorted ? ctx->cneg : nullptr, part, ctx->G);
         else
-            km::k_p2p_update<3><<<1, tpb, 0, ctx->stream>>>(
+            km::k_p2p_update<3><<<1, tpb, sm, ctx->stream>>>(
                 p2p_view(ctx), ctx->red, ctx->nE, ctx->mu, ctx->K, ctx->st, ctx->trace_E,
-                ctx->trace_J, ctx->trace_cap, ctx->sorted ? ctx->cneg : nullptr);
+                ctx->trace_J, ctx->trace_cap, ctx->sorted ? ctx->cneg : nullptr, part, ctx->G);
         ctx->launches += 1;
         CK(cudaGetLastError());
         return KMEANS_OK;

@@ -505,17 +505,18 @@ def test_p2p_exchange_protocol_emulated(P, n, rounds):
 
 
 @pytest.mark.parametrize("sort", SORT)
-def test_p2p_single_rank_iteration(sort):
+@pytest.mark.parametrize("K", [8, 40])
+def test_p2p_single_rank_iteration(sort, K):
     """The iteration with the exchange over peer memory (k_p2p_update, 1-rank
     communicator: the rank maps only itself) equals the single-GPU run."""
     w = datagen.WORKLOADS["C2"]
     N = 200_000
     X = datagen.generate(w, N=N)
-    init = datagen.one_per_blob_init(w, N=N)
+    init = datagen.one_per_blob_init(w, N=N) if K == 8 else datagen.init_indices(w, N=N, K=K)
     uid = km.comm_unique_id()
     comm = km.comm_init(1, uid, 0, 0)
     try:
-        with km.Context(X, w.M, comm=comm, global_offset=0, global_N=N, sort=sort) as c:
+        with km.Context(X, K, comm=comm, global_offset=0, global_N=N, sort=sort) as c:
             c.p2p_open([c.p2p_handle()])
             rd = c.fit(init, w.tol, w.max_iter)
             a = c.assign(rd["centroids"])
@@ -523,7 +524,7 @@ def test_p2p_single_rank_iteration(sort):
                 c.p2p_open([c.p2p_handle()])   # only once
     finally:
         km.comm_destroy(comm)
-    with km.Context(X, w.M, sort=sort) as c:
+    with km.Context(X, K, sort=sort) as c:
         rs = c.fit(init, w.tol, w.max_iter)
         b = c.assign(rs["centroids"])
     assert rd["iters"] == rs["iters"]
