@@ -88,7 +88,9 @@ typedef struct kmeans_opts {
  * cannot be its points' argmin (exact; labels are returned in the caller's
  * order) -- when K > 16 or N*K*d >= 3.84e8 (N >= 8e6 at K = 16, d = 3);
  * below that the full scan is faster (the pruned kernel has a fixed per-chunk
- * latency, measured in DESIGN.md section 5).  Both flags: KMEANS_EINVAL. */
+ * latency, measured in DESIGN.md section 5).  Shards of more than 2^31 - 1
+ * points always take the full scan (KMEANS_EINVAL with FORCE_SORT).  Both
+ * flags: KMEANS_EINVAL. */
 
 /* Fills *opts with the defaults above. */
 void kmeans_opts_init(kmeans_opts* opts);

@@ -11,6 +11,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <climits>
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
@@ -1213,6 +1214,13 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
     if (opts.flags & KMEANS_FLAG_NO_SORT) ctx->sorted = false;
     else if (opts.flags & KMEANS_FLAG_FORCE_SORT) ctx->sorted = true;
     else ctx->sorted = K > 16 || (double)N * K * d >= 3.84e8;   // see kmeans.h
+    if (ctx->sorted && N > INT32_MAX) {   // the sort's permutation is int32
+        if (opts.flags & KMEANS_FLAG_FORCE_SORT) {
+            set_error("KMEANS_FLAG_FORCE_SORT: the sorted path holds at most 2^31 - 1 points per shard");
+            return fail(KMEANS_EINVAL);
+        }
+        ctx->sorted = false;
+    }
     kmeans_status s = configure(ctx);
     if (s != KMEANS_OK) return fail(s);
     tr.mark(ctx->stream, "stream + configure");
