@@ -787,7 +787,7 @@ struct PCfg {
     static constexpr int kSlots = LARGE ? KM_LARGE_SLOTS : KM_SORTED_SLOTS;   // column slots per pass
     static constexpr int kCap = LARGE ? KM_LARGE_CAP : 16;   // refined candidates kept
     // winning-slot cache for passes > 0 (large K); small K recomputes the argmin
-    static constexpr int kSlotCache = LARGE ? kSChunkPoints : 2;
+    static constexpr int kSlotCache = 2;   // (large K: the winning-slot cache lives in global scratch)
 };
 
 template <int D, bool LARGE>
@@ -845,7 +845,7 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
                 const int* __restrict__ slist, const int* __restrict__ scount,
                 double* __restrict__ rows, int row_stride, int32_t* __restrict__ labels,
                 int* __restrict__ cand_count, int* __restrict__ heavy,
-                int* __restrict__ heavy_count) {
+                int* __restrict__ heavy_count, unsigned short* __restrict__ slot_g) {
     using C = PCfg<LARGE>;
     // Prologue before pdl_wait() touches only what no predecessor writes: the
     // chunk box and the points (the TMA ring is filled here, so with PDL the
@@ -1251,11 +1251,10 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
                         if (db.x < bb.x) { bb.x = db.x; s2 = j; }
                         if (db.y < bb.y) { bb.y = db.y; s3 = j; }
                     }
-                    if (LARGE && npass > 1) {
-                        S.slot[off] = (unsigned short)s0;
-                        S.slot[off + 1] = (unsigned short)s1;
-                        S.slot[off + kWarpTile] = (unsigned short)s2;
-                        S.slot[off + kWarpTile + 1] = (unsigned short)s3;
+                    if (LARGE && npass > 1) {   // winning slots for the later passes
+                        unsigned short* sg = slot_g + (size_t)chunk * kSChunkPoints;
+                        *reinterpret_cast<ushort2*>(sg + off) = make_ushort2(s0, s1);
+                        *reinterpret_cast<ushort2*>(sg + off + kWarpTile) = make_ushort2(s2, s3);
                     }
                     if ((MODE & kModeLabels) && pass == 0) {
                         float4 t;
@@ -1269,10 +1268,13 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
                         if (pb + 1 < n) J += (double)bb.y;
                     }
                 } else {
-                    s0 = S.slot[off];
-                    s1 = S.slot[off + 1];
-                    s2 = S.slot[off + kWarpTile];
-                    s3 = S.slot[off + kWarpTile + 1];
+                    const unsigned short* sg = slot_g + (size_t)chunk * kSChunkPoints;
+                    const ushort2 a = *reinterpret_cast<const ushort2*>(sg + off);
+                    const ushort2 b = *reinterpret_cast<const ushort2*>(sg + off + kWarpTile);
+                    s0 = a.x;
+                    s1 = a.y;
+                    s2 = b.x;
+                    s3 = b.y;
                 }
                 if (MODE & kModeReduce) {
                     const unsigned w = C::kSlots;

@@ -142,6 +142,7 @@ struct kmeans_ctx {
     int merge_smem = 0;           // k_merge_sparse dynamic shared memory (K x 4 doubles)
     int* heavy = nullptr;         // chunks deferred to k_assign_heavy (sorted, large K)
     int* heavy_count = nullptr;
+    unsigned short* slotg = nullptr;   // large K: winning-slot scratch, 1024 per chunk
     int heavy_smem = 0;
     int heavy_grid = 0;
     bool sorted = false;          // points held in Morton order (path 0 default)
@@ -328,7 +329,7 @@ ChunkFn pick_chunk(int d, int K, int mode) {
 
 using PrunedFn = void (*)(const float*, int64_t, int, const float4*, const DevState*, int, int,
                           const float*, const int*, const int*, double*, int, int32_t*, int*,
-                          int*, int*);
+                          int*, int*, unsigned short*);
 using HeavyFn = void (*)(const float*, int64_t, int, const float4*, const DevState*, int, int,
                          const float*, const int*, const int*, const int*, const int*, double*, int,
                          int32_t*);
@@ -511,7 +512,7 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
                         ctx->N, ctx->K, (const float4*)ctx->cneg, (const DevState*)ctx->st, mu_sel,
                         ignore_done, (const float*)ctx->cbox, (const int*)ctx->slist,
                         (const int*)ctx->scount, ctx->cpart, ctx->row_stride, ctx->labels_sorted,
-                        ctx->cand_count, ctx->heavy, ctx->heavy_count));
+                        ctx->cand_count, ctx->heavy, ctx->heavy_count, ctx->slotg));
         if (A) ctx->launches += 1;
         if (A && ctx->path == 1) {
             HeavyFn hf = pick_heavy(ctx->d, mode);
@@ -1124,6 +1125,7 @@ void kmeans_destroy(kmeans_ctx* ctx) {
         pool_free(ctx, ctx->scount);
         pool_free(ctx, ctx->heavy);
         pool_free(ctx, ctx->heavy_count);
+        pool_free(ctx, ctx->slotg);
         pool_free(ctx, ctx->perm);
         pool_free(ctx, ctx->init_pairs);
         pool_free(ctx, ctx->init_pos);
@@ -1242,7 +1244,9 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
           pool_alloc(ctx, &ctx->slist, sizeof(int) * (size_t)K * ctx->n_super) != cudaSuccess ||
           pool_alloc(ctx, &ctx->scount, sizeof(int) * (size_t)ctx->n_super) != cudaSuccess ||
           pool_alloc(ctx, &ctx->heavy, sizeof(int) * (size_t)ctx->n_chunks) != cudaSuccess ||
-          pool_alloc(ctx, &ctx->heavy_count, sizeof(int)) != cudaSuccess)) ||
+          pool_alloc(ctx, &ctx->heavy_count, sizeof(int)) != cudaSuccess ||
+          pool_alloc(ctx, &ctx->slotg, sizeof(unsigned short) * km::kSChunkPoints *
+                                           (size_t)ctx->n_chunks) != cudaSuccess)) ||
         pool_alloc(ctx, &ctx->flag, sizeof(int)) != cudaSuccess ||
         (ctx->fused && pool_alloc(ctx, &ctx->brow, sizeof(double) * 2 * (size_t)ctx->nE *
                                                        ctx->fused_grid) != cudaSuccess)) {
