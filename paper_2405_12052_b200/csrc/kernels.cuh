@@ -223,6 +223,9 @@ constexpr int kLaneTile = 2 * kWarpTile;                 // 128 points per warp-
 #ifndef KM_TWO_CAND
 #define KM_TWO_CAND 1   // register path for two-candidate chunks (K <= 16)
 #endif
+#ifndef KM_CAND_UNROLL2
+#define KM_CAND_UNROLL2 1   // multi-candidate argmin: two candidates per loop step
+#endif
 #ifndef KM_LARGE_SLOTS
 #define KM_LARGE_SLOTS 8
 #endif
@@ -1241,8 +1244,31 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
                     ba = dist2(P[h].xa, P[h].ya, P[h].za, cc);
                     bb = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
                     s0 = s1 = s2 = s3 = 0;
+                    int j = 1;
+#if KM_CAND_UNROLL2
+                    // two candidates per step (independent distance chains), the
+                    // strict-< updates still in ascending j
 #pragma unroll 1
-                    for (int j = 1; j < ncand; ++j) {
+                    for (; j + 1 < ncand; j += 2) {
+                        float4 c2;
+                        cand_at(j, cc);
+                        cand_at(j + 1, c2);
+                        const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
+                        const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
+                        const float2 ea = dist2(P[h].xa, P[h].ya, P[h].za, c2);
+                        const float2 eb = dist2(P[h].xb, P[h].yb, P[h].zb, c2);
+                        if (da.x < ba.x) { ba.x = da.x; s0 = j; }
+                        if (da.y < ba.y) { ba.y = da.y; s1 = j; }
+                        if (db.x < bb.x) { bb.x = db.x; s2 = j; }
+                        if (db.y < bb.y) { bb.y = db.y; s3 = j; }
+                        if (ea.x < ba.x) { ba.x = ea.x; s0 = j + 1; }
+                        if (ea.y < ba.y) { ba.y = ea.y; s1 = j + 1; }
+                        if (eb.x < bb.x) { bb.x = eb.x; s2 = j + 1; }
+                        if (eb.y < bb.y) { bb.y = eb.y; s3 = j + 1; }
+                    }
+#endif
+#pragma unroll 1
+                    for (; j < ncand; ++j) {
                         cand_at(j, cc);
                         const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
                         const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);

@@ -31,6 +31,8 @@ VARIANTS = {
     "sg256": ("KM_SPARSE_GROUP=256",),
     "m32": ("KM_MORTON32=1",),
     "m64": ("KM_MORTON32=0",),
+    "cu0": ("KM_CAND_UNROLL2=0",),
+    "cu1": ("KM_CAND_UNROLL2=1",),
     "ef0": ("KM_EVICT_FIRST=0",),
     "ef1": ("KM_EVICT_FIRST=1",),
     "cm10": ("KM_CHUNK_MINB=10",),
