@@ -293,6 +293,10 @@ def main():
     ctx.iterate(args.warmup)
     ctx.poll()
     barrier()
+    # the dominant kernel alone, once right before the timed region (GPU warm);
+    # again right after it (see below) -- the roofline uses the mean of the two
+    pre_assign = (None if info["fused"] else
+                  ctx.profile_stage(max(20, min(args.steps, 200)), 1, timed=True) / 1e3)
 
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -360,14 +364,18 @@ def main():
         kname = "k_fused_iterate"
         stage_ms = {"fused_iteration": ms_per_step}
     else:
-        t_assign = time_assign(ctx)
+        post_assign = time_assign(ctx)
+        # kernel time "around" the timed region: the mean of the measurements
+        # right before and right after it (clocks drift under sustained load)
+        t_assign = 0.5 * (pre_assign + post_assign)
         if info["sorted"]:
             kname = ("k_assign_pruned" if info["path"] == 0
                      else "k_prune+k_assign_pruned+k_assign_heavy")
         else:
             kname = "k_assign_chunk" if info["path"] == 0 else "k_assign_large"
         # per-stage device time (each stage alone, back-to-back launches)
-        stage_ms = {"assign": t_assign * 1e3, "row_merge": time_assign(ctx, 2) * 1e3}
+        stage_ms = {"assign": t_assign * 1e3, "assign_before": pre_assign * 1e3,
+                    "assign_after": post_assign * 1e3, "row_merge": time_assign(ctx, 2) * 1e3}
         stage_ms["merge_update_and_gaps"] = ms_per_step - stage_ms["assign"] - stage_ms["row_merge"]
         stage_ms["k_merge_alone"] = time_assign(ctx, 3) * 1e3   # the P>1 path's group merge
     roofline = roofline_of(t_assign, kname, bool(info["sorted"]))
