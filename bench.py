@@ -276,11 +276,16 @@ def main():
         datagen.generate(gen_w, a, b - a, N=global_N, out=Xh.numpy())
     init = datagen.init_indices(gen_w, N=global_N, K=w.K)
 
+    exchange = {"mode": args.exchange if distributed else "none"}
+
     def make_ctx(points, sort):
         c = km.Context(points, w.K, device=local, comm=comm, global_offset=a, global_N=global_N,
                        sort=sort)
         if distributed and args.exchange == "p2p":
-            kdist.enable_p2p(c)   # collective: all-gathers the IPC handles
+            # collective: all-gathers the IPC handles; all ranks fall back to
+            # the NCCL allreduce if any rank cannot map its peers
+            if not kdist.enable_p2p(c):
+                exchange["mode"] = "nccl (p2p mapping unavailable)"
         return c
 
     ctx = make_ctx(Xh if Xd is None else Xd, False if args.no_sort else None)
@@ -444,7 +449,7 @@ def main():
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": dict(workload_config(w, P, args.scaling), gen=args.gen,
-                           **({"exchange": args.exchange} if P > 1 else {})),
+                           **({"exchange": exchange["mode"]} if P > 1 else {})),
             "roofline": roofline, "roofline_hbm": roofline_hbm, "stage_ms": stage_ms,
             "roofline_fullscan": fullscan, "candidates": cand,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),

@@ -267,6 +267,9 @@ kmeans_status kmeans_generate(const kmeans_mixture* mix, int64_t start, int64_t 
  * IPC mapping fails (e.g. no peer access). */
 kmeans_status kmeans_p2p_handle(kmeans_ctx* ctx, unsigned char handle[64]);
 kmeans_status kmeans_p2p_open(kmeans_ctx* ctx, const unsigned char* handles);
+/* Back to the NCCL allreduce (e.g. when some rank could not map its peers;
+ * every rank must then disable).  Synchronises the context's stream. */
+kmeans_status kmeans_p2p_disable(kmeans_ctx* ctx);
 
 /* Self-test of the exchange protocol on ONE GPU: P emulated ranks as P blocks
  * of one cooperative launch (ranks that wait on one another must not be

@@ -972,6 +972,19 @@ kmeans_status kmeans_p2p_open(kmeans_ctx* ctx, const unsigned char* handles) {
     return KMEANS_OK;
 }
 
+kmeans_status kmeans_p2p_disable(kmeans_ctx* ctx) {
+    CHECK_CTX(ctx);
+    DeviceGuard g(ctx->device);
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->p2p) {
+        ctx->p2p = false;
+        if (ctx->graph) cudaGraphExecDestroy(ctx->graph);   // back to the NCCL iteration
+        if (ctx->graph_u) cudaGraphExecDestroy(ctx->graph_u);
+        ctx->graph = ctx->graph_u = nullptr;
+    }
+    return KMEANS_OK;
+}
+
 kmeans_status kmeans_p2p_selftest(int device, int P, int n, int rounds, const double* vals,
                                   double* out) {
     if (P < 1 || P > 64 || n < 1 || rounds < 1 || !vals || !out) {

@@ -41,12 +41,25 @@ def init_comm(rank: int, world: int, device: int, group=None) -> int:
     return km.comm_init(world, uid, rank, device)
 
 
-def enable_p2p(ctx, group=None):
+def enable_p2p(ctx, group=None) -> bool:
     """Switch a communicator context to the P2P exchange (kmeans_p2p_handle /
-    kmeans_p2p_open): the IPC handles are all-gathered over torch.distributed."""
+    kmeans_p2p_open): the IPC handles are all-gathered over torch.distributed.
+    All-or-nothing: if any rank cannot map its peers, every rank stays on the
+    NCCL allreduce.  Returns whether the exchange is on."""
     import torch.distributed as dist
     h = ctx.p2p_handle()
     world = dist.get_world_size(group)
     handles = [None] * world
     dist.all_gather_object(handles, h, group=group)
-    ctx.p2p_open(handles)
+    try:
+        ctx.p2p_open(handles)
+        ok = True
+    except Exception:
+        ok = False
+    oks = [None] * world
+    dist.all_gather_object(oks, ok, group=group)
+    if not all(oks):
+        if ok:
+            ctx.p2p_disable()
+        return False
+    return True

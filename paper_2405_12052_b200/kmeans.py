@@ -87,6 +87,7 @@ SIGNATURES = {
     "kmeans_generate": (I, [P, I64, I64, P, I, P]),
     "kmeans_p2p_handle": (I, [P, P]),
     "kmeans_p2p_open": (I, [P, P]),
+    "kmeans_p2p_disable": (I, [P]),
     "kmeans_p2p_selftest": (I, [I, I, I, I, P, P]),
 }
 
@@ -292,6 +293,10 @@ class Context:
         blob = b"".join(handles)
         buf = (ctypes.c_ubyte * len(blob)).from_buffer_copy(blob)
         _check(lib().kmeans_p2p_open(self._h, buf), "kmeans_p2p_open")
+
+    def p2p_disable(self):
+        """Back to the NCCL allreduce (kmeans_p2p_disable)."""
+        _check(lib().kmeans_p2p_disable(self._h), "kmeans_p2p_disable")
 
     def candidate_stats(self) -> dict:
         """Sorted path: centroid candidates per chunk in the last assign pass."""

@@ -102,8 +102,23 @@ def _worker(rank, world, port, q):
             def p2p_open(self, handles):
                 self.opened = list(handles)
         fc = FakeCtx()
-        kdist.enable_p2p(fc)
-        out["p2p_handles_ok"] = fc.opened == [bytes([q + 1]) * 64 for q in range(world)]
+        on = kdist.enable_p2p(fc)
+        out["p2p_handles_ok"] = on and fc.opened == [bytes([q + 1]) * 64 for q in range(world)]
+
+        # all-or-nothing: if one rank cannot map its peers, every rank disables
+        class FailingCtx(FakeCtx):
+            disabled = False
+
+            def p2p_open(self, handles):
+                if rank == 1:
+                    raise RuntimeError("no peer access")
+                self.opened = list(handles)
+
+            def p2p_disable(self):
+                self.disabled = True
+        fc2 = FailingCtx()
+        on2 = kdist.enable_p2p(fc2)
+        out["p2p_fallback_ok"] = (not on2) and (fc2.disabled == (rank != 1))
         q.put((rank, out))
         dist.destroy_process_group()
     except Exception as e:  # pragma: no cover - surfaced by the assertion below
@@ -129,6 +144,7 @@ def test_distributed_decomposition_gloo(world):
         assert res[r]["step_ok"]
         assert res[r]["replicated"]
         assert res[r]["p2p_handles_ok"]
+        assert res[r]["p2p_fallback_ok"]
     # shards cover [0, N) contiguously
     spans = sorted(res[r]["shards"] for r in range(world))
     assert spans[0][0] == 0 and spans[-1][1] == 40_001
