@@ -533,6 +533,26 @@ def test_p2p_single_rank_iteration(sort, K):
     assert np.array_equal(a["counts"], b["counts"]) and np.array_equal(a["sums"], b["sums"])
 
 
+def test_p2p_disable_returns_to_nccl():
+    """kmeans_p2p_disable after a P2P run: the next run uses the NCCL
+    allreduce (graphs rebuilt) and gives the same result."""
+    w = datagen.WORKLOADS["C2"]
+    N = 100_000
+    X = datagen.generate(w, N=N)
+    init = datagen.one_per_blob_init(w, N=N)
+    comm = km.comm_init(1, km.comm_unique_id(), 0, 0)
+    try:
+        with km.Context(X, w.M, comm=comm, global_offset=0, global_N=N) as c:
+            c.p2p_open([c.p2p_handle()])
+            a = c.fit(init, w.tol, w.max_iter)
+            c.p2p_disable()
+            b = c.fit(init, w.tol, w.max_iter)
+    finally:
+        km.comm_destroy(comm)
+    assert a["iters"] == b["iters"] and np.array_equal(a["centroids"], b["centroids"])
+    assert np.array_equal(a["labels"], b["labels"])
+
+
 # --------------------------------------------------------------------------
 # full-size checks in the launch configuration bench.py times
 # --------------------------------------------------------------------------
