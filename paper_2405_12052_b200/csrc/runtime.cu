@@ -195,6 +195,9 @@ struct CreateTrace {
     }
 };
 
+#ifndef KM_FUSED_TPW
+#define KM_FUSED_TPW 2   // measured: 1, 2, 4, 8, 16, 32 -- 2 best from N = 1e4 to 1e6
+#endif
 #ifndef KM_MORTON32
 #define KM_MORTON32 0   // 32-bit Morton keys (see sort_points): 2 ms faster create at
                         // NS, but 10 bits per axis over a box stretched by far outliers
@@ -454,9 +457,11 @@ kmeans_status configure(kmeans_ctx* ctx) {
                                                               km::kFusedWarps * 32,
                                                               ctx->fused_smem) == cudaSuccess &&
                 occ >= 1) {
-                // ~4 warp-tiles (512 points) per warp, <= 1 block per SM (co-resident)
+                // ~KM_FUSED_TPW warp-tiles (128 points each) per warp, <= 1 block per
+                // SM (co-resident)
                 const int64_t tiles = (ctx->N + 127) / 128;
-                const int64_t need = (tiles + 4 * km::kFusedWarps - 1) / (4 * km::kFusedWarps);
+                const int64_t per = (int64_t)KM_FUSED_TPW * km::kFusedWarps;
+                const int64_t need = (tiles + per - 1) / per;
                 ctx->fused_grid = (int)std::min<int64_t>(std::max<int64_t>(need, 1), sms);
                 ctx->fused = true;
             }
