@@ -807,26 +807,18 @@ struct PrunedSmem {
     __device__ __forceinline__ double2* col_b(int k) { return B[k]; }
 };
 
-// Small K: the slot columns (only the rare >= 3-candidate chunks use them) share
-// the ring's memory -- such a chunk drains the ring first and then reads its
-// points from global memory -- so a CTA needs ~6.4 KB and more CTAs (more bytes
-// in flight) fit on an SM.
+// Small K: no per-lane columns.  The rare >= 3-candidate chunks add each
+// point set into a 16-slot table T with one fixed butterfly per slot present
+// in the warp, so a CTA needs ~6.9 KB (3D) and more CTAs (more bytes in
+// flight) fit on an SM.
 template <int D>
 struct PrunedSmem<D, false> {
-    static_assert(2 * PCfg<false>::kSlots * 32 * sizeof(double2) <=
-                      kSortedStages * D * kSortedUnit * sizeof(float),
-                  "slot columns must fit in the ring");
-    union {
-        float ring[kSortedStages][D * kSortedUnit];
-        double2 AB[2][PCfg<false>::kSlots][32];
-    } u;
+    float ring[kSortedStages][D * kSortedUnit];
     uint64_t bar[kSortedStages];
     float4 cand[PCfg<false>::kCap];
     int candk[PCfg<false>::kCap];
-    unsigned short slot[PCfg<false>::kSlotCache];
-    __device__ __forceinline__ float* ring_at(int s) { return u.ring[s]; }
-    __device__ __forceinline__ double2* col_a(int k) { return u.AB[0][k]; }
-    __device__ __forceinline__ double2* col_b(int k) { return u.AB[1][k]; }
+    double T[PCfg<false>::kCap * 4];   // per slot {Sx, Sy, Sz, n}
+    __device__ __forceinline__ float* ring_at(int s) { return ring[s]; }
 };
 
 // {k, n} in one double's bits: k in the low word, n in the high word
@@ -1196,6 +1188,115 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
 
     // ---- several candidates ----
     const int ncand = big ? gcount : nc;   // slots = indices into the candidate list
+    if constexpr (!LARGE) {
+        // small K, >= 3 candidates: one pass over the TMA ring; each point set
+        // (one point per lane) is added to T[slot] by one fixed butterfly per
+        // slot present in the warp, counts by ballot
+        double* T = S.T;
+        for (int q = lane; q < 4 * ncand; q += 32) T[q] = 0.0;
+        __syncwarp();
+        double J = 0.0;
+        auto agg = [&](bool valid, int sl, float px, float py, float pz) {
+            unsigned pres = __reduce_or_sync(0xffffffffu, valid ? (1u << sl) : 0u);
+            while (pres) {
+                const int q = __ffs(pres) - 1;
+                pres &= pres - 1;
+                const bool mine = valid && sl == q;
+                const unsigned cnt = __popc(__ballot_sync(0xffffffffu, mine));
+                double sx = mine ? (double)px : 0.0, sy = mine ? (double)py : 0.0;
+                double sz = mine ? (double)pz : 0.0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    sx += __shfl_xor_sync(0xffffffffu, sx, o);
+                    sy += __shfl_xor_sync(0xffffffffu, sy, o);
+                    if (D == 3) sz += __shfl_xor_sync(0xffffffffu, sz, o);
+                }
+                if (lane == 0) {
+                    double* t = T + 4 * q;
+                    t[0] += sx;
+                    t[1] += sy;
+                    t[2] += sz;
+                    t[3] += (double)cnt;
+                }
+            }
+            __syncwarp();
+        };
+#pragma unroll 1
+        for (int u = 0; u < nunit; ++u) {
+            Pts P[kUnitSub];
+            fetch(u, P);
+#pragma unroll
+            for (int h = 0; h < kUnitSub; ++h) {
+                const int off = u * kSortedUnit + h * kLaneTile + 2 * lane;   // in-chunk index
+                const int64_t pa = base + off, pb = pa + kWarpTile;
+                float4 cc;
+                cand_at(0, cc);
+                float2 ba = dist2(P[h].xa, P[h].ya, P[h].za, cc);
+                float2 bb = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
+                int s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+                int j = 1;
+#pragma unroll 1
+                for (; j + 1 < ncand; j += 2) {   // two candidates per step, ascending
+                    float4 c2;
+                    cand_at(j, cc);
+                    cand_at(j + 1, c2);
+                    const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
+                    const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
+                    const float2 ea = dist2(P[h].xa, P[h].ya, P[h].za, c2);
+                    const float2 eb = dist2(P[h].xb, P[h].yb, P[h].zb, c2);
+                    if (da.x < ba.x) { ba.x = da.x; s0 = j; }
+                    if (da.y < ba.y) { ba.y = da.y; s1 = j; }
+                    if (db.x < bb.x) { bb.x = db.x; s2 = j; }
+                    if (db.y < bb.y) { bb.y = db.y; s3 = j; }
+                    if (ea.x < ba.x) { ba.x = ea.x; s0 = j + 1; }
+                    if (ea.y < ba.y) { ba.y = ea.y; s1 = j + 1; }
+                    if (eb.x < bb.x) { bb.x = eb.x; s2 = j + 1; }
+                    if (eb.y < bb.y) { bb.y = eb.y; s3 = j + 1; }
+                }
+                if (j < ncand) {
+                    cand_at(j, cc);
+                    const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
+                    const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
+                    if (da.x < ba.x) { ba.x = da.x; s0 = j; }
+                    if (da.y < ba.y) { ba.y = da.y; s1 = j; }
+                    if (db.x < bb.x) { bb.x = db.x; s2 = j; }
+                    if (db.y < bb.y) { bb.y = db.y; s3 = j; }
+                }
+                if (MODE & kModeLabels) {
+                    float4 t;
+                    *reinterpret_cast<int2*>(labels + pa) = make_int2(cand_at(s0, t), cand_at(s1, t));
+                    *reinterpret_cast<int2*>(labels + pb) = make_int2(cand_at(s2, t), cand_at(s3, t));
+                }
+                if (MODE & kModeReduce) {
+                    if (pa < n) J += (double)ba.x;
+                    if (pa + 1 < n) J += (double)ba.y;
+                    if (pb < n) J += (double)bb.x;
+                    if (pb + 1 < n) J += (double)bb.y;
+                    agg(pa < n, s0, P[h].xa.x, P[h].ya.x, P[h].za.x);
+                    agg(pa + 1 < n, s1, P[h].xa.y, P[h].ya.y, P[h].za.y);
+                    agg(pb < n, s2, P[h].xb.x, P[h].yb.x, P[h].zb.x);
+                    agg(pb + 1 < n, s3, P[h].xb.y, P[h].yb.y, P[h].zb.y);
+                }
+            }
+        }
+        if (!(MODE & kModeReduce)) return;
+        // row entries in slot (= ascending k) order: lane -> (slot, half)
+        {
+            const int q = lane, sl = q >> 1;   // ncand <= 16: one pass of 32 lanes
+            if (sl < ncand) {
+                const double* t = T + 4 * sl;
+                reinterpret_cast<double2*>(row + kRowHead)[q] =
+                    (q & 1) ? make_double2(t[2], pack_kn(S.candk[sl], (int)t[3]))
+                            : make_double2(t[0], t[1]);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
+        if (lane == 0) {
+            row[0] = J;
+            row[1] = (double)ncand;
+        }
+    } else {
     double J = 0.0;
     auto accumulate = [&](int l, float px, float py, float pz) {
         double2 a = S.col_a(l)[lane], b = S.col_b(l)[lane];
@@ -1208,13 +1309,6 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
         S.col_a(l)[lane] = a;
         S.col_b(l)[lane] = b;
     };
-    if (!LARGE) {
-        // the slot columns live in the ring: drain the copies in flight first;
-        // every pass then reads the points from global memory
-        const unsigned nq = __shfl_sync(0xffffffffu, issued, 0);
-        for (unsigned q = 0; q < nq; ++q) mbar_wait(&S.bar[q % SS], (q / SS) & 1u);
-        __syncwarp();
-    }
     const int npass = (MODE & kModeReduce) ? (ncand + C::kSlots - 1) / C::kSlots : 1;
 #pragma unroll 1
     for (int pass = 0; pass < npass; ++pass) {
@@ -1340,6 +1434,7 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
     if (lane == 0) {
         row[0] = J;
         row[1] = (double)ncand;
+    }
     }
 }
 
