@@ -94,6 +94,13 @@ def test_invalid_arguments_rejected_before_device_work(km):
     assert L.kmeans_iterate(None, 1) == -1
     assert L.kmeans_update(None, None, None) == -1
     assert L.kmeans_profile_stage(None, 1, 1, None) == -1
+    assert L.kmeans_p2p_handle(None, None) == -1
+    assert L.kmeans_p2p_open(None, None) == -1
+    assert L.kmeans_p2p_disable(None) == -1
+    assert L.kmeans_p2p_selftest(0, 0, 5, 1, None, None) == -1     # P < 1
+    assert L.kmeans_p2p_selftest(0, 65, 5, 1, None, None) == -1    # P > 64
+    assert L.kmeans_release_memory(-1) == -1
+    assert L.kmeans_generate(None, 0, 1, None, 0, None) == -1
     L.kmeans_destroy(None)  # NULL-safe
     assert L.kmeans_last_error()  # a message was recorded
 

@@ -487,6 +487,28 @@ def test_device_generator_matches_host_recipe(name, N, start, count):
         assert np.array_equal(got[p], host[p])
 
 
+def test_generator_and_memory_cache_edges():
+    """kmeans_generate rejects out-of-range requests; kmeans_release_memory
+    empties the block cache and later contexts still work."""
+    import torch
+    w = datagen.WORKLOADS["C2"]
+    spec = datagen.mixture_spec(w, 1000)
+    out = torch.empty((10, 3), dtype=torch.float32, device="cuda")
+    with pytest.raises(km.KMeansError) as e:
+        km.generate(spec, 995, 10, out)   # past N
+    assert e.value.name == "KMEANS_EINVAL"
+    km.generate(spec, 990, 10, out)
+    assert np.array_equal(out.cpu().numpy(), datagen.generate(w, 990, 10, N=1000))
+    X = datagen.generate(w, N=50_000)
+    init = datagen.init_indices(w, N=50_000)
+    with km.Context(X, 8) as c:
+        a = c.fit(init, 0.0, 3)
+    km.release_memory(0)
+    with km.Context(X, 8) as c:
+        b = c.fit(init, 0.0, 3)
+    assert np.array_equal(a["centroids"], b["centroids"])
+
+
 @pytest.mark.parametrize("P,n,rounds", [(1, 5, 3), (2, 65, 6), (3, 1, 4), (8, 4097, 5),
                                          (16, 33, 9), (64, 200, 3)])
 def test_p2p_exchange_protocol_emulated(P, n, rounds):
