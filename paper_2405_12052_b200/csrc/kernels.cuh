@@ -1946,12 +1946,10 @@ k_merge_sparse(const double* __restrict__ rows, int row_stride, int n_chunks, in
         __syncthreads();   // the batch buffer is reused
     }
     __syncthreads();
-#ifndef KM_EXP_NOWRITE
     for (int k = tid; k < K; k += blockDim.x) {
         for (int j = 0; j < D; ++j) gpart[(size_t)(k * D + j) * n_groups + g] = T[4 * k + j];
         gpart[(size_t)(K * D + k) * n_groups + g] = T[4 * k + 3];
     }
-#endif
     if (tid == 0) {
         double J = 0.0;
         for (int cc = 0; cc < nch; ++cc) J += hj[cc];
