@@ -1189,22 +1189,36 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
     // ---- several candidates ----
     const int ncand = big ? gcount : nc;   // slots = indices into the candidate list
     if constexpr (!LARGE) {
-        // small K, >= 3 candidates: one pass over the TMA ring; each point set
-        // (one point per lane) is added to T[slot] by one fixed butterfly per
-        // slot present in the warp, counts by ballot
+        // small K, >= 3 candidates: one pass over the TMA ring; the points of a
+        // warp-tile are added to T[slot] by one fixed butterfly per slot
+        // present in the warp, counts by ballot
         double* T = S.T;
         for (int q = lane; q < 4 * ncand; q += 32) T[q] = 0.0;
         __syncwarp();
         double J = 0.0;
-        auto agg = [&](bool valid, int sl, float px, float py, float pz) {
-            unsigned pres = __reduce_or_sync(0xffffffffu, valid ? (1u << sl) : 0u);
+        // the 4 points of a lane (a0, a1, b0, b1) at once: per slot present in
+        // the warp, each lane sums its points of that slot in that order, then
+        // one fixed butterfly over the lanes; counts by ballot
+        auto agg4 = [&](const bool (&v)[4], const int (&sl)[4], const float (&px)[4],
+                        const float (&py)[4], const float (&pz)[4]) {
+            unsigned mine_bits = 0u;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (v[i]) mine_bits |= 1u << sl[i];
+            unsigned pres = __reduce_or_sync(0xffffffffu, mine_bits);
             while (pres) {
                 const int q = __ffs(pres) - 1;
                 pres &= pres - 1;
-                const bool mine = valid && sl == q;
-                const unsigned cnt = __popc(__ballot_sync(0xffffffffu, mine));
-                double sx = mine ? (double)px : 0.0, sy = mine ? (double)py : 0.0;
-                double sz = mine ? (double)pz : 0.0;
+                double sx = 0.0, sy = 0.0, sz = 0.0;
+                unsigned cnt = 0u;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const bool m = v[i] && sl[i] == q;
+                    sx += m ? (double)px[i] : 0.0;
+                    sy += m ? (double)py[i] : 0.0;
+                    sz += m ? (double)pz[i] : 0.0;
+                    cnt += __popc(__ballot_sync(0xffffffffu, m));
+                }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
                     sx += __shfl_xor_sync(0xffffffffu, sx, o);
@@ -1272,10 +1286,12 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
                     if (pa + 1 < n) J += (double)ba.y;
                     if (pb < n) J += (double)bb.x;
                     if (pb + 1 < n) J += (double)bb.y;
-                    agg(pa < n, s0, P[h].xa.x, P[h].ya.x, P[h].za.x);
-                    agg(pa + 1 < n, s1, P[h].xa.y, P[h].ya.y, P[h].za.y);
-                    agg(pb < n, s2, P[h].xb.x, P[h].yb.x, P[h].zb.x);
-                    agg(pb + 1 < n, s3, P[h].xb.y, P[h].yb.y, P[h].zb.y);
+                    const bool vv[4] = {pa < n, pa + 1 < n, pb < n, pb + 1 < n};
+                    const int ss[4] = {s0, s1, s2, s3};
+                    const float xx[4] = {P[h].xa.x, P[h].xa.y, P[h].xb.x, P[h].xb.y};
+                    const float yy[4] = {P[h].ya.x, P[h].ya.y, P[h].yb.x, P[h].yb.y};
+                    const float zz[4] = {P[h].za.x, P[h].za.y, P[h].zb.x, P[h].zb.y};
+                    agg4(vv, ss, xx, yy, zz);
                 }
             }
         }
