@@ -239,7 +239,7 @@ constexpr int kChunkTiles = KM_CHUNK_TILES;
 constexpr int kChunkPoints = kLaneTile * kChunkTiles;    // 2048
 constexpr int kStages = 3;
 #ifndef KM_SPARSE_GROUP
-#define KM_SPARSE_GROUP 64
+#define KM_SPARSE_GROUP 128   // measured at C5: 64 -> 128 saves ~5 us per iteration (k_merge reads half the groups); 256 is slower
 #endif
 constexpr int kGroupChunks = KM_SPARSE_GROUP;   // chunks per group, large-K sparse rows (<= 256)
 #ifndef KM_ROW_GROUP
