@@ -1850,7 +1850,7 @@ __global__ void k_super_bbox(const float* __restrict__ cbox, int n_chunks, int d
 }
 
 // ---------------------------------------------------------------------------
-// k_merge_sparse: group g sums the sparse rows of chunks [64g, 64g + 64) into
+// k_merge_sparse: group g sums the sparse rows of its kGroupChunks chunks into
 // a dense shared table T[K][4].  Entries are staged in shared memory with
 // independent loads; then warp w adds, chunk by chunk in ascending order, the
 // entries whose k lies in its own range of T -- every sum is taken in chunk
