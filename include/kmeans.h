@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define KMEANS_ABI_VERSION 1
+#define KMEANS_ABI_VERSION 2   /* 2: kmeans_info.fused / fused_grid, profile_stage, P2P exchange, generator */
 #define KMEANS_MAX_K 1024
 
 typedef struct kmeans_ctx kmeans_ctx; /* opaque */

@@ -18,6 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("KMEANS_LIB_OVERRIDE") or os.path.join(HERE, "libkmeans.so")
 
 KMEANS_OK = 0
+ABI_VERSION = 2   # include/kmeans.h KMEANS_ABI_VERSION
 STATUS = {0: "KMEANS_OK", -1: "KMEANS_EINVAL", -2: "KMEANS_ENONFINITE", -3: "KMEANS_ENOMEM",
           -4: "KMEANS_ECUDA", -5: "KMEANS_ENCCL", -6: "KMEANS_ESTATE"}
 LAYOUT_AOS, LAYOUT_SOA = 0, 1
@@ -106,6 +107,9 @@ def lib():
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
+        if L.kmeans_abi_version() != ABI_VERSION:   # the Info / Opts layouts below
+            raise ImportError(f"{LIB_PATH}: ABI {L.kmeans_abi_version()}, binding expects "
+                              f"{ABI_VERSION}; rebuild the library")
         _lib = L
     return _lib
 

@@ -53,7 +53,7 @@ def test_library_is_sm100a_only():
 
 def test_status_strings_and_version(km):
     L = km.lib()
-    assert L.kmeans_abi_version() == 1
+    assert L.kmeans_abi_version() == 2
     for code, name in km.STATUS.items():
         assert L.kmeans_status_string(code).decode().startswith(name)
 
