@@ -204,7 +204,8 @@ def run_reference(args, w):
         "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps * (w.N / n),
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
-        "config": dict(workload_config(w, args.gpus, args.scaling), gen=args.gen),
+        "config": dict(workload_config(w, args.gpus, args.scaling), gen=args.gen,
+                       **({"exchange": args.exchange} if args.gpus > 1 else {})),
         "cpu_baseline": {"value": value, "unit": "points·iter/s", "cores": 1,
                          "kind": "oracle", "sample": sample, "cpu": cpu_model()},
         "e2e": {"value": value, "unit": "points·iter/s", "h2d_bytes_per_step": 0,
