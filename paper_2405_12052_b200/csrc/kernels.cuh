@@ -2018,18 +2018,16 @@ __device__ __forceinline__ void block_merge_groups(const double* part, int G, in
 constexpr int kMergeRegs = 6;
 
 template <int D>
-__global__ void __launch_bounds__(kRowGroup)
-k_merge_sparse16(const double* __restrict__ cpart, int n_chunks, int K, double* __restrict__ gpart,
-                 int n_groups, const DevState* __restrict__ st, int ignore_done) {
-    __shared__ double T[kMergeWarps][16][4];   // [warp][k]{Sx, Sy, Sz, n}
+__device__ __forceinline__ void merge16_body(const double* __restrict__ cpart, int n_chunks, int K,
+                                             double* __restrict__ gpart, int n_groups,
+                                             const DevState* __restrict__ st, int ignore_done,
+                                             const int g) {
+    __shared__ __align__(16) double T[kMergeWarps][16][4];   // [warp][k]{Sx, Sy, Sz, n}
     __shared__ double WJ[kMergeWarps];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int g = blockIdx.x;
     const int c = g * kRowGroup + tid;
     const double* row = cpart + (size_t)c * kRowDoubles;
     const double2* ent = reinterpret_cast<const double2*>(row + kRowHead);
-    pdl_trigger();
-    pdl_wait();   // the rows are written
     // round 1 (independent loads): done flag, head, entry slots 0 and 1
     const int done = ignore_done ? 0 : st->done;
     double2 head = make_double2(0.0, 0.0);
@@ -2139,6 +2137,16 @@ k_merge_sparse16(const double* __restrict__ cpart, int n_chunks, int K, double* 
         }
     }
 }
+
+template <int D>
+__global__ void __launch_bounds__(kRowGroup)
+k_merge_sparse16(const double* __restrict__ cpart, int n_chunks, int K, double* __restrict__ gpart,
+                 int n_groups, const DevState* __restrict__ st, int ignore_done) {
+    pdl_trigger();
+    pdl_wait();   // the rows are written
+    merge16_body<D>(cpart, n_chunks, K, gpart, n_groups, st, ignore_done, blockIdx.x);
+}
+
 
 // k_merge_rows (dense rows): group g sums the rows of chunks
 // [kDenseGroup g, kDenseGroup (g+1)).  Thread (r, q), r < 4, sums entry q of rows
@@ -2437,6 +2445,7 @@ k_merge_update(const double* __restrict__ part, int G, int nE, double* __restric
     __syncthreads();
     update_body<D>(mu_buf, K, rs, st, trace_E, trace_J, trace_cap, cneg);
 }
+
 
 // ---------------------------------------------------------------------------
 // k_fused_iterate (full-scan path, K <= 16, one GPU): up to n_iter whole Lloyd

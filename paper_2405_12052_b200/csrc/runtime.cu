@@ -227,6 +227,7 @@ cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
     return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
+
 // Device allocation for a context (through the block cache).  Freed blocks
 // must be idle: callers synchronise ctx->stream before pool_free.
 template <class T>
