@@ -79,6 +79,8 @@ typedef struct kmeans_opts {
 /* kmeans_opts.flags */
 #define KMEANS_FLAG_NO_SORT 1     /* keep the caller's point order: full-scan assign kernels */
 #define KMEANS_FLAG_FORCE_SORT 2  /* always use the sorted (pruned) path */
+#define KMEANS_FLAG_BIG_CHUNKS 8  /* sorted path, K <= 16: 2048-point chunks at any N
+                                     (default: from 4e7 points per shard) */
 #define KMEANS_FLAG_NO_FUSED 4    /* full-scan path: never use the one-launch
                                      multi-iteration kernel (k_fused_iterate) that
                                      kmeans_iterate / kmeans_fit_ctx use for small

@@ -832,7 +832,7 @@ __device__ __forceinline__ double pack_kn(int k, int n) {
 #ifndef KM_PRUNED_MINB
 #define KM_PRUNED_MINB (D == 2 ? 32 : 28)
 #endif
-template <int D, int MODE, bool LARGE>
+template <int D, int MODE, bool LARGE, int CHT = KM_SORTED_CHUNK_TILES>
 __global__ void __launch_bounds__(32, LARGE ? 1 : KM_PRUNED_MINB)
 k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
                 const float4* __restrict__ cneg_buf, const DevState* __restrict__ st,
@@ -854,11 +854,15 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
     constexpr int kUnitFloats = D * kSortedUnit;
     constexpr unsigned kUnitBytes = kUnitFloats * 4;
     constexpr int SS = kSortedStages;
-    const int64_t base = (int64_t)chunk * kSChunkPoints;
+    // chunk of CHT warp-tiles (1024 points by default; 2048 for large small-K
+    // shards, chosen at create -- the large-K kernels assume 1024)
+    constexpr int CHP = CHT * kLaneTile, CHU = CHP / kSortedUnit;
+    static_assert(!LARGE || CHP == kSChunkPoints, "large K: 1024-point chunks");
+    const int64_t base = (int64_t)chunk * CHP;
     const int64_t rem = n - base;
     const int64_t nu64 = (rem + kSortedUnit - 1) / kSortedUnit;
-    const int nunit = nu64 < kSortedUnits ? (int)nu64 : kSortedUnits;
-    const int npts = rem < kSChunkPoints ? (int)rem : kSChunkPoints;
+    const int nunit = nu64 < CHU ? (int)nu64 : CHU;
+    const int npts = rem < CHP ? (int)rem : CHP;
     const float* src = X + (base >> 6) * (D * kWarpTile);
 
     // point stream: units 0..nunit-1 through the TMA ring (unit q in stage q % SS)

@@ -195,6 +195,9 @@ struct CreateTrace {
     }
 };
 
+#ifndef KM_BIG_CHUNK_MIN_N
+#define KM_BIG_CHUNK_MIN_N 40000000   // shards of >= this many points use 2048-point chunks
+#endif
 #ifndef KM_FUSED_TPW
 #define KM_FUSED_TPW 2   // measured: 1, 2, 4, 8, 16, 32 -- 2 best from N = 1e4 to 1e6
 #endif
@@ -349,20 +352,23 @@ HeavyFn pick_heavy(int d, int mode) {
     return km::k_assign_heavy<3, 3>;
 }
 
-template <bool LARGE>
+template <bool LARGE, int CHT>
 PrunedFn pick_pruned_l(int d, int mode) {
     if (d == 2) {
-        if (mode == 1) return km::k_assign_pruned<2, 1, LARGE>;
-        if (mode == 2) return km::k_assign_pruned<2, 2, LARGE>;
-        return km::k_assign_pruned<2, 3, LARGE>;
+        if (mode == 1) return km::k_assign_pruned<2, 1, LARGE, CHT>;
+        if (mode == 2) return km::k_assign_pruned<2, 2, LARGE, CHT>;
+        return km::k_assign_pruned<2, 3, LARGE, CHT>;
     }
-    if (mode == 1) return km::k_assign_pruned<3, 1, LARGE>;
-    if (mode == 2) return km::k_assign_pruned<3, 2, LARGE>;
-    return km::k_assign_pruned<3, 3, LARGE>;
+    if (mode == 1) return km::k_assign_pruned<3, 1, LARGE, CHT>;
+    if (mode == 2) return km::k_assign_pruned<3, 2, LARGE, CHT>;
+    return km::k_assign_pruned<3, 3, LARGE, CHT>;
 }
 
-PrunedFn pick_pruned(int d, int K, int mode) {
-    return K <= 16 ? pick_pruned_l<false>(d, mode) : pick_pruned_l<true>(d, mode);
+// chunk_points: 1024, or (small K) 2048 for large shards
+PrunedFn pick_pruned(int d, int K, int mode, int chunk_points = km::kSChunkPoints) {
+    if (K > 16) return pick_pruned_l<true, KM_SORTED_CHUNK_TILES>(d, mode);
+    return chunk_points == 2 * km::kSChunkPoints ? pick_pruned_l<false, 2 * KM_SORTED_CHUNK_TILES>(d, mode)
+                                                 : pick_pruned_l<false, KM_SORTED_CHUNK_TILES>(d, mode);
 }
 
 int pruned_smem(int d, int K) {
@@ -407,10 +413,15 @@ kmeans_status configure(kmeans_ctx* ctx) {
         // Morton-sorted shard, per-chunk pruning (any K), sparse chunk rows
         ctx->tpb = 32;
         ctx->smem = pruned_smem(ctx->d, ctx->K);
+        // small K: 2048-point chunks for large shards (fewer rows and CTAs: 2-3%
+        // per iteration at N = 1e8), 1024 below (shorter CTAs: 14% at 1.25e7)
+        const bool big = ctx->N >= (int64_t)KM_BIG_CHUNK_MIN_N ||
+                         (ctx->flags & KMEANS_FLAG_BIG_CHUNKS);
+        ctx->chunk_points = (ctx->K <= 16 && big) ? 2 * km::kSChunkPoints : km::kSChunkPoints;
         for (int mode = 1; mode <= 3; ++mode)
-            CK(cudaFuncSetAttribute((const void*)pick_pruned(ctx->d, ctx->K, mode),
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
-        ctx->chunk_points = km::kSChunkPoints;
+            CK(cudaFuncSetAttribute(
+                (const void*)pick_pruned(ctx->d, ctx->K, mode, ctx->chunk_points),
+                cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
         ctx->n_chunks = (int)((ctx->N + ctx->chunk_points - 1) / ctx->chunk_points);
         // sparse rows: <= 16 entries (k_merge_sparse16) or up to K (k_merge_sparse)
         ctx->row_stride = ctx->K <= 16 ? km::kRowDoubles : km::kRowHead + 4 * ctx->K;
@@ -512,7 +523,7 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
                     ctx->scount, ctx->heavy_count);
             ctx->launches += 1;
         }
-        PrunedFn f = pick_pruned(ctx->d, ctx->K, mode);
+        PrunedFn f = pick_pruned(ctx->d, ctx->K, mode, ctx->chunk_points);
         if (A)
             CK(launch_k(f, ctx->n_chunks, 32, ctx->smem, ctx->stream, ctx->path == 0, ctx->X,
                         ctx->N, ctx->K, (const float4*)ctx->cneg, (const DevState*)ctx->st, mu_sel,

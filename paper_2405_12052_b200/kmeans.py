@@ -25,6 +25,7 @@ LAYOUT_AOS, LAYOUT_SOA = 0, 1
 FLAG_NO_SORT = 1
 FLAG_FORCE_SORT = 2
 FLAG_NO_FUSED = 4
+FLAG_BIG_CHUNKS = 8
 MAX_K = 1024
 
 
@@ -164,7 +165,8 @@ class Context:
 
     def __init__(self, points, K: int, *, d: int | None = None, layout: str = "aos",
                  device: int = -1, stream=None, comm=None, global_offset: int = 0,
-                 global_N: int = 0, sort: bool | None = None, fused: bool = True):
+                 global_N: int = 0, sort: bool | None = None, fused: bool = True,
+                 big_chunks: bool = False):
         pts = _as_f32_points(points)
         shape = tuple(pts.shape)
         if layout == "aos":
@@ -184,6 +186,8 @@ class Context:
         o.flags = 0 if sort is None else (FLAG_FORCE_SORT if sort else FLAG_NO_SORT)
         if not fused:   # full-scan path: one graph launch per iteration instead of k_fused_iterate
             o.flags |= FLAG_NO_FUSED
+        if big_chunks:  # sorted path: 2048-point chunks regardless of N
+            o.flags |= FLAG_BIG_CHUNKS
         h = ctypes.c_void_p()
         _check(lib().kmeans_create(ctypes.byref(h), _ptr(pts), self.N, self.d, self.K,
                                    ctypes.byref(o)), "kmeans_create")

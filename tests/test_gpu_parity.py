@@ -41,7 +41,7 @@ def check_step(X, mu, ctx=None, tag="", sort=True):
     K = mu.shape[0]
     own = ctx is None
     if own:
-        ctx = km.Context(X, K, sort=sort)
+        ctx = km.Context(X, K, **ctx_kwargs(sort))
     try:
         g = ctx.assign(mu)
         mu_next, E = ctx.update()
@@ -81,7 +81,13 @@ def perturbed_centroids(X, K, seed):
 # --------------------------------------------------------------------------
 # per-step parity over the configs (small N) and K / ragged-N sweeps
 # --------------------------------------------------------------------------
-SORT = [pytest.param(True, id="sorted"), pytest.param(False, id="unsorted")]
+SORT = [pytest.param(True, id="sorted"), pytest.param(False, id="unsorted"),
+        pytest.param("big", id="sorted2048")]
+
+
+def ctx_kwargs(sort):
+    """Context options of a SORT parameter ("big": sorted, 2048-point chunks)."""
+    return dict(sort=True, big_chunks=True) if sort == "big" else dict(sort=sort)
 
 
 @pytest.mark.parametrize("sort", SORT)
@@ -190,7 +196,7 @@ def test_step_parity_soa_layout_and_device_input():
 # --------------------------------------------------------------------------
 def check_fit(X, K, init, tol, max_iter, tag="", sort=True, fused=True):
     o = oracle.fit(X, K, init, tol, max_iter)
-    with km.Context(X, K, sort=sort, fused=fused) as c:
+    with km.Context(X, K, fused=fused, **ctx_kwargs(sort)) as c:
         g = c.fit(init, tol, max_iter)
     assert g["iters"] == o["iters"], f"{tag}: iters {g['iters']} vs {o['iters']}"
     assert np.array_equal(g["labels"], o["labels"]), tag
@@ -373,7 +379,7 @@ def test_profile_stages_leave_state(sort, K):
     X = datagen.generate(w, N=200_000)
     init = datagen.init_indices(w, N=200_000)[:8]
     init = np.concatenate([init, np.arange(1000, 1000 + K - 8)]) if K > 8 else init
-    with km.Context(X, K, sort=sort) as c:
+    with km.Context(X, K, **ctx_kwargs(sort)) as c:
         ref = c.fit(init, 0.0, 5)
         c.start(init_idx=init, tol=0.0, max_iter=5)
         c.iterate(2)
@@ -395,10 +401,10 @@ def test_deterministic_bitwise(sort):
     w = datagen.WORKLOADS["NS"]
     X = datagen.generate(w, N=400_000)
     init = datagen.init_indices(w, N=400_000)
-    with km.Context(X, 16, sort=sort) as c:
+    with km.Context(X, 16, **ctx_kwargs(sort)) as c:
         a = c.fit(init, 0.0, 6)
         b = c.fit(init, 0.0, 6)
-    with km.Context(X, 16, sort=sort) as c:
+    with km.Context(X, 16, **ctx_kwargs(sort)) as c:
         e = c.fit(init, 0.0, 6)
     for r in (b, e):
         assert np.array_equal(a["labels"], r["labels"])
@@ -425,7 +431,7 @@ def test_fake_sharding_matches_oracle(P, sort):
     for r in range(P):
         a, b = datagen.shard_range(N, P, r)
         Xs = datagen.generate(w, a, b - a, N=N)
-        with km.Context(Xs, 16, sort=sort) as c:
+        with km.Context(Xs, 16, **ctx_kwargs(sort)) as c:
             g = c.assign(mu)
         labels.append(g["labels"])
         counts += g["counts"]
@@ -538,7 +544,7 @@ def test_p2p_single_rank_iteration(sort, K):
     uid = km.comm_unique_id()
     comm = km.comm_init(1, uid, 0, 0)
     try:
-        with km.Context(X, K, comm=comm, global_offset=0, global_N=N, sort=sort) as c:
+        with km.Context(X, K, comm=comm, global_offset=0, global_N=N, **ctx_kwargs(sort)) as c:
             c.p2p_open([c.p2p_handle()])
             rd = c.fit(init, w.tol, w.max_iter)
             a = c.assign(rd["centroids"])
@@ -546,7 +552,7 @@ def test_p2p_single_rank_iteration(sort, K):
                 c.p2p_open([c.p2p_handle()])   # only once
     finally:
         km.comm_destroy(comm)
-    with km.Context(X, K, sort=sort) as c:
+    with km.Context(X, K, **ctx_kwargs(sort)) as c:
         rs = c.fit(init, w.tol, w.max_iter)
         b = c.assign(rs["centroids"])
     assert rd["iters"] == rs["iters"]
@@ -587,10 +593,10 @@ def test_full_size_ns_step_parity(sort):
     w = datagen.WORKLOADS["NS"]
     X = datagen.generate(w)
     mu = X[datagen.init_indices(w)].astype(np.float64)
-    with km.Context(X, w.K, sort=sort) as c:
+    with km.Context(X, w.K, **ctx_kwargs(sort)) as c:
         info = c.info()
-        assert info["path"] == 0 and info["sorted"] == int(sort)
-        assert info["grid"] == (w.N + 1023) // 1024 if sort else (w.N + 2047) // 2048
+        assert info["path"] == 0 and info["sorted"] == int(bool(sort))
+        assert info["grid"] == (w.N + 2047) // 2048   # 2048-point chunks at this N (both paths)
         check_step(X, mu, ctx=c, tag="NS full")
 
 
