@@ -185,7 +185,7 @@ kmeans_status kmeans_profile_assign(kmeans_ctx* ctx, int n);
  * KMEANS_EINVAL if n < 0 or stage is not 0..3. */
 kmeans_status kmeans_profile_stage(kmeans_ctx* ctx, int n, int stage, float* ms_per_launch);
 
-/* Sorted path: centroid candidates per 1024-point chunk in the last assign
+/* Sorted path: centroid candidates per chunk (1024 or 2048 points) in the last assign
  * pass -- mean, maximum, number of single-candidate chunks, number of chunks
  * (any may be NULL).  KMEANS_ESTATE on an unsorted context.  Synchronous. */
 kmeans_status kmeans_candidate_stats(kmeans_ctx* ctx, double* mean, int* max, int64_t* single,
@@ -197,7 +197,7 @@ kmeans_status kmeans_get_stream(kmeans_ctx* ctx, void** stream);
 typedef struct kmeans_info {
     int64_t N, global_N, global_offset, ldx;
     int d, K;
-    int grid;               /* blocks of the assign kernel: 1024-point chunks (sorted),
+    int grid;               /* blocks of the assign kernel: 1024/2048-point chunks (sorted),
                                2048-point chunks (full scan, K <= 16) or a persistent
                                multiple of the SM count (full scan, K > 16) */
     int block;              /* threads per block of the assign kernel */
