@@ -195,6 +195,9 @@ struct CreateTrace {
     }
 };
 
+#ifndef KM_BIG_CHUNK_TILES
+#define KM_BIG_CHUNK_TILES 16   // 2048-point chunks for large shards
+#endif
 #ifndef KM_BIG_CHUNK_MIN_N
 #define KM_BIG_CHUNK_MIN_N 40000000   // shards of >= this many points use 2048-point chunks
 #endif
@@ -367,8 +370,9 @@ PrunedFn pick_pruned_l(int d, int mode) {
 // chunk_points: 1024, or (small K) 2048 for large shards
 PrunedFn pick_pruned(int d, int K, int mode, int chunk_points = km::kSChunkPoints) {
     if (K > 16) return pick_pruned_l<true, KM_SORTED_CHUNK_TILES>(d, mode);
-    return chunk_points == 2 * km::kSChunkPoints ? pick_pruned_l<false, 2 * KM_SORTED_CHUNK_TILES>(d, mode)
-                                                 : pick_pruned_l<false, KM_SORTED_CHUNK_TILES>(d, mode);
+    return chunk_points == KM_BIG_CHUNK_TILES * km::kLaneTile
+               ? pick_pruned_l<false, KM_BIG_CHUNK_TILES>(d, mode)
+               : pick_pruned_l<false, KM_SORTED_CHUNK_TILES>(d, mode);
 }
 
 int pruned_smem(int d, int K) {
@@ -417,7 +421,8 @@ kmeans_status configure(kmeans_ctx* ctx) {
         // per iteration at N = 1e8), 1024 below (shorter CTAs: 14% at 1.25e7)
         const bool big = ctx->N >= (int64_t)KM_BIG_CHUNK_MIN_N ||
                          (ctx->flags & KMEANS_FLAG_BIG_CHUNKS);
-        ctx->chunk_points = (ctx->K <= 16 && big) ? 2 * km::kSChunkPoints : km::kSChunkPoints;
+        ctx->chunk_points = (ctx->K <= 16 && big) ? KM_BIG_CHUNK_TILES * km::kLaneTile
+                                                  : km::kSChunkPoints;
         for (int mode = 1; mode <= 3; ++mode)
             CK(cudaFuncSetAttribute(
                 (const void*)pick_pruned(ctx->d, ctx->K, mode, ctx->chunk_points),
