@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--iters", type=int, default=10, help="Lloyd iterations before timing")
     ap.add_argument("--no-sort", action="store_true")
     ap.add_argument("--force-sort", action="store_true")
+    ap.add_argument("--big-chunks", action="store_true", help="2048-point chunks at any N")
     ap.add_argument("--K", type=int, default=0, help="override K (init = first K seeded indices)")
     ap.add_argument("--N", type=int, default=0, help="override N (a prefix-shaped draw of the workload)")
     a = ap.parse_args()
@@ -47,7 +48,8 @@ def main():
     for lib in a.libs:
         km._lib = None
         km.LIB_PATH = os.path.abspath(lib)
-        ctx = km.Context(X, w.K, sort=False if a.no_sort else (True if getattr(a, "force_sort", False) else None))
+        ctx = km.Context(X, w.K, sort=False if a.no_sort else (True if getattr(a, "force_sort", False) else None),
+                         big_chunks=a.big_chunks)
         ctx.start(init_idx=init, tol=0.0, max_iter=1 << 30)
         ctx.iterate(a.iters)
         ctx.poll()
