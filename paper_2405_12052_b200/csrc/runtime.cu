@@ -204,6 +204,9 @@ struct CreateTrace {
 #ifndef KM_FUSED_TPW
 #define KM_FUSED_TPW 2   // measured: 1, 2, 4, 8, 16, 32 -- 2 best from N = 1e4 to 1e6
 #endif
+#ifndef KM_MORTON_EXTRA
+#define KM_MORTON_EXTRA 6   // Morton bits per axis beyond log2(N) / d
+#endif
 #ifndef KM_MORTON32
 #define KM_MORTON32 0   // 32-bit Morton keys (see sort_points): 2 ms faster create at
                         // NS, but 10 bits per axis over a box stretched by far outliers
@@ -864,7 +867,7 @@ kmeans_status sort_points(kmeans_ctx* ctx, const float* src, int64_t si, int64_t
     while (lg < 40 && (int64_t(1) << lg) < N) ++lg;
     const bool k32 = KM_MORTON32 != 0;
     const int qcap = k32 ? 32 / d : (d == 2 ? 32 : 21);
-    const int qbits = std::min(qcap, (lg + d - 1) / d + 6);
+    const int qbits = std::min(qcap, (lg + d - 1) / d + KM_MORTON_EXTRA);
     const size_t ksz = k32 ? sizeof(uint32_t) : sizeof(unsigned long long);
     if (pool_alloc(ctx, &ctx->perm, sizeof(int32_t) * N) != cudaSuccess ||
         pool_alloc(ctx, &ctx->init_pairs, sizeof(int2) * ctx->K) != cudaSuccess ||
