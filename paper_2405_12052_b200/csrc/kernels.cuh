@@ -1785,9 +1785,9 @@ k_prune(const float4* __restrict__ cneg_buf, const DevState* __restrict__ st, in
     auto bounds = [&](int k, double& dmin2, double& dmax2) {
         dmin2 = 0.0;
         dmax2 = 0.0;
-#pragma unroll
         const float4 v = cneg[k];
         const float cv[3] = {-v.x, -v.y, -v.z};
+#pragma unroll
         for (int j = 0; j < D; ++j) {
             const double cj = (double)cv[j];
             const double dm = fmax(fmax(lo[j] - cj, cj - hi[j]), 0.0);
