@@ -1937,30 +1937,41 @@ k_merge_sparse(const double* __restrict__ rows, int row_stride, int n_chunks, in
         for (int r = 0; r < 4; ++r)
             if (dst[r] >= 0) E[dst[r]] = tmp[r];
         __syncthreads();
-        // warp w owns k in [w kw, (w + 1) kw): every warp walks the batch's
-        // chunks in ascending order and adds the entries of its k range (the
-        // entries of one row have distinct k: no conflicts within a chunk;
-        // __syncwarp orders consecutive chunks) -- no block barrier per chunk
+        // warp w owns k in [w kw, (w + 1) kw) and walks the batch's entries in
+        // windows of 32 consecutive entries (entry order = chunk order).  Lanes
+        // of one window holding the same k (entries of different chunks) are
+        // found with __match_any_sync and add in lane order, one round per
+        // rank; __syncwarp orders the rounds and the windows -- every T[k] is
+        // summed in ascending chunk order, no atomics, no block barrier
         {
             const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
             const int kw = (K + nw - 1) / nw, klo = warp * kw, khi = klo + kw;
-            int c = 0;
-            while (c < nch && off[c + 1] <= b0) ++c;   // first chunk with entries in the batch
-            for (; c < nch && off[c] < b0 + bn; ++c) {
-                const int e0 = max(off[c], b0), e1 = min(off[c + 1], b0 + bn);
-                for (int e = e0 + lane; e < e1; e += 32) {
-                    const double2 v1 = E[2 * (e - b0) + 1];
+            for (int w0 = 0; w0 < bn; w0 += 32) {
+                const int e = w0 + lane;
+                double2 v0 = make_double2(0.0, 0.0), v1 = make_double2(0.0, 0.0);
+                int k = -1;
+                if (e < bn) {
+                    v1 = E[2 * e + 1];
                     const int2 kn = *reinterpret_cast<const int2*>(&v1.y);   // {k, n}
-                    if (kn.x >= klo && kn.x < khi) {
-                        const double2 v0 = E[2 * (e - b0)];
-                        double* t = T + 4 * kn.x;
-                        t[0] += v0.x;
-                        t[1] += v0.y;
-                        t[2] += v1.x;
-                        t[3] += (double)kn.y;
-                    }
+                    if (kn.x >= klo && kn.x < khi) { k = kn.x; v0 = E[2 * e]; }
                 }
-                __syncwarp();
+                const unsigned peers = __match_any_sync(0xffffffffu, k);
+                const int rank = __popc(peers & ((1u << lane) - 1u));
+                const int rmax = __reduce_max_sync(0xffffffffu, k >= 0 ? rank : 0);
+                const double n = (double)reinterpret_cast<const int2*>(&v1.y)->y;
+                for (int r = 0; r <= rmax; ++r) {
+                    if (k >= 0 && rank == r) {
+                        double2* t = reinterpret_cast<double2*>(T + 4 * k);
+                        double2 a = t[0], b = t[1];
+                        a.x += v0.x;
+                        a.y += v0.y;
+                        b.x += v1.x;
+                        b.y += n;
+                        t[0] = a;
+                        t[1] = b;
+                    }
+                    __syncwarp();
+                }
             }
         }
         __syncthreads();   // the batch buffer is reused
