@@ -690,3 +690,21 @@ def test_heavy_chunks_large_k():
     with km.Context(X, w.K) as c:
         r = c.fit(init, 0.0, 2)
     assert np.array_equal(r["labels"], o1["labels"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_blobs", [1, 2, 5])
+def test_large_k_row_merge_repeated_k_windows(n_blobs):
+    """Large-K row merge (k_merge_sparse) when consecutive chunks hold the same
+    few clusters: K = 64 with only n_blobs occupied, so each chunk row has 1-2
+    entries and one 32-entry window of the merge repeats the same k up to 31
+    times (the __match_any_sync rounds).  Counts must stay exact and sums,
+    inertia, mu^{t+1}, E within the step bars; the other 64 - n_blobs clusters
+    are empty and keep their centroids."""
+    rng = np.random.default_rng(100 + n_blobs)
+    N, K = 500_003, 64
+    centers = rng.uniform(-50, 50, (n_blobs, 3))
+    X = (centers[rng.integers(0, n_blobs, N)] + rng.normal(0, 1.0, (N, 3))).astype(np.float32)
+    mu = np.concatenate([centers, rng.uniform(1e3, 2e3, (K - n_blobs, 3))]).astype(np.float64)
+    g, o = check_step(X, mu, tag=f"repeated-k {n_blobs}")
+    assert np.count_nonzero(o["counts"]) == n_blobs
