@@ -298,6 +298,36 @@ def test_hand_worked_runs_on_gpu(golden_dir, name):
     assert r["inertia"] == g["inertia"]
 
 
+@pytest.mark.parametrize("sort", SORT)
+@pytest.mark.parametrize("reps", [1, 3000])
+def test_form_d_fma_golden_on_gpu(golden_dir, sort, reps):
+    """tests/golden/fma_form_d.json (reading R6): the GPU's
+    form D rounds its fma once -- the 2D distance is the hand-derived
+    29.23716926574707 (inertia of one point at one centroid), and in 3D the
+    fma decides the argmin (label 1; a separately rounded evaluation ties and
+    gives 0).  reps > 1 fills several chunks (every chunk box is one point:
+    both centroids stay candidates on the pruned path)."""
+    g = json.load(open(os.path.join(golden_dir, "fma_form_d.json")))
+    d2 = g["distance_2d"]
+    X2 = np.array([d2["x"]] * reps, np.float32)
+    with km.Context(X2, 1, **ctx_kwargs(sort)) as c:
+        r = c.assign(np.array([d2["c"]], np.float64))
+    assert r["inertia"] == reps * d2["expect"] or \
+        abs(r["inertia"] - reps * d2["expect"]) <= 1e-12 * reps * d2["expect"]
+    if reps == 1:
+        assert r["inertia"] == d2["expect"]
+    a = g["argmin_3d"]
+    X3 = np.array([a["x"]] * reps, np.float32)
+    with km.Context(X3, 2, **ctx_kwargs(sort)) as c:
+        r = c.assign(np.array(a["centroids"], np.float64))
+    assert np.all(r["labels"] == a["expect_label"])
+    assert r["counts"].tolist() == [0, reps]
+    if reps == 1:
+        assert r["inertia"] == a["expect_dmin"]
+    else:
+        assert abs(r["inertia"] - reps * a["expect_dmin"]) <= 1e-12 * reps * a["expect_dmin"]
+
+
 def test_special_cases_k1_kn_tol0_maxiter1():
     rng = np.random.default_rng(8)
     X = rng.normal(0, 1, (9, 2)).astype(np.float32)

@@ -70,6 +70,30 @@ def test_dist_symmetry_and_zero():
         assert float(oracle.dist(a, a)) == 0.0
 
 
+def test_dist_fma_step_single_rounding(golden_dir):
+    """Form D's fma step rounds ONCE (reading R6): the
+    hand-derived value of tests/golden/fma_form_d.json, which a separately
+    rounded s + e_j*e_j (or another coordinate order) misses by one ulp."""
+    g = load(golden_dir, "fma_form_d.json")
+    d2 = g["distance_2d"]
+    assert float(oracle.dist(d2["x"], d2["c"])) == d2["expect"]
+    assert d2["expect"] != d2["separately_rounded_would_give"]
+    a = g["argmin_3d"]
+    for c, want in zip(a["centroids"], a["expect_dist"]):
+        assert float(oracle.dist(a["x"], c)) == want
+
+
+def test_argmin_decided_by_fma_rounding(golden_dir):
+    """The label of golden argmin_3d: with form D's single rounding centroid 1
+    is strictly nearer; a separately rounded evaluation would tie and give 0."""
+    a = load(golden_dir, "fma_form_d.json")["argmin_3d"]
+    X = np.array([a["x"]] * 3, np.float32)
+    r = oracle.partials(X, np.array(a["centroids"], float))
+    assert r["labels"].tolist() == [a["expect_label"]] * 3
+    assert [float(v) for v in r["dmin"]] == [a["expect_dmin"]] * 3
+    assert r["J"] == 3 * a["expect_dmin"]
+
+
 def test_dist_operand_order_matters_not_reassociated():
     """Form D subtracts per coordinate before squaring.  The expanded form
     |x|^2 - 2x.c + |c|^2 loses everything here (catastrophic cancellation);
