@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--e2e-iters", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--repeats", type=int, default=3,
+                    help="timed repeats of exactly --steps steps each; the median is reported")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU time of the oracle baseline sample")
     ap.add_argument("--ref-seconds", type=float, default=60.0,
@@ -151,61 +153,89 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU oracle baseline (rank 0, N = 1 only) and the reference arm
 # ---------------------------------------------------------------------------
-def oracle_sample(w, target_s: float):
-    """Times the oracle (as it stands, single thread) on a prefix of the
-    workload: whole Lloyd iterations (oracle.step) until ~target_s of CPU."""
+def oracle_points(w) -> int:
+    """Prefix of the workload the oracle is timed on (both oracle legs use the
+    same sample, so cpu_baseline and the reference arm agree): 8e6 points
+    (96 MB, past the host caches) at K <= 16, 2e5 at K = 1024 (the oracle is
+    exactly linear in N K)."""
+    return min(w.N, 8_000_000 if w.K <= 16 else 200_000)
+
+
+class PinnedCore:
+    """Pins the calling thread to one host core (the oracle is single-threaded;
+    `taskset -c <core>` equivalent) and restores the old mask afterwards."""
+
+    def __enter__(self):
+        self.old = os.sched_getaffinity(0)
+        self.core = max(self.old)   # the highest allowed core (away from core 0's IRQs)
+        os.sched_setaffinity(0, {self.core})
+        return self
+
+    def __exit__(self, *a):
+        os.sched_setaffinity(0, self.old)
+
+
+def oracle_run(w, iters: int, warmup: int = 1):
+    """Times `iters` whole Lloyd iterations (oracle.step, the oracle as it
+    stands, single thread pinned to one core) on oracle_points(w) points,
+    after `warmup` untimed ones.  Returns per-iteration seconds."""
     import oracle
     from paper_2405_12052_b200 import datagen
-    n = min(w.N, 2_000_000 if w.K <= 16 else 100_000)
+    n = oracle_points(w)
     X = datagen.generate(w, 0, n, N=w.N)
-    mu = X[datagen.init_indices(w, N=n, K=w.K)].astype(np.float64) if w.planted_sites == 0 \
-        else X[:w.K].astype(np.float64) + np.arange(w.K)[:, None]
+    mu = X[datagen.init_indices(w, N=n, K=w.K)].astype(np.float64)
+    times = []
+    with PinnedCore() as pin:
+        for _ in range(warmup):
+            mu = oracle.step(X, mu)["mu_next"]
+        for _ in range(iters):
+            t0 = time.perf_counter()
+            mu = oracle.step(X, mu)["mu_next"]
+            times.append(time.perf_counter() - t0)
+    return dict(n=n, times=times, core=pin.core)
+
+
+def oracle_sample(w, target_s: float):
+    """cpu_baseline: ~target_s seconds of oracle iterations (median per
+    iteration, reported as points·iter/s)."""
+    import oracle
+    from paper_2405_12052_b200 import datagen
+    n = oracle_points(w)
+    X = datagen.generate(w, 0, min(n, 50_000), N=w.N)
     t0 = time.perf_counter()
-    r = oracle.step(X, mu)
-    one = time.perf_counter() - t0
-    iters = max(1, int(target_s / max(one, 1e-6)) - 1)
-    mu = r["mu_next"]
-    t0 = time.perf_counter()
-    for _ in range(iters):
-        mu = oracle.step(X, mu)["mu_next"]
-    dt = time.perf_counter() - t0
-    return dict(value=n * iters / dt, n=n, iters=iters, seconds=dt)
+    oracle.step(X, X[:w.K].astype(np.float64) + 0.5)
+    per_iter = (time.perf_counter() - t0) * n / X.shape[0]
+    iters = max(3, int(target_s / max(per_iter, 1e-9)))
+    r = oracle_run(w, iters)
+    med = statistics.median(r["times"])
+    return dict(value=r["n"] / med, n=r["n"], iters=iters, seconds=sum(r["times"]),
+                core=r["core"])
 
 
 def run_reference(args, w):
+    """The reference arm: the oracle as it stands (there is no reference
+    implementation -- /root/reference is a paper), one whole Lloyd iteration
+    per step on the oracle_points(w)-point prefix of the same workload,
+    single thread pinned to one core; ms_per_step is the sample's own."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0  # under torchrun only rank 0 runs the oracle
-    import oracle
-    from paper_2405_12052_b200 import datagen
-    # size the per-step sample so the whole run takes ~args.ref_seconds of CPU
-    n_cal = min(w.N, 20_000)
-    Xc = datagen.generate(w, 0, n_cal, N=w.N)
-    muc = Xc[:w.K].astype(np.float64) + 0.5
-    t0 = time.perf_counter()
-    oracle.step(Xc, muc)
-    per_point = (time.perf_counter() - t0) / n_cal
-    n = int(args.ref_seconds / max(1, args.steps + args.warmup) / per_point)
-    n = max(min(w.N, 2 * w.K, 1000), min(w.N, n))
-    X = datagen.generate(w, 0, n, N=w.N)
-    mu = X[datagen.init_indices(w, N=n, K=w.K)].astype(np.float64)
-    for _ in range(args.warmup):
-        mu = oracle.step(X, mu)["mu_next"]
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        mu = oracle.step(X, mu)["mu_next"]
-    dt = time.perf_counter() - t0
+    r = oracle_run(w, args.steps, warmup=args.warmup)
+    n = r["n"]
+    dt = sum(r["times"])
     value = n * args.steps / dt
     sample = (f"{n} of {w.N} points (prefix of the seeded {w.name} workload), "
-              f"{args.steps} whole Lloyd iterations (oracle.step)")
+              f"{args.steps} whole Lloyd iterations (oracle.step) after {args.warmup} warm-up, "
+              f"single thread pinned to core {r['core']}; ms_per_step is this sample's")
     line = {
         "impl": "reference", "metric": "Lloyd points·iter/s", "value": value,
         "unit": "points·iter/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps * (w.N / n),
+        "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
         "config": dict(workload_config(w, args.gpus, args.scaling), gen=args.gen,
                        **({"exchange": args.exchange} if args.gpus > 1 else {})),
+        "sample_points": n,
         "cpu_baseline": {"value": value, "unit": "points·iter/s", "cores": 1,
                          "kind": "oracle", "sample": sample, "cpu": cpu_model()},
         "e2e": {"value": value, "unit": "points·iter/s", "h2d_bytes_per_step": 0,
@@ -265,7 +295,8 @@ def main():
 
     # shard (contiguous ceiling partition, PAPER.md:97 / SPEC.md:236)
     global_N = w.N if args.scaling == "strong" else w.N * P
-    a, b = datagen.shard_range(global_N, P, rank)
+    from paper_2405_12052_b200 import dist as kdist_
+    a, b = kdist_.shard(global_N, P, rank)   # ValueError on every rank if a shard is empty
     gen_w = w if args.scaling == "strong" else dataclasses.replace(w, N=global_N)
     Xh = torch.empty((b - a, w.d), dtype=torch.float32, pin_memory=True)
     Xd = None
@@ -279,9 +310,9 @@ def main():
 
     exchange = {"mode": args.exchange if distributed else "none"}
 
-    def make_ctx(points, sort):
+    def make_ctx(points, sort, expected_iters=0):
         c = km.Context(points, w.K, device=local, comm=comm, global_offset=a, global_N=global_N,
-                       sort=sort)
+                       sort=sort, expected_iters=expected_iters)
         if distributed and args.exchange == "p2p":
             # collective: all-gathers the IPC handles; all ranks fall back to
             # the NCCL allreduce if any rank cannot map its peers
@@ -289,7 +320,8 @@ def main():
                 exchange["mode"] = "nccl (p2p mapping unavailable)"
         return c
 
-    ctx = make_ctx(Xh if Xd is None else Xd, False if args.no_sort else None)
+    ctx = make_ctx(Xh if Xd is None else Xd, False if args.no_sort else None,
+                   expected_iters=args.warmup + args.repeats * args.steps)
     del Xd   # the context holds its own (sorted) copy
     info = ctx.info()
     stream = torch.cuda.ExternalStream(ctx.stream)
@@ -306,19 +338,23 @@ def main():
 
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    launches0 = ctx.info()["kernel_launches"]
+    rep_ms = []
+    launches_per_rep = []
     with ClockSampler(local) as clocks:
-        barrier()
-        e0.record(stream)
-        ctx.iterate(args.steps)
-        e1.record(stream)
-        e1.synchronize()
-        barrier()
-    launches = ctx.info()["kernel_launches"] - launches0
-    ms = e0.elapsed_time(e1)
-    ms = max_over_ranks(ms)
+        for _ in range(args.repeats):   # each repeat: exactly K steps between barriers
+            launches0 = ctx.info()["kernel_launches"]
+            barrier()
+            e0.record(stream)
+            ctx.iterate(args.steps)
+            e1.record(stream)
+            e1.synchronize()
+            barrier()
+            launches_per_rep.append(ctx.info()["kernel_launches"] - launches0)
+            rep_ms.append(max_over_ranks(e0.elapsed_time(e1)))
+    ms = statistics.median(rep_ms)
+    launches = launches_per_rep[rep_ms.index(ms)] if ms in rep_ms else launches_per_rep[0]
     st = ctx.poll()
-    assert st["iters"] == args.warmup + args.steps, st
+    assert st["iters"] == args.warmup + args.repeats * args.steps, st
 
     value = global_N * args.steps / (ms / 1e3)   # whole-job points·iter/s
     ms_per_step = ms / args.steps
@@ -405,31 +441,43 @@ def main():
         labels_h = torch.empty(n_local, dtype=torch.int32, pin_memory=True)
         ctx.close()
 
-        def e2e_step():
-            barrier()
-            t0 = time.perf_counter()
-            c2 = make_ctx(Xh, False if args.no_sort else None)
-            t1 = time.perf_counter()
-            r = c2.fit(init, 0.0, args.e2e_iters, out_labels=labels_h, traces=False)
-            t2 = time.perf_counter()
-            c2.close()
-            t3 = time.perf_counter()
-            barrier()
-            assert r["iters"] == args.e2e_iters
-            return max_over_ranks(t3 - t0), (t1 - t0, t2 - t1, t3 - t2)
+        def e2e_run(sort):
+            def e2e_step():
+                barrier()
+                t0 = time.perf_counter()
+                c2 = make_ctx(Xh, sort, expected_iters=args.e2e_iters)
+                t1 = time.perf_counter()
+                r = c2.fit(init, 0.0, args.e2e_iters, out_labels=labels_h, traces=False)
+                t2 = time.perf_counter()
+                srt = c2.info()["sorted"]
+                c2.close()
+                t3 = time.perf_counter()
+                barrier()
+                assert r["iters"] == args.e2e_iters
+                return max_over_ranks(t3 - t0), (t1 - t0, t2 - t1, t3 - t2), srt
 
-        e2e_step()   # warm-up step (first-use costs: allocations, module loading)
-        steps = [e2e_step() for _ in range(args.e2e_steps)]
-        dt = sum(x[0] for x in steps) / len(steps)
-        parts = [sum(x[1][i] for x in steps) / len(steps) for i in range(3)]
-        e2e = {"value": global_N * args.e2e_iters / dt, "unit": "points·iter/s",
-               "h2d_bytes_per_step": int(Xh.numel() * 4 + 8 * w.K),
-               "d2h_bytes_per_step": int(n_local * 4 + 8 * w.K * w.d + 16),
-               "step": f"one kmeans_create + kmeans_fit_ctx ({args.e2e_iters} iterations, "
-                       "labels out) + kmeans_destroy call from pinned host memory",
-               "steps_timed": args.e2e_steps, "warmup_steps": 1,
-               "seconds_per_step": dt,
-               "breakdown_s": {"create": parts[0], "fit": parts[1], "destroy": parts[2]}}
+            e2e_step()   # warm-up step (first-use costs: allocations, module loading)
+            steps = [e2e_step() for _ in range(args.e2e_steps)]
+            dts = sorted(x[0] for x in steps)
+            dt = statistics.median(dts)
+            parts = [statistics.median(x[1][i] for x in steps) for i in range(3)]
+            return {"value": global_N * args.e2e_iters / dt, "unit": "points·iter/s",
+                    "h2d_bytes_per_step": int(Xh.numel() * 4 + 8 * w.K),
+                    "d2h_bytes_per_step": int(n_local * 4 + 8 * w.K * w.d + 16),
+                    "step": f"one kmeans_create (opts.expected_iters = {args.e2e_iters}) + "
+                            f"kmeans_fit_ctx ({args.e2e_iters} iterations, labels out) + "
+                            "kmeans_destroy call from pinned host memory",
+                    "steps_timed": args.e2e_steps, "warmup_steps": 1,
+                    "seconds_per_step": dt, "sorted": steps[0][2],
+                    "breakdown_s": {"create": parts[0], "fit": parts[1], "destroy": parts[2]}}
+
+        # the library's own path choice (the call a user makes) ...
+        e2e = e2e_run(False if args.no_sort else None)
+        # ... and the other path beside it, for reference
+        alt = e2e_run(bool(not e2e["sorted"]))
+        e2e["other_path"] = {"sorted": alt["sorted"], "value": alt["value"],
+                             "seconds_per_step": alt["seconds_per_step"],
+                             "breakdown_s": alt["breakdown_s"]}
     else:
         ctx.close()
 
@@ -438,7 +486,8 @@ def main():
         s = oracle_sample(w, args.cpu_seconds)
         cpu = {"value": s["value"], "unit": "points·iter/s", "cores": 1, "kind": "oracle",
                "sample": f"{s['iters']} Lloyd iterations (oracle.step) on the first {s['n']} "
-                         f"points of {w.name}, single-threaded C oracle, {s['seconds']:.1f} s",
+                         f"points of {w.name}, single-threaded C oracle pinned to core "
+                         f"{s['core']}, {s['seconds']:.1f} s, median iteration",
                "cpu": cpu_model(), "host_cores": os.cpu_count()}
 
     if distributed:
@@ -447,7 +496,8 @@ def main():
         line = {
             "metric": "Lloyd points·iter/s", "value": value, "unit": "points·iter/s",
             "n_gpus": P, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
+            "ms_per_step": ms_per_step,
+            "repeats_ms_per_step": [m / args.steps for m in rep_ms], "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": dict(workload_config(w, P, args.scaling), gen=args.gen,
                            **({"exchange": exchange["mode"]} if P > 1 else {})),

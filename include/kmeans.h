@@ -24,7 +24,12 @@
  *     memory of the context's device (CUDA unified addressing decides); the
  *     caller owns it, and the library never keeps it past the call.
  *   - After KMEANS_ECUDA or KMEANS_ENCCL a context is unusable (sticky error);
- *     only kmeans_destroy is valid.
+ *     only kmeans_destroy is valid.  (Exception: a failed kmeans_p2p_open
+ *     leaves the context usable -- see there.)
+ *   - A distributed context never waits forever for a peer: an exchange that
+ *     a peer does not join within opts.comm_timeout_s fails the call with
+ *     KMEANS_ENCCL (P2P exchange: a bounded spin in the kernel; NCCL: the
+ *     host polls ncclCommGetAsyncError and aborts the communicator).
  *   - A context is not thread-safe; distinct contexts are independent.
  *   - kmeans_last_error() returns a thread-local message for the last failure.
  *
@@ -40,7 +45,8 @@
 extern "C" {
 #endif
 
-#define KMEANS_ABI_VERSION 2   /* 2: kmeans_info.fused / fused_grid, profile_stage, P2P exchange, generator */
+#define KMEANS_ABI_VERSION 3   /* 3: kmeans_opts.rank / nranks / expected_iters / comm_timeout_s,
+                                  bounded P2P waits, kmeans_p2p_selftest dead-rank arguments */
 #define KMEANS_MAX_K 1024
 
 typedef struct kmeans_ctx kmeans_ctx; /* opaque */
@@ -74,6 +80,19 @@ typedef struct kmeans_opts {
     int64_t global_offset;  /* first global index of this rank's shard */
     int64_t global_N;       /* total points over all ranks; 0 = N */
     int flags;              /* KMEANS_FLAG_* bits */
+    int rank;               /* without nccl_comm: this rank of a P2P-only group (0 <= rank < nranks) */
+    int nranks;             /* without nccl_comm: group size; 0 = not distributed.  A P2P-only
+                               group exchanges through kmeans_p2p_handle / kmeans_p2p_open
+                               (no NCCL); the exchange must be opened before kmeans_start /
+                               kmeans_assign (KMEANS_ESTATE otherwise).  With nccl_comm the
+                               communicator's rank and size are used and these are ignored. */
+    int expected_iters;     /* hint for the path choice: Lloyd iterations the caller will run on
+                               this context (0 = unknown).  The sorted path costs a one-time
+                               Morton sort at create (about 0.1 ms per million points) that
+                               pays off only over enough iterations; kmeans_fit passes
+                               max_iter. */
+    double comm_timeout_s;  /* distributed: seconds to wait for a peer in an exchange before
+                               failing with KMEANS_ENCCL; 0 = 60 s */
 } kmeans_opts;
 
 /* kmeans_opts.flags */
@@ -90,7 +109,9 @@ typedef struct kmeans_opts {
  * cannot be its points' argmin (exact; labels are returned in the caller's
  * order) -- when K > 16 or N*K*d >= 3.84e8 (N >= 8e6 at K = 16, d = 3);
  * below that the full scan is faster (the pruned kernel has a fixed per-chunk
- * latency, measured in DESIGN.md section 5).  Shards of more than 2^31 - 1
+ * latency, measured in DESIGN.md section 5).  With opts.expected_iters > 0 and
+ * K <= 16 the sort must also pay for itself over that many iterations
+ * ("Path choice").  Shards of more than 2^31 - 1
  * points always take the full scan (KMEANS_EINVAL with FORCE_SORT).  Both
  * flags: KMEANS_EINVAL. */
 
@@ -265,8 +286,12 @@ kmeans_status kmeans_generate(const kmeans_mixture* mix, int64_t start, int64_t 
  *      peers' buffers; from then on the iteration, kmeans_start's mu^0
  *      assembly and kmeans_assign use the exchange.  Collective: every rank
  *      must open before any rank iterates.
- * KMEANS_EINVAL without a communicator, or on a second open; KMEANS_ECUDA if
- * IPC mapping fails (e.g. no peer access). */
+ * The group is the NCCL communicator's, or opts.rank / opts.nranks of a
+ * P2P-only context.  KMEANS_EINVAL on a single-GPU context or a second open;
+ * KMEANS_ECUDA if IPC mapping fails (e.g. no peer access) -- NOT sticky: the
+ * mappings made so far are closed and the context stays usable (a
+ * communicator context can go on with the NCCL allreduce after
+ * kmeans_p2p_disable; every rank must then disable). */
 kmeans_status kmeans_p2p_handle(kmeans_ctx* ctx, unsigned char handle[64]);
 kmeans_status kmeans_p2p_open(kmeans_ctx* ctx, const unsigned char* handles);
 /* Back to the NCCL allreduce (e.g. when some rank could not map its peers;
@@ -278,10 +303,14 @@ kmeans_status kmeans_p2p_disable(kmeans_ctx* ctx);
  * separate launches on one GPU), each with its own exchange buffer; in round
  * i rank r contributes vals[i][r][0..n) (host, rounds x P x n doubles) and
  * out[i][r][0..n) (host) receives what rank r computed -- the rank-ordered sum
- * over q of vals[i][q].  Synchronous.  KMEANS_EINVAL for P not in [1, 64],
- * n < 1, rounds < 1 or NULL pointers. */
+ * over q of vals[i][q].  dead_rank in [0, P) never publishes (-1: none): the
+ * other ranks must give up after timeout_s seconds (0 = 60 s); failed (host,
+ * P ints, may be NULL) receives per rank the 1-based round whose exchange
+ * failed, 0 if none (the dead rank itself: 0).  Synchronous.  Returns
+ * KMEANS_ENCCL if any exchange failed; KMEANS_EINVAL for P not in [1, 64],
+ * n < 1, rounds < 1, dead_rank >= P, timeout_s < 0 or NULL vals / out. */
 kmeans_status kmeans_p2p_selftest(int device, int P, int n, int rounds, const double* vals,
-                                  double* out);
+                                  double* out, int dead_rank, double timeout_s, int* failed);
 
 /* NULL-safe; frees all device memory of the context (not the caller's stream
  * or communicator).  Freed blocks go to a library-owned cache per device that

@@ -45,7 +45,17 @@ struct DevState {
     double tol;
     double E;
     double J;
+    int err;        // kErrExchangeTimeout: a peer never published (the run stopped)
+    int pad;
 };
+enum : int { kErrExchangeTimeout = 1 };
+
+// Global nanosecond timer (bounded waits on peers).
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // Programmatic dependent launch (PDL): a kernel launched with programmatic
 // stream serialization may start before its predecessor finishes; it must not
@@ -2387,12 +2397,10 @@ __device__ void update_body(double* __restrict__ mu_buf, int K, const double* re
                             DevState* __restrict__ st, double* __restrict__ trace_E,
                             double* __restrict__ trace_J, int trace_cap,
                             float4* __restrict__ cneg) {
-    __shared__ double red_sm[32];
     const int t = st->t;
     const double* mu_old = mu_buf + (size_t)(t & 1) * K * D;
     double* mu_new = mu_buf + (size_t)((t + 1) & 1) * K * D;
     const int tid = threadIdx.x;
-    double e_acc = 0.0;
     for (int q = tid; q < K * D; q += blockDim.x) {
         const int k = q / D;
         const double nk = red[K * D + k];
@@ -2404,31 +2412,27 @@ __device__ void update_body(double* __restrict__ mu_buf, int K, const double* re
             reinterpret_cast<float*>(&cneg[K + k])[j] = -__double2float_rn(old);
             reinterpret_cast<float*>(&cneg[k])[j] = -__double2float_rn(nw);
         }
-        const double diff = nw - old;
-        e_acc += diff * diff;
     }
-    const int lane = tid & 31, warp = tid >> 5;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) e_acc += __shfl_xor_sync(0xffffffffu, e_acc, o);
-    if (lane == 0) red_sm[warp] = e_acc;
-    __syncthreads();
-    if (warp == 0) {
-        const int nw = blockDim.x >> 5;
-        double v = (lane < nw) ? red_sm[lane] : 0.0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) {
-            const double E = v;
-            const double J = red[K * D + K];
-            st->E = E;
-            st->J = J;
-            if (t < trace_cap) {
-                trace_E[t] = E;
-                trace_J[t] = J;
-            }
-            st->t = t + 1;
-            st->done = (E < st->tol) || (t + 1 >= st->max_iter);
+    __syncthreads();   // mu_new visible to the block
+    if (tid == 0) {
+        // E = sum_k sum_j (mu^{t+1} - mu^t)^2 serially, k-major with j inner:
+        // the oracle's order, so E -- and the E < tol stop
+        // decision -- has the same bits on every path (fused, unfused, P2P)
+        double E = 0.0;
+#pragma unroll 8
+        for (int q = 0; q < K * D; ++q) {
+            const double diff = mu_new[q] - mu_old[q];
+            E = __dadd_rn(E, __dmul_rn(diff, diff));   // no FMA contraction (the oracle's -ffp-contract=off)
         }
+        const double J = red[K * D + K];
+        st->E = E;
+        st->J = J;
+        if (t < trace_cap) {
+            trace_E[t] = E;
+            trace_J[t] = J;
+        }
+        st->t = t + 1;
+        st->done = (E < st->tol) || (t + 1 >= st->max_iter);
     }
 }
 
@@ -2609,7 +2613,7 @@ k_fused_iterate(const float* __restrict__ X, int64_t n, int K, int n_chunks,
             double E = 0.0;   // k-major, j inner: the oracle's order
             for (int q = 0; q < K * D; ++q) {
                 const double dlt = mu_n[q] - mu_s[q];
-                E += dlt * dlt;
+                E = __dadd_rn(E, __dmul_rn(dlt, dlt));   // no FMA contraction
             }
             sh_E = E;
         }
@@ -2656,6 +2660,7 @@ struct P2PView {
     double* const* xb;       // [P] exchange buffers (index rank = own)
     uint64_t* const* xf;     // [P] epoch flags
     int P, rank, cap;
+    uint64_t timeout_ns;     // bound on the wait for a peer's epoch (0 = none)
 };
 
 __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
@@ -2669,9 +2674,14 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
 
 // Block-wide: out[i] = sum over ranks q (ascending) of rank q's local[i], i < n.
 // `out` may alias `local` (local is fully sent before out is written).
-__device__ void p2p_exchange(const P2PView& v, const double* local, int n, int slot, uint64_t epoch,
+// Returns false (the same in every thread; out untouched) when some peer's
+// epoch did not arrive within v.timeout_ns -- a dead or hung rank fails the
+// exchange instead of hanging this one forever.
+__device__ bool p2p_exchange(const P2PView& v, const double* local, int n, int slot, uint64_t epoch,
                              double* out) {
+    __shared__ int s_late;
     const int tid = threadIdx.x;
+    if (tid == 0) s_late = 0;
     for (int i = tid; i < n; i += blockDim.x) {
         const double x = local[i];
         for (int q = 0; q < v.P; ++q) v.xb[q][((size_t)slot * v.P + v.rank) * v.cap + i] = x;
@@ -2681,10 +2691,18 @@ __device__ void p2p_exchange(const P2PView& v, const double* local, int n, int s
     if (tid < v.P) st_release_sys(&v.xf[tid][slot * v.P + v.rank], epoch);
     if (tid < v.P) {
         const uint64_t* f = &v.xf[v.rank][slot * v.P + tid];
-        while (ld_acquire_sys(f) != epoch) __nanosleep(64);
+        const uint64_t t0 = v.timeout_ns ? global_ns() : 0;
+        while (ld_acquire_sys(f) != epoch) {
+            if (v.timeout_ns && global_ns() - t0 > v.timeout_ns) {
+                s_late = 1;
+                break;
+            }
+            __nanosleep(64);
+        }
     }
     __threadfence_system();
     __syncthreads();
+    if (s_late) return false;
     const double* mine = v.xb[v.rank] + (size_t)slot * v.P * v.cap;
     for (int i = tid; i < n; i += blockDim.x) {
         double s = 0.0;
@@ -2692,15 +2710,26 @@ __device__ void p2p_exchange(const P2PView& v, const double* local, int n, int s
         out[i] = s;
     }
     __syncthreads();
+    return true;
 }
 
 __device__ __forceinline__ uint64_t iter_epoch(const DevState* st) {
     return ((uint64_t)(unsigned)(st->gen & 0x7fffffff) << 32) | (uint64_t)(unsigned)(st->t + 1);
 }
 
+// A failed exchange stops the run: err records it, done turns every later
+// kernel of the iteration into a no-op; the host reports KMEANS_ENCCL.
+__device__ __forceinline__ void exchange_failed(DevState* st) {
+    if (threadIdx.x == 0) {
+        st->err = kErrExchangeTimeout;
+        st->done = 1;
+    }
+}
+
 // Host-driven exchange (mu^0 assembly, kmeans_assign): buf <- sum over ranks.
-__global__ void k_p2p_allreduce(P2PView v, double* buf, int n, int slot, uint64_t epoch) {
-    p2p_exchange(v, buf, n, slot, epoch, buf);
+__global__ void k_p2p_allreduce(P2PView v, double* buf, int n, int slot, uint64_t epoch,
+                                DevState* st) {
+    if (!p2p_exchange(v, buf, n, slot, epoch, buf)) exchange_failed(st);
 }
 
 // The iteration's exchange fused with the update: red <- sum over ranks of the
@@ -2719,7 +2748,10 @@ __global__ void k_p2p_update(P2PView v, double* __restrict__ red, int nE, double
         __threadfence_block();
         __syncthreads();
     }
-    p2p_exchange(v, red, nE, st->t & 1, iter_epoch(st), red);
+    if (!p2p_exchange(v, red, nE, st->t & 1, iter_epoch(st), red)) {
+        exchange_failed(st);
+        return;
+    }
     __threadfence();
     __syncthreads();
     update_body<D>(mu_buf, K, red, st, trace_E, trace_J, trace_cap, cneg);
@@ -2729,17 +2761,23 @@ __global__ void k_p2p_update(P2PView v, double* __restrict__ red, int nE, double
 // on one another must not be separate launches on one GPU): ONE cooperative
 // launch, block r = rank r, each with its own exchange buffer in this GPU's
 // memory.  Round i: rank r contributes vals[i][r][0..n) and writes what it
-// received to out[i][r][0..n).
+// received to out[i][r][0..n).  dead_rank (>= 0) never publishes: the others
+// must time out (failed[r] = round + 1) instead of hanging.
 __global__ void k_p2p_emulate(double* const* xb, uint64_t* const* xf, int P, int cap, int n,
                               int rounds, const double* __restrict__ vals, double* __restrict__ out,
-                              double* __restrict__ scratch) {
-    P2PView v{xb, xf, P, (int)blockIdx.x, cap};
+                              double* __restrict__ scratch, int dead_rank, uint64_t timeout_ns,
+                              int* __restrict__ failed) {
+    P2PView v{xb, xf, P, (int)blockIdx.x, cap, timeout_ns};
     double* loc = scratch + (size_t)blockIdx.x * cap;
+    if ((int)blockIdx.x == dead_rank) return;   // a rank that never publishes
     for (int i = 0; i < rounds; ++i) {
         for (int e = threadIdx.x; e < n; e += blockDim.x)
             loc[e] = vals[((size_t)i * P + blockIdx.x) * n + e];
         __syncthreads();
-        p2p_exchange(v, loc, n, i & 1, (1ull << 40) + (uint64_t)i + 1, loc);
+        if (!p2p_exchange(v, loc, n, i & 1, (1ull << 40) + (uint64_t)i + 1, loc)) {
+            if (threadIdx.x == 0) failed[blockIdx.x] = i + 1;   // round of the failure
+            return;
+        }
         for (int e = threadIdx.x; e < n; e += blockDim.x)
             out[((size_t)i * P + blockIdx.x) * n + e] = loc[e];
         __syncthreads();

@@ -22,6 +22,7 @@
 #include <mutex>
 #include <unordered_map>
 #include <string>
+#include <thread>
 #include <vector>
 
 #ifdef KMEANS_WITH_NCCL
@@ -116,6 +117,8 @@ struct kmeans_ctx {
     int d = 0, K = 0;
     void* comm = nullptr;
     int nranks = 1, rank = 0;
+    bool group = false;           // distributed: NCCL communicator or a P2P-only group
+    double comm_timeout_s = 60.0;
 
     float* X = nullptr;          // AoSoA fp32: ldx/64 tiles of [x64 y64 (z64)]
     double* mu = nullptr;        // 2 x Kpad x d (ping-pong by t & 1)
@@ -465,7 +468,7 @@ kmeans_status configure(kmeans_ctx* ctx) {
         ctx->row_stride = km::kRowDoubles;
         ctx->G = (ctx->n_chunks + km::kDenseGroup - 1) / km::kDenseGroup;  // groups
         // small single-GPU shard: whole iterations in one cooperative launch
-        if (!ctx->comm && !(ctx->flags & KMEANS_FLAG_NO_FUSED) &&
+        if (!ctx->group && !(ctx->flags & KMEANS_FLAG_NO_FUSED) &&
             ctx->n_chunks <= 4 * sms * km::kFusedWarps) {
             ctx->fused_smem = fused_smem(ctx->d, ctx->K);
             FusedFn ff = pick_fused(ctx->d, ctx->K);
@@ -617,6 +620,7 @@ km::P2PView p2p_view(const kmeans_ctx* ctx) {
     v.P = ctx->nranks;
     v.rank = ctx->rank;
     v.cap = ctx->xcap;
+    v.timeout_ns = (uint64_t)(ctx->comm_timeout_s * 1e9);
     return v;
 }
 
@@ -624,12 +628,17 @@ kmeans_status allreduce(kmeans_ctx* ctx, double* buf, size_t count) {
     if (ctx->p2p) {   // host-driven exchange over peer memory (slots 2/3)
         const uint64_t n = ++ctx->xcount;
         km::k_p2p_allreduce<<<1, 256, 0, ctx->stream>>>(p2p_view(ctx), buf, (int)count,
-                                                       2 + (int)(n & 1), (1ull << 63) | n);
+                                                       2 + (int)(n & 1), (1ull << 63) | n,
+                                                       ctx->st);
         ctx->launches += 1;
         CK(cudaGetLastError());
         return KMEANS_OK;
     }
-    if (!ctx->comm) return KMEANS_OK;
+    if (!ctx->group) return KMEANS_OK;
+    if (!ctx->comm) {   // a P2P-only group before kmeans_p2p_open: nothing to exchange with
+        set_error("P2P-only group: call kmeans_p2p_handle / kmeans_p2p_open first");
+        return KMEANS_ESTATE;
+    }
 #ifdef KMEANS_WITH_NCCL
     ncclResult_t r = ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)ctx->comm,
                                    ctx->stream);
@@ -666,7 +675,7 @@ kmeans_status launch_update(kmeans_ctx* ctx) {
 
 // Single GPU and a small enough group table: merge + update in one block.
 bool fused_update(const kmeans_ctx* ctx) {
-    return !ctx->comm && (int64_t)ctx->nE * ctx->G <= 400000 && ctx->nE * 8 <= 48 * 1024;
+    return !ctx->group && (int64_t)ctx->nE * ctx->G <= 400000 && ctx->nE * 8 <= 48 * 1024;
 }
 
 // P2P exchange and a small group table: merge + exchange + update in one block.
@@ -748,14 +757,61 @@ kmeans_status ensure_graph(kmeans_ctx* ctx) {
     return KMEANS_OK;
 }
 
+#ifdef KMEANS_WITH_NCCL
+// Communicators this library aborted (kmeans_comm_destroy must not free them again).
+std::mutex g_abort_mu;
+std::vector<void*> g_aborted;
+#endif
+
+// Waits for the context's stream.  With an NCCL communicator in use the wait
+// is a poll: ncclCommGetAsyncError is checked while the stream runs, and a
+// reported error or a wait longer than comm_timeout_s (a dead or hung peer)
+// aborts the communicator -- KMEANS_ENCCL, sticky -- instead of blocking this
+// rank forever.  (The P2P exchange bounds its own spin on the device.)
 kmeans_status sync(kmeans_ctx* ctx) {
+#ifdef KMEANS_WITH_NCCL
+    if (ctx->comm && !ctx->p2p) {
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int spin = 0;; ++spin) {
+            const cudaError_t e = cudaStreamQuery(ctx->stream);
+            if (e == cudaSuccess) return KMEANS_OK;
+            if (e != cudaErrorNotReady) return cuda_fail(ctx, e, "cudaStreamQuery");
+            ncclResult_t ar = ncclSuccess;
+            ncclCommGetAsyncError((ncclComm_t)ctx->comm, &ar);
+            const double waited =
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            if ((ar != ncclSuccess && ar != ncclInProgress) || waited > ctx->comm_timeout_s) {
+                if (ar != ncclSuccess && ar != ncclInProgress)
+                    set_error("NCCL asynchronous error: %s", ncclGetErrorString(ar));
+                else
+                    set_error("collective did not complete within %.1f s (peer dead or hung)",
+                              ctx->comm_timeout_s);
+                ncclCommAbort((ncclComm_t)ctx->comm);
+                {
+                    std::lock_guard<std::mutex> lk(g_abort_mu);
+                    g_aborted.push_back(ctx->comm);
+                }
+                ctx->sticky = KMEANS_ENCCL;
+                return KMEANS_ENCCL;
+            }
+            if (spin > 100) std::this_thread::sleep_for(std::chrono::microseconds(50));
+        }
+    }
+#endif
     CK(cudaStreamSynchronize(ctx->stream));
     return KMEANS_OK;
 }
 
 kmeans_status read_state(kmeans_ctx* ctx, DevState* h) {
     CK(cudaMemcpyAsync(h, ctx->st, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    kmeans_status s = sync(ctx);
+    if (s != KMEANS_OK) return s;
+    if (h->err) {   // a P2P exchange timed out on the device (the run was stopped)
+        set_error("P2P exchange: a peer did not publish within %.1f s (dead or hung rank)",
+                  ctx->comm_timeout_s);
+        ctx->sticky = KMEANS_ENCCL;
+        return KMEANS_ENCCL;
+    }
     return KMEANS_OK;
 }
 
@@ -781,6 +837,11 @@ kmeans_status stage_centroids(kmeans_ctx* ctx) {
     CK(cudaGetLastError());
     return KMEANS_OK;
 }
+
+// Device E/J traces: kmeans_start keeps kTraceCap entries (the kernels skip
+// t >= trace_cap); kmeans_fit_ctx grows them to max_iter only when the caller
+// asks for the traces (its own buffers bound the size).
+constexpr int kTraceCap = 4096;
 
 kmeans_status ensure_trace(kmeans_ctx* ctx, int cap) {
     if (cap <= ctx->trace_cap) return KMEANS_OK;
@@ -943,8 +1004,8 @@ int kmeans_abi_version(void) { return KMEANS_ABI_VERSION; }
 
 kmeans_status kmeans_p2p_handle(kmeans_ctx* ctx, unsigned char handle[64]) {
     CHECK_CTX(ctx);
-    if (!handle || !ctx->comm || ctx->p2p) {
-        set_error("kmeans_p2p_handle: needs a handle buffer and an NCCL context not yet opened");
+    if (!handle || !ctx->group || ctx->p2p) {
+        set_error("kmeans_p2p_handle: needs a handle buffer and a distributed context not yet opened");
         return KMEANS_EINVAL;
     }
     DeviceGuard g(ctx->device);
@@ -980,7 +1041,18 @@ kmeans_status kmeans_p2p_open(kmeans_ctx* ctx, const unsigned char* handles) {
         } else {
             cudaIpcMemHandle_t h;
             memcpy(&h, handles + 64 * (size_t)q, 64);
-            CK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+            const cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) {
+                // not sticky: undo the mappings made so far and leave the context
+                // usable, so that every rank can fall back to the NCCL allreduce
+                cudaGetLastError();
+                for (void* o : ctx->xopened) cudaIpcCloseMemHandle(o);
+                ctx->xopened.clear();
+                cudaGetLastError();
+                set_error("kmeans_p2p_open: cudaIpcOpenMemHandle(rank %d): %s", q,
+                          cudaGetErrorString(e));
+                return KMEANS_ECUDA;
+            }
             ctx->xopened.push_back(base);
         }
         tab[q] = base;
@@ -1011,11 +1083,13 @@ kmeans_status kmeans_p2p_disable(kmeans_ctx* ctx) {
 }
 
 kmeans_status kmeans_p2p_selftest(int device, int P, int n, int rounds, const double* vals,
-                                  double* out) {
-    if (P < 1 || P > 64 || n < 1 || rounds < 1 || !vals || !out) {
+                                  double* out, int dead_rank, double timeout_s, int* failed) {
+    if (P < 1 || P > 64 || n < 1 || rounds < 1 || !vals || !out || dead_rank >= P ||
+        !(timeout_s >= 0.0)) {
         set_error("kmeans_p2p_selftest: bad argument");
         return KMEANS_EINVAL;
     }
+    const uint64_t tmo = (uint64_t)((timeout_s > 0.0 ? timeout_s : 60.0) * 1e9);
     DeviceGuard g(device);
     kmeans_ctx* ctx = nullptr;   // for CK
     int coop = 0;
@@ -1025,9 +1099,12 @@ kmeans_status kmeans_p2p_selftest(int device, int P, int n, int rounds, const do
                        sizeof(uint64_t) * km::kXSlots * P;
     char* arena = nullptr;
     double *dv = nullptr, *dout = nullptr, *scratch = nullptr;
+    int* dfail = nullptr;
     void** tab = nullptr;
     const size_t nv = (size_t)rounds * P * n;
     cudaError_t e = cudaMalloc(&arena, per * P);
+    if (e == cudaSuccess) e = cudaMalloc(&dfail, sizeof(int) * P);
+    if (e == cudaSuccess) e = cudaMemset(dfail, 0, sizeof(int) * P);
     if (e == cudaSuccess) e = cudaMemset(arena, 0, per * P);
     if (e == cudaSuccess) e = cudaMalloc(&dv, sizeof(double) * nv);
     if (e == cudaSuccess) e = cudaMalloc(&dout, sizeof(double) * nv);
@@ -1043,9 +1120,11 @@ kmeans_status kmeans_p2p_selftest(int device, int P, int n, int rounds, const do
     if (e == cudaSuccess) {
         double* const* xb = reinterpret_cast<double* const*>(tab);
         uint64_t* const* xf = reinterpret_cast<uint64_t* const*>(tab + P);
-        int cap_ = cap, P_ = P, n_ = n, r_ = rounds;
-        void* args[] = {(void*)&xb, (void*)&xf, (void*)&P_, (void*)&cap_, (void*)&n_, (void*)&r_,
-                        (void*)&dv, (void*)&dout, (void*)&scratch};
+        int cap_ = cap, P_ = P, n_ = n, r_ = rounds, dead = dead_rank;
+        uint64_t tmo_ = tmo;
+        void* args[] = {(void*)&xb,   (void*)&xf,    (void*)&P_,      (void*)&cap_,
+                        (void*)&n_,   (void*)&r_,    (void*)&dv,      (void*)&dout,
+                        (void*)&scratch, (void*)&dead, (void*)&tmo_, (void*)&dfail};
         // all P "ranks" co-resident (they wait on one another): a cooperative launch
         e = coop ? cudaLaunchCooperativeKernel((const void*)km::k_p2p_emulate, dim3(P), dim3(128),
                                                args, 0, 0)
@@ -1053,12 +1132,21 @@ kmeans_status kmeans_p2p_selftest(int device, int P, int n, int rounds, const do
     }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e == cudaSuccess) e = cudaMemcpy(out, dout, sizeof(double) * nv, cudaMemcpyDeviceToHost);
+    std::vector<int> hf(P, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(hf.data(), dfail, sizeof(int) * P, cudaMemcpyDeviceToHost);
+    cudaFree(dfail);
     cudaFree(arena);
     cudaFree(dv);
     cudaFree(dout);
     cudaFree(scratch);
     cudaFree(tab);
     CK(e);
+    if (failed) memcpy(failed, hf.data(), sizeof(int) * P);
+    for (int r = 0; r < P; ++r)
+        if (hf[r]) {
+            set_error("kmeans_p2p_selftest: rank %d timed out in round %d", r, hf[r]);
+            return KMEANS_ENCCL;
+        }
     return KMEANS_OK;
 }
 
@@ -1137,6 +1225,10 @@ void kmeans_opts_init(kmeans_opts* o) {
     o->global_offset = 0;
     o->global_N = 0;
     o->flags = 0;
+    o->rank = 0;
+    o->nranks = 0;
+    o->expected_iters = 0;
+    o->comm_timeout_s = 0.0;
 }
 
 void kmeans_destroy(kmeans_ctx* ctx) {
@@ -1194,7 +1286,11 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
     const int64_t gN = opts.global_N > 0 ? opts.global_N : N;
     if (!points || N < 1 || (d != 2 && d != 3) || K < 1 || K > KMEANS_MAX_K || K > gN ||
         (opts.layout != KMEANS_LAYOUT_AOS && opts.layout != KMEANS_LAYOUT_SOA) ||
-        opts.global_offset < 0 || opts.global_offset + N > gN || (!opts.nccl_comm && gN != N)) {
+        opts.global_offset < 0 || opts.global_offset + N > gN || opts.expected_iters < 0 ||
+        !(opts.comm_timeout_s >= 0.0) ||
+        (!opts.nccl_comm && (opts.nranks < 0 || (opts.nranks > 0 && (opts.rank < 0 ||
+                                                                    opts.rank >= opts.nranks)))) ||
+        (!opts.nccl_comm && opts.nranks == 0 && gN != N)) {
         set_error("invalid argument (N=%lld d=%d K=%d global_N=%lld offset=%lld)", (long long)N, d,
                   K, (long long)gN, (long long)opts.global_offset);
         return KMEANS_EINVAL;
@@ -1223,6 +1319,12 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
     ctx->global_N = gN;
     ctx->global_offset = opts.global_offset;
     ctx->comm = opts.nccl_comm;
+    ctx->group = opts.nccl_comm != nullptr || opts.nranks > 0;
+    if (!opts.nccl_comm && opts.nranks > 0) {   // P2P-only group
+        ctx->nranks = opts.nranks;
+        ctx->rank = opts.rank;
+    }
+    if (opts.comm_timeout_s > 0.0) ctx->comm_timeout_s = opts.comm_timeout_s;
     // padded so every full 2048-point chunk (and every large-path tile) is in bounds
     ctx->ldx = round_up(N, km::kChunkPoints) + km::kChunkPoints;
 #ifdef KMEANS_WITH_NCCL
@@ -1253,7 +1355,19 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
     ctx->flags = opts.flags;
     if (opts.flags & KMEANS_FLAG_NO_SORT) ctx->sorted = false;
     else if (opts.flags & KMEANS_FLAG_FORCE_SORT) ctx->sorted = true;
-    else ctx->sorted = K > 16 || (double)N * K * d >= 3.84e8;   // see kmeans.h
+    else {
+        ctx->sorted = K > 16 || (double)N * K * d >= 3.84e8;   // see kmeans.h
+        if (ctx->sorted && K <= 16 && opts.expected_iters > 0) {
+            // the Morton sort must pay for itself over the expected iterations
+            // (measured at N = 1e8, d = 3, K = 16: sort +
+            // gather + keys ~0.098 ns per point; full scan at ~48% of the FP32
+            // lanes; pruned pass at ~6.5 TB/s)
+            const double t_sort = 0.098e-9 * (double)N;
+            const double t_full = 2.0 * d * K * (double)N / (0.48 * 3.72e13);
+            const double t_pruned = 4.0 * d * (double)N / 6.5e12;
+            if ((double)opts.expected_iters * (t_full - t_pruned) < t_sort) ctx->sorted = false;
+        }
+    }
     if (ctx->sorted && N > INT32_MAX) {   // the sort's permutation is int32
         if (opts.flags & KMEANS_FLAG_FORCE_SORT) {
             set_error("KMEANS_FLAG_FORCE_SORT: the sorted path holds at most 2^31 - 1 points per shard");
@@ -1367,6 +1481,10 @@ kmeans_status kmeans_start(kmeans_ctx* ctx, const int64_t* init_idx, const doubl
         set_error("kmeans_start: need init_idx or centroids, tol >= 0, max_iter >= 1");
         return KMEANS_EINVAL;
     }
+    if (ctx->group && !ctx->comm && !ctx->p2p) {
+        set_error("P2P-only group: call kmeans_p2p_handle / kmeans_p2p_open first");
+        return KMEANS_ESTATE;
+    }
     DeviceGuard g(ctx->device);
     kmeans_status s;
     if (init_idx) {
@@ -1401,7 +1519,8 @@ kmeans_status kmeans_start(kmeans_ctx* ctx, const int64_t* init_idx, const doubl
         CK(cudaGetLastError());
         // CC1: assemble mu^0 from the owners (exact: one x plus zeros)
         if ((s = allreduce(ctx, ctx->mu, (size_t)n)) != KMEANS_OK) return s;
-        CK(cudaStreamSynchronize(ctx->stream));  // idx vector lifetime
+        DevState h;   // waits (idx vector lifetime) and reports a failed exchange
+        if ((s = read_state(ctx, &h)) != KMEANS_OK) return s;
     } else {
         std::vector<double> c;
         if ((s = fetch_centroids(ctx, centroids, c)) != KMEANS_OK) return s;
@@ -1409,7 +1528,7 @@ kmeans_status kmeans_start(kmeans_ctx* ctx, const int64_t* init_idx, const doubl
                            ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
     }
-    if ((s = ensure_trace(ctx, max_iter)) != KMEANS_OK) return s;
+    if ((s = ensure_trace(ctx, std::min(max_iter, kTraceCap))) != KMEANS_OK) return s;
     ctx->assigned = false;
     ctx->gen += 1;   // new epochs for the iteration exchanges of this run
     if ((s = write_state(ctx, 0, 0, max_iter, tol)) != KMEANS_OK) return s;
@@ -1504,6 +1623,10 @@ kmeans_status kmeans_assign(kmeans_ctx* ctx, const double* centroids, int32_t* l
         set_error("centroids is NULL");
         return KMEANS_EINVAL;
     }
+    if (ctx->group && !ctx->comm && !ctx->p2p) {
+        set_error("P2P-only group: call kmeans_p2p_handle / kmeans_p2p_open first");
+        return KMEANS_ESTATE;
+    }
     DeviceGuard g(ctx->device);
     kmeans_status s;
     std::vector<double> c;
@@ -1521,10 +1644,13 @@ kmeans_status kmeans_assign(kmeans_ctx* ctx, const double* centroids, int32_t* l
     std::vector<double> red(ctx->nE);
     CK(cudaMemcpyAsync(red.data(), ctx->red, sizeof(double) * ctx->nE, cudaMemcpyDeviceToHost,
                        ctx->stream));
-    if (labels)
+    DevState h;   // the kernels (and the exchange) completed without error ...
+    if ((s = read_state(ctx, &h)) != KMEANS_OK) return s;
+    if (labels) {   // ... before any output is written
         CK(cudaMemcpyAsync(labels, ctx->labels, sizeof(int32_t) * ctx->N, cudaMemcpyDefault,
                            ctx->stream));
-    if ((s = sync(ctx)) != KMEANS_OK) return s;
+        if ((s = sync(ctx)) != KMEANS_OK) return s;
+    }
     const int K = ctx->K, d = ctx->d;
     if (inertia) CK(cudaMemcpy(inertia, &red[(size_t)K * d + K], sizeof(double), cudaMemcpyDefault));
     if (counts) {
@@ -1571,6 +1697,7 @@ kmeans_status kmeans_fit_ctx(kmeans_ctx* ctx, const int64_t* init_idx, double to
     DeviceGuard g(ctx->device);
     kmeans_status s = kmeans_start(ctx, init_idx, nullptr, tol, max_iter);
     if (s != KMEANS_OK) return s;
+    if ((E_trace || J_trace) && (s = ensure_trace(ctx, max_iter)) != KMEANS_OK) return s;
     // Graph replays in chunks; the device stop flag turns surplus iterations
     // into no-ops, the host polls once per chunk.
     int chunk = 4, t = 0, done = 0;
@@ -1606,7 +1733,10 @@ kmeans_status kmeans_fit(const float* points, int64_t N, int d, int K, const int
         return KMEANS_EINVAL;
     }
     kmeans_ctx* ctx = nullptr;
-    kmeans_status s = kmeans_create(&ctx, points, N, d, K, nullptr);
+    kmeans_opts o;
+    kmeans_opts_init(&o);
+    o.expected_iters = max_iter;   // the path choice weighs the sort against the run
+    kmeans_status s = kmeans_create(&ctx, points, N, d, K, &o);
     if (s != KMEANS_OK) return s;
     s = kmeans_fit_ctx(ctx, init_idx, tol, max_iter, labels, centroids, iters, inertia, nullptr,
                        nullptr);
@@ -1790,6 +1920,14 @@ kmeans_status kmeans_comm_init(void** comm, int nranks, const unsigned char id[1
 kmeans_status kmeans_comm_destroy(void* comm) {
     if (!comm) return KMEANS_OK;
 #ifdef KMEANS_WITH_NCCL
+    {   // already aborted (and freed) by a context that timed out on it
+        std::lock_guard<std::mutex> lk(g_abort_mu);
+        auto it = std::find(g_aborted.begin(), g_aborted.end(), comm);
+        if (it != g_aborted.end()) {
+            g_aborted.erase(it);
+            return KMEANS_OK;
+        }
+    }
     ncclResult_t r = ncclCommDestroy((ncclComm_t)comm);
     if (r != ncclSuccess) {
         set_error("ncclCommDestroy: %s", ncclGetErrorString(r));

@@ -15,8 +15,24 @@ from . import datagen
 from . import kmeans as km
 
 
+def check_shards(global_N: int, world: int) -> None:
+    """Every rank must own at least one point: the ceiling partition leaves the
+    last ranks empty when (world - 1) * ceil(N / world) >= N (e.g. N = 5 over
+    4 ranks), and an empty rank would fail kmeans_create while its peers
+    enter the collectives.  Raises the same ValueError on every rank (the test
+    needs no communication)."""
+    if world < 1 or global_N < 1:
+        raise ValueError(f"need global_N >= 1 and world >= 1 (got {global_N}, {world})")
+    c = -(-global_N // world)
+    if (world - 1) * c >= global_N:
+        raise ValueError(f"global_N={global_N} over {world} ranks leaves rank {world - 1} "
+                         "without points (contiguous ceiling partition)")
+
+
 def shard(global_N: int, world: int, rank: int) -> tuple[int, int]:
-    """[a, b) owned by `rank` (contiguous ceiling partition)."""
+    """[a, b) owned by `rank` (contiguous ceiling partition); ValueError on
+    every rank if some rank would own no point (check_shards)."""
+    check_shards(global_N, world)
     return datagen.shard_range(global_N, world, rank)
 
 

@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("KMEANS_LIB_OVERRIDE") or os.path.join(HERE, "libkmeans.so")
 
 KMEANS_OK = 0
-ABI_VERSION = 2   # include/kmeans.h KMEANS_ABI_VERSION
+ABI_VERSION = 3   # include/kmeans.h KMEANS_ABI_VERSION
 STATUS = {0: "KMEANS_OK", -1: "KMEANS_EINVAL", -2: "KMEANS_ENONFINITE", -3: "KMEANS_ENOMEM",
           -4: "KMEANS_ECUDA", -5: "KMEANS_ENCCL", -6: "KMEANS_ESTATE"}
 LAYOUT_AOS, LAYOUT_SOA = 0, 1
@@ -39,7 +39,9 @@ class KMeansError(RuntimeError):
 class Opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("layout", ctypes.c_int),
                 ("nccl_comm", ctypes.c_void_p), ("global_offset", ctypes.c_int64),
-                ("global_N", ctypes.c_int64), ("flags", ctypes.c_int)]
+                ("global_N", ctypes.c_int64), ("flags", ctypes.c_int), ("rank", ctypes.c_int),
+                ("nranks", ctypes.c_int), ("expected_iters", ctypes.c_int),
+                ("comm_timeout_s", ctypes.c_double)]
 
 
 class Info(ctypes.Structure):
@@ -90,7 +92,7 @@ SIGNATURES = {
     "kmeans_p2p_handle": (I, [P, P]),
     "kmeans_p2p_open": (I, [P, P]),
     "kmeans_p2p_disable": (I, [P]),
-    "kmeans_p2p_selftest": (I, [I, I, I, I, P, P]),
+    "kmeans_p2p_selftest": (I, [I, I, I, I, P, P, I, D, P]),
 }
 
 _lib = None
@@ -129,33 +131,39 @@ def _ptr(a):
     if a is None:
         return None
     if _is_torch(a):
-        assert a.is_contiguous(), "tensor must be contiguous"
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
         return ctypes.c_void_p(a.data_ptr())
-    assert a.flags["C_CONTIGUOUS"], "array must be C-contiguous"
+    if not a.flags["C_CONTIGUOUS"]:
+        raise ValueError("array must be C-contiguous")
     return ctypes.c_void_p(a.ctypes.data)
+
+
+def _torch_checked(a, dtype_name: str):
+    import torch
+    want = getattr(torch, dtype_name)
+    if a.dtype != want:
+        raise TypeError(f"tensor must be {dtype_name}, got {a.dtype}")
+    if not a.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return a
 
 
 def _as_f32_points(points):
     if _is_torch(points):
-        import torch
-        assert points.dtype == torch.float32 and points.is_contiguous()
-        return points
+        return _torch_checked(points, "float32")
     return np.ascontiguousarray(points, dtype=np.float32)
 
 
 def _as_f64(a):
     if _is_torch(a):
-        import torch
-        assert a.dtype == torch.float64 and a.is_contiguous()
-        return a
+        return _torch_checked(a, "float64")
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
 def _as_i64(a):
     if _is_torch(a):
-        import torch
-        assert a.dtype == torch.int64 and a.is_contiguous()
-        return a
+        return _torch_checked(a, "int64")
     return np.ascontiguousarray(a, dtype=np.int64)
 
 
@@ -166,14 +174,30 @@ class Context:
     def __init__(self, points, K: int, *, d: int | None = None, layout: str = "aos",
                  device: int = -1, stream=None, comm=None, global_offset: int = 0,
                  global_N: int = 0, sort: bool | None = None, fused: bool = True,
-                 big_chunks: bool = False):
+                 big_chunks: bool = False, rank: int = 0, nranks: int = 0,
+                 expected_iters: int = 0, comm_timeout_s: float = 0.0):
         pts = _as_f32_points(points)
         shape = tuple(pts.shape)
+        if layout not in ("aos", "soa"):
+            raise ValueError(f"layout must be 'aos' or 'soa', got {layout!r}")
         if layout == "aos":
-            N, dd = (shape[0], shape[1]) if len(shape) == 2 else (shape[0] // (d or 1), d)
+            if len(shape) == 2:
+                N, dd = shape
+            elif len(shape) == 1:
+                if d is None:
+                    raise ValueError("1-D AoS points need d (points are N*d floats)")
+                if shape[0] % d:
+                    raise ValueError(f"{shape[0]} floats is not a multiple of d={d}")
+                N, dd = shape[0] // d, d
+            else:
+                raise ValueError(f"AoS points must be N x d (or flat with d), got shape {shape}")
         else:
+            if len(shape) != 2:
+                raise ValueError(f"SoA points must be d x N, got shape {shape}")
             dd, N = shape
-        self.N, self.d, self.K = int(N), int(dd if d is None else d), int(K)
+        if d is not None and int(d) != int(dd):
+            raise ValueError(f"d={d} does not match the points' shape {shape}")
+        self.N, self.d, self.K = int(N), int(dd), int(K)
         o = Opts()
         lib().kmeans_opts_init(ctypes.byref(o))
         o.device = device
@@ -188,6 +212,10 @@ class Context:
             o.flags |= FLAG_NO_FUSED
         if big_chunks:  # sorted path: 2048-point chunks regardless of N
             o.flags |= FLAG_BIG_CHUNKS
+        o.rank = rank                   # P2P-only group (no NCCL communicator)
+        o.nranks = nranks
+        o.expected_iters = expected_iters
+        o.comm_timeout_s = comm_timeout_s
         h = ctypes.c_void_p()
         _check(lib().kmeans_create(ctypes.byref(h), _ptr(pts), self.N, self.d, self.K,
                                    ctypes.byref(o)), "kmeans_create")
@@ -330,6 +358,8 @@ class Context:
 def fit(points, K: int, init_idx, tol: float, max_iter: int, *, labels=True):
     """kmeans_fit: the whole Lloyd run on one GPU, points N x d."""
     pts = _as_f32_points(points)
+    if len(pts.shape) != 2:
+        raise ValueError(f"points must be N x d, got shape {tuple(pts.shape)}")
     N, d = int(pts.shape[0]), int(pts.shape[1])
     idx = _as_i64(init_idx)
     lab = np.empty(N, np.int32) if labels else None
@@ -350,7 +380,8 @@ def comm_unique_id() -> bytes:
 
 
 def comm_init(nranks: int, uid: bytes, rank: int, device: int) -> int:
-    assert len(uid) == 128
+    if len(uid) != 128:
+        raise ValueError("an NCCL unique id is 128 bytes")
     buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid)
     c = ctypes.c_void_p()
     _check(lib().kmeans_comm_init(ctypes.byref(c), int(nranks), buf, int(rank), int(device)),
@@ -367,13 +398,17 @@ def release_memory(device: int = 0):
     _check(lib().kmeans_release_memory(int(device)), "kmeans_release_memory")
 
 
-def p2p_selftest(vals, device: int = 0):
+def p2p_selftest(vals, device: int = 0, dead_rank: int = -1, timeout_s: float = 0.0,
+                 failed=None):
     """kmeans_p2p_selftest: vals (rounds, P, n) float64 -> what each emulated
-    rank computed, same shape."""
+    rank computed, same shape.  dead_rank never publishes; `failed` (P int32,
+    optional) receives each rank's failed round (1-based, 0 = none)."""
     v = np.ascontiguousarray(vals, dtype=np.float64)
     rounds, P, n = v.shape
     out = np.empty_like(v)
-    _check(lib().kmeans_p2p_selftest(int(device), int(P), int(n), int(rounds), _ptr(v), _ptr(out)),
+    f = failed if failed is not None else np.zeros(P, np.int32)
+    _check(lib().kmeans_p2p_selftest(int(device), int(P), int(n), int(rounds), _ptr(v), _ptr(out),
+                                     int(dead_rank), float(timeout_s), _ptr(f)),
            "kmeans_p2p_selftest")
     return out
 

@@ -53,7 +53,7 @@ def test_library_is_sm100a_only():
 
 def test_status_strings_and_version(km):
     L = km.lib()
-    assert L.kmeans_abi_version() == 2
+    assert L.kmeans_abi_version() == 3 == km.ABI_VERSION
     for code, name in km.STATUS.items():
         assert L.kmeans_status_string(code).decode().startswith(name)
 
@@ -97,12 +97,46 @@ def test_invalid_arguments_rejected_before_device_work(km):
     assert L.kmeans_p2p_handle(None, None) == -1
     assert L.kmeans_p2p_open(None, None) == -1
     assert L.kmeans_p2p_disable(None) == -1
-    assert L.kmeans_p2p_selftest(0, 0, 5, 1, None, None) == -1     # P < 1
-    assert L.kmeans_p2p_selftest(0, 65, 5, 1, None, None) == -1    # P > 64
+    assert L.kmeans_p2p_selftest(0, 0, 5, 1, None, None, -1, 0.0, None) == -1     # P < 1
+    assert L.kmeans_p2p_selftest(0, 65, 5, 1, None, None, -1, 0.0, None) == -1    # P > 64
+    v = np.zeros((1, 2, 5))
+    vp = ctypes.c_void_p(v.ctypes.data)
+    assert L.kmeans_p2p_selftest(0, 2, 5, 1, vp, vp, 2, 0.0, None) == -1   # dead_rank >= P
+    assert L.kmeans_p2p_selftest(0, 2, 5, 1, vp, vp, -1, -1.0, None) == -1  # timeout < 0
+    # P2P-only group: rank outside [0, nranks), negative hints
+    o2 = km.Opts()
+    L.kmeans_opts_init(ctypes.byref(o2))
+    assert o2.nranks == 0 and o2.rank == 0 and o2.expected_iters == 0 and o2.comm_timeout_s == 0.0
+    o2.nranks, o2.rank = 2, 2
+    assert L.kmeans_create(ctypes.byref(h), p, 10, 3, 2, ctypes.byref(o2)) == -1
+    o2.nranks, o2.rank, o2.expected_iters = 2, 0, -1
+    assert L.kmeans_create(ctypes.byref(h), p, 10, 3, 2, ctypes.byref(o2)) == -1
+    o2.expected_iters, o2.comm_timeout_s = 0, float("nan")
+    assert L.kmeans_create(ctypes.byref(h), p, 10, 3, 2, ctypes.byref(o2)) == -1
     assert L.kmeans_release_memory(-1) == -1
     assert L.kmeans_generate(None, 0, 1, None, 0, None) == -1
     L.kmeans_destroy(None)  # NULL-safe
     assert L.kmeans_last_error()  # a message was recorded
+
+
+def test_binding_validates_shapes_and_dtypes(km):
+    """Python-side validation raises ValueError / TypeError (not assert, which
+    python -O strips) before any library call."""
+    with pytest.raises(ValueError):
+        km.Context(np.zeros(6, np.float32), K=2)            # 1-D AoS without d
+    with pytest.raises(ValueError):
+        km.Context(np.zeros(7, np.float32), K=2, d=3)       # not a multiple of d
+    with pytest.raises(ValueError):
+        km.Context(np.zeros((4, 3), np.float32), K=2, d=2)  # d contradicts the shape
+    with pytest.raises(ValueError):
+        km.Context(np.zeros((4, 3), np.float32), K=2, layout="xyz")
+    with pytest.raises(ValueError):
+        km._ptr(np.zeros((4, 6))[:, ::2])                    # not contiguous
+    torch = pytest.importorskip("torch")
+    with pytest.raises(TypeError):
+        km._as_f64(torch.zeros(3, dtype=torch.float32))
+    with pytest.raises(ValueError):
+        km.comm_init(2, b"short", 0, 0)
 
 
 def test_binding_raises_typed_error(km):

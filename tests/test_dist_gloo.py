@@ -153,8 +153,14 @@ def test_distributed_decomposition_gloo(world):
 
 def test_shard_partition_properties():
     from paper_2405_12052_b200 import dist as kdist
-    for N in [1, 7, 100, 1_000_003]:
+    for N in [1, 5, 7, 100, 1_000_003]:
         for P in [1, 2, 3, 4, 8]:
+            c = -(-N // P)
+            if (P - 1) * c >= N:   # some rank would own no point: refused on every rank
+                for r in range(P):
+                    with pytest.raises(ValueError):
+                        kdist.shard(N, P, r)
+                continue
             spans = [kdist.shard(N, P, r) for r in range(P)]
             assert spans[0][0] == 0 and spans[-1][1] == N
             assert all(spans[i][1] == spans[i + 1][0] for i in range(P - 1))

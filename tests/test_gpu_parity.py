@@ -281,14 +281,18 @@ def test_kmeans_fit_convenience_call():
     np.testing.assert_allclose(g["centroids"], o["centroids"], rtol=1e-6)
 
 
+@pytest.mark.parametrize("path", [dict(), dict(fused=False), dict(sort=True)],
+                         ids=["fused", "unfused", "sorted"])
 @pytest.mark.parametrize("name", ["w1.json", "w2.json", "w3.json", "w4.json"])
-def test_hand_worked_runs_on_gpu(golden_dir, name):
+def test_hand_worked_runs_on_gpu(golden_dir, name, path):
     """Tiny integer examples: every sum is exact in any order, so the GPU's
-    per-iteration E and J must equal the hand-derived values exactly."""
+    per-iteration E and J must equal the hand-derived values exactly -- on the
+    one-launch fused kernel, the per-iteration graph (k_merge_update: E summed
+    serially k-major like the oracle) and the sorted path."""
     g = json.load(open(os.path.join(golden_dir, name)))
     X = np.array(g["points"], np.float32)
     K = len(g["init_idx"])
-    with km.Context(X, K) as c:
+    with km.Context(X, K, **path) as c:
         r = c.fit(g["init_idx"], g["tol"], g["max_iter"])
     assert r["iters"] == g["iters"]
     assert r["labels"].tolist() == g["labels"]
@@ -738,3 +742,101 @@ def test_large_k_row_merge_repeated_k_windows(n_blobs):
     mu = np.concatenate([centers, rng.uniform(1e3, 2e3, (K - n_blobs, 3))]).astype(np.float64)
     g, o = check_step(X, mu, tag=f"repeated-k {n_blobs}")
     assert np.count_nonzero(o["counts"]) == n_blobs
+
+
+# --------------------------------------------------------------------------
+# failure behaviour of the distributed path, trace sizing, path choice
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("P,dead", [(2, 1), (4, 0), (8, 5)])
+def test_p2p_exchange_dead_rank_times_out(P, dead):
+    """A rank that never publishes (dead or hung peer): every other emulated
+    rank gives up after the timeout -- the exchange fails with KMEANS_ENCCL
+    in round 1 instead of spinning forever (kernels.cuh p2p_exchange)."""
+    vals = np.ones((3, P, 17))
+    failed = np.zeros(P, np.int32)
+    with pytest.raises(km.KMeansError) as e:
+        km.p2p_selftest(vals, dead_rank=dead, timeout_s=0.05, failed=failed)
+    assert e.value.name == "KMEANS_ENCCL"
+    assert failed[dead] == 0
+    assert all(failed[r] == 1 for r in range(P) if r != dead), failed
+
+
+def test_p2p_only_group_without_nccl():
+    """A P2P-only context (opts.rank / opts.nranks, no NCCL communicator):
+    iterating before kmeans_p2p_open is KMEANS_ESTATE; after opening (1 rank:
+    it maps only itself) the run equals the single-GPU run bit for bit."""
+    w = datagen.WORKLOADS["C2"]
+    N = 120_000
+    X = datagen.generate(w, N=N)
+    init = datagen.one_per_blob_init(w, N=N)
+    with km.Context(X, w.M) as c:
+        ref = c.fit(init, w.tol, w.max_iter)
+    with km.Context(X, w.M, rank=0, nranks=1) as c:
+        assert c.info()["nranks"] == 1 and c.info()["fused"] == 0
+        with pytest.raises(km.KMeansError) as e:
+            c.fit(init, w.tol, w.max_iter)
+        assert e.value.name == "KMEANS_ESTATE"
+        c.p2p_open([c.p2p_handle()])
+        r = c.fit(init, w.tol, w.max_iter)
+    assert r["iters"] == ref["iters"]
+    assert np.array_equal(r["labels"], ref["labels"])
+    assert np.array_equal(r["centroids"], ref["centroids"])
+
+
+def test_p2p_open_failure_is_not_sticky():
+    """a failing cudaIpcOpenMemHandle (corrupt peer handle) returns
+    KMEANS_ECUDA without poisoning the context: it answers later calls, and a
+    second open attempt is still possible."""
+    X = datagen.generate(datagen.WORKLOADS["C2"], N=10_000)
+    with km.Context(X, 8, rank=0, nranks=2, global_N=20_000) as c:
+        own = c.p2p_handle()
+        with pytest.raises(km.KMeansError) as e:
+            c.p2p_open([own, bytes(64)])
+        assert e.value.name == "KMEANS_ECUDA"
+        assert c.info()["nranks"] == 2          # not sticky
+        c.p2p_disable()
+        with pytest.raises(km.KMeansError) as e:
+            c.p2p_open([own, b"\x01" * 64])
+        assert e.value.name == "KMEANS_ECUDA"
+
+
+def test_start_does_not_size_traces_by_max_iter():
+    """kmeans_start(max_iter = 2^30) must not allocate 2 x 8 GiB of
+    E/J traces; kmeans_fit_ctx with caller trace buffers beyond the default
+    cap still returns every iteration's E and J."""
+    import torch
+    w = datagen.WORKLOADS["C1"]
+    X = datagen.generate(w)
+    init = datagen.init_indices(w)
+    with km.Context(X, w.K, fused=False) as c:
+        torch.cuda.synchronize()
+        free0 = torch.cuda.mem_get_info()[0]
+        c.start(init_idx=init, tol=0.0, max_iter=1 << 30)
+        c.iterate(3)
+        assert c.poll()["iters"] == 3
+        free1 = torch.cuda.mem_get_info()[0]
+        assert free0 - free1 < (256 << 20), (free0 - free1)
+    with km.Context(X, w.K) as c:
+        r = c.fit(init, 0.0, 5000)
+    o = oracle.fit(X, w.K, init, 0.0, 30)
+    assert r["iters"] == 5000 and r["E_trace"].shape == (5000,)
+    assert np.array_equal(r["E_trace"][30:], np.zeros(4970))   # converged long before
+    np.testing.assert_allclose(r["J_trace"][:30], o["J_trace"], rtol=1e-9)
+
+
+def test_expected_iters_weighs_the_sort():
+    """opts.expected_iters: at N K d >= 3.84e8 (K <= 16) the sorted path is the
+    default, but a 20-iteration run does not pay back the create-time sort
+    (DESIGN.md section 5): full scan.  Results are identical either way."""
+    w = datagen.WORKLOADS["NS"]
+    N = 8_100_000
+    X = datagen.generate(w, N=N)
+    init = datagen.init_indices(w, N=N)
+    res = {}
+    for hint, sorted_ in [(0, 1), (20, 0), (1000, 1)]:
+        with km.Context(X, w.K, expected_iters=hint) as c:
+            assert c.info()["sorted"] == sorted_, hint
+            res[hint] = c.fit(init, 0.0, 3)
+    for hint in (20, 1000):
+        assert np.array_equal(res[hint]["labels"], res[0]["labels"])
+        np.testing.assert_allclose(res[hint]["centroids"], res[0]["centroids"], rtol=1e-12)
