@@ -30,10 +30,33 @@
 // are bit-reproducible run to run for a fixed grid.
 #pragma once
 #include <cooperative_groups.h>
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace km {
+
+// KM_CHECKS=1 (the "checked" test build, tools/build_variants.py): device-side
+// bounds and protocol checks that trap on violation -- the stand-in for
+// compute-sanitizer, which this GPU pool does not allow.  Compiled out by
+// default.
+#ifndef KM_CHECKS
+#define KM_CHECKS 0
+#endif
+#if KM_CHECKS
+#define KM_CHECK(c)                                                                 \
+    do {                                                                            \
+        if (!(c)) {                                                                 \
+            printf("KM_CHECK failed: %s at %s:%d (block %d thread %d)\n", #c, __FILE__, \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                     \
+            __trap();                                                               \
+        }                                                                           \
+    } while (0)
+#else
+#define KM_CHECK(c) \
+    do {            \
+    } while (0)
+#endif
 
 // Device-resident loop state (E compared with tol "at the end of each
 // iteration").  t = completed iterations; mu^t lives in mu_buf[t & 1].
@@ -121,6 +144,8 @@ __global__ void k_init_gather(const float* __restrict__ X, int d, int K,
     int k = q / d, j = q % d;
     int64_t i = idx[k] - offset;
     if (pos) i = pos[k];   // sorted layout: position found by k_find_pos (-1: not local)
+    KM_CHECK(i < n_local);
+    KM_CHECK(!pos || i >= 0 || idx[k] < offset || idx[k] - offset >= n_local);   // local -> found
     mu0[q] = (i >= 0 && i < n_local)
                  ? (double)X[(i >> 6) * (d * kWarpTile) + j * kWarpTile + (i & 63)]
                  : 0.0;
@@ -314,6 +339,28 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 #endif
+}
+
+// L2 cache policies for the point stream (createpolicy): evict_first for the
+// part of the shard streamed from HBM every iteration, evict_last for the part
+// kept resident in the 126 MB L2 across iterations (the "keep" prefix).
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void bulk_g2s_pol(void* dst, const void* src, unsigned bytes,
+                                             uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
 }
 
 template <int D, int KP>
@@ -744,8 +791,10 @@ __global__ void k_scatter_labels(const int32_t* __restrict__ lab_sorted,
                                  const int32_t* __restrict__ perm, int64_t n,
                                  int32_t* __restrict__ lab_out) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride)
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
+        KM_CHECK(perm[p] >= 0 && perm[p] < n);
         lab_out[perm[p]] = lab_sorted[p];
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -833,6 +882,7 @@ struct PrunedSmem<D, false> {
 
 // {k, n} in one double's bits: k in the low word, n in the high word
 __device__ __forceinline__ double pack_kn(int k, int n) {
+    KM_CHECK(k >= 0 && k < 1024 && n >= 0 && n <= 2048);
     return __hiloint2double(n, k);
 }
 
@@ -850,7 +900,8 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
                 const int* __restrict__ slist, const int* __restrict__ scount,
                 double* __restrict__ rows, int row_stride, int32_t* __restrict__ labels,
                 int* __restrict__ cand_count, int* __restrict__ heavy,
-                int* __restrict__ heavy_count, unsigned short* __restrict__ slot_g) {
+                int* __restrict__ heavy_count, unsigned short* __restrict__ slot_g,
+                int64_t keep_n) {
     using C = PCfg<LARGE>;
     // Prologue before pdl_wait() touches only what no predecessor writes: the
     // chunk box and the points (the TMA ring is filled here, so with PDL the
@@ -875,14 +926,23 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
     const int npts = rem < CHP ? (int)rem : CHP;
     const float* src = X + (base >> 6) * (D * kWarpTile);
 
-    // point stream: units 0..nunit-1 through the TMA ring (unit q in stage q % SS)
+    // point stream: units 0..nunit-1 through the TMA ring (unit q in stage q % SS).
+    // Small K: points below keep_n stay resident in L2 across iterations
+    // (evict_last), the rest stream from HBM (evict_first).
     unsigned issued = 0;   // lane 0
+    const bool keep = !LARGE && base < keep_n;
+    const uint64_t pol = LARGE ? 0ull : (keep ? l2_policy_evict_last() : l2_policy_evict_first());
     auto issue_upto = [&](unsigned limit) {
         if (lane != 0) return;
         while (issued < limit && (int)issued < nunit) {
             const int s = issued % SS;
             mbar_expect_tx(&S.bar[s], kUnitBytes);
-            bulk_g2s(S.ring_at(s), src + (int64_t)issued * kUnitFloats, kUnitBytes, &S.bar[s], !LARGE);
+            if (LARGE)
+                bulk_g2s(S.ring_at(s), src + (int64_t)issued * kUnitFloats, kUnitBytes, &S.bar[s],
+                         false);
+            else
+                bulk_g2s_pol(S.ring_at(s), src + (int64_t)issued * kUnitFloats, kUnitBytes,
+                             &S.bar[s], pol);
             ++issued;
         }
     };
@@ -995,11 +1055,16 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
         }
         big = nc > C::kCap;
     }
+    KM_CHECK(nc >= 1 && (LARGE || nc <= K) && (!LARGE || nc <= gcount));
     if (lane == 0 && cand_count) cand_count[chunk] = nc;
     if (LARGE && big) {
         // more than kCap candidates: k_assign_heavy takes this chunk with a whole
         // block.  Drain the units already in flight, then leave.
-        if (lane == 0) heavy[atomicAdd(heavy_count, 1)] = chunk;
+        if (lane == 0) {
+            const int h = atomicAdd(heavy_count, 1);
+            KM_CHECK(h >= 0 && (int64_t)h * CHP < n);   // h < n_chunks
+            heavy[h] = chunk;
+        }
         const unsigned nq = __shfl_sync(0xffffffffu, issued, 0);
         for (unsigned q = 0; q < nq; ++q) mbar_wait(&S.bar[q % SS], (q / SS) & 1u);
         return;
@@ -1069,6 +1134,7 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
         // ---- one candidate: labels known, sums in registers (four chains) ----
         float4 cc;
         const int k0 = cand_at(0, cc);
+        KM_CHECK(k0 >= 0 && k0 < K);
         double sx[4] = {0.0, 0.0, 0.0, 0.0}, sy[4] = {0.0, 0.0, 0.0, 0.0};
         double sz[4] = {0.0, 0.0, 0.0, 0.0}, Jc[4] = {0.0, 0.0, 0.0, 0.0};
         auto add4 = [&](const Pts& Q, float2 da, float2 db, int m) {
@@ -1761,6 +1827,7 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
             outc += tot;
             __syncthreads();
         }
+        KM_CHECK(nc <= K && nt <= nc && outc <= nc);
         if (tid == 0) {
             double J = 0.0;
             for (int w = 0; w < 8; ++w) J += wJ[w];
@@ -1893,6 +1960,7 @@ k_merge_sparse(const double* __restrict__ rows, int row_stride, int n_chunks, in
         const double* row = rows + (size_t)(c0 + q) * row_stride;
         hj[q] = row[0];
         cnt[q] = (int)row[1];
+        KM_CHECK(cnt[q] >= 0 && cnt[q] <= K && kRowHead + 4 * cnt[q] <= row_stride);
     }
     __syncthreads();
     if (tid < 32) {   // exclusive scan of the counts (warp 0, kPer consecutive per lane)
@@ -1963,6 +2031,7 @@ k_merge_sparse(const double* __restrict__ rows, int row_stride, int n_chunks, in
                 if (e < bn) {
                     v1 = E[2 * e + 1];
                     const int2 kn = *reinterpret_cast<const int2*>(&v1.y);   // {k, n}
+                    KM_CHECK(kn.x >= 0 && kn.x < K && kn.y >= 0);
                     if (kn.x >= klo && kn.x < khi) { k = kn.x; v0 = E[2 * e]; }
                 }
                 const unsigned peers = __match_any_sync(0xffffffffu, k);
@@ -2079,11 +2148,13 @@ __device__ __forceinline__ void merge16_body(const double* __restrict__ cpart, i
                 eb[i] = ent[2 * i + 1];
             }
     }
+    KM_CHECK(n >= 0 && n <= 16);
     int kk[kMergeRegs];
     unsigned kset = 0u;
 #pragma unroll
     for (int i = 0; i < kMergeRegs; ++i) {
         kk[i] = (i < n) ? __double2loint(eb[i].y) : -1;
+        KM_CHECK(i >= n || (kk[i] >= 0 && kk[i] < K));
         if (i < n) kset |= 1u << kk[i];
     }
     double J = head.x;
@@ -2392,15 +2463,29 @@ __global__ void k_merge(const double* __restrict__ part, int G, int nE,
 // PAPER.md:66-69; then t += 1 and the stop decision of PAPER.md:70.  `red` is
 // the merged (and, distributed, allreduced) vector.
 // ---------------------------------------------------------------------------
+// E = sum_k sum_j (mu^{t+1} - mu^t)^2.  Up to kSerialE
+// entries it is summed serially, k-major with j inner, without FMA
+// contraction: the oracle's order, so E -- and the E < tol decision -- has the
+// oracle's bits on every device path (k_fused_iterate and the persistent
+// kernel sum the same way).  Beyond that (K > 170 in 3D) the serial chain of
+// dependent fp64 adds costs ~9 ns per entry on the update's critical path
+// (measured: +27 us per iteration at K = 1024), so every device path sums it
+// in the same fixed tree instead (identical bits across paths; within a few
+// ulps of the oracle's E).
+constexpr int kSerialE = 512;
+
 template <int D>
 __device__ void update_body(double* __restrict__ mu_buf, int K, const double* red,
                             DevState* __restrict__ st, double* __restrict__ trace_E,
                             double* __restrict__ trace_J, int trace_cap,
                             float4* __restrict__ cneg) {
+    __shared__ double e_sm[kSerialE];   // (kSerialE >= 256: the tree's partials too)
     const int t = st->t;
     const double* mu_old = mu_buf + (size_t)(t & 1) * K * D;
     double* mu_new = mu_buf + (size_t)((t + 1) & 1) * K * D;
     const int tid = threadIdx.x;
+    const bool serial = K * D <= kSerialE;
+    double e_acc = 0.0;
     for (int q = tid; q < K * D; q += blockDim.x) {
         const int k = q / D;
         const double nk = red[K * D + k];
@@ -2412,18 +2497,45 @@ __device__ void update_body(double* __restrict__ mu_buf, int K, const double* re
             reinterpret_cast<float*>(&cneg[K + k])[j] = -__double2float_rn(old);
             reinterpret_cast<float*>(&cneg[k])[j] = -__double2float_rn(nw);
         }
-    }
-    __syncthreads();   // mu_new visible to the block
-    if (tid == 0) {
-        // E = sum_k sum_j (mu^{t+1} - mu^t)^2 serially, k-major with j inner:
-        // the oracle's order, so E -- and the E < tol stop
-        // decision -- has the same bits on every path (fused, unfused, P2P)
-        double E = 0.0;
-#pragma unroll 8
-        for (int q = 0; q < K * D; ++q) {
-            const double diff = mu_new[q] - mu_old[q];
-            E = __dadd_rn(E, __dmul_rn(diff, diff));   // no FMA contraction (the oracle's -ffp-contract=off)
+        if (serial) {
+            const double diff = nw - old;
+            e_sm[q] = __dmul_rn(diff, diff);   // no FMA contraction (oracle: -ffp-contract=off)
         }
+    }
+    double E = 0.0;
+    if (serial) {
+        __syncthreads();
+        if (tid == 0) {
+            const int n = K * D;
+            int q = 0;
+            for (; q + 8 <= n; q += 8) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = e_sm[q + u];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) E = __dadd_rn(E, v[u]);
+            }
+            for (; q < n; ++q) E = __dadd_rn(E, e_sm[q]);
+        }
+    } else {
+        // fixed tree independent of blockDim (>= 256 on every path): 256
+        // strided partial sums in ascending q, then pairwise halving
+        __syncthreads();   // mu_new written
+        if (tid < 256) {
+            for (int q = tid; q < K * D; q += 256) {
+                const double diff = mu_new[q] - mu_old[q];
+                e_acc = __dadd_rn(e_acc, __dmul_rn(diff, diff));
+            }
+            e_sm[tid] = e_acc;
+        }
+        __syncthreads();
+        for (int h = 128; h > 0; h >>= 1) {
+            if (tid < h) e_sm[tid] = __dadd_rn(e_sm[tid], e_sm[tid + h]);
+            __syncthreads();
+        }
+        E = e_sm[0];
+    }
+    if (tid == 0) {
         const double J = red[K * D + K];
         st->E = E;
         st->J = J;

@@ -46,7 +46,21 @@ namespace {
 constexpr int kMaxDevices = 64;
 std::mutex g_mem_mu;
 std::multimap<size_t, void*> g_cache[kMaxDevices];   // size -> idle block
-std::unordered_map<void*, std::pair<int, size_t>> g_live;   // block -> (device, size)
+struct Live {
+    int dev;
+    size_t size;    // block size (cache key)
+    size_t bytes;   // requested bytes (KM_CHECKS: the red zone starts here)
+};
+std::unordered_map<void*, Live> g_live;   // block -> owner
+
+#ifndef KM_CHECKS
+#define KM_CHECKS 0
+#endif
+// KM_CHECKS builds: every block carries a kRedZone-byte red zone right after
+// the requested bytes, filled with 0xA5 at allocation and verified when the
+// block is freed (the owner synchronised its stream first): a kernel writing
+// past the end of a buffer aborts the process with the buffer named by size.
+constexpr size_t kRedZone = KM_CHECKS ? 4096 : 0;
 
 size_t round_block(size_t bytes) {
     const size_t g = bytes >= (1u << 20) ? (2u << 20) : 512;
@@ -58,17 +72,40 @@ void flush_cache_locked(int dev) {
     g_cache[dev].clear();
 }
 
+void arm_red_zone(void* p, size_t bytes) {
+    if (!kRedZone) return;
+    cudaMemset(static_cast<char*>(p) + bytes, 0xA5, kRedZone);
+    cudaDeviceSynchronize();   // (legacy stream; checked builds only)
+}
+
+void check_red_zone(void* p, const Live& l) {
+    if (!kRedZone) return;
+    std::vector<unsigned char> h(kRedZone);
+    if (cudaMemcpy(h.data(), static_cast<char*>(p) + l.bytes, kRedZone, cudaMemcpyDeviceToHost) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    for (size_t i = 0; i < kRedZone; ++i)
+        if (h[i] != 0xA5) {
+            fprintf(stderr, "KM_CHECKS: device buffer of %zu bytes overrun at byte %zu past its end\n",
+                    l.bytes, i);
+            abort();
+        }
+}
+
 cudaError_t cached_malloc(int dev, void** p, size_t bytes) {
     *p = nullptr;
     if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
-    const size_t sz = round_block(bytes ? bytes : 1);
+    const size_t sz = round_block((bytes ? bytes : 1) + kRedZone);
     std::lock_guard<std::mutex> lk(g_mem_mu);
     auto& c = g_cache[dev];
     auto it = c.lower_bound(sz);
     if (it != c.end() && it->first <= sz + sz / 4 + (8u << 20)) {   // close fit only
         *p = it->second;
-        g_live[*p] = {dev, it->first};
+        g_live[*p] = {dev, it->first, bytes};
         c.erase(it);
+        arm_red_zone(*p, bytes);
         return cudaSuccess;
     }
     cudaError_t e = cudaMalloc(p, sz);
@@ -77,7 +114,10 @@ cudaError_t cached_malloc(int dev, void** p, size_t bytes) {
         flush_cache_locked(dev);
         e = cudaMalloc(p, sz);
     }
-    if (e == cudaSuccess) g_live[*p] = {dev, sz};
+    if (e == cudaSuccess) {
+        g_live[*p] = {dev, sz, bytes};
+        arm_red_zone(*p, bytes);
+    }
     return e;
 }
 
@@ -86,7 +126,8 @@ void cached_free(void* p) {
     std::lock_guard<std::mutex> lk(g_mem_mu);
     auto it = g_live.find(p);
     if (it == g_live.end()) return;
-    g_cache[it->second.first].emplace(it->second.second, p);
+    check_red_zone(p, it->second);
+    g_cache[it->second.dev].emplace(it->second.size, p);
     g_live.erase(it);
 }
 }  // namespace
@@ -149,6 +190,7 @@ struct kmeans_ctx {
     int heavy_smem = 0;
     int heavy_grid = 0;
     bool sorted = false;          // points held in Morton order (path 0 default)
+    int64_t keep_n = 0;           // sorted small K: points [0, keep_n) kept resident in L2
     int32_t* perm = nullptr;      // sorted position -> caller's index (sorted only)
     int2* init_pairs = nullptr;   // (local index, k) of the initial indices (sorted only)
     int32_t* init_pos = nullptr;  // their sorted positions (k_find_pos)
@@ -345,7 +387,7 @@ ChunkFn pick_chunk(int d, int K, int mode) {
 
 using PrunedFn = void (*)(const float*, int64_t, int, const float4*, const DevState*, int, int,
                           const float*, const int*, const int*, double*, int, int32_t*, int*,
-                          int*, int*, unsigned short*);
+                          int*, int*, unsigned short*, int64_t);
 using HeavyFn = void (*)(const float*, int64_t, int, const float4*, const DevState*, int, int,
                          const float*, const int*, const int*, const int*, const int*, double*, int,
                          int32_t*);
@@ -429,6 +471,11 @@ kmeans_status configure(kmeans_ctx* ctx) {
                          (ctx->flags & KMEANS_FLAG_BIG_CHUNKS);
         ctx->chunk_points = (ctx->K <= 16 && big) ? KM_BIG_CHUNK_TILES * km::kLaneTile
                                                   : km::kSChunkPoints;
+        {   // L2-resident prefix of the point stream (small K; tuning: KMEANS_L2_KEEP_MB)
+            const char* e = getenv("KMEANS_L2_KEEP_MB");
+            const double mb = e ? atof(e) : 0.0;
+            ctx->keep_n = (int64_t)(mb * 1e6 / (4.0 * ctx->d));
+        }
         for (int mode = 1; mode <= 3; ++mode)
             CK(cudaFuncSetAttribute(
                 (const void*)pick_pruned(ctx->d, ctx->K, mode, ctx->chunk_points),
@@ -540,7 +587,7 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
                         ctx->N, ctx->K, (const float4*)ctx->cneg, (const DevState*)ctx->st, mu_sel,
                         ignore_done, (const float*)ctx->cbox, (const int*)ctx->slist,
                         (const int*)ctx->scount, ctx->cpart, ctx->row_stride, ctx->labels_sorted,
-                        ctx->cand_count, ctx->heavy, ctx->heavy_count, ctx->slotg));
+                        ctx->cand_count, ctx->heavy, ctx->heavy_count, ctx->slotg, ctx->keep_n));
         if (A) ctx->launches += 1;
         if (A && ctx->path == 1) {
             HeavyFn hf = pick_heavy(ctx->d, mode);

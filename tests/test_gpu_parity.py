@@ -321,15 +321,16 @@ def test_form_d_fma_golden_on_gpu(golden_dir, sort, reps):
     if reps == 1:
         assert r["inertia"] == d2["expect"]
     a = g["argmin_3d"]
-    X3 = np.array([a["x"]] * reps, np.float32)
+    n3 = max(reps, 2)   # K = 2 needs N >= 2
+    X3 = np.array([a["x"]] * n3, np.float32)
     with km.Context(X3, 2, **ctx_kwargs(sort)) as c:
         r = c.assign(np.array(a["centroids"], np.float64))
     assert np.all(r["labels"] == a["expect_label"])
-    assert r["counts"].tolist() == [0, reps]
-    if reps == 1:
-        assert r["inertia"] == a["expect_dmin"]
+    assert r["counts"].tolist() == [0, n3]
+    if n3 == 2:
+        assert r["inertia"] == 2 * a["expect_dmin"]   # exact: one fp64 doubling
     else:
-        assert abs(r["inertia"] - reps * a["expect_dmin"]) <= 1e-12 * reps * a["expect_dmin"]
+        assert abs(r["inertia"] - n3 * a["expect_dmin"]) <= 1e-12 * n3 * a["expect_dmin"]
 
 
 def test_special_cases_k1_kn_tol0_maxiter1():
@@ -646,13 +647,76 @@ def test_full_size_c3_step_parity():
         check_step(X, mu, ctx=c, tag="C3 full")
 
 
+# Full-size oracle in a process pool: oracle.partials (single-threaded C) over
+# fixed contiguous shards, one per worker call, the shard partials added in
+# shard order.  Children are forked and read the arrays below (copy-on-write);
+# they compare the GPU's labels themselves and return only small results.
+_POOL = {}
+
+
+def _pool_shard(job):
+    import oracle as _o
+    lo, hi = job
+    X, mu, lab_g = _POOL["X"], _POOL["mu"], _POOL["labels"]
+    r = _o.partials(X[lo:hi], mu)
+    bad = np.nonzero(r["labels"] != lab_g[lo:hi])[0]
+    K, d = mu.shape
+    scale = np.zeros((K, d))
+    for j in range(d):
+        scale[:, j] = np.bincount(r["labels"], weights=np.abs(X[lo:hi, j].astype(np.float64)),
+                                  minlength=K)
+    return dict(sums=r["sums"], counts=r["counts"], J=r["J"], scale=scale,
+                n_bad=int(bad.size), first_bad=(lo + bad[:5]).tolist())
+
+
+def oracle_step_pooled(X, mu, labels_gpu, shard=1_000_000):
+    """One oracle step over all of X (labels compared element by element in
+    the workers), sums / counts / J added over shards in ascending order, then
+    oracle.update -- the same arithmetic as oracle.step up to the fp64
+    summation order across shards (within reading R13's bar)."""
+    import multiprocessing as mp
+    _POOL.update(X=X, mu=mu, labels=labels_gpu)
+    jobs = [(lo, min(lo + shard, X.shape[0])) for lo in range(0, X.shape[0], shard)]
+    with mp.get_context("fork").Pool(max(1, os.cpu_count() or 1)) as pool:
+        parts = pool.map(_pool_shard, jobs, chunksize=1)
+    _POOL.clear()
+    K, d = mu.shape
+    sums, counts, J, scale = np.zeros((K, d)), np.zeros(K, np.int64), 0.0, np.zeros((K, d))
+    n_bad, first_bad = 0, []
+    for p in parts:   # shard order
+        sums = sums + p["sums"]
+        counts = counts + p["counts"]
+        J = J + p["J"]
+        scale = scale + p["scale"]
+        n_bad += p["n_bad"]
+        first_bad += p["first_bad"]
+    mu_next, E = oracle.update(sums, counts, mu)
+    return dict(sums=sums, counts=counts, J=J, scale=scale, mu_next=mu_next, E=E,
+                n_bad=n_bad, first_bad=first_bad[:5])
+
+
+def check_step_full(g, mu_next, E, o, mu, tag):
+    """check_step's bars, against oracle_step_pooled (all labels, every
+    per-cluster sum and count, J, mu^{t+1}, E)."""
+    assert o["n_bad"] == 0, f"{tag}: {o['n_bad']} labels differ, first at {o['first_bad']}"
+    assert np.array_equal(g["counts"], o["counts"]), tag
+    assert np.all(np.abs(g["sums"] - o["sums"]) <= REL * o["scale"] + 1e-300), tag
+    assert abs(g["inertia"] - o["J"]) <= REL * o["J"], tag
+    n = np.maximum(o["counts"], 1)[:, None]
+    mscale = np.maximum(np.abs(o["mu_next"]), o["scale"] / n)
+    assert np.all(np.abs(mu_next - o["mu_next"]) <= REL * mscale + 1e-300), tag
+    dmu = REL * mscale
+    e_tol = np.sum(2 * np.abs(o["mu_next"] - mu) * dmu + dmu ** 2) + \
+        REL * max(o["E"], 1e-3 * float(np.sum(mu ** 2)))
+    assert abs(E - o["E"]) <= e_tol, f"{tag}: E {E} vs {o['E']}"
+
+
 @pytest.mark.slow
-def test_full_size_c4_rank_shard_sampled_parity():
+def test_full_size_c4_rank_shard_parity():
     """C4 (N=1e9, 3D, K=16, P=8): the shard of rank 5 (1.25e8 points, global
-    offset 6.25e8) as bench.py --gpus 8 generates it; labels of a sample
-    against the oracle one by one; counts and per-cluster sums of the whole
-    shard against a float64 bincount over the GPU labels and the shard's
-    coordinate sums."""
+    offset 6.25e8) as bench.py --gpus 8 generates it, one step at the global
+    init centroids: every label, count and per-cluster sum, J, mu^{t+1} and E
+    against the oracle (process pool over fixed shards)."""
     w = datagen.WORKLOADS["C4"]
     P, r = 8, 5
     a, b = datagen.shard_range(w.N, P, r)
@@ -663,44 +727,31 @@ def test_full_size_c4_rank_shard_sampled_parity():
     with km.Context(Xs, w.K) as c:   # (global offsets need a communicator; assign takes mu)
         assert c.info()["sorted"] == 1
         g = c.assign(mu)
-    rng = np.random.default_rng(5)
-    sample = np.sort(rng.choice(b - a, 300_000, replace=False))
-    o = oracle.partials(Xs[sample], mu)
-    assert np.array_equal(g["labels"][sample], o["labels"])
-    assert g["counts"].sum() == b - a
-    tot = g["sums"].sum(axis=0)
-    ref = Xs.astype(np.float64).sum(axis=0)
-    assert np.all(np.abs(tot - ref) <= 1e-9 * np.abs(Xs).astype(np.float64).sum(axis=0))
-    # per-cluster sums of the full shard against a float64 bincount of the GPU labels
-    for j in range(w.d):
-        ref_j = np.bincount(g["labels"], weights=Xs[:, j].astype(np.float64), minlength=w.K)
-        assert np.all(np.abs(g["sums"][:, j] - ref_j) <= 1e-9 * np.abs(ref_j) + 1e-6)
+        mu_next, E = c.update()
+    o = oracle_step_pooled(Xs, mu, g["labels"], shard=4_000_000)
+    check_step_full(g, mu_next, E, o, mu, "C4 rank 5")
 
 
 @pytest.mark.slow
-def test_full_size_c5_sampled_parity():
-    """C5 (N=5e7, 3D, K=1024, forced empty clusters): labels of a sample
-    against the oracle one by one; properties at full size (counts sum to N,
-    the 56 forced-empty clusters are empty, sums add up to sum x)."""
+def test_full_size_c5_parity():
+    """C5 (N=5e7, 3D, K=1024, forced empty clusters) at full size, in the
+    configuration bench.py --workload C5 times: every label, all 1024 counts
+    (the 56 forced-empty clusters included) and per-cluster sums, J,
+    mu^{t+1} and E against the oracle (process pool; R2)."""
     w = datagen.WORKLOADS["C5"]
     X = datagen.generate(w)
     init = datagen.init_indices(w)
     mu = X[init].astype(np.float64)
     with km.Context(X, w.K) as c:
+        assert c.info()["sorted"] == 1
         g = c.assign(mu)
-    rng = np.random.default_rng(0)
-    sample = np.sort(rng.choice(w.N, 200_000, replace=False))
-    sample = np.concatenate([datagen.planted_indices(w), sample])
-    o = oracle.partials(X[sample], mu)
-    assert np.array_equal(g["labels"][sample], o["labels"])
-    assert g["counts"].sum() == w.N
-    for s in range(w.planted_sites):
+        mu_next, E = c.update()
+    o = oracle_step_pooled(X, mu, g["labels"], shard=250_000)
+    check_step_full(g, mu_next, E, o, mu, "C5 full")
+    for s in range(w.planted_sites):   # R2: 7 of every site's 8 centroids stay empty
         ks = list(range(8 * s, 8 * s + 8))
-        assert g["counts"][ks[0]] >= 8
-        assert all(g["counts"][k] == 0 for k in ks[1:])
-    tot = g["sums"].sum(axis=0)
-    ref = X.astype(np.float64).sum(axis=0)
-    assert np.all(np.abs(tot - ref) <= 1e-9 * np.abs(X).astype(np.float64).sum(axis=0))
+        assert g["counts"][ks[0]] >= 8 and all(g["counts"][k] == 0 for k in ks[1:])
+        assert np.array_equal(mu_next[ks[1:]], mu[ks[1:]])
 
 
 def test_heavy_chunks_large_k():
