@@ -333,7 +333,8 @@ def main():
     barrier()
     # the dominant kernel alone, once right before the timed region (GPU warm);
     # again right after it (see below) -- the roofline uses the mean of the two
-    pre_assign = (None if info["fused"] else
+    one_kernel = bool(info["fused"] or info["persistent"])   # the iteration is one kernel
+    pre_assign = (None if one_kernel else
                   ctx.profile_stage(max(20, min(args.steps, 200)), 1, timed=True) / 1e3)
 
     e0 = torch.cuda.Event(enable_timing=True)
@@ -399,12 +400,17 @@ def main():
                     traffic=traffic, peak_source=f"148 SMs x 128 FP32 lanes x {sm_max_mhz:.0f} MHz",
                     hbm_frac=ach_gbs / hbm_gbs, **common)
 
-    if info["fused"]:
-        # small full-scan shard: the whole iteration is ONE kernel (k_fused_iterate,
-        # many iterations per cooperative launch) -- its time per iteration is the step
+    if one_kernel:
+        # the whole iteration is ONE kernel, many iterations per cooperative
+        # launch (k_fused_iterate: small full-scan shards; k_persist_iterate:
+        # the sorted small-K path) -- its time per iteration is the step
         t_assign = ms_per_step / 1e3
-        kname = "k_fused_iterate"
-        stage_ms = {"fused_iteration": ms_per_step}
+        kname = "k_fused_iterate" if info["fused"] else "k_persist_iterate"
+        stage_ms = {"iteration": ms_per_step}
+        if info["persistent"]:
+            # for reference: the multi-kernel path's assign kernel and row merge alone
+            stage_ms["k_assign_pruned_alone"] = time_assign(ctx) * 1e3
+            stage_ms["row_merge_alone"] = time_assign(ctx, 2) * 1e3
     else:
         post_assign = time_assign(ctx)
         # kernel time "around" the timed region: the mean of the measurements
@@ -506,9 +512,11 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "kernels_per_step": info["kernels_per_iter"],
             "clocks": clk,
-            "launch": {"grid": info["grid"], "block": info["block"],
-                       "smem_bytes": info["smem_bytes"], "path": info["path"],
-                       "sorted": info["sorted"]},
+            "launch": ({"grid": info["persist_grid"], "kernel": "k_persist_iterate",
+                        "sorted": 1, "persistent": 1} if info["persistent"] else
+                       {"grid": info["grid"], "block": info["block"],
+                        "smem_bytes": info["smem_bytes"], "path": info["path"],
+                        "sorted": info["sorted"]}),
         }
         print(json.dumps(line), flush=True)
     if distributed:

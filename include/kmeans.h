@@ -100,6 +100,13 @@ typedef struct kmeans_opts {
 #define KMEANS_FLAG_FORCE_SORT 2  /* always use the sorted (pruned) path */
 #define KMEANS_FLAG_BIG_CHUNKS 8  /* sorted path, K <= 16: 2048-point chunks at any N
                                      (default: from 4e7 points per shard) */
+#define KMEANS_FLAG_PERSIST 16    /* sorted path, K <= 16, shards of >= 256 x (SMs x warps per
+                                     block) points: run kmeans_iterate's iterations inside ONE
+                                     persistent kernel (k_persist_iterate: static unit ranges per
+                                     warp, block / grid last-arriver merges, update and P2P
+                                     exchange in the kernel, a device flag per iteration; SURVEY.md
+                                     NEXT-1) instead of the per-iteration kernel graph.  Opt-in:
+                                     measured slower than the graph */
 #define KMEANS_FLAG_NO_FUSED 4    /* full-scan path: never use the one-launch
                                      multi-iteration kernel (k_fused_iterate) that
                                      kmeans_iterate / kmeans_fit_ctx use for small
@@ -230,6 +237,8 @@ typedef struct kmeans_info {
     int sorted;             /* 1 = Morton-sorted shard with per-chunk pruning */
     int fused;              /* 1 = kmeans_iterate runs k_fused_iterate (grid = fused_grid) */
     int fused_grid;         /* its cooperative grid (blocks of 256 threads) */
+    int persistent;         /* 1 = kmeans_iterate runs k_persist_iterate (KMEANS_FLAG_PERSIST) */
+    int persist_grid;       /* its cooperative grid (one block per SM) */
 } kmeans_info;
 
 kmeans_status kmeans_get_info(kmeans_ctx* ctx, kmeans_info* info);

@@ -71,7 +71,7 @@ struct DevState {
     int err;        // kErrExchangeTimeout: a peer never published (the run stopped)
     int pad;
 };
-enum : int { kErrExchangeTimeout = 1 };
+enum : int { kErrExchangeTimeout = 1, kErrIterationTimeout = 2 };
 
 // Global nanosecond timer (bounded waits on peers).
 __device__ __forceinline__ uint64_t global_ns() {
@@ -886,6 +886,413 @@ __device__ __forceinline__ double pack_kn(int k, int n) {
     return __hiloint2double(n, k);
 }
 
+// A lane's 4 points of one 128-point warp-tile: a = (2L, 2L+1), b = (64+2L, 64+2L+1).
+struct LanePts {
+    float2 xa, ya, za, xb, yb, zb;
+};
+
+// Form D for two points at once (packed f32x2): e_j = x_j + (-c_j), s = e_0 e_0,
+// s = fma(e_j, e_j, s) -- reading R6.  cc = negated staged centroid.
+template <int D>
+__device__ __forceinline__ float2 form_d2(float2 x, float2 y, float2 z, const float4& cc) {
+    float2 e0 = __fadd2_rn(x, make_float2(cc.x, cc.x));
+    float2 e1 = __fadd2_rn(y, make_float2(cc.y, cc.y));
+    float2 sq = __fmul2_rn(e0, e0);
+    sq = __ffma2_rn(e1, e1, sq);
+    if (D == 3) {
+        float2 e2 = __fadd2_rn(z, make_float2(cc.z, cc.z));
+        sq = __ffma2_rn(e2, e2, sq);
+    }
+    return sq;
+}
+
+// Exact box bound of one centroid c against the box [lo, hi] (fp64): the min
+// and max squared distance from the box to c.
+template <int D>
+__device__ __forceinline__ void box_bounds(const float (&c)[3], const double (&lo)[3],
+                                           const double (&hi)[3], double& dmin2, double& dmax2) {
+    dmin2 = 0.0;
+    dmax2 = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        const double cj = (double)c[j];
+        const double dm = fmax(fmax(lo[j] - cj, cj - hi[j]), 0.0);
+        dmin2 += dm * dm;
+        const double dx = fmax(fabs(cj - lo[j]), fabs(hi[j] - cj));
+        dmax2 += dx * dx;
+    }
+}
+
+// Exclusion threshold from M = min_k dmax2_k: b is excluded when dmin2_b > thr.
+__device__ __forceinline__ double prune_threshold(double M) {
+    return (M > 1e37) ? (double)pos_inf() : M * (1.0 + 1e-5) + 0x1p-100;
+}
+
+// ---------------------------------------------------------------------------
+// small_chunk (sorted path, K <= 16): one warp, one chunk of points
+// [base, base + npts) streamed as nunit 256-point units by `fetch` (which waits
+// for unit u's TMA stage, loads the lane's points and refills the ring).  Lane
+// k tests centroid k against the chunk box (bx: lane j < 2D holds lo/hi of
+// axis j): the candidates; then the exact strict-< argmin over them (lowest k
+// on ties), form-D distances, and the fused fp64 sums / counts / inertia ->
+// the chunk's sparse row [J, count, entries {Sx, Sy, Sz, (k, n)}] (ascending
+// k).  Used by k_assign_pruned (one chunk per CTA) and k_persist_iterate.
+// ACC: instead of the row, lane 0 adds the chunk's entries to the warp's
+// dense table acc[4 k + {0, 1, 2, 3}] = {Sx, Sy, Sz, n}, acc[64] = J (shared
+// memory; chunks in the warp's fixed order) -- k_persist_iterate.
+// ---------------------------------------------------------------------------
+template <int D, int MODE, bool ACC = false, class Fetch>
+__device__ __forceinline__ void small_chunk(PrunedSmem<D, false>& S, int lane, int K, float4 cl,
+                                            float bx, int64_t base, int64_t n, int nunit,
+                                            int npts, double* __restrict__ row,
+                                            int32_t* __restrict__ labels, int* cand_slot,
+                                            Fetch&& fetch, double* acc = nullptr) {
+    const int64_t rem = n - base;
+    double lo[3], hi[3];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        lo[j] = (double)__shfl_sync(0xffffffffu, bx, j);
+        hi[j] = (double)__shfl_sync(0xffffffffu, bx, D + j);
+    }
+    int nc = 0;   // candidates
+    {
+        float c[3] = {0.f, 0.f, 0.f};
+        double dmin2 = 0.0, dmax2 = 0.0;
+        const bool is_k = lane < K;
+        if (is_k) {
+            c[0] = -cl.x;
+            c[1] = -cl.y;
+            c[2] = -cl.z;
+            box_bounds<D>(c, lo, hi, dmin2, dmax2);
+        }
+        double M = is_k ? dmax2 : (double)pos_inf();
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
+        const bool cand = is_k && dmin2 <= prune_threshold(M);
+        const unsigned mask = __ballot_sync(0xffffffffu, cand);
+        nc = __popc(mask);
+        if (cand) {
+            const int sl = __popc(mask & ((1u << lane) - 1u));
+            S.cand[sl] = make_float4(-c[0], -c[1], D == 3 ? -c[2] : 0.0f, 0.0f);
+            S.candk[sl] = lane;
+        }
+    }
+    KM_CHECK(nc >= 1 && nc <= K);
+    if (lane == 0 && cand_slot) *cand_slot = nc;
+    __syncwarp();
+    auto cand_at = [&](int j, float4& cc) -> int {   // candidate j: negated centroid, index
+        cc = S.cand[j];
+        return S.candk[j];
+    };
+
+    if (nc == 1) {
+        // ---- one candidate: labels known, sums in registers (four chains) ----
+        float4 cc;
+        const int k0 = cand_at(0, cc);
+        KM_CHECK(k0 >= 0 && k0 < K);
+        double sx[4] = {0.0, 0.0, 0.0, 0.0}, sy[4] = {0.0, 0.0, 0.0, 0.0};
+        double sz[4] = {0.0, 0.0, 0.0, 0.0}, Jc[4] = {0.0, 0.0, 0.0, 0.0};
+        auto add4 = [&](const LanePts& Q, float2 da, float2 db, int m) {
+            // m: bit mask of the valid points (a0, a1, b0, b1)
+            if (m & 1) { sx[0] += (double)Q.xa.x; sy[0] += (double)Q.ya.x; sz[0] += (double)Q.za.x; Jc[0] += (double)da.x; }
+            if (m & 2) { sx[1] += (double)Q.xa.y; sy[1] += (double)Q.ya.y; sz[1] += (double)Q.za.y; Jc[1] += (double)da.y; }
+            if (m & 4) { sx[2] += (double)Q.xb.x; sy[2] += (double)Q.yb.x; sz[2] += (double)Q.zb.x; Jc[2] += (double)db.x; }
+            if (m & 8) { sx[3] += (double)Q.xb.y; sy[3] += (double)Q.yb.y; sz[3] += (double)Q.zb.y; Jc[3] += (double)db.y; }
+        };
+#pragma unroll 1
+        for (int u = 0; u < nunit; ++u) {
+            LanePts P[kUnitSub];
+            fetch(u, P);
+#pragma unroll
+            for (int h = 0; h < kUnitSub; ++h) {
+                const float2 da = form_d2<D>(P[h].xa, P[h].ya, P[h].za, cc);
+                const float2 db = form_d2<D>(P[h].xb, P[h].yb, P[h].zb, cc);
+                const int64_t pa = base + (int64_t)u * kSortedUnit + h * kLaneTile + 2 * lane;
+                const int64_t pb = pa + kWarpTile;
+                if (MODE & kModeLabels) {
+                    *reinterpret_cast<int2*>(labels + pa) = make_int2(k0, k0);
+                    *reinterpret_cast<int2*>(labels + pb) = make_int2(k0, k0);
+                }
+                if (MODE & kModeReduce) {
+                    if ((int64_t)u * kSortedUnit + (h + 1) * kLaneTile <= rem)
+                        add4(P[h], da, db, 15);
+                    else
+                        add4(P[h], da, db, (pa < n ? 1 : 0) | (pa + 1 < n ? 2 : 0) |
+                                               (pb < n ? 4 : 0) | (pb + 1 < n ? 8 : 0));
+                }
+            }
+        }
+        if (!(MODE & kModeReduce)) return;
+        double sxt = (sx[0] + sx[1]) + (sx[2] + sx[3]);
+        double syt = (sy[0] + sy[1]) + (sy[2] + sy[3]);
+        double szt = (sz[0] + sz[1]) + (sz[2] + sz[3]);
+        double J = (Jc[0] + Jc[1]) + (Jc[2] + Jc[3]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            sxt += __shfl_xor_sync(0xffffffffu, sxt, o);
+            syt += __shfl_xor_sync(0xffffffffu, syt, o);
+            szt += __shfl_xor_sync(0xffffffffu, szt, o);
+            J += __shfl_xor_sync(0xffffffffu, J, o);
+        }
+        if (ACC) {
+            if (lane == 0) {
+                double* a = acc + 4 * k0;
+                a[0] += sxt;
+                a[1] += syt;
+                a[2] += szt;
+                a[3] += (double)npts;
+                acc[64] += J;
+            }
+        } else if (lane == 0) {   // sparse row: J, 1 entry {Sx, Sy, Sz, (k, n)}
+            row[0] = J;
+            row[1] = 1.0;
+            reinterpret_cast<double2*>(row + kRowHead)[0] = make_double2(sxt, syt);
+            reinterpret_cast<double2*>(row + kRowHead)[1] = make_double2(szt, pack_kn(k0, npts));
+        }
+        return;
+    }
+
+#if KM_TWO_CAND
+    if (nc == 2) {
+        // ---- two candidates (nearly every multi-candidate chunk at NS): the
+        // strict-< argmin of the pair (lowest k on ties: the list ascends in k),
+        // sums of both candidates in registers (selects; adding +0.0 leaves a
+        // sum unchanged), two chains (a- and b-points) ----
+        float4 c0, c1;
+        const int k0 = cand_at(0, c0), k1 = cand_at(1, c1);
+        double s0[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+        double s1[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+        double Jc[2] = {0.0, 0.0};
+        int n1[2] = {0, 0}, nv[2] = {0, 0};
+        auto add = [&](int ch, float px, float py, float pz, float d0, float d1) {
+            const bool w1 = d1 < d0;
+            const double x = (double)px, y = (double)py, z = (double)pz;
+            s0[ch][0] += w1 ? 0.0 : x;
+            s0[ch][1] += w1 ? 0.0 : y;
+            s1[ch][0] += w1 ? x : 0.0;
+            s1[ch][1] += w1 ? y : 0.0;
+            if (D == 3) {
+                s0[ch][2] += w1 ? 0.0 : z;
+                s1[ch][2] += w1 ? z : 0.0;
+            }
+            Jc[ch] += (double)(w1 ? d1 : d0);
+            n1[ch] += w1 ? 1 : 0;
+            nv[ch] += 1;
+        };
+#pragma unroll 1
+        for (int u = 0; u < nunit; ++u) {
+            LanePts P[kUnitSub];
+            fetch(u, P);
+#pragma unroll
+            for (int h = 0; h < kUnitSub; ++h) {
+                const float2 a0 = form_d2<D>(P[h].xa, P[h].ya, P[h].za, c0);
+                const float2 a1 = form_d2<D>(P[h].xa, P[h].ya, P[h].za, c1);
+                const float2 b0 = form_d2<D>(P[h].xb, P[h].yb, P[h].zb, c0);
+                const float2 b1 = form_d2<D>(P[h].xb, P[h].yb, P[h].zb, c1);
+                const int64_t pa = base + (int64_t)u * kSortedUnit + h * kLaneTile + 2 * lane;
+                const int64_t pb = pa + kWarpTile;
+                if (MODE & kModeLabels) {
+                    *reinterpret_cast<int2*>(labels + pa) =
+                        make_int2(a1.x < a0.x ? k1 : k0, a1.y < a0.y ? k1 : k0);
+                    *reinterpret_cast<int2*>(labels + pb) =
+                        make_int2(b1.x < b0.x ? k1 : k0, b1.y < b0.y ? k1 : k0);
+                }
+                if (MODE & kModeReduce) {
+                    if (pa < n) add(0, P[h].xa.x, P[h].ya.x, P[h].za.x, a0.x, a1.x);
+                    if (pa + 1 < n) add(0, P[h].xa.y, P[h].ya.y, P[h].za.y, a0.y, a1.y);
+                    if (pb < n) add(1, P[h].xb.x, P[h].yb.x, P[h].zb.x, b0.x, b1.x);
+                    if (pb + 1 < n) add(1, P[h].xb.y, P[h].yb.y, P[h].zb.y, b0.y, b1.y);
+                }
+            }
+        }
+        if (!(MODE & kModeReduce)) return;
+        double v[7] = {s0[0][0] + s0[1][0], s0[0][1] + s0[1][1], s0[0][2] + s0[1][2],
+                       s1[0][0] + s1[1][0], s1[0][1] + s1[1][1], s1[0][2] + s1[1][2],
+                       Jc[0] + Jc[1]};
+        int c1n = n1[0] + n1[1], cvn = nv[0] + nv[1];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+            for (int q = 0; q < 7; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+            c1n += __shfl_xor_sync(0xffffffffu, c1n, o);
+            cvn += __shfl_xor_sync(0xffffffffu, cvn, o);
+        }
+        if (ACC) {
+            if (lane == 0) {
+                double* a = acc + 4 * k0;
+                a[0] += v[0];
+                a[1] += v[1];
+                a[2] += v[2];
+                a[3] += (double)(cvn - c1n);
+                double* b = acc + 4 * k1;
+                b[0] += v[3];
+                b[1] += v[4];
+                b[2] += v[5];
+                b[3] += (double)c1n;
+                acc[64] += v[6];
+            }
+        } else if (lane == 0) {   // sparse row: J, 2 entries (ascending k)
+            row[0] = v[6];
+            row[1] = 2.0;
+            double2* e = reinterpret_cast<double2*>(row + kRowHead);
+            e[0] = make_double2(v[0], v[1]);
+            e[1] = make_double2(v[2], pack_kn(k0, cvn - c1n));
+            e[2] = make_double2(v[3], v[4]);
+            e[3] = make_double2(v[5], pack_kn(k1, c1n));
+        }
+        return;
+    }
+#endif
+
+    // ---- several candidates ----
+    const int ncand = nc;
+    // >= 3 candidates: one pass over the TMA ring; the points of a
+    // warp-tile are added to T[slot] by one fixed butterfly per slot
+    // present in the warp, counts by ballot
+    double* T = S.T;
+    for (int q = lane; q < 4 * ncand; q += 32) T[q] = 0.0;
+    __syncwarp();
+    double J = 0.0;
+    // the 4 points of a lane (a0, a1, b0, b1) at once: per slot present in
+    // the warp, each lane sums its points of that slot in that order, then
+    // one fixed butterfly over the lanes; counts by ballot
+    auto agg4 = [&](const bool (&v)[4], const int (&sl)[4], const float (&px)[4],
+                    const float (&py)[4], const float (&pz)[4]) {
+        unsigned mine_bits = 0u;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (v[i]) mine_bits |= 1u << sl[i];
+        unsigned pres = __reduce_or_sync(0xffffffffu, mine_bits);
+        while (pres) {
+            const int q = __ffs(pres) - 1;
+            pres &= pres - 1;
+            double sx = 0.0, sy = 0.0, sz = 0.0;
+            unsigned cnt = 0u;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const bool m = v[i] && sl[i] == q;
+                sx += m ? (double)px[i] : 0.0;
+                sy += m ? (double)py[i] : 0.0;
+                sz += m ? (double)pz[i] : 0.0;
+                cnt += __popc(__ballot_sync(0xffffffffu, m));
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                sx += __shfl_xor_sync(0xffffffffu, sx, o);
+                sy += __shfl_xor_sync(0xffffffffu, sy, o);
+                if (D == 3) sz += __shfl_xor_sync(0xffffffffu, sz, o);
+            }
+            if (lane == 0) {
+                double* t = T + 4 * q;
+                t[0] += sx;
+                t[1] += sy;
+                t[2] += sz;
+                t[3] += (double)cnt;
+            }
+        }
+        __syncwarp();
+    };
+#pragma unroll 1
+    for (int u = 0; u < nunit; ++u) {
+        LanePts P[kUnitSub];
+        fetch(u, P);
+#pragma unroll
+        for (int h = 0; h < kUnitSub; ++h) {
+            const int off = u * kSortedUnit + h * kLaneTile + 2 * lane;   // in-chunk index
+            const int64_t pa = base + off, pb = pa + kWarpTile;
+            float4 cc;
+            cand_at(0, cc);
+            float2 ba = form_d2<D>(P[h].xa, P[h].ya, P[h].za, cc);
+            float2 bb = form_d2<D>(P[h].xb, P[h].yb, P[h].zb, cc);
+            int s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+            int j = 1;
+#pragma unroll 1
+            for (; j + 1 < ncand; j += 2) {   // two candidates per step, ascending
+                float4 c2;
+                cand_at(j, cc);
+                cand_at(j + 1, c2);
+                const float2 da = form_d2<D>(P[h].xa, P[h].ya, P[h].za, cc);
+                const float2 db = form_d2<D>(P[h].xb, P[h].yb, P[h].zb, cc);
+                const float2 ea = form_d2<D>(P[h].xa, P[h].ya, P[h].za, c2);
+                const float2 eb = form_d2<D>(P[h].xb, P[h].yb, P[h].zb, c2);
+                if (da.x < ba.x) { ba.x = da.x; s0 = j; }
+                if (da.y < ba.y) { ba.y = da.y; s1 = j; }
+                if (db.x < bb.x) { bb.x = db.x; s2 = j; }
+                if (db.y < bb.y) { bb.y = db.y; s3 = j; }
+                if (ea.x < ba.x) { ba.x = ea.x; s0 = j + 1; }
+                if (ea.y < ba.y) { ba.y = ea.y; s1 = j + 1; }
+                if (eb.x < bb.x) { bb.x = eb.x; s2 = j + 1; }
+                if (eb.y < bb.y) { bb.y = eb.y; s3 = j + 1; }
+            }
+            if (j < ncand) {
+                cand_at(j, cc);
+                const float2 da = form_d2<D>(P[h].xa, P[h].ya, P[h].za, cc);
+                const float2 db = form_d2<D>(P[h].xb, P[h].yb, P[h].zb, cc);
+                if (da.x < ba.x) { ba.x = da.x; s0 = j; }
+                if (da.y < ba.y) { ba.y = da.y; s1 = j; }
+                if (db.x < bb.x) { bb.x = db.x; s2 = j; }
+                if (db.y < bb.y) { bb.y = db.y; s3 = j; }
+            }
+            if (MODE & kModeLabels) {
+                float4 t;
+                *reinterpret_cast<int2*>(labels + pa) = make_int2(cand_at(s0, t), cand_at(s1, t));
+                *reinterpret_cast<int2*>(labels + pb) = make_int2(cand_at(s2, t), cand_at(s3, t));
+            }
+            if (MODE & kModeReduce) {
+                if (pa < n) J += (double)ba.x;
+                if (pa + 1 < n) J += (double)ba.y;
+                if (pb < n) J += (double)bb.x;
+                if (pb + 1 < n) J += (double)bb.y;
+                const bool vv[4] = {pa < n, pa + 1 < n, pb < n, pb + 1 < n};
+                const int ss[4] = {s0, s1, s2, s3};
+                const float xx[4] = {P[h].xa.x, P[h].xa.y, P[h].xb.x, P[h].xb.y};
+                const float yy[4] = {P[h].ya.x, P[h].ya.y, P[h].yb.x, P[h].yb.y};
+                const float zz[4] = {P[h].za.x, P[h].za.y, P[h].zb.x, P[h].zb.y};
+                agg4(vv, ss, xx, yy, zz);
+            }
+        }
+    }
+    if (!(MODE & kModeReduce)) return;
+    if (ACC) {   // slots in ascending k order
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
+        if (lane == 0) {
+            for (int sl = 0; sl < ncand; ++sl) {
+                double* a = acc + 4 * S.candk[sl];
+                const double* t = T + 4 * sl;
+                a[0] += t[0];
+                a[1] += t[1];
+                a[2] += t[2];
+                a[3] += t[3];
+            }
+            acc[64] += J;
+        }
+        return;
+    }
+    // row entries in slot (= ascending k) order: lane -> (slot, half)
+    {
+        const int q = lane, sl = q >> 1;   // ncand <= 16: one pass of 32 lanes
+        if (sl < ncand) {
+            const double* t = T + 4 * sl;
+            reinterpret_cast<double2*>(row + kRowHead)[q] =
+                (q & 1) ? make_double2(t[2], pack_kn(S.candk[sl], (int)t[3]))
+                        : make_double2(t[0], t[1]);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
+    if (lane == 0) {
+        row[0] = J;
+        row[1] = (double)ncand;
+    }
+}
+
+// Small K: resident CTAs per SM the register budget is cut for (more CTAs =
+// more bytes in flight; measured: 28 best in 3D, 32 -- the per-SM block limit --
+// in 2D; a 64-register 3D kernel loses more to its two-candidate path)
+#ifndef KM_PRUNED_MINB
+#define KM_PRUNED_MINB (D == 2 ? 32 : 28)
+#endif
 // Small K: resident CTAs per SM the register budget is cut for (more CTAs =
 // more bytes in flight; measured: 28 best in 3D, 32 -- the per-SM block limit --
 // in 2D; a 64-register 3D kernel loses more to its two-candidate path)
@@ -963,118 +1370,8 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
         for (unsigned q = 0; q < (unsigned)min(SS, nunit); ++q) mbar_wait(&S.bar[q % SS], 0u);
         return;
     }
-
-    // ---- candidates of this chunk ----
-    double lo[3], hi[3];
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-        lo[j] = (double)__shfl_sync(0xffffffffu, bx, j);
-        hi[j] = (double)__shfl_sync(0xffffffffu, bx, D + j);
-    }
-    auto stage_c = [&](int k, float (&c)[3]) {   // staged fp32 centroid k
-        const float4 v = __ldg(&cneg[k]);
-        c[0] = -v.x;
-        c[1] = -v.y;
-        c[2] = -v.z;
-    };
-    auto bounds = [&](const float (&c)[3], double& dmin2, double& dmax2) {
-        dmin2 = 0.0;
-        dmax2 = 0.0;
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-            const double cj = (double)c[j];
-            const double dm = fmax(fmax(lo[j] - cj, cj - hi[j]), 0.0);
-            dmin2 += dm * dm;
-            const double dx = fmax(fabs(cj - lo[j]), fabs(hi[j] - cj));
-            dmax2 += dx * dx;
-        }
-    };
-    auto warp_min = [&](double v) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
-        return v;
-    };
-    auto threshold = [&](double M) {
-        return (M > 1e37) ? (double)pos_inf() : M * (1.0 + 1e-5) + 0x1p-100;
-    };
-    int nc = 0;          // refined candidates
-    bool big = false;    // candidates = the unrefined super list (global)
-    const int* glist = nullptr;
-    int gcount = 0;
-    if (!LARGE) {
-        float c[3] = {0.f, 0.f, 0.f};
-        double dmin2 = 0.0, dmax2 = 0.0;
-        const bool is_k = lane < K;
-        if (is_k) {
-            c[0] = -cl.x;
-            c[1] = -cl.y;
-            c[2] = -cl.z;
-            bounds(c, dmin2, dmax2);
-        }
-        const double thr = threshold(warp_min(is_k ? dmax2 : (double)pos_inf()));
-        const bool cand = is_k && dmin2 <= thr;
-        const unsigned mask = __ballot_sync(0xffffffffu, cand);
-        nc = __popc(mask);
-        if (cand) {
-            const int sl = __popc(mask & ((1u << lane) - 1u));
-            S.cand[sl] = make_float4(-c[0], -c[1], D == 3 ? -c[2] : 0.0f, 0.0f);
-            S.candk[sl] = lane;
-        }
-    } else {
-        const int sup = chunk / kSuperChunks;
-        glist = slist + (size_t)sup * K;
-        gcount = sup_count;
-        double M = (double)pos_inf();
-        for (int i = lane; i < gcount; i += 32) {
-            float c[3];
-            stage_c(__ldg(&glist[i]), c);
-            double a, b;
-            bounds(c, a, b);
-            M = fmin(M, b);
-        }
-        const double thr = threshold(warp_min(M));
-        for (int i0 = 0; i0 < gcount; i0 += 32) {
-            const int i = i0 + lane;
-            float c[3] = {0.f, 0.f, 0.f};
-            int k = 0;
-            bool cand = false;
-            if (i < gcount) {
-                k = __ldg(&glist[i]);
-                stage_c(k, c);
-                double a, b;
-                bounds(c, a, b);
-                cand = a <= thr;
-            }
-            const unsigned mask = __ballot_sync(0xffffffffu, cand);
-            const int sl = nc + __popc(mask & ((1u << lane) - 1u));
-            if (cand && sl < C::kCap) {
-                S.cand[sl] = make_float4(-c[0], -c[1], D == 3 ? -c[2] : 0.0f, 0.0f);
-                S.candk[sl] = k;
-            }
-            nc += __popc(mask);
-        }
-        big = nc > C::kCap;
-    }
-    KM_CHECK(nc >= 1 && (LARGE || nc <= K) && (!LARGE || nc <= gcount));
-    if (lane == 0 && cand_count) cand_count[chunk] = nc;
-    if (LARGE && big) {
-        // more than kCap candidates: k_assign_heavy takes this chunk with a whole
-        // block.  Drain the units already in flight, then leave.
-        if (lane == 0) {
-            const int h = atomicAdd(heavy_count, 1);
-            KM_CHECK(h >= 0 && (int64_t)h * CHP < n);   // h < n_chunks
-            heavy[h] = chunk;
-        }
-        const unsigned nq = __shfl_sync(0xffffffffu, issued, 0);
-        for (unsigned q = 0; q < nq; ++q) mbar_wait(&S.bar[q % SS], (q / SS) & 1u);
-        return;
-    }
-    __syncwarp();
-
-    struct Pts {
-        float2 xa, ya, za, xb, yb, zb;
-    };
-    auto fetch = [&](unsigned q, Pts (&P)[kUnitSub]) {
+    // a lane's points of unit q (waits for its stage, then refills the ring)
+    auto fetch = [&](unsigned q, LanePts (&P)[kUnitSub]) {
         const int s = q % SS;
         mbar_wait(&S.bar[s], (q / SS) & 1u);
 #pragma unroll
@@ -1093,298 +1390,330 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
         __syncwarp();
         issue_upto(q + SS);
     };
-    // the same points from global memory (passes > 0; L2-resident by then)
-    auto reload = [&](int u, Pts (&P)[kUnitSub]) {
-#pragma unroll
-        for (int h = 0; h < kUnitSub; ++h) {
-            const int64_t pa = base + (int64_t)u * kSortedUnit + h * kLaneTile + 2 * lane;
-            P[h].xa = ld_stream2(tile_coord<D>(X, pa, 0));
-            P[h].ya = ld_stream2(tile_coord<D>(X, pa, 1));
-            P[h].za = (D == 3) ? ld_stream2(tile_coord<D>(X, pa, 2)) : make_float2(0.f, 0.f);
-            P[h].xb = ld_stream2(tile_coord<D>(X, pa + kWarpTile, 0));
-            P[h].yb = ld_stream2(tile_coord<D>(X, pa + kWarpTile, 1));
-            P[h].zb = (D == 3) ? ld_stream2(tile_coord<D>(X, pa + kWarpTile, 2))
-                               : make_float2(0.f, 0.f);
-        }
-    };
-    auto dist2 = [&](float2 x, float2 y, float2 z, const float4& cc) {
-        float2 e0 = __fadd2_rn(x, make_float2(cc.x, cc.x));
-        float2 e1 = __fadd2_rn(y, make_float2(cc.y, cc.y));
-        float2 sq = __fmul2_rn(e0, e0);
-        sq = __ffma2_rn(e1, e1, sq);
-        if (D == 3) {
-            float2 e2 = __fadd2_rn(z, make_float2(cc.z, cc.z));
-            sq = __ffma2_rn(e2, e2, sq);
-        }
-        return sq;
-    };
-    // candidate j as a negated fp32 centroid and its index
-    auto cand_at = [&](int j, float4& cc) -> int {
-        if (!LARGE || !big) {
-            cc = S.cand[j];
-            return S.candk[j];
-        }
-        const int k = __ldg(&glist[j]);
-        cc = __ldg(&cneg[k]);
-        return k;
-    };
-    double* row = rows + (size_t)chunk * row_stride;
-
-    if (nc == 1) {
-        // ---- one candidate: labels known, sums in registers (four chains) ----
-        float4 cc;
-        const int k0 = cand_at(0, cc);
-        KM_CHECK(k0 >= 0 && k0 < K);
-        double sx[4] = {0.0, 0.0, 0.0, 0.0}, sy[4] = {0.0, 0.0, 0.0, 0.0};
-        double sz[4] = {0.0, 0.0, 0.0, 0.0}, Jc[4] = {0.0, 0.0, 0.0, 0.0};
-        auto add4 = [&](const Pts& Q, float2 da, float2 db, int m) {
-            // m: bit mask of the valid points (a0, a1, b0, b1)
-            if (m & 1) { sx[0] += (double)Q.xa.x; sy[0] += (double)Q.ya.x; sz[0] += (double)Q.za.x; Jc[0] += (double)da.x; }
-            if (m & 2) { sx[1] += (double)Q.xa.y; sy[1] += (double)Q.ya.y; sz[1] += (double)Q.za.y; Jc[1] += (double)da.y; }
-            if (m & 4) { sx[2] += (double)Q.xb.x; sy[2] += (double)Q.yb.x; sz[2] += (double)Q.zb.x; Jc[2] += (double)db.x; }
-            if (m & 8) { sx[3] += (double)Q.xb.y; sy[3] += (double)Q.yb.y; sz[3] += (double)Q.zb.y; Jc[3] += (double)db.y; }
-        };
-#pragma unroll 1
-        for (int u = 0; u < nunit; ++u) {
-            Pts P[kUnitSub];
-            fetch(u, P);
-#pragma unroll
-            for (int h = 0; h < kUnitSub; ++h) {
-                const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
-                const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
-                const int64_t pa = base + (int64_t)u * kSortedUnit + h * kLaneTile + 2 * lane;
-                const int64_t pb = pa + kWarpTile;
-                if (MODE & kModeLabels) {
-                    *reinterpret_cast<int2*>(labels + pa) = make_int2(k0, k0);
-                    *reinterpret_cast<int2*>(labels + pb) = make_int2(k0, k0);
-                }
-                if (MODE & kModeReduce) {
-                    if ((int64_t)u * kSortedUnit + (h + 1) * kLaneTile <= rem)
-                        add4(P[h], da, db, 15);
-                    else
-                        add4(P[h], da, db, (pa < n ? 1 : 0) | (pa + 1 < n ? 2 : 0) |
-                                               (pb < n ? 4 : 0) | (pb + 1 < n ? 8 : 0));
-                }
-            }
-        }
-        if (!(MODE & kModeReduce)) return;
-        double sxt = (sx[0] + sx[1]) + (sx[2] + sx[3]);
-        double syt = (sy[0] + sy[1]) + (sy[2] + sy[3]);
-        double szt = (sz[0] + sz[1]) + (sz[2] + sz[3]);
-        double J = (Jc[0] + Jc[1]) + (Jc[2] + Jc[3]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            sxt += __shfl_xor_sync(0xffffffffu, sxt, o);
-            syt += __shfl_xor_sync(0xffffffffu, syt, o);
-            szt += __shfl_xor_sync(0xffffffffu, szt, o);
-            J += __shfl_xor_sync(0xffffffffu, J, o);
-        }
-        if (lane == 0) {   // sparse row: J, 1 entry {Sx, Sy, Sz, (k, n)}
-            row[0] = J;
-            row[1] = 1.0;
-            reinterpret_cast<double2*>(row + kRowHead)[0] = make_double2(sxt, syt);
-            reinterpret_cast<double2*>(row + kRowHead)[1] = make_double2(szt, pack_kn(k0, npts));
-        }
-        return;
-    }
-
-#if KM_TWO_CAND
-    if (!LARGE && nc == 2) {
-        // ---- two candidates (nearly every multi-candidate chunk at NS): the
-        // strict-< argmin of the pair (lowest k on ties: the list ascends in k),
-        // sums of both candidates in registers (selects; adding +0.0 leaves a
-        // sum unchanged), two chains (a- and b-points) ----
-        float4 c0, c1;
-        const int k0 = cand_at(0, c0), k1 = cand_at(1, c1);
-        double s0[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
-        double s1[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
-        double Jc[2] = {0.0, 0.0};
-        int n1[2] = {0, 0}, nv[2] = {0, 0};
-        auto add = [&](int ch, float px, float py, float pz, float d0, float d1) {
-            const bool w1 = d1 < d0;
-            const double x = (double)px, y = (double)py, z = (double)pz;
-            s0[ch][0] += w1 ? 0.0 : x;
-            s0[ch][1] += w1 ? 0.0 : y;
-            s1[ch][0] += w1 ? x : 0.0;
-            s1[ch][1] += w1 ? y : 0.0;
-            if (D == 3) {
-                s0[ch][2] += w1 ? 0.0 : z;
-                s1[ch][2] += w1 ? z : 0.0;
-            }
-            Jc[ch] += (double)(w1 ? d1 : d0);
-            n1[ch] += w1 ? 1 : 0;
-            nv[ch] += 1;
-        };
-#pragma unroll 1
-        for (int u = 0; u < nunit; ++u) {
-            Pts P[kUnitSub];
-            fetch(u, P);
-#pragma unroll
-            for (int h = 0; h < kUnitSub; ++h) {
-                const float2 a0 = dist2(P[h].xa, P[h].ya, P[h].za, c0);
-                const float2 a1 = dist2(P[h].xa, P[h].ya, P[h].za, c1);
-                const float2 b0 = dist2(P[h].xb, P[h].yb, P[h].zb, c0);
-                const float2 b1 = dist2(P[h].xb, P[h].yb, P[h].zb, c1);
-                const int64_t pa = base + (int64_t)u * kSortedUnit + h * kLaneTile + 2 * lane;
-                const int64_t pb = pa + kWarpTile;
-                if (MODE & kModeLabels) {
-                    *reinterpret_cast<int2*>(labels + pa) =
-                        make_int2(a1.x < a0.x ? k1 : k0, a1.y < a0.y ? k1 : k0);
-                    *reinterpret_cast<int2*>(labels + pb) =
-                        make_int2(b1.x < b0.x ? k1 : k0, b1.y < b0.y ? k1 : k0);
-                }
-                if (MODE & kModeReduce) {
-                    if (pa < n) add(0, P[h].xa.x, P[h].ya.x, P[h].za.x, a0.x, a1.x);
-                    if (pa + 1 < n) add(0, P[h].xa.y, P[h].ya.y, P[h].za.y, a0.y, a1.y);
-                    if (pb < n) add(1, P[h].xb.x, P[h].yb.x, P[h].zb.x, b0.x, b1.x);
-                    if (pb + 1 < n) add(1, P[h].xb.y, P[h].yb.y, P[h].zb.y, b0.y, b1.y);
-                }
-            }
-        }
-        if (!(MODE & kModeReduce)) return;
-        double v[7] = {s0[0][0] + s0[1][0], s0[0][1] + s0[1][1], s0[0][2] + s0[1][2],
-                       s1[0][0] + s1[1][0], s1[0][1] + s1[1][1], s1[0][2] + s1[1][2],
-                       Jc[0] + Jc[1]};
-        int c1n = n1[0] + n1[1], cvn = nv[0] + nv[1];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-            for (int q = 0; q < 7; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
-            c1n += __shfl_xor_sync(0xffffffffu, c1n, o);
-            cvn += __shfl_xor_sync(0xffffffffu, cvn, o);
-        }
-        if (lane == 0) {   // sparse row: J, 2 entries (ascending k)
-            row[0] = v[6];
-            row[1] = 2.0;
-            double2* e = reinterpret_cast<double2*>(row + kRowHead);
-            e[0] = make_double2(v[0], v[1]);
-            e[1] = make_double2(v[2], pack_kn(k0, cvn - c1n));
-            e[2] = make_double2(v[3], v[4]);
-            e[3] = make_double2(v[5], pack_kn(k1, c1n));
-        }
-        return;
-    }
-#endif
-
-    // ---- several candidates ----
-    const int ncand = big ? gcount : nc;   // slots = indices into the candidate list
     if constexpr (!LARGE) {
-        // small K, >= 3 candidates: one pass over the TMA ring; the points of a
-        // warp-tile are added to T[slot] by one fixed butterfly per slot
-        // present in the warp, counts by ballot
-        double* T = S.T;
-        for (int q = lane; q < 4 * ncand; q += 32) T[q] = 0.0;
+        small_chunk<D, MODE>(S, lane, K, cl, bx, base, n, nunit, npts,
+                             rows + (size_t)chunk * row_stride, labels,
+                             cand_count ? cand_count + chunk : nullptr, fetch);
+        return;
+    } else {
+
+        // ---- candidates of this chunk ----
+        double lo[3], hi[3];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            lo[j] = (double)__shfl_sync(0xffffffffu, bx, j);
+            hi[j] = (double)__shfl_sync(0xffffffffu, bx, D + j);
+        }
+        auto stage_c = [&](int k, float (&c)[3]) {   // staged fp32 centroid k
+            const float4 v = __ldg(&cneg[k]);
+            c[0] = -v.x;
+            c[1] = -v.y;
+            c[2] = -v.z;
+        };
+        auto bounds = [&](const float (&c)[3], double& dmin2, double& dmax2) {
+            dmin2 = 0.0;
+            dmax2 = 0.0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                const double cj = (double)c[j];
+                const double dm = fmax(fmax(lo[j] - cj, cj - hi[j]), 0.0);
+                dmin2 += dm * dm;
+                const double dx = fmax(fabs(cj - lo[j]), fabs(hi[j] - cj));
+                dmax2 += dx * dx;
+            }
+        };
+        auto warp_min = [&](double v) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+            return v;
+        };
+        auto threshold = [&](double M) {
+            return (M > 1e37) ? (double)pos_inf() : M * (1.0 + 1e-5) + 0x1p-100;
+        };
+        int nc = 0;          // refined candidates
+        bool big = false;    // candidates = the unrefined super list (global)
+        const int* glist = nullptr;
+        int gcount = 0;
+        {
+            const int sup = chunk / kSuperChunks;
+            glist = slist + (size_t)sup * K;
+            gcount = sup_count;
+            double M = (double)pos_inf();
+            for (int i = lane; i < gcount; i += 32) {
+                float c[3];
+                stage_c(__ldg(&glist[i]), c);
+                double a, b;
+                bounds(c, a, b);
+                M = fmin(M, b);
+            }
+            const double thr = threshold(warp_min(M));
+            for (int i0 = 0; i0 < gcount; i0 += 32) {
+                const int i = i0 + lane;
+                float c[3] = {0.f, 0.f, 0.f};
+                int k = 0;
+                bool cand = false;
+                if (i < gcount) {
+                    k = __ldg(&glist[i]);
+                    stage_c(k, c);
+                    double a, b;
+                    bounds(c, a, b);
+                    cand = a <= thr;
+                }
+                const unsigned mask = __ballot_sync(0xffffffffu, cand);
+                const int sl = nc + __popc(mask & ((1u << lane) - 1u));
+                if (cand && sl < C::kCap) {
+                    S.cand[sl] = make_float4(-c[0], -c[1], D == 3 ? -c[2] : 0.0f, 0.0f);
+                    S.candk[sl] = k;
+                }
+                nc += __popc(mask);
+            }
+            big = nc > C::kCap;
+        }
+        KM_CHECK(nc >= 1 && (LARGE || nc <= K) && (!LARGE || nc <= gcount));
+        if (lane == 0 && cand_count) cand_count[chunk] = nc;
+        if (LARGE && big) {
+            // more than kCap candidates: k_assign_heavy takes this chunk with a whole
+            // block.  Drain the units already in flight, then leave.
+            if (lane == 0) {
+                const int h = atomicAdd(heavy_count, 1);
+                KM_CHECK(h >= 0 && (int64_t)h * CHP < n);   // h < n_chunks
+                heavy[h] = chunk;
+            }
+            const unsigned nq = __shfl_sync(0xffffffffu, issued, 0);
+            for (unsigned q = 0; q < nq; ++q) mbar_wait(&S.bar[q % SS], (q / SS) & 1u);
+            return;
+        }
         __syncwarp();
+
+        // the same points from global memory (passes > 0; L2-resident by then)
+        auto reload = [&](int u, LanePts (&P)[kUnitSub]) {
+#pragma unroll
+            for (int h = 0; h < kUnitSub; ++h) {
+                const int64_t pa = base + (int64_t)u * kSortedUnit + h * kLaneTile + 2 * lane;
+                P[h].xa = ld_stream2(tile_coord<D>(X, pa, 0));
+                P[h].ya = ld_stream2(tile_coord<D>(X, pa, 1));
+                P[h].za = (D == 3) ? ld_stream2(tile_coord<D>(X, pa, 2)) : make_float2(0.f, 0.f);
+                P[h].xb = ld_stream2(tile_coord<D>(X, pa + kWarpTile, 0));
+                P[h].yb = ld_stream2(tile_coord<D>(X, pa + kWarpTile, 1));
+                P[h].zb = (D == 3) ? ld_stream2(tile_coord<D>(X, pa + kWarpTile, 2))
+                                   : make_float2(0.f, 0.f);
+            }
+        };
+        auto dist2 = [&](float2 x, float2 y, float2 z, const float4& cc) {
+            float2 e0 = __fadd2_rn(x, make_float2(cc.x, cc.x));
+            float2 e1 = __fadd2_rn(y, make_float2(cc.y, cc.y));
+            float2 sq = __fmul2_rn(e0, e0);
+            sq = __ffma2_rn(e1, e1, sq);
+            if (D == 3) {
+                float2 e2 = __fadd2_rn(z, make_float2(cc.z, cc.z));
+                sq = __ffma2_rn(e2, e2, sq);
+            }
+            return sq;
+        };
+        // candidate j as a negated fp32 centroid and its index
+        auto cand_at = [&](int j, float4& cc) -> int {
+            if (!LARGE || !big) {
+                cc = S.cand[j];
+                return S.candk[j];
+            }
+            const int k = __ldg(&glist[j]);
+            cc = __ldg(&cneg[k]);
+            return k;
+        };
+        double* row = rows + (size_t)chunk * row_stride;
+
+        if (nc == 1) {
+            // ---- one candidate: labels known, sums in registers (four chains) ----
+            float4 cc;
+            const int k0 = cand_at(0, cc);
+            KM_CHECK(k0 >= 0 && k0 < K);
+            double sx[4] = {0.0, 0.0, 0.0, 0.0}, sy[4] = {0.0, 0.0, 0.0, 0.0};
+            double sz[4] = {0.0, 0.0, 0.0, 0.0}, Jc[4] = {0.0, 0.0, 0.0, 0.0};
+            auto add4 = [&](const LanePts& Q, float2 da, float2 db, int m) {
+                // m: bit mask of the valid points (a0, a1, b0, b1)
+                if (m & 1) { sx[0] += (double)Q.xa.x; sy[0] += (double)Q.ya.x; sz[0] += (double)Q.za.x; Jc[0] += (double)da.x; }
+                if (m & 2) { sx[1] += (double)Q.xa.y; sy[1] += (double)Q.ya.y; sz[1] += (double)Q.za.y; Jc[1] += (double)da.y; }
+                if (m & 4) { sx[2] += (double)Q.xb.x; sy[2] += (double)Q.yb.x; sz[2] += (double)Q.zb.x; Jc[2] += (double)db.x; }
+                if (m & 8) { sx[3] += (double)Q.xb.y; sy[3] += (double)Q.yb.y; sz[3] += (double)Q.zb.y; Jc[3] += (double)db.y; }
+            };
+#pragma unroll 1
+            for (int u = 0; u < nunit; ++u) {
+                LanePts P[kUnitSub];
+                fetch(u, P);
+#pragma unroll
+                for (int h = 0; h < kUnitSub; ++h) {
+                    const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
+                    const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
+                    const int64_t pa = base + (int64_t)u * kSortedUnit + h * kLaneTile + 2 * lane;
+                    const int64_t pb = pa + kWarpTile;
+                    if (MODE & kModeLabels) {
+                        *reinterpret_cast<int2*>(labels + pa) = make_int2(k0, k0);
+                        *reinterpret_cast<int2*>(labels + pb) = make_int2(k0, k0);
+                    }
+                    if (MODE & kModeReduce) {
+                        if ((int64_t)u * kSortedUnit + (h + 1) * kLaneTile <= rem)
+                            add4(P[h], da, db, 15);
+                        else
+                            add4(P[h], da, db, (pa < n ? 1 : 0) | (pa + 1 < n ? 2 : 0) |
+                                                   (pb < n ? 4 : 0) | (pb + 1 < n ? 8 : 0));
+                    }
+                }
+            }
+            if (!(MODE & kModeReduce)) return;
+            double sxt = (sx[0] + sx[1]) + (sx[2] + sx[3]);
+            double syt = (sy[0] + sy[1]) + (sy[2] + sy[3]);
+            double szt = (sz[0] + sz[1]) + (sz[2] + sz[3]);
+            double J = (Jc[0] + Jc[1]) + (Jc[2] + Jc[3]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                sxt += __shfl_xor_sync(0xffffffffu, sxt, o);
+                syt += __shfl_xor_sync(0xffffffffu, syt, o);
+                szt += __shfl_xor_sync(0xffffffffu, szt, o);
+                J += __shfl_xor_sync(0xffffffffu, J, o);
+            }
+            if (lane == 0) {   // sparse row: J, 1 entry {Sx, Sy, Sz, (k, n)}
+                row[0] = J;
+                row[1] = 1.0;
+                reinterpret_cast<double2*>(row + kRowHead)[0] = make_double2(sxt, syt);
+                reinterpret_cast<double2*>(row + kRowHead)[1] = make_double2(szt, pack_kn(k0, npts));
+            }
+            return;
+        }
+
+        // ---- several candidates ----
+        const int ncand = big ? gcount : nc;   // slots = indices into the candidate list
+        {
         double J = 0.0;
-        // the 4 points of a lane (a0, a1, b0, b1) at once: per slot present in
-        // the warp, each lane sums its points of that slot in that order, then
-        // one fixed butterfly over the lanes; counts by ballot
-        auto agg4 = [&](const bool (&v)[4], const int (&sl)[4], const float (&px)[4],
-                        const float (&py)[4], const float (&pz)[4]) {
-            unsigned mine_bits = 0u;
+        auto accumulate = [&](int l, float px, float py, float pz) {
+            double2 a = S.col_a(l)[lane], b = S.col_b(l)[lane];
+            a.x += (double)px;
+            a.y += (double)py;
+            if (D == 3) b.x += (double)pz;
+            int2 c = *reinterpret_cast<int2*>(&b.y);
+            c.x += 1;
+            b.y = *reinterpret_cast<double*>(&c);
+            S.col_a(l)[lane] = a;
+            S.col_b(l)[lane] = b;
+        };
+        const int npass = (MODE & kModeReduce) ? (ncand + C::kSlots - 1) / C::kSlots : 1;
+#pragma unroll 1
+        for (int pass = 0; pass < npass; ++pass) {
+            const int s_lo = pass * C::kSlots;
+            if (MODE & kModeReduce) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-                if (v[i]) mine_bits |= 1u << sl[i];
-            unsigned pres = __reduce_or_sync(0xffffffffu, mine_bits);
-            while (pres) {
-                const int q = __ffs(pres) - 1;
-                pres &= pres - 1;
-                double sx = 0.0, sy = 0.0, sz = 0.0;
-                unsigned cnt = 0u;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const bool m = v[i] && sl[i] == q;
-                    sx += m ? (double)px[i] : 0.0;
-                    sy += m ? (double)py[i] : 0.0;
-                    sz += m ? (double)pz[i] : 0.0;
-                    cnt += __popc(__ballot_sync(0xffffffffu, m));
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    sx += __shfl_xor_sync(0xffffffffu, sx, o);
-                    sy += __shfl_xor_sync(0xffffffffu, sy, o);
-                    if (D == 3) sz += __shfl_xor_sync(0xffffffffu, sz, o);
-                }
-                if (lane == 0) {
-                    double* t = T + 4 * q;
-                    t[0] += sx;
-                    t[1] += sy;
-                    t[2] += sz;
-                    t[3] += (double)cnt;
+                for (int k = 0; k < C::kSlots; ++k) {
+                    S.col_a(k)[lane] = make_double2(0.0, 0.0);
+                    S.col_b(k)[lane] = make_double2(0.0, 0.0);
                 }
             }
             __syncwarp();
-        };
 #pragma unroll 1
-        for (int u = 0; u < nunit; ++u) {
-            Pts P[kUnitSub];
-            fetch(u, P);
+            for (int u = 0; u < nunit; ++u) {
+                LanePts P[kUnitSub];
+                if (pass == 0 && LARGE) fetch(u, P);
+                else reload(u, P);
 #pragma unroll
-            for (int h = 0; h < kUnitSub; ++h) {
-                const int off = u * kSortedUnit + h * kLaneTile + 2 * lane;   // in-chunk index
-                const int64_t pa = base + off, pb = pa + kWarpTile;
-                float4 cc;
-                cand_at(0, cc);
-                float2 ba = dist2(P[h].xa, P[h].ya, P[h].za, cc);
-                float2 bb = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
-                int s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-                int j = 1;
+                for (int h = 0; h < kUnitSub; ++h) {
+                    const int off = u * kSortedUnit + h * kLaneTile + 2 * lane;   // in-chunk index
+                    const int64_t pa = base + off, pb = pa + kWarpTile;
+                    int s0, s1, s2, s3;
+                    float2 ba, bb;
+                    if (pass == 0 || !LARGE) {
+                        float4 cc;
+                        cand_at(0, cc);
+                        ba = dist2(P[h].xa, P[h].ya, P[h].za, cc);
+                        bb = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
+                        s0 = s1 = s2 = s3 = 0;
+                        int j = 1;
+#if KM_CAND_UNROLL2
+                        // two candidates per step (independent distance chains), the
+                        // strict-< updates still in ascending j
 #pragma unroll 1
-                for (; j + 1 < ncand; j += 2) {   // two candidates per step, ascending
-                    float4 c2;
-                    cand_at(j, cc);
-                    cand_at(j + 1, c2);
-                    const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
-                    const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
-                    const float2 ea = dist2(P[h].xa, P[h].ya, P[h].za, c2);
-                    const float2 eb = dist2(P[h].xb, P[h].yb, P[h].zb, c2);
-                    if (da.x < ba.x) { ba.x = da.x; s0 = j; }
-                    if (da.y < ba.y) { ba.y = da.y; s1 = j; }
-                    if (db.x < bb.x) { bb.x = db.x; s2 = j; }
-                    if (db.y < bb.y) { bb.y = db.y; s3 = j; }
-                    if (ea.x < ba.x) { ba.x = ea.x; s0 = j + 1; }
-                    if (ea.y < ba.y) { ba.y = ea.y; s1 = j + 1; }
-                    if (eb.x < bb.x) { bb.x = eb.x; s2 = j + 1; }
-                    if (eb.y < bb.y) { bb.y = eb.y; s3 = j + 1; }
-                }
-                if (j < ncand) {
-                    cand_at(j, cc);
-                    const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
-                    const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
-                    if (da.x < ba.x) { ba.x = da.x; s0 = j; }
-                    if (da.y < ba.y) { ba.y = da.y; s1 = j; }
-                    if (db.x < bb.x) { bb.x = db.x; s2 = j; }
-                    if (db.y < bb.y) { bb.y = db.y; s3 = j; }
-                }
-                if (MODE & kModeLabels) {
-                    float4 t;
-                    *reinterpret_cast<int2*>(labels + pa) = make_int2(cand_at(s0, t), cand_at(s1, t));
-                    *reinterpret_cast<int2*>(labels + pb) = make_int2(cand_at(s2, t), cand_at(s3, t));
-                }
-                if (MODE & kModeReduce) {
-                    if (pa < n) J += (double)ba.x;
-                    if (pa + 1 < n) J += (double)ba.y;
-                    if (pb < n) J += (double)bb.x;
-                    if (pb + 1 < n) J += (double)bb.y;
-                    const bool vv[4] = {pa < n, pa + 1 < n, pb < n, pb + 1 < n};
-                    const int ss[4] = {s0, s1, s2, s3};
-                    const float xx[4] = {P[h].xa.x, P[h].xa.y, P[h].xb.x, P[h].xb.y};
-                    const float yy[4] = {P[h].ya.x, P[h].ya.y, P[h].yb.x, P[h].yb.y};
-                    const float zz[4] = {P[h].za.x, P[h].za.y, P[h].zb.x, P[h].zb.y};
-                    agg4(vv, ss, xx, yy, zz);
+                        for (; j + 1 < ncand; j += 2) {
+                            float4 c2;
+                            cand_at(j, cc);
+                            cand_at(j + 1, c2);
+                            const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
+                            const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
+                            const float2 ea = dist2(P[h].xa, P[h].ya, P[h].za, c2);
+                            const float2 eb = dist2(P[h].xb, P[h].yb, P[h].zb, c2);
+                            if (da.x < ba.x) { ba.x = da.x; s0 = j; }
+                            if (da.y < ba.y) { ba.y = da.y; s1 = j; }
+                            if (db.x < bb.x) { bb.x = db.x; s2 = j; }
+                            if (db.y < bb.y) { bb.y = db.y; s3 = j; }
+                            if (ea.x < ba.x) { ba.x = ea.x; s0 = j + 1; }
+                            if (ea.y < ba.y) { ba.y = ea.y; s1 = j + 1; }
+                            if (eb.x < bb.x) { bb.x = eb.x; s2 = j + 1; }
+                            if (eb.y < bb.y) { bb.y = eb.y; s3 = j + 1; }
+                        }
+#endif
+#pragma unroll 1
+                        for (; j < ncand; ++j) {
+                            cand_at(j, cc);
+                            const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
+                            const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
+                            if (da.x < ba.x) { ba.x = da.x; s0 = j; }
+                            if (da.y < ba.y) { ba.y = da.y; s1 = j; }
+                            if (db.x < bb.x) { bb.x = db.x; s2 = j; }
+                            if (db.y < bb.y) { bb.y = db.y; s3 = j; }
+                        }
+                        if (LARGE && npass > 1) {   // winning slots for the later passes
+                            unsigned short* sg = slot_g + (size_t)chunk * kSChunkPoints;
+                            *reinterpret_cast<ushort2*>(sg + off) = make_ushort2(s0, s1);
+                            *reinterpret_cast<ushort2*>(sg + off + kWarpTile) = make_ushort2(s2, s3);
+                        }
+                        if ((MODE & kModeLabels) && pass == 0) {
+                            float4 t;
+                            *reinterpret_cast<int2*>(labels + pa) = make_int2(cand_at(s0, t), cand_at(s1, t));
+                            *reinterpret_cast<int2*>(labels + pb) = make_int2(cand_at(s2, t), cand_at(s3, t));
+                        }
+                        if ((MODE & kModeReduce) && pass == 0) {
+                            if (pa < n) J += (double)ba.x;
+                            if (pa + 1 < n) J += (double)ba.y;
+                            if (pb < n) J += (double)bb.x;
+                            if (pb + 1 < n) J += (double)bb.y;
+                        }
+                    } else {
+                        const unsigned short* sg = slot_g + (size_t)chunk * kSChunkPoints;
+                        const ushort2 a = *reinterpret_cast<const ushort2*>(sg + off);
+                        const ushort2 b = *reinterpret_cast<const ushort2*>(sg + off + kWarpTile);
+                        s0 = a.x;
+                        s1 = a.y;
+                        s2 = b.x;
+                        s3 = b.y;
+                    }
+                    if (MODE & kModeReduce) {
+                        const unsigned w = C::kSlots;
+                        if (pa < n && (unsigned)(s0 - s_lo) < w) accumulate(s0 - s_lo, P[h].xa.x, P[h].ya.x, P[h].za.x);
+                        if (pa + 1 < n && (unsigned)(s1 - s_lo) < w) accumulate(s1 - s_lo, P[h].xa.y, P[h].ya.y, P[h].za.y);
+                        if (pb < n && (unsigned)(s2 - s_lo) < w) accumulate(s2 - s_lo, P[h].xb.x, P[h].yb.x, P[h].zb.x);
+                        if (pb + 1 < n && (unsigned)(s3 - s_lo) < w) accumulate(s3 - s_lo, P[h].xb.y, P[h].yb.y, P[h].zb.y);
+                    }
                 }
             }
-        }
-        if (!(MODE & kModeReduce)) return;
-        // row entries in slot (= ascending k) order: lane -> (slot, half)
-        {
-            const int q = lane, sl = q >> 1;   // ncand <= 16: one pass of 32 lanes
-            if (sl < ncand) {
-                const double* t = T + 4 * sl;
-                reinterpret_cast<double2*>(row + kRowHead)[q] =
-                    (q & 1) ? make_double2(t[2], pack_kn(S.candk[sl], (int)t[3]))
-                            : make_double2(t[0], t[1]);
+            if (!(MODE & kModeReduce)) return;   // labels only: one pass
+            __syncwarp();
+            // lane L (< 2 kSlots) sums slot s_lo + (L >> 1), half (L & 1), over the
+            // 32 lanes in a rotated (bank-conflict-free) order -> row entry of the slot
+            const int sl = lane >> 1;
+            if (sl < C::kSlots && s_lo + sl < ncand) {
+                const double2* col = (lane & 1) ? S.col_b(0) : S.col_a(0);
+                double v0 = 0.0, v1 = 0.0;
+                long long cnt = 0;
+#pragma unroll 8
+                for (int r = 0; r < 32; ++r) {
+                    const int t = (r + lane) & 31;
+                    const double2 w2 = col[sl * 32 + t];
+                    v0 += w2.x;
+                    if (lane & 1) cnt += reinterpret_cast<const int2*>(&w2.y)->x;
+                    else v1 += w2.y;
+                }
+                float4 t;
+                const int k = cand_at(s_lo + sl, t);
+                reinterpret_cast<double2*>(row + kRowHead)[2 * (s_lo + sl) + (lane & 1)] =
+                        (lane & 1) ? make_double2(v0, pack_kn(k, (int)cnt)) : make_double2(v0, v1);
             }
+            __syncwarp();
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
@@ -1392,148 +1721,9 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
             row[0] = J;
             row[1] = (double)ncand;
         }
-    } else {
-    double J = 0.0;
-    auto accumulate = [&](int l, float px, float py, float pz) {
-        double2 a = S.col_a(l)[lane], b = S.col_b(l)[lane];
-        a.x += (double)px;
-        a.y += (double)py;
-        if (D == 3) b.x += (double)pz;
-        int2 c = *reinterpret_cast<int2*>(&b.y);
-        c.x += 1;
-        b.y = *reinterpret_cast<double*>(&c);
-        S.col_a(l)[lane] = a;
-        S.col_b(l)[lane] = b;
-    };
-    const int npass = (MODE & kModeReduce) ? (ncand + C::kSlots - 1) / C::kSlots : 1;
-#pragma unroll 1
-    for (int pass = 0; pass < npass; ++pass) {
-        const int s_lo = pass * C::kSlots;
-        if (MODE & kModeReduce) {
-#pragma unroll
-            for (int k = 0; k < C::kSlots; ++k) {
-                S.col_a(k)[lane] = make_double2(0.0, 0.0);
-                S.col_b(k)[lane] = make_double2(0.0, 0.0);
-            }
         }
-        __syncwarp();
-#pragma unroll 1
-        for (int u = 0; u < nunit; ++u) {
-            Pts P[kUnitSub];
-            if (pass == 0 && LARGE) fetch(u, P);
-            else reload(u, P);
-#pragma unroll
-            for (int h = 0; h < kUnitSub; ++h) {
-                const int off = u * kSortedUnit + h * kLaneTile + 2 * lane;   // in-chunk index
-                const int64_t pa = base + off, pb = pa + kWarpTile;
-                int s0, s1, s2, s3;
-                float2 ba, bb;
-                if (pass == 0 || !LARGE) {
-                    float4 cc;
-                    cand_at(0, cc);
-                    ba = dist2(P[h].xa, P[h].ya, P[h].za, cc);
-                    bb = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
-                    s0 = s1 = s2 = s3 = 0;
-                    int j = 1;
-#if KM_CAND_UNROLL2
-                    // two candidates per step (independent distance chains), the
-                    // strict-< updates still in ascending j
-#pragma unroll 1
-                    for (; j + 1 < ncand; j += 2) {
-                        float4 c2;
-                        cand_at(j, cc);
-                        cand_at(j + 1, c2);
-                        const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
-                        const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
-                        const float2 ea = dist2(P[h].xa, P[h].ya, P[h].za, c2);
-                        const float2 eb = dist2(P[h].xb, P[h].yb, P[h].zb, c2);
-                        if (da.x < ba.x) { ba.x = da.x; s0 = j; }
-                        if (da.y < ba.y) { ba.y = da.y; s1 = j; }
-                        if (db.x < bb.x) { bb.x = db.x; s2 = j; }
-                        if (db.y < bb.y) { bb.y = db.y; s3 = j; }
-                        if (ea.x < ba.x) { ba.x = ea.x; s0 = j + 1; }
-                        if (ea.y < ba.y) { ba.y = ea.y; s1 = j + 1; }
-                        if (eb.x < bb.x) { bb.x = eb.x; s2 = j + 1; }
-                        if (eb.y < bb.y) { bb.y = eb.y; s3 = j + 1; }
-                    }
-#endif
-#pragma unroll 1
-                    for (; j < ncand; ++j) {
-                        cand_at(j, cc);
-                        const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
-                        const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
-                        if (da.x < ba.x) { ba.x = da.x; s0 = j; }
-                        if (da.y < ba.y) { ba.y = da.y; s1 = j; }
-                        if (db.x < bb.x) { bb.x = db.x; s2 = j; }
-                        if (db.y < bb.y) { bb.y = db.y; s3 = j; }
-                    }
-                    if (LARGE && npass > 1) {   // winning slots for the later passes
-                        unsigned short* sg = slot_g + (size_t)chunk * kSChunkPoints;
-                        *reinterpret_cast<ushort2*>(sg + off) = make_ushort2(s0, s1);
-                        *reinterpret_cast<ushort2*>(sg + off + kWarpTile) = make_ushort2(s2, s3);
-                    }
-                    if ((MODE & kModeLabels) && pass == 0) {
-                        float4 t;
-                        *reinterpret_cast<int2*>(labels + pa) = make_int2(cand_at(s0, t), cand_at(s1, t));
-                        *reinterpret_cast<int2*>(labels + pb) = make_int2(cand_at(s2, t), cand_at(s3, t));
-                    }
-                    if ((MODE & kModeReduce) && pass == 0) {
-                        if (pa < n) J += (double)ba.x;
-                        if (pa + 1 < n) J += (double)ba.y;
-                        if (pb < n) J += (double)bb.x;
-                        if (pb + 1 < n) J += (double)bb.y;
-                    }
-                } else {
-                    const unsigned short* sg = slot_g + (size_t)chunk * kSChunkPoints;
-                    const ushort2 a = *reinterpret_cast<const ushort2*>(sg + off);
-                    const ushort2 b = *reinterpret_cast<const ushort2*>(sg + off + kWarpTile);
-                    s0 = a.x;
-                    s1 = a.y;
-                    s2 = b.x;
-                    s3 = b.y;
-                }
-                if (MODE & kModeReduce) {
-                    const unsigned w = C::kSlots;
-                    if (pa < n && (unsigned)(s0 - s_lo) < w) accumulate(s0 - s_lo, P[h].xa.x, P[h].ya.x, P[h].za.x);
-                    if (pa + 1 < n && (unsigned)(s1 - s_lo) < w) accumulate(s1 - s_lo, P[h].xa.y, P[h].ya.y, P[h].za.y);
-                    if (pb < n && (unsigned)(s2 - s_lo) < w) accumulate(s2 - s_lo, P[h].xb.x, P[h].yb.x, P[h].zb.x);
-                    if (pb + 1 < n && (unsigned)(s3 - s_lo) < w) accumulate(s3 - s_lo, P[h].xb.y, P[h].yb.y, P[h].zb.y);
-                }
-            }
-        }
-        if (!(MODE & kModeReduce)) return;   // labels only: one pass
-        __syncwarp();
-        // lane L (< 2 kSlots) sums slot s_lo + (L >> 1), half (L & 1), over the
-        // 32 lanes in a rotated (bank-conflict-free) order -> row entry of the slot
-        const int sl = lane >> 1;
-        if (sl < C::kSlots && s_lo + sl < ncand) {
-            const double2* col = (lane & 1) ? S.col_b(0) : S.col_a(0);
-            double v0 = 0.0, v1 = 0.0;
-            long long cnt = 0;
-#pragma unroll 8
-            for (int r = 0; r < 32; ++r) {
-                const int t = (r + lane) & 31;
-                const double2 w2 = col[sl * 32 + t];
-                v0 += w2.x;
-                if (lane & 1) cnt += reinterpret_cast<const int2*>(&w2.y)->x;
-                else v1 += w2.y;
-            }
-            float4 t;
-            const int k = cand_at(s_lo + sl, t);
-            reinterpret_cast<double2*>(row + kRowHead)[2 * (s_lo + sl) + (lane & 1)] =
-                    (lane & 1) ? make_double2(v0, pack_kn(k, (int)cnt)) : make_double2(v0, v1);
-        }
-        __syncwarp();
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
-    if (lane == 0) {
-        row[0] = J;
-        row[1] = (double)ncand;
-    }
-    }
+    }   // LARGE
 }
-
 
 // ---------------------------------------------------------------------------
 // k_assign_heavy (large K): the chunks with more than kCap refined candidates

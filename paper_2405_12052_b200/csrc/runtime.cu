@@ -31,6 +31,7 @@
 
 #include "../../include/kmeans.h"
 #include "kernels.cuh"
+#include "persist.cuh"
 
 using km::DevState;
 
@@ -210,6 +211,11 @@ struct kmeans_ctx {
     std::vector<void*> xopened;   // peers' buffers opened by IPC (closed at destroy)
     void** xtab = nullptr;    // device [2P]: xb pointers then xf pointers
     bool fused = false;       // small full-scan shard: k_fused_iterate (one launch, many iterations)
+    bool persist = false;     // sorted K <= 16: k_persist_iterate (one launch, many iterations)
+    int persist_grid = 0;
+    int persist_smem = 0;
+    km::PersistSync* psync = nullptr;
+    double* pcol = nullptr;   // k_persist_iterate block columns [nE][persist_grid]
     int fused_grid = 0;
     int fused_smem = 0;
     double* brow = nullptr;   // k_fused_iterate block rows [2][nE][fused_grid]
@@ -296,8 +302,10 @@ bool p2p_one_kernel(const kmeans_ctx* ctx);
 
 // kernels of this library per iteration: [prune], assign, [heavy], [row merge],
 // merge + update (fused into one kernel on a single GPU when small enough)
+bool persist_active(const kmeans_ctx* ctx);
+
 int kernels_per_iter(const kmeans_ctx* ctx) {
-    if (ctx->fused) return 1;   // one launch covers many iterations
+    if (ctx->fused || persist_active(ctx)) return 1;   // one launch covers many iterations
     int n = ctx->sorted ? (ctx->path == 1 ? 6 : 4) : (ctx->path == 0 ? 4 : 3);
     if (fused_update(ctx) || p2p_one_kernel(ctx)) n -= 1;
     return n;
@@ -423,6 +431,19 @@ PrunedFn pick_pruned(int d, int K, int mode, int chunk_points = km::kSChunkPoint
                : pick_pruned_l<false, KM_SORTED_CHUNK_TILES>(d, mode);
 }
 
+using PersistFn = void (*)(const float*, int64_t, int, int, const float*, float4*, double*,
+                           DevState*, double*, double*, int, double*, double*, double*,
+                           km::PersistSync*, int64_t, int, km::P2PView);
+
+PersistFn pick_persist(int d, int chunk_points) {
+    const bool big = chunk_points == KM_BIG_CHUNK_TILES * km::kLaneTile;
+    if (d == 2)
+        return big ? km::k_persist_iterate<2, KM_BIG_CHUNK_TILES>
+                   : km::k_persist_iterate<2, KM_SORTED_CHUNK_TILES>;
+    return big ? km::k_persist_iterate<3, KM_BIG_CHUNK_TILES>
+               : km::k_persist_iterate<3, KM_SORTED_CHUNK_TILES>;
+}
+
 int pruned_smem(int d, int K) {
     if (K <= 16)
         return d == 2 ? sizeof(km::PrunedSmem<2, false>) : sizeof(km::PrunedSmem<3, false>);
@@ -503,6 +524,28 @@ kmeans_status configure(kmeans_ctx* ctx) {
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &hocc, (const void*)pick_heavy(ctx->d, 1), 256, ctx->heavy_smem));
             ctx->heavy_grid = sms * std::max(hocc, 1);
+        }
+        if (ctx->path == 0 && (ctx->flags & KMEANS_FLAG_PERSIST)) {
+            // the whole iteration as one persistent kernel (one block per SM)
+            PersistFn pf = pick_persist(ctx->d, ctx->chunk_points);
+            const int W = ctx->d == 2 ? km::PersistCfg<2>::kWarps : km::PersistCfg<3>::kWarps;
+            ctx->persist_smem = W * ctx->smem + W * km::kAccStride * (int)sizeof(double);
+            int occ = 0, coop = 0;
+            if (ctx->persist_smem <= maxSmem &&
+                cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device) ==
+                    cudaSuccess &&
+                coop &&
+                cudaFuncSetAttribute((const void*)pf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     ctx->persist_smem) == cudaSuccess &&
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)pf, W * 32,
+                                                              ctx->persist_smem) == cudaSuccess &&
+                occ >= 1) {
+                // every warp of the grid must own >= 1 of the shard's 256-point units
+                ctx->persist = sms <= km::kBlockGroup * km::kMaxBlockGroups &&
+                               (ctx->N + km::kSortedUnit - 1) / km::kSortedUnit >= (int64_t)sms * W;
+                ctx->persist_grid = sms;
+            }
+            cudaGetLastError();
         }
     } else if (ctx->path == 0) {
         ctx->tpb = 32;
@@ -720,6 +763,12 @@ kmeans_status launch_update(kmeans_ctx* ctx) {
     return KMEANS_OK;
 }
 
+// The persistent kernel runs the iteration when the context has it and the
+// exchange (if any) is the P2P one (an NCCL call cannot run inside a kernel).
+bool persist_active(const kmeans_ctx* ctx) {
+    return ctx->persist && (!ctx->group || ctx->p2p);
+}
+
 // Single GPU and a small enough group table: merge + update in one block.
 bool fused_update(const kmeans_ctx* ctx) {
     return !ctx->group && (int64_t)ctx->nE * ctx->G <= 400000 && ctx->nE * 8 <= 48 * 1024;
@@ -853,11 +902,16 @@ kmeans_status read_state(kmeans_ctx* ctx, DevState* h) {
     CK(cudaMemcpyAsync(h, ctx->st, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
     kmeans_status s = sync(ctx);
     if (s != KMEANS_OK) return s;
-    if (h->err) {   // a P2P exchange timed out on the device (the run was stopped)
+    if (h->err == km::kErrExchangeTimeout) {   // a P2P exchange timed out (the run was stopped)
         set_error("P2P exchange: a peer did not publish within %.1f s (dead or hung rank)",
                   ctx->comm_timeout_s);
         ctx->sticky = KMEANS_ENCCL;
         return KMEANS_ENCCL;
+    }
+    if (h->err) {   // the persistent kernel waited too long for an iteration's update
+        set_error("k_persist_iterate: an iteration's update was not published in time");
+        ctx->sticky = KMEANS_ECUDA;
+        return KMEANS_ECUDA;
     }
     return KMEANS_OK;
 }
@@ -1310,6 +1364,8 @@ void kmeans_destroy(kmeans_ctx* ctx) {
         pool_free(ctx, ctx->cand_count);
         pool_free(ctx, ctx->labels_sorted);
         pool_free(ctx, ctx->brow);
+        pool_free(ctx, ctx->psync);
+        pool_free(ctx, ctx->pcol);
         for (void* p : ctx->xopened) cudaIpcCloseMemHandle(p);
         if (ctx->xown) cudaFree(ctx->xown);
         pool_free(ctx, ctx->xtab);
@@ -1448,7 +1504,12 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
                                            (size_t)ctx->n_chunks) != cudaSuccess)) ||
         pool_alloc(ctx, &ctx->flag, sizeof(int)) != cudaSuccess ||
         (ctx->fused && pool_alloc(ctx, &ctx->brow, sizeof(double) * 2 * (size_t)ctx->nE *
-                                                       ctx->fused_grid) != cudaSuccess)) {
+                                                       ctx->fused_grid) != cudaSuccess) ||
+        (ctx->persist &&
+         (pool_alloc(ctx, &ctx->psync, sizeof(km::PersistSync)) != cudaSuccess ||
+          pool_alloc(ctx, &ctx->pcol, sizeof(double) * ctx->nE *
+                                          (size_t)(ctx->persist_grid + km::kMaxBlockGroups)) !=
+              cudaSuccess))) {
         cudaGetLastError();
         set_error("device allocation failed (%zu bytes of points)", bytesX);
         return fail(KMEANS_ENOMEM);
@@ -1576,6 +1637,9 @@ kmeans_status kmeans_start(kmeans_ctx* ctx, const int64_t* init_idx, const doubl
         CK(cudaStreamSynchronize(ctx->stream));
     }
     if ((s = ensure_trace(ctx, std::min(max_iter, kTraceCap))) != KMEANS_OK) return s;
+    if (ctx->persist) {   // the persistent kernel's counters start from zero
+        CK(cudaMemsetAsync(ctx->psync, 0, sizeof(km::PersistSync), ctx->stream));
+    }
     ctx->assigned = false;
     ctx->gen += 1;   // new epochs for the iteration exchanges of this run
     if ((s = write_state(ctx, 0, 0, max_iter, tol)) != KMEANS_OK) return s;
@@ -1602,6 +1666,31 @@ kmeans_status kmeans_iterate(kmeans_ctx* ctx, int n) {
         CK(cudaLaunchCooperativeKernel((const void*)ff, dim3(ctx->fused_grid),
                                        dim3(km::kFusedWarps * 32), args, ctx->fused_smem,
                                        ctx->stream));
+        ctx->launches += 1;
+        return KMEANS_OK;
+    }
+    if (persist_active(ctx)) {   // n iterations (or until the stop rule) in one launch
+        if (n == 0) return KMEANS_OK;
+        PersistFn pf = pick_persist(ctx->d, ctx->chunk_points);
+        // the flag counts this launch's iterations from zero
+        CK(cudaMemsetAsync(ctx->psync, 0, sizeof(unsigned long long), ctx->stream));
+        km::P2PView pv{};
+        if (ctx->p2p) pv = p2p_view(ctx);
+        else pv.P = 1;
+        int n_iter = n;
+        const float* X = ctx->X;
+        const float* cbox = ctx->cbox;
+        double* gcol = ctx->pcol + (size_t)ctx->nE * ctx->persist_grid;
+        void* args[] = {(void*)&X,           (void*)&ctx->N,        (void*)&ctx->K,
+                        (void*)&ctx->n_chunks, (void*)&cbox,        (void*)&ctx->cneg,
+                        (void*)&ctx->mu,     (void*)&ctx->st,       (void*)&ctx->trace_E,
+                        (void*)&ctx->trace_J, (void*)&ctx->trace_cap, (void*)&ctx->pcol,
+                        (void*)&gcol,        (void*)&ctx->red,      (void*)&ctx->psync,
+                        (void*)&ctx->keep_n,
+                        (void*)&n_iter,      (void*)&pv};
+        const int W = ctx->d == 2 ? km::PersistCfg<2>::kWarps : km::PersistCfg<3>::kWarps;
+        CK(cudaLaunchCooperativeKernel((const void*)pf, dim3(ctx->persist_grid), dim3(W * 32),
+                                       args, ctx->persist_smem, ctx->stream));
         ctx->launches += 1;
         return KMEANS_OK;
     }
@@ -1918,6 +2007,8 @@ kmeans_status kmeans_get_info(kmeans_ctx* ctx, kmeans_info* info) {
     info->sorted = ctx->sorted ? 1 : 0;
     info->fused = ctx->fused ? 1 : 0;
     info->fused_grid = ctx->fused_grid;
+    info->persistent = persist_active(ctx) ? 1 : 0;
+    info->persist_grid = ctx->persist_grid;
     info->rank = ctx->rank;
     return KMEANS_OK;
 }

@@ -26,6 +26,7 @@ FLAG_NO_SORT = 1
 FLAG_FORCE_SORT = 2
 FLAG_NO_FUSED = 4
 FLAG_BIG_CHUNKS = 8
+FLAG_PERSIST = 16
 MAX_K = 1024
 
 
@@ -51,7 +52,8 @@ class Info(ctypes.Structure):
                 ("block", ctypes.c_int), ("smem_bytes", ctypes.c_int), ("path", ctypes.c_int),
                 ("kernels_per_iter", ctypes.c_int), ("kernel_launches", ctypes.c_int64),
                 ("nranks", ctypes.c_int), ("rank", ctypes.c_int), ("sorted", ctypes.c_int),
-                ("fused", ctypes.c_int), ("fused_grid", ctypes.c_int)]
+                ("fused", ctypes.c_int), ("fused_grid", ctypes.c_int),
+                ("persistent", ctypes.c_int), ("persist_grid", ctypes.c_int)]
 
 
 class Mixture(ctypes.Structure):
@@ -174,7 +176,7 @@ class Context:
     def __init__(self, points, K: int, *, d: int | None = None, layout: str = "aos",
                  device: int = -1, stream=None, comm=None, global_offset: int = 0,
                  global_N: int = 0, sort: bool | None = None, fused: bool = True,
-                 big_chunks: bool = False, rank: int = 0, nranks: int = 0,
+                 big_chunks: bool = False, persist: bool = False, rank: int = 0, nranks: int = 0,
                  expected_iters: int = 0, comm_timeout_s: float = 0.0):
         pts = _as_f32_points(points)
         shape = tuple(pts.shape)
@@ -212,6 +214,8 @@ class Context:
             o.flags |= FLAG_NO_FUSED
         if big_chunks:  # sorted path: 2048-point chunks regardless of N
             o.flags |= FLAG_BIG_CHUNKS
+        if persist:  # sorted path: k_persist_iterate instead of the per-iteration kernel graph
+            o.flags |= FLAG_PERSIST
         o.rank = rank                   # P2P-only group (no NCCL communicator)
         o.nranks = nranks
         o.expected_iters = expected_iters

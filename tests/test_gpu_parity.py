@@ -891,3 +891,91 @@ def test_expected_iters_weighs_the_sort():
     for hint in (20, 1000):
         assert np.array_equal(res[hint]["labels"], res[0]["labels"])
         np.testing.assert_allclose(res[hint]["centroids"], res[0]["centroids"], rtol=1e-12)
+
+
+# --------------------------------------------------------------------------
+# k_persist_iterate (sorted path, K <= 16: the whole iteration in one kernel)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("big", [False, True])
+@pytest.mark.parametrize("name,N,K", [("NS", 1_100_003, 16), ("C3", 1_300_000, 16),
+                                      ("C2", 1_200_000, 8), ("C1", 1_400_001, 4),
+                                      ("NS", 300_001, 16), ("NS", 1_000, 3)])
+def test_persistent_iteration_matches_oracle(name, N, K, big):
+    """The persistent kernel (one launch, many iterations, static unit ranges,
+    last-arriver block / grid merges, flag-released updates) against the
+    oracle over several iterations -- labels and counts exact, centroids per
+    R13 -- and against the multi-kernel path (same labels, centroids within
+    1e-12), including launches split at arbitrary iteration counts.  Shards
+    too small to give every warp of the grid a 256-point unit (the last two
+    cases) run the multi-kernel path instead."""
+    w = datagen.WORKLOADS[name]
+    X = datagen.generate(w, N=N)
+    init = datagen.init_indices(w, N=N, K=K)
+    T = 7
+    o = oracle.fit(X, K, init, 0.0, T)
+    with km.Context(X, K, sort=True, big_chunks=big, persist=True) as c:
+        assert c.info()["persistent"] == int(N > 1_000_000)
+        r = c.fit(init, 0.0, T)
+        c.start(init_idx=init, tol=0.0, max_iter=T)
+        for n in (1, 2, 3, 5):   # 1 + 2 + 3 + (1 of 5: max_iter stops it)
+            c.iterate(n)
+        st = c.poll()
+        assert st["iters"] == T and st["done"]
+        split = c.read_centroids()
+        split_labels = c.final_labels()
+    with km.Context(X, K, sort=True, big_chunks=big) as c:
+        assert c.info()["persistent"] == 0
+        g = c.fit(init, 0.0, T)
+    assert r["iters"] == T
+    assert np.array_equal(r["labels"], o["labels"])
+    assert np.array_equal(r["labels"], g["labels"]) and np.array_equal(split_labels, r["labels"])
+    np.testing.assert_allclose(r["centroids"], o["centroids"], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(r["centroids"], g["centroids"], rtol=1e-12, atol=1e-14)
+    assert np.array_equal(split, r["centroids"])   # same bits however the launches are split
+    np.testing.assert_allclose(r["J_trace"], o["J_trace"], rtol=1e-9)
+
+
+def test_persistent_stop_rule_inside_a_launch():
+    """E < tol fires in the middle of one persistent launch: the iteration
+    count is the oracle's, later iterations are no-ops, and the next launch
+    returns immediately."""
+    w = datagen.WORKLOADS["NS"]
+    N = 1_500_000
+    X = datagen.generate(w, N=N)
+    init = datagen.one_per_blob_init(w, N=N)
+    o = oracle.fit(X, w.M, init, w.tol, w.max_iter)
+    with km.Context(X, w.M, sort=True, persist=True) as c:
+        assert c.info()["persistent"] == 1
+        c.start(init_idx=init, tol=w.tol, max_iter=w.max_iter)
+        c.iterate(w.max_iter)
+        st = c.poll()
+        assert st["done"] and st["iters"] == o["iters"]
+        c.iterate(10)
+        assert c.poll()["iters"] == o["iters"]
+        cent = c.read_centroids()
+        lab = c.final_labels()
+    assert np.array_equal(lab, o["labels"])
+    np.testing.assert_allclose(cent, o["centroids"], rtol=1e-9)
+
+
+def test_persistent_deterministic_and_p2p_single_rank():
+    """Bit-reproducible across runs and contexts (dynamic chunk tickets do not
+    change the sums), and a 1-rank P2P group runs the exchange inside the
+    persistent kernel with the same bits as the single-GPU run."""
+    w = datagen.WORKLOADS["NS"]
+    N = 1_600_000
+    X = datagen.generate(w, N=N)
+    init = datagen.init_indices(w, N=N)
+    runs = []
+    for _ in range(2):
+        with km.Context(X, 16, sort=True, persist=True) as c:
+            runs.append(c.fit(init, 0.0, 6))
+            runs.append(c.fit(init, 0.0, 6))
+    with km.Context(X, 16, sort=True, persist=True, rank=0, nranks=1) as c:
+        c.p2p_open([c.p2p_handle()])
+        assert c.info()["persistent"] == 1
+        runs.append(c.fit(init, 0.0, 6))
+    for r in runs[1:]:
+        assert np.array_equal(r["labels"], runs[0]["labels"])
+        assert np.array_equal(r["centroids"], runs[0]["centroids"])
+        assert np.array_equal(r["E_trace"], runs[0]["E_trace"])

@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--no-sort", action="store_true")
     ap.add_argument("--force-sort", action="store_true")
     ap.add_argument("--big-chunks", action="store_true", help="2048-point chunks at any N")
+    ap.add_argument("--persist", action="store_true",
+                    help="sorted K <= 16: k_persist_iterate instead of the per-iteration kernel graph")
     ap.add_argument("--K", type=int, default=0, help="override K (init = first K seeded indices)")
     ap.add_argument("--N", type=int, default=0, help="override N (a prefix-shaped draw of the workload)")
     a = ap.parse_args()
@@ -49,7 +51,7 @@ def main():
         km._lib = None
         km.LIB_PATH = os.path.abspath(lib)
         ctx = km.Context(X, w.K, sort=False if a.no_sort else (True if getattr(a, "force_sort", False) else None),
-                         big_chunks=a.big_chunks)
+                         big_chunks=a.big_chunks, persist=a.persist)
         ctx.start(init_idx=init, tol=0.0, max_iter=1 << 30)
         ctx.iterate(a.iters)
         ctx.poll()
@@ -69,7 +71,8 @@ def main():
         gbs = 4 * w.d * w.N / (t / 1e3) / 1e9
         print(json.dumps({"lib": os.path.basename(lib), "N": w.N, "sorted": info["sorted"], "assign_ms": round(t, 4), "row_merge_ms": round(t_rm, 4),
                           "iter_ms": round(ti, 4), "hbm_frac": round(gbs / peak, 4),
-                          "grid": info["grid"], "smem": info["smem_bytes"],
+                          "iter_hbm_frac": round(4 * w.d * w.N / (ti / 1e3) / 1e9 / peak, 4),
+                          "grid": info["grid"], "smem": info["smem_bytes"], "persistent": info["persistent"],
                           "cand_mean": round(cand.get("mean", 0), 3)}), flush=True)
         ctx.close()
 
