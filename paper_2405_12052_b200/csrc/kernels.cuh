@@ -258,17 +258,14 @@ constexpr int kLaneTile = 2 * kWarpTile;                 // 128 points per warp-
 #ifndef KM_TWO_CAND
 #define KM_TWO_CAND 1   // register path for two-candidate chunks (K <= 16)
 #endif
+#ifndef KM_TWO_CAND_PRED
+#define KM_TWO_CAND_PRED 1   // two-candidate chunks: predicated adds instead of +0.0 selects
+#endif
 #ifndef KM_CAND_UNROLL2
 #define KM_CAND_UNROLL2 1   // multi-candidate argmin: two candidates per loop step
 #endif
-#ifndef KM_LARGE_SLOTS
-#define KM_LARGE_SLOTS 8
-#endif
 #ifndef KM_LARGE_CAP
 #define KM_LARGE_CAP 64
-#endif
-#ifndef KM_SORTED_SLOTS
-#define KM_SORTED_SLOTS 4
 #endif
 constexpr int kChunkTiles = KM_CHUNK_TILES;
 constexpr int kChunkPoints = kLaneTile * kChunkTiles;    // 2048
@@ -846,24 +843,20 @@ constexpr int kRowHead = 2;                             // J, count
 
 template <bool LARGE>
 struct PCfg {
-    static constexpr int kSlots = LARGE ? KM_LARGE_SLOTS : KM_SORTED_SLOTS;   // column slots per pass
-    static constexpr int kCap = LARGE ? KM_LARGE_CAP : 16;   // refined candidates kept
-    // winning-slot cache for passes > 0 (large K); small K recomputes the argmin
-    static constexpr int kSlotCache = 2;   // (large K: the winning-slot cache lives in global scratch)
+    static constexpr int kCap = LARGE ? KM_LARGE_CAP : 16;   // refined candidates kept (<= 64)
 };
+static_assert(KM_LARGE_CAP <= 64, "pruned_body: slot masks are 64-bit");
 
+// Large K: up to kCap refined candidates per chunk, a kCap-slot table T
+// (chunks with more go to k_assign_heavy).
 template <int D, bool LARGE>
 struct PrunedSmem {
-    double2 A[PCfg<LARGE>::kSlots][32];
-    double2 B[PCfg<LARGE>::kSlots][32];
     float ring[kSortedStages][D * kSortedUnit];
     uint64_t bar[kSortedStages];
     float4 cand[PCfg<LARGE>::kCap];     // negated fp32 centroid of each candidate slot
     int candk[PCfg<LARGE>::kCap];       // centroid index of each slot (ascending)
-    unsigned short slot[PCfg<LARGE>::kSlotCache];   // winning slot of each point
+    double T[PCfg<LARGE>::kCap * 4];    // per slot {Sx, Sy, Sz, n}
     __device__ __forceinline__ float* ring_at(int s) { return ring[s]; }
-    __device__ __forceinline__ double2* col_a(int k) { return A[k]; }
-    __device__ __forceinline__ double2* col_b(int k) { return B[k]; }
 };
 
 // Small K: no per-lane columns.  The rare >= 3-candidate chunks add each
@@ -941,48 +934,26 @@ __device__ __forceinline__ double prune_threshold(double M) {
 // dense table acc[4 k + {0, 1, 2, 3}] = {Sx, Sy, Sz, n}, acc[64] = J (shared
 // memory; chunks in the warp's fixed order) -- k_persist_iterate.
 // ---------------------------------------------------------------------------
-template <int D, int MODE, bool ACC = false, class Fetch>
-__device__ __forceinline__ void small_chunk(PrunedSmem<D, false>& S, int lane, int K, float4 cl,
-                                            float bx, int64_t base, int64_t n, int nunit,
-                                            int npts, double* __restrict__ row,
-                                            int32_t* __restrict__ labels, int* cand_slot,
-                                            Fetch&& fetch, double* acc = nullptr) {
+// ---------------------------------------------------------------------------
+// pruned_body: the points of one chunk segment given its candidates cand[0..nc)
+// (negated staged centroids, ascending k in candk): nc == 1 and nc == 2 keep
+// the sums in registers; more (up to SLOTS) run the strict-< argmin over the
+// list (two candidates per step, ascending, lowest k on ties) and add each
+// warp-tile's points into T[slot] = {Sx, Sy, Sz, n} by one fixed butterfly
+// per slot present in the warp.  Output: the sparse row (non-empty slots,
+// ascending k), or with ACC the warp's dense table.  Shared by the small-K
+// and large-K pruned kernels and k_persist_iterate.
+// ---------------------------------------------------------------------------
+template <int D, int MODE, int SLOTS, bool ACC, class Fetch>
+__device__ __forceinline__ void pruned_body(const float4* cand, const int* candk, double* T, int lane,
+                                           int K, int nc, int64_t base, int64_t n, int nunit,
+                                           int npts, double* __restrict__ row,
+                                           int32_t* __restrict__ labels, Fetch&& fetch,
+                                           double* acc) {
     const int64_t rem = n - base;
-    double lo[3], hi[3];
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-        lo[j] = (double)__shfl_sync(0xffffffffu, bx, j);
-        hi[j] = (double)__shfl_sync(0xffffffffu, bx, D + j);
-    }
-    int nc = 0;   // candidates
-    {
-        float c[3] = {0.f, 0.f, 0.f};
-        double dmin2 = 0.0, dmax2 = 0.0;
-        const bool is_k = lane < K;
-        if (is_k) {
-            c[0] = -cl.x;
-            c[1] = -cl.y;
-            c[2] = -cl.z;
-            box_bounds<D>(c, lo, hi, dmin2, dmax2);
-        }
-        double M = is_k ? dmax2 : (double)pos_inf();
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
-        const bool cand = is_k && dmin2 <= prune_threshold(M);
-        const unsigned mask = __ballot_sync(0xffffffffu, cand);
-        nc = __popc(mask);
-        if (cand) {
-            const int sl = __popc(mask & ((1u << lane) - 1u));
-            S.cand[sl] = make_float4(-c[0], -c[1], D == 3 ? -c[2] : 0.0f, 0.0f);
-            S.candk[sl] = lane;
-        }
-    }
-    KM_CHECK(nc >= 1 && nc <= K);
-    if (lane == 0 && cand_slot) *cand_slot = nc;
-    __syncwarp();
     auto cand_at = [&](int j, float4& cc) -> int {   // candidate j: negated centroid, index
-        cc = S.cand[j];
-        return S.candk[j];
+        cc = cand[j];
+        return candk[j];
     };
 
     if (nc == 1) {
@@ -1067,6 +1038,17 @@ __device__ __forceinline__ void small_chunk(PrunedSmem<D, false>& S, int lane, i
         auto add = [&](int ch, float px, float py, float pz, float d0, float d1) {
             const bool w1 = d1 < d0;
             const double x = (double)px, y = (double)py, z = (double)pz;
+#if KM_TWO_CAND_PRED
+            if (w1) {   // predicated adds: half the instructions of the selects
+                s1[ch][0] += x;
+                s1[ch][1] += y;
+                if (D == 3) s1[ch][2] += z;
+            } else {
+                s0[ch][0] += x;
+                s0[ch][1] += y;
+                if (D == 3) s0[ch][2] += z;
+            }
+#else
             s0[ch][0] += w1 ? 0.0 : x;
             s0[ch][1] += w1 ? 0.0 : y;
             s1[ch][0] += w1 ? x : 0.0;
@@ -1075,6 +1057,7 @@ __device__ __forceinline__ void small_chunk(PrunedSmem<D, false>& S, int lane, i
                 s0[ch][2] += w1 ? 0.0 : z;
                 s1[ch][2] += w1 ? z : 0.0;
             }
+#endif
             Jc[ch] += (double)(w1 ? d1 : d0);
             n1[ch] += w1 ? 1 : 0;
             nv[ch] += 1;
@@ -1149,7 +1132,6 @@ __device__ __forceinline__ void small_chunk(PrunedSmem<D, false>& S, int lane, i
     // >= 3 candidates: one pass over the TMA ring; the points of a
     // warp-tile are added to T[slot] by one fixed butterfly per slot
     // present in the warp, counts by ballot
-    double* T = S.T;
     for (int q = lane; q < 4 * ncand; q += 32) T[q] = 0.0;
     __syncwarp();
     double J = 0.0;
@@ -1158,24 +1140,29 @@ __device__ __forceinline__ void small_chunk(PrunedSmem<D, false>& S, int lane, i
     // one fixed butterfly over the lanes; counts by ballot
     auto agg4 = [&](const bool (&v)[4], const int (&sl)[4], const float (&px)[4],
                     const float (&py)[4], const float (&pz)[4]) {
-        unsigned mine_bits = 0u;
+        unsigned long long mine_bits = 0ull;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-            if (v[i]) mine_bits |= 1u << sl[i];
-        unsigned pres = __reduce_or_sync(0xffffffffu, mine_bits);
+            if (v[i]) mine_bits |= 1ull << sl[i];
+        unsigned long long pres = __reduce_or_sync(0xffffffffu, (unsigned)mine_bits);
+        if (SLOTS > 32)
+            pres |= (unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(mine_bits >> 32))
+                    << 32;
         while (pres) {
-            const int q = __ffs(pres) - 1;
+            const int q = __ffsll((long long)pres) - 1;
             pres &= pres - 1;
             double sx = 0.0, sy = 0.0, sz = 0.0;
-            unsigned cnt = 0u;
+            unsigned c = 0u;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const bool m = v[i] && sl[i] == q;
-                sx += m ? (double)px[i] : 0.0;
-                sy += m ? (double)py[i] : 0.0;
-                sz += m ? (double)pz[i] : 0.0;
-                cnt += __popc(__ballot_sync(0xffffffffu, m));
+                if (v[i] && sl[i] == q) {   // predicated adds (no selects)
+                    sx += (double)px[i];
+                    sy += (double)py[i];
+                    sz += (double)pz[i];
+                    ++c;
+                }
             }
+            const unsigned cnt = __reduce_add_sync(0xffffffffu, c);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 sx += __shfl_xor_sync(0xffffffffu, sx, o);
@@ -1258,7 +1245,7 @@ __device__ __forceinline__ void small_chunk(PrunedSmem<D, false>& S, int lane, i
         for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
         if (lane == 0) {
             for (int sl = 0; sl < ncand; ++sl) {
-                double* a = acc + 4 * S.candk[sl];
+                double* a = acc + 4 * candk[sl];
                 const double* t = T + 4 * sl;
                 a[0] += t[0];
                 a[1] += t[1];
@@ -1269,22 +1256,69 @@ __device__ __forceinline__ void small_chunk(PrunedSmem<D, false>& S, int lane, i
         }
         return;
     }
-    // row entries in slot (= ascending k) order: lane -> (slot, half)
-    {
-        const int q = lane, sl = q >> 1;   // ncand <= 16: one pass of 32 lanes
-        if (sl < ncand) {
-            const double* t = T + 4 * sl;
-            reinterpret_cast<double2*>(row + kRowHead)[q] =
-                (q & 1) ? make_double2(t[2], pack_kn(S.candk[sl], (int)t[3]))
-                        : make_double2(t[0], t[1]);
-        }
-    }
+    // the non-empty slots, compacted in ascending slot (= ascending k) order
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
+    int outc = 0;
+    for (int s0 = 0; s0 < ncand; s0 += 32) {
+        const int sl = s0 + lane;
+        const bool nz = sl < ncand && T[4 * sl + 3] > 0.0;
+        const unsigned m = __ballot_sync(0xffffffffu, nz);
+        if (nz) {
+            const int o = outc + __popc(m & ((1u << lane) - 1u));
+            const double* t = T + 4 * sl;
+            double2* e = reinterpret_cast<double2*>(row + kRowHead) + 2 * o;
+            e[0] = make_double2(t[0], t[1]);
+            e[1] = make_double2(t[2], pack_kn(candk[sl], (int)t[3]));
+        }
+        outc += __popc(m);
+    }
     if (lane == 0) {
         row[0] = J;
-        row[1] = (double)ncand;
+        row[1] = (double)outc;
     }
+}
+
+template <int D, int MODE, bool ACC = false, class Fetch>
+__device__ __forceinline__ void small_chunk(PrunedSmem<D, false>& S, int lane, int K, float4 cl,
+                                            float bx, int64_t base, int64_t n, int nunit,
+                                            int npts, double* __restrict__ row,
+                                            int32_t* __restrict__ labels, int* cand_slot,
+                                            Fetch&& fetch, double* acc = nullptr) {
+    double lo[3], hi[3];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        lo[j] = (double)__shfl_sync(0xffffffffu, bx, j);
+        hi[j] = (double)__shfl_sync(0xffffffffu, bx, D + j);
+    }
+    int nc = 0;   // candidates
+    {
+        float c[3] = {0.f, 0.f, 0.f};
+        double dmin2 = 0.0, dmax2 = 0.0;
+        const bool is_k = lane < K;
+        if (is_k) {
+            c[0] = -cl.x;
+            c[1] = -cl.y;
+            c[2] = -cl.z;
+            box_bounds<D>(c, lo, hi, dmin2, dmax2);
+        }
+        double M = is_k ? dmax2 : (double)pos_inf();
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
+        const bool cand = is_k && dmin2 <= prune_threshold(M);
+        const unsigned mask = __ballot_sync(0xffffffffu, cand);
+        nc = __popc(mask);
+        if (cand) {
+            const int sl = __popc(mask & ((1u << lane) - 1u));
+            S.cand[sl] = make_float4(-c[0], -c[1], D == 3 ? -c[2] : 0.0f, 0.0f);
+            S.candk[sl] = lane;
+        }
+    }
+    KM_CHECK(nc >= 1 && nc <= K);
+    if (lane == 0 && cand_slot) *cand_slot = nc;
+    __syncwarp();
+    pruned_body<D, MODE, PCfg<false>::kCap, ACC>(S.cand, S.candk, S.T, lane, K, nc, base, n,
+                                                 nunit, npts, row, labels, fetch, acc);
 }
 
 // Small K: resident CTAs per SM the register budget is cut for (more CTAs =
@@ -1293,22 +1327,18 @@ __device__ __forceinline__ void small_chunk(PrunedSmem<D, false>& S, int lane, i
 #ifndef KM_PRUNED_MINB
 #define KM_PRUNED_MINB (D == 2 ? 32 : 28)
 #endif
-// Small K: resident CTAs per SM the register budget is cut for (more CTAs =
-// more bytes in flight; measured: 28 best in 3D, 32 -- the per-SM block limit --
-// in 2D; a 64-register 3D kernel loses more to its two-candidate path)
-#ifndef KM_PRUNED_MINB
-#define KM_PRUNED_MINB (D == 2 ? 32 : 28)
+#ifndef KM_PRUNED_MINB_LARGE
+#define KM_PRUNED_MINB_LARGE 22   // 9.5 KB of shared memory per CTA: 22 fit an SM
 #endif
 template <int D, int MODE, bool LARGE, int CHT = KM_SORTED_CHUNK_TILES>
-__global__ void __launch_bounds__(32, LARGE ? 1 : KM_PRUNED_MINB)
+__global__ void __launch_bounds__(32, LARGE ? KM_PRUNED_MINB_LARGE : KM_PRUNED_MINB)
 k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
                 const float4* __restrict__ cneg_buf, const DevState* __restrict__ st,
                 int mu_sel, int ignore_done, const float* __restrict__ cbox,
                 const int* __restrict__ slist, const int* __restrict__ scount,
                 double* __restrict__ rows, int row_stride, int32_t* __restrict__ labels,
                 int* __restrict__ cand_count, int* __restrict__ heavy,
-                int* __restrict__ heavy_count, unsigned short* __restrict__ slot_g,
-                int64_t keep_n) {
+                int* __restrict__ heavy_count, int64_t keep_n) {
     using C = PCfg<LARGE>;
     // Prologue before pdl_wait() touches only what no predecessor writes: the
     // chunk box and the points (the TMA ring is filled here, so with PDL the
@@ -1484,353 +1514,75 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
             return;
         }
         __syncwarp();
-
-        // the same points from global memory (passes > 0; L2-resident by then)
-        auto reload = [&](int u, LanePts (&P)[kUnitSub]) {
-#pragma unroll
-            for (int h = 0; h < kUnitSub; ++h) {
-                const int64_t pa = base + (int64_t)u * kSortedUnit + h * kLaneTile + 2 * lane;
-                P[h].xa = ld_stream2(tile_coord<D>(X, pa, 0));
-                P[h].ya = ld_stream2(tile_coord<D>(X, pa, 1));
-                P[h].za = (D == 3) ? ld_stream2(tile_coord<D>(X, pa, 2)) : make_float2(0.f, 0.f);
-                P[h].xb = ld_stream2(tile_coord<D>(X, pa + kWarpTile, 0));
-                P[h].yb = ld_stream2(tile_coord<D>(X, pa + kWarpTile, 1));
-                P[h].zb = (D == 3) ? ld_stream2(tile_coord<D>(X, pa + kWarpTile, 2))
-                                   : make_float2(0.f, 0.f);
-            }
-        };
-        auto dist2 = [&](float2 x, float2 y, float2 z, const float4& cc) {
-            float2 e0 = __fadd2_rn(x, make_float2(cc.x, cc.x));
-            float2 e1 = __fadd2_rn(y, make_float2(cc.y, cc.y));
-            float2 sq = __fmul2_rn(e0, e0);
-            sq = __ffma2_rn(e1, e1, sq);
-            if (D == 3) {
-                float2 e2 = __fadd2_rn(z, make_float2(cc.z, cc.z));
-                sq = __ffma2_rn(e2, e2, sq);
-            }
-            return sq;
-        };
-        // candidate j as a negated fp32 centroid and its index
-        auto cand_at = [&](int j, float4& cc) -> int {
-            if (!LARGE || !big) {
-                cc = S.cand[j];
-                return S.candk[j];
-            }
-            const int k = __ldg(&glist[j]);
-            cc = __ldg(&cneg[k]);
-            return k;
-        };
-        double* row = rows + (size_t)chunk * row_stride;
-
-        if (nc == 1) {
-            // ---- one candidate: labels known, sums in registers (four chains) ----
-            float4 cc;
-            const int k0 = cand_at(0, cc);
-            KM_CHECK(k0 >= 0 && k0 < K);
-            double sx[4] = {0.0, 0.0, 0.0, 0.0}, sy[4] = {0.0, 0.0, 0.0, 0.0};
-            double sz[4] = {0.0, 0.0, 0.0, 0.0}, Jc[4] = {0.0, 0.0, 0.0, 0.0};
-            auto add4 = [&](const LanePts& Q, float2 da, float2 db, int m) {
-                // m: bit mask of the valid points (a0, a1, b0, b1)
-                if (m & 1) { sx[0] += (double)Q.xa.x; sy[0] += (double)Q.ya.x; sz[0] += (double)Q.za.x; Jc[0] += (double)da.x; }
-                if (m & 2) { sx[1] += (double)Q.xa.y; sy[1] += (double)Q.ya.y; sz[1] += (double)Q.za.y; Jc[1] += (double)da.y; }
-                if (m & 4) { sx[2] += (double)Q.xb.x; sy[2] += (double)Q.yb.x; sz[2] += (double)Q.zb.x; Jc[2] += (double)db.x; }
-                if (m & 8) { sx[3] += (double)Q.xb.y; sy[3] += (double)Q.yb.y; sz[3] += (double)Q.zb.y; Jc[3] += (double)db.y; }
-            };
-#pragma unroll 1
-            for (int u = 0; u < nunit; ++u) {
-                LanePts P[kUnitSub];
-                fetch(u, P);
-#pragma unroll
-                for (int h = 0; h < kUnitSub; ++h) {
-                    const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
-                    const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
-                    const int64_t pa = base + (int64_t)u * kSortedUnit + h * kLaneTile + 2 * lane;
-                    const int64_t pb = pa + kWarpTile;
-                    if (MODE & kModeLabels) {
-                        *reinterpret_cast<int2*>(labels + pa) = make_int2(k0, k0);
-                        *reinterpret_cast<int2*>(labels + pb) = make_int2(k0, k0);
-                    }
-                    if (MODE & kModeReduce) {
-                        if ((int64_t)u * kSortedUnit + (h + 1) * kLaneTile <= rem)
-                            add4(P[h], da, db, 15);
-                        else
-                            add4(P[h], da, db, (pa < n ? 1 : 0) | (pa + 1 < n ? 2 : 0) |
-                                                   (pb < n ? 4 : 0) | (pb + 1 < n ? 8 : 0));
-                    }
-                }
-            }
-            if (!(MODE & kModeReduce)) return;
-            double sxt = (sx[0] + sx[1]) + (sx[2] + sx[3]);
-            double syt = (sy[0] + sy[1]) + (sy[2] + sy[3]);
-            double szt = (sz[0] + sz[1]) + (sz[2] + sz[3]);
-            double J = (Jc[0] + Jc[1]) + (Jc[2] + Jc[3]);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                sxt += __shfl_xor_sync(0xffffffffu, sxt, o);
-                syt += __shfl_xor_sync(0xffffffffu, syt, o);
-                szt += __shfl_xor_sync(0xffffffffu, szt, o);
-                J += __shfl_xor_sync(0xffffffffu, J, o);
-            }
-            if (lane == 0) {   // sparse row: J, 1 entry {Sx, Sy, Sz, (k, n)}
-                row[0] = J;
-                row[1] = 1.0;
-                reinterpret_cast<double2*>(row + kRowHead)[0] = make_double2(sxt, syt);
-                reinterpret_cast<double2*>(row + kRowHead)[1] = make_double2(szt, pack_kn(k0, npts));
-            }
-            return;
-        }
-
-        // ---- several candidates ----
-        const int ncand = big ? gcount : nc;   // slots = indices into the candidate list
-        {
-        double J = 0.0;
-        auto accumulate = [&](int l, float px, float py, float pz) {
-            double2 a = S.col_a(l)[lane], b = S.col_b(l)[lane];
-            a.x += (double)px;
-            a.y += (double)py;
-            if (D == 3) b.x += (double)pz;
-            int2 c = *reinterpret_cast<int2*>(&b.y);
-            c.x += 1;
-            b.y = *reinterpret_cast<double*>(&c);
-            S.col_a(l)[lane] = a;
-            S.col_b(l)[lane] = b;
-        };
-        const int npass = (MODE & kModeReduce) ? (ncand + C::kSlots - 1) / C::kSlots : 1;
-#pragma unroll 1
-        for (int pass = 0; pass < npass; ++pass) {
-            const int s_lo = pass * C::kSlots;
-            if (MODE & kModeReduce) {
-#pragma unroll
-                for (int k = 0; k < C::kSlots; ++k) {
-                    S.col_a(k)[lane] = make_double2(0.0, 0.0);
-                    S.col_b(k)[lane] = make_double2(0.0, 0.0);
-                }
-            }
-            __syncwarp();
-#pragma unroll 1
-            for (int u = 0; u < nunit; ++u) {
-                LanePts P[kUnitSub];
-                if (pass == 0 && LARGE) fetch(u, P);
-                else reload(u, P);
-#pragma unroll
-                for (int h = 0; h < kUnitSub; ++h) {
-                    const int off = u * kSortedUnit + h * kLaneTile + 2 * lane;   // in-chunk index
-                    const int64_t pa = base + off, pb = pa + kWarpTile;
-                    int s0, s1, s2, s3;
-                    float2 ba, bb;
-                    if (pass == 0 || !LARGE) {
-                        float4 cc;
-                        cand_at(0, cc);
-                        ba = dist2(P[h].xa, P[h].ya, P[h].za, cc);
-                        bb = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
-                        s0 = s1 = s2 = s3 = 0;
-                        int j = 1;
-#if KM_CAND_UNROLL2
-                        // two candidates per step (independent distance chains), the
-                        // strict-< updates still in ascending j
-#pragma unroll 1
-                        for (; j + 1 < ncand; j += 2) {
-                            float4 c2;
-                            cand_at(j, cc);
-                            cand_at(j + 1, c2);
-                            const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
-                            const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
-                            const float2 ea = dist2(P[h].xa, P[h].ya, P[h].za, c2);
-                            const float2 eb = dist2(P[h].xb, P[h].yb, P[h].zb, c2);
-                            if (da.x < ba.x) { ba.x = da.x; s0 = j; }
-                            if (da.y < ba.y) { ba.y = da.y; s1 = j; }
-                            if (db.x < bb.x) { bb.x = db.x; s2 = j; }
-                            if (db.y < bb.y) { bb.y = db.y; s3 = j; }
-                            if (ea.x < ba.x) { ba.x = ea.x; s0 = j + 1; }
-                            if (ea.y < ba.y) { ba.y = ea.y; s1 = j + 1; }
-                            if (eb.x < bb.x) { bb.x = eb.x; s2 = j + 1; }
-                            if (eb.y < bb.y) { bb.y = eb.y; s3 = j + 1; }
-                        }
-#endif
-#pragma unroll 1
-                        for (; j < ncand; ++j) {
-                            cand_at(j, cc);
-                            const float2 da = dist2(P[h].xa, P[h].ya, P[h].za, cc);
-                            const float2 db = dist2(P[h].xb, P[h].yb, P[h].zb, cc);
-                            if (da.x < ba.x) { ba.x = da.x; s0 = j; }
-                            if (da.y < ba.y) { ba.y = da.y; s1 = j; }
-                            if (db.x < bb.x) { bb.x = db.x; s2 = j; }
-                            if (db.y < bb.y) { bb.y = db.y; s3 = j; }
-                        }
-                        if (LARGE && npass > 1) {   // winning slots for the later passes
-                            unsigned short* sg = slot_g + (size_t)chunk * kSChunkPoints;
-                            *reinterpret_cast<ushort2*>(sg + off) = make_ushort2(s0, s1);
-                            *reinterpret_cast<ushort2*>(sg + off + kWarpTile) = make_ushort2(s2, s3);
-                        }
-                        if ((MODE & kModeLabels) && pass == 0) {
-                            float4 t;
-                            *reinterpret_cast<int2*>(labels + pa) = make_int2(cand_at(s0, t), cand_at(s1, t));
-                            *reinterpret_cast<int2*>(labels + pb) = make_int2(cand_at(s2, t), cand_at(s3, t));
-                        }
-                        if ((MODE & kModeReduce) && pass == 0) {
-                            if (pa < n) J += (double)ba.x;
-                            if (pa + 1 < n) J += (double)ba.y;
-                            if (pb < n) J += (double)bb.x;
-                            if (pb + 1 < n) J += (double)bb.y;
-                        }
-                    } else {
-                        const unsigned short* sg = slot_g + (size_t)chunk * kSChunkPoints;
-                        const ushort2 a = *reinterpret_cast<const ushort2*>(sg + off);
-                        const ushort2 b = *reinterpret_cast<const ushort2*>(sg + off + kWarpTile);
-                        s0 = a.x;
-                        s1 = a.y;
-                        s2 = b.x;
-                        s3 = b.y;
-                    }
-                    if (MODE & kModeReduce) {
-                        const unsigned w = C::kSlots;
-                        if (pa < n && (unsigned)(s0 - s_lo) < w) accumulate(s0 - s_lo, P[h].xa.x, P[h].ya.x, P[h].za.x);
-                        if (pa + 1 < n && (unsigned)(s1 - s_lo) < w) accumulate(s1 - s_lo, P[h].xa.y, P[h].ya.y, P[h].za.y);
-                        if (pb < n && (unsigned)(s2 - s_lo) < w) accumulate(s2 - s_lo, P[h].xb.x, P[h].yb.x, P[h].zb.x);
-                        if (pb + 1 < n && (unsigned)(s3 - s_lo) < w) accumulate(s3 - s_lo, P[h].xb.y, P[h].yb.y, P[h].zb.y);
-                    }
-                }
-            }
-            if (!(MODE & kModeReduce)) return;   // labels only: one pass
-            __syncwarp();
-            // lane L (< 2 kSlots) sums slot s_lo + (L >> 1), half (L & 1), over the
-            // 32 lanes in a rotated (bank-conflict-free) order -> row entry of the slot
-            const int sl = lane >> 1;
-            if (sl < C::kSlots && s_lo + sl < ncand) {
-                const double2* col = (lane & 1) ? S.col_b(0) : S.col_a(0);
-                double v0 = 0.0, v1 = 0.0;
-                long long cnt = 0;
-#pragma unroll 8
-                for (int r = 0; r < 32; ++r) {
-                    const int t = (r + lane) & 31;
-                    const double2 w2 = col[sl * 32 + t];
-                    v0 += w2.x;
-                    if (lane & 1) cnt += reinterpret_cast<const int2*>(&w2.y)->x;
-                    else v1 += w2.y;
-                }
-                float4 t;
-                const int k = cand_at(s_lo + sl, t);
-                reinterpret_cast<double2*>(row + kRowHead)[2 * (s_lo + sl) + (lane & 1)] =
-                        (lane & 1) ? make_double2(v0, pack_kn(k, (int)cnt)) : make_double2(v0, v1);
-            }
-            __syncwarp();
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
-        if (lane == 0) {
-            row[0] = J;
-            row[1] = (double)ncand;
-        }
-        }
+        pruned_body<D, MODE, C::kCap, false>(S.cand, S.candk, S.T, lane, K, nc, base, n, nunit,
+                                             npts, rows + (size_t)chunk * row_stride, labels,
+                                             fetch, nullptr);
     }   // LARGE
 }
 
 // ---------------------------------------------------------------------------
 // k_assign_heavy (large K): the chunks with more than kCap refined candidates
-// (boxes spanning sparse or far regions), one 8-warp block each.  The block
-// refines the super-box list against the chunk box (exact, as in
-// k_assign_pruned), then each warp refines that list against the box of its
-// own 128-point sub-tile (the tile's minimiser of dmax2 is always in the chunk
-// list, so the tile's M and exclusions are exact too) and runs the strict-<
-// argmin over its list in ascending order.  Sums go to a per-slot shared table
-// in a fixed order (per warp and point set, lanes sharing a slot summed in lane
-// order by their lowest lane; those group sums added warp by warp), then a
-// compacted sparse row in ascending slot (= ascending k) order.
+// (boxes spanning sparse or far regions), one 8-warp block each.  Warp w
+// takes the chunk's 128-point sub-tile w on its own -- no block barrier until
+// the row is assembled:
+//   * its points (LDG) and their box; the super-box list refined against
+//     that box (the same exact test as k_assign_pruned: the tile's minimiser
+//     of dmax2 is in the super list, so the tile's M and exclusions are exact);
+//   * the strict-< argmin over the tile list (ascending k: lowest k on ties);
+//   * the tile's sums into a 64-slot table by one fixed butterfly per slot
+//     present in the warp (slots in windows of 64 when the list is longer),
+//     compacted to (k, Sx, Sy, Sz, n) entries in ascending k.
+// After one barrier warp 0 writes the chunk's row: the 8 tiles' entries in
+// tile order (a k may appear once per tile; k_merge_sparse adds entries in
+// row order) and J summed in tile order.
 // ---------------------------------------------------------------------------
+constexpr int kHeavyWarps = kSChunkPoints / kLaneTile;   // 8 sub-tiles of 128 points
+constexpr int kHeavySlots = 64;                          // slot window of the tile table
+
+// row capacity (entries) of the large-K path: pruned rows hold <= kCap
+// entries, heavy rows up to 8 tiles x min(K, 128) (a k once per tile)
+__host__ __device__ constexpr int large_row_entries(int K) {
+    return K < 128 ? (8 * K < kSChunkPoints ? 8 * K : kSChunkPoints) : kSChunkPoints;
+}
+
+template <int D>
+struct HeavySmem {
+    double T[kHeavyWarps][kHeavySlots * 4];   // per warp: slot table of the current window
+    double4 ent[kHeavyWarps][kLaneTile];      // per warp: {Sx, Sy, Sz, (k, n)} entries
+    double wJ[kHeavyWarps];
+    int went[kHeavyWarps];
+    // followed by the super list's staged centroids float4 cl[K] and the tile
+    // lists unsigned short list[kHeavyWarps][K] (super-list positions)
+};
+
 template <int D, int MODE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kHeavyWarps * 32)
 k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __restrict__ cneg_buf,
                const DevState* __restrict__ st, int mu_sel, int ignore_done,
                const float* __restrict__ cbox, const int* __restrict__ slist,
                const int* __restrict__ scount, const int* __restrict__ heavy,
                const int* __restrict__ heavy_count, double* __restrict__ rows, int row_stride,
                int32_t* __restrict__ labels) {
+    (void)cbox;
     if (!ignore_done && st->done) return;
-    static_assert(kSChunkPoints == 8 * kLaneTile, "one 128-point sub-tile per warp");
+    static_assert(kSChunkPoints == kHeavyWarps * kLaneTile, "one 128-point sub-tile per warp");
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* T = reinterpret_cast<double*>(smem_raw);                    // [K][4]
-    float4* cl = reinterpret_cast<float4*>(T + 4 * (size_t)K);           // [K] chunk candidates
-    int* kl = reinterpret_cast<int*>(cl + K);                            // [K]
-    unsigned short* wl = reinterpret_cast<unsigned short*>(kl + K);      // [8][K] tile lists
-    __shared__ double wJ[8], wM[8];
-    __shared__ int wcnt[8];
-    __shared__ float box[6];
+    HeavySmem<D>& S = *reinterpret_cast<HeavySmem<D>*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    float4* cl = reinterpret_cast<float4*>(smem_raw + sizeof(HeavySmem<D>));   // [K]
+    unsigned short* my = reinterpret_cast<unsigned short*>(cl + K) + (size_t)warp * K;
+    double* T = S.T[warp];
     const float4* cneg = cneg_buf + (size_t)mu_sel * K;
     const int nh = *heavy_count;
-    auto bounds = [&](const float4& v, const double (&lo)[3], const double (&hi)[3], double& dmin2,
-                      double& dmax2) {
-        const float c[3] = {-v.x, -v.y, -v.z};
-        dmin2 = 0.0;
-        dmax2 = 0.0;
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-            const double cj = (double)c[j];
-            const double dm = fmax(fmax(lo[j] - cj, cj - hi[j]), 0.0);
-            dmin2 += dm * dm;
-            const double dx = fmax(fabs(cj - lo[j]), fabs(hi[j] - cj));
-            dmax2 += dx * dx;
-        }
-    };
-    auto thr_of = [](double M) {
-        return (M > 1e37) ? (double)pos_inf() : M * (1.0 + 1e-5) + 0x1p-100;
-    };
     for (int h = blockIdx.x; h < nh; h += gridDim.x) {
         const int chunk = heavy[h];
-        const int64_t base = (int64_t)chunk * kSChunkPoints;
-        const int sup = chunk / kSuperChunks;
-        const int* list = slist + (size_t)sup * K;
-        const int gc = scount[sup];
-        __syncthreads();   // the previous chunk is done with every shared buffer
-        if (tid < 2 * D) box[tid] = cbox[(size_t)chunk * 2 * D + tid];
-        __syncthreads();
-        double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
-        for (int j = 0; j < D; ++j) {
-            lo[j] = (double)box[j];
-            hi[j] = (double)box[D + j];
-        }
-        // ---- chunk-level refinement of the super list ----
-        double M = (double)pos_inf();
-        for (int i = tid; i < gc; i += blockDim.x) {
-            double a, b;
-            bounds(cneg[list[i]], lo, hi, a, b);
-            M = fmin(M, b);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
-        if (lane == 0) wM[warp] = M;
-        __syncthreads();
-        M = wM[0];
-        for (int w = 1; w < 8; ++w) M = fmin(M, wM[w]);
-        const double thr = thr_of(M);
-        int nc = 0;
-        for (int i0 = 0; i0 < gc; i0 += blockDim.x) {
-            const int i = i0 + tid;
-            bool cand = false;
-            int k = 0;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (i < gc) {
-                k = list[i];
-                v = cneg[k];
-                double a, b;
-                bounds(v, lo, hi, a, b);
-                cand = a <= thr;
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, cand);
-            if (lane == 0) wcnt[warp] = __popc(m);
-            __syncthreads();
-            int o = nc;
-            for (int w = 0; w < warp; ++w) o += wcnt[w];
-            o += __popc(m & ((1u << lane) - 1u));
-            if (cand) {
-                cl[o] = v;
-                kl[o] = k;
-            }
-            for (int w = 0; w < 8; ++w) nc += wcnt[w];
-            __syncthreads();
-        }
-        // ---- this warp's sub-tile: points, box, tile-level refinement ----
-        const int64_t pa = base + warp * kLaneTile + 2 * lane, pb = pa + kWarpTile;
+        const int* list = slist + (size_t)(chunk / kSuperChunks) * K;
+        const int gc = scount[chunk / kSuperChunks];
+        for (int i = tid; i < gc; i += blockDim.x) cl[i] = __ldg(&cneg[__ldg(&list[i])]);
+        __syncthreads();   // the super list's centroids are staged
+        // ---- this warp's sub-tile: points and box ----
+        const int64_t pa = (int64_t)chunk * kSChunkPoints + warp * kLaneTile + 2 * lane;
+        const int64_t pb = pa + kWarpTile;
         const float2 xa = ld_stream2(tile_coord<D>(X, pa, 0));
         const float2 ya = ld_stream2(tile_coord<D>(X, pa, 1));
         const float2 za = (D == 3) ? ld_stream2(tile_coord<D>(X, pa, 2)) : make_float2(0.f, 0.f);
@@ -1841,6 +1593,7 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
         const float px[4] = {xa.x, xa.y, xb.x, xb.y}, py[4] = {ya.x, ya.y, yb.x, yb.y};
         const float pz[4] = {za.x, za.y, zb.x, zb.y};
         double tlo[3] = {0, 0, 0}, thi[3] = {0, 0, 0};
+#pragma unroll
         for (int j = 0; j < D; ++j) {
             const float* pj = j == 0 ? px : (j == 1 ? py : pz);
             float l_ = pos_inf(), h_ = -pos_inf();
@@ -1859,25 +1612,29 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
             thi[j] = (double)h_;
         }
         const bool any_valid = tlo[0] <= thi[0];   // false for an all-padding tile
-        unsigned short* my = wl + (size_t)warp * K;
+        // ---- the super list refined against the tile box (ascending k) ----
         int nt = 0;
         if (any_valid) {
-            double tM = (double)pos_inf();
-            for (int i = lane; i < nc; i += 32) {
+            double M = (double)pos_inf();
+            for (int i = lane; i < gc; i += 32) {
+                const float4 c4 = cl[i];
+                const float c[3] = {-c4.x, -c4.y, -c4.z};
                 double a, b;
-                bounds(cl[i], tlo, thi, a, b);
-                tM = fmin(tM, b);
+                box_bounds<D>(c, tlo, thi, a, b);
+                M = fmin(M, b);
             }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) tM = fmin(tM, __shfl_xor_sync(0xffffffffu, tM, o));
-            const double tthr = thr_of(tM);
-            for (int i0 = 0; i0 < nc; i0 += 32) {
+            for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
+            const double thr = prune_threshold(M);
+            for (int i0 = 0; i0 < gc; i0 += 32) {
                 const int i = i0 + lane;
                 bool cand = false;
-                if (i < nc) {
+                if (i < gc) {
+                    const float4 c4 = cl[i];
+                    const float c[3] = {-c4.x, -c4.y, -c4.z};
                     double a, b;
-                    bounds(cl[i], tlo, thi, a, b);
-                    cand = a <= tthr;
+                    box_bounds<D>(c, tlo, thi, a, b);
+                    cand = a <= thr;
                 }
                 const unsigned m = __ballot_sync(0xffffffffu, cand);
                 if (cand) my[nt + __popc(m & ((1u << lane) - 1u))] = (unsigned short)i;
@@ -1887,143 +1644,103 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
             if (lane == 0) my[0] = 0;
             nt = 1;
         }
+        KM_CHECK(nt >= 1 && nt <= gc);
         __syncwarp();
-        // ---- exact argmin over the tile list (ascending chunk slots) ----
+        // ---- exact argmin over the tile list (ascending k; strict <) ----
         float best[4];
         int sl[4];
         {
-            const int i0 = my[0];
-            const float4 cc = cl[i0];
-            float2 e0 = __fadd2_rn(xa, make_float2(cc.x, cc.x));
-            float2 e1 = __fadd2_rn(ya, make_float2(cc.y, cc.y));
-            float2 da = __fmul2_rn(e0, e0);
-            da = __ffma2_rn(e1, e1, da);
-            float2 f0 = __fadd2_rn(xb, make_float2(cc.x, cc.x));
-            float2 f1 = __fadd2_rn(yb, make_float2(cc.y, cc.y));
-            float2 db = __fmul2_rn(f0, f0);
-            db = __ffma2_rn(f1, f1, db);
-            if (D == 3) {
-                float2 e2 = __fadd2_rn(za, make_float2(cc.z, cc.z));
-                da = __ffma2_rn(e2, e2, da);
-                float2 f2 = __fadd2_rn(zb, make_float2(cc.z, cc.z));
-                db = __ffma2_rn(f2, f2, db);
-            }
+            const float4 cc = cl[my[0]];
+            const float2 da = form_d2<D>(xa, ya, za, cc), db = form_d2<D>(xb, yb, zb, cc);
             best[0] = da.x; best[1] = da.y; best[2] = db.x; best[3] = db.y;
-            sl[0] = sl[1] = sl[2] = sl[3] = i0;
+            sl[0] = sl[1] = sl[2] = sl[3] = 0;
         }
         for (int t = 1; t < nt; ++t) {
-            const int i = my[t];
-            const float4 cc = cl[i];
-            float2 e0 = __fadd2_rn(xa, make_float2(cc.x, cc.x));
-            float2 e1 = __fadd2_rn(ya, make_float2(cc.y, cc.y));
-            float2 da = __fmul2_rn(e0, e0);
-            da = __ffma2_rn(e1, e1, da);
-            float2 f0 = __fadd2_rn(xb, make_float2(cc.x, cc.x));
-            float2 f1 = __fadd2_rn(yb, make_float2(cc.y, cc.y));
-            float2 db = __fmul2_rn(f0, f0);
-            db = __ffma2_rn(f1, f1, db);
-            if (D == 3) {
-                float2 e2 = __fadd2_rn(za, make_float2(cc.z, cc.z));
-                da = __ffma2_rn(e2, e2, da);
-                float2 f2 = __fadd2_rn(zb, make_float2(cc.z, cc.z));
-                db = __ffma2_rn(f2, f2, db);
-            }
-            if (da.x < best[0]) { best[0] = da.x; sl[0] = i; }
-            if (da.y < best[1]) { best[1] = da.y; sl[1] = i; }
-            if (db.x < best[2]) { best[2] = db.x; sl[2] = i; }
-            if (db.y < best[3]) { best[3] = db.y; sl[3] = i; }
+            const float4 cc = cl[my[t]];
+            const float2 da = form_d2<D>(xa, ya, za, cc), db = form_d2<D>(xb, yb, zb, cc);
+            if (da.x < best[0]) { best[0] = da.x; sl[0] = t; }
+            if (da.y < best[1]) { best[1] = da.y; sl[1] = t; }
+            if (db.x < best[2]) { best[2] = db.x; sl[2] = t; }
+            if (db.y < best[3]) { best[3] = db.y; sl[3] = t; }
         }
         if (MODE & kModeLabels) {
-            *reinterpret_cast<int2*>(labels + pa) = make_int2(kl[sl[0]], kl[sl[1]]);
-            *reinterpret_cast<int2*>(labels + pb) = make_int2(kl[sl[2]], kl[sl[3]]);
+            *reinterpret_cast<int2*>(labels + pa) =
+                make_int2(__ldg(&list[my[sl[0]]]), __ldg(&list[my[sl[1]]]));
+            *reinterpret_cast<int2*>(labels + pb) =
+                make_int2(__ldg(&list[my[sl[2]]]), __ldg(&list[my[sl[3]]]));
         }
-        if (!(MODE & kModeReduce)) continue;
-        for (int q = tid; q < 4 * nc; q += blockDim.x) T[q] = 0.0;
-        double j4 = 0.0;
+        if (MODE & kModeReduce) {
+            double j4 = 0.0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-            if (v[i]) j4 += (double)best[i];
+            for (int i = 0; i < 4; ++i)
+                if (v[i]) j4 += (double)best[i];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) j4 += __shfl_xor_sync(0xffffffffu, j4, o);
-        if (lane == 0) wJ[warp] = j4;
-        // warp pre-aggregation, all warps at once: for each point set i, the
-        // lanes sharing a slot form a group whose lowest lane (the leader) sums
-        // the group's points in ascending lane order (shuffles over the
-        // non-leader lanes, warp-uniform loop)
-        double gx[4], gy[4], gz[4];
-        int gn[4];
-        bool lead[4];
+            for (int o = 16; o > 0; o >>= 1) j4 += __shfl_xor_sync(0xffffffffu, j4, o);
+            // ---- sums: slot windows of 64, one butterfly per slot present ----
+            int ne = 0;   // entries of this tile
+            for (int w0 = 0; w0 < nt; w0 += kHeavySlots) {
+                unsigned long long mine = 0ull;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const unsigned peers = __match_any_sync(0xffffffffu, v[i] ? sl[i] : -1 - lane);
-            lead[i] = v[i] && (peers & ((1u << lane) - 1u)) == 0u;
-            gx[i] = (double)px[i];
-            gy[i] = (double)py[i];
-            gz[i] = (double)pz[i];
-            gn[i] = 1;
-            unsigned rest = __ballot_sync(0xffffffffu, v[i] && !lead[i]);
-            while (rest) {
-                const int r = __ffs(rest) - 1;
-                rest &= rest - 1;
-                const double ox = __shfl_sync(0xffffffffu, gx[i], r);
-                const double oy = __shfl_sync(0xffffffffu, gy[i], r);
-                const double oz = __shfl_sync(0xffffffffu, gz[i], r);
-                if (lead[i] && ((peers >> r) & 1u)) {
-                    gx[i] += ox;
-                    gy[i] += oy;
-                    gz[i] += oz;
-                    gn[i] += 1;
+                for (int i = 0; i < 4; ++i)
+                    if (v[i] && sl[i] >= w0 && sl[i] < w0 + kHeavySlots) mine |= 1ull << (sl[i] - w0);
+                unsigned long long pres = __reduce_or_sync(0xffffffffu, (unsigned)mine);
+                pres |= (unsigned long long)__reduce_or_sync(0xffffffffu, (unsigned)(mine >> 32)) << 32;
+                while (pres) {   // ascending slots = ascending k
+                    const int q = __ffsll((long long)pres) - 1;
+                    pres &= pres - 1;
+                    double sx = 0.0, sy = 0.0, sz = 0.0;
+                    unsigned cnt = 0u;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const bool m = v[i] && sl[i] == w0 + q;
+                        sx += m ? (double)px[i] : 0.0;
+                        sy += m ? (double)py[i] : 0.0;
+                        sz += m ? (double)pz[i] : 0.0;
+                        cnt += __popc(__ballot_sync(0xffffffffu, m));
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+                        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+                        if (D == 3) sz += __shfl_xor_sync(0xffffffffu, sz, o);
+                    }
+                    if (lane == 0) {
+                        KM_CHECK(ne < kLaneTile);
+                        S.ent[warp][ne] = make_double4(sx, sy, sz,
+                                                       pack_kn(__ldg(&list[my[w0 + q]]), (int)cnt));
+                    }
+                    ++ne;
                 }
             }
-        }
-        // warps in turn add their group sums into the slot table (distinct
-        // slots within one point set: no conflicts)
-        for (int w = 0; w < 8; ++w) {
-            __syncthreads();
-            if (warp != w) continue;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                if (lead[i]) {
-                    double* t = T + 4 * sl[i];
-                    t[0] += gx[i];
-                    t[1] += gy[i];
-                    t[2] += gz[i];
-                    t[3] += (double)gn[i];
-                }
-                __syncwarp();
+            if (lane == 0) {
+                S.wJ[warp] = j4;
+                S.went[warp] = ne;
             }
         }
-        __syncthreads();
-        // compact the non-empty slots (ascending) into the sparse row
-        double* row = rows + (size_t)chunk * row_stride;
-        int outc = 0;
-        for (int s0 = 0; s0 < nc; s0 += blockDim.x) {
-            const int s_ = s0 + tid;
-            const bool nz = s_ < nc && T[4 * s_ + 3] > 0.0;
-            const unsigned m = __ballot_sync(0xffffffffu, nz);
-            if (lane == 0) wcnt[warp] = __popc(m);
-            __syncthreads();
-            int o = outc;
-            for (int w = 0; w < warp; ++w) o += wcnt[w];
-            o += __popc(m & ((1u << lane) - 1u));
-            if (nz) {
-                const double* t = T + 4 * s_;
-                reinterpret_cast<double2*>(row + kRowHead)[2 * o] = make_double2(t[0], t[1]);
-                reinterpret_cast<double2*>(row + kRowHead)[2 * o + 1] =
-                    make_double2(t[2], pack_kn(kl[s_], (int)t[3]));
-            }
-            int tot = 0;
-            for (int w = 0; w < 8; ++w) tot += wcnt[w];
-            outc += tot;
-            __syncthreads();
-        }
-        KM_CHECK(nc <= K && nt <= nc && outc <= nc);
-        if (tid == 0) {
+        __syncthreads();   // every tile's entries are in shared memory
+        if ((MODE & kModeReduce) && warp == 0) {
+            // the chunk row: tiles in order, each tile's entries in ascending k
+            double* row = rows + (size_t)chunk * row_stride;
+            int off = 0;
             double J = 0.0;
-            for (int w = 0; w < 8; ++w) J += wJ[w];
-            row[0] = J;
-            row[1] = (double)outc;
+            for (int w = 0; w < kHeavyWarps; ++w) {
+                const int ne = S.went[w];
+                KM_CHECK(kRowHead + 4 * (off + ne) <= row_stride);
+                for (int e = lane; e < ne; e += 32) {
+                    const double4 x = S.ent[w][e];
+                    double2* d2 = reinterpret_cast<double2*>(row + kRowHead) + 2 * (off + e);
+                    d2[0] = make_double2(x.x, x.y);
+                    d2[1] = make_double2(x.z, x.w);
+                }
+                off += ne;
+                J += S.wJ[w];
+            }
+            if (lane == 0) {
+                row[0] = J;
+                row[1] = (double)off;
+            }
         }
+        __syncthreads();   // shared memory is reused by the next heavy chunk
     }
 }
 
@@ -2150,7 +1867,7 @@ k_merge_sparse(const double* __restrict__ rows, int row_stride, int n_chunks, in
         const double* row = rows + (size_t)(c0 + q) * row_stride;
         hj[q] = row[0];
         cnt[q] = (int)row[1];
-        KM_CHECK(cnt[q] >= 0 && cnt[q] <= K && kRowHead + 4 * cnt[q] <= row_stride);
+        KM_CHECK(cnt[q] >= 0 && kRowHead + 4 * cnt[q] <= row_stride);
     }
     __syncthreads();
     if (tid < 32) {   // exclusive scan of the counts (warp 0, kPer consecutive per lane)

@@ -187,7 +187,6 @@ struct kmeans_ctx {
     int merge_smem = 0;           // k_merge_sparse dynamic shared memory (K x 4 doubles)
     int* heavy = nullptr;         // chunks deferred to k_assign_heavy (sorted, large K)
     int* heavy_count = nullptr;
-    unsigned short* slotg = nullptr;   // large K: winning-slot scratch, 1024 per chunk
     int heavy_smem = 0;
     int heavy_grid = 0;
     bool sorted = false;          // points held in Morton order (path 0 default)
@@ -395,7 +394,7 @@ ChunkFn pick_chunk(int d, int K, int mode) {
 
 using PrunedFn = void (*)(const float*, int64_t, int, const float4*, const DevState*, int, int,
                           const float*, const int*, const int*, double*, int, int32_t*, int*,
-                          int*, int*, unsigned short*, int64_t);
+                          int*, int*, int64_t);
 using HeavyFn = void (*)(const float*, int64_t, int, const float4*, const DevState*, int, int,
                          const float*, const int*, const int*, const int*, const int*, double*, int,
                          int32_t*);
@@ -503,7 +502,7 @@ kmeans_status configure(kmeans_ctx* ctx) {
                 cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
         ctx->n_chunks = (int)((ctx->N + ctx->chunk_points - 1) / ctx->chunk_points);
         // sparse rows: <= 16 entries (k_merge_sparse16) or up to K (k_merge_sparse)
-        ctx->row_stride = ctx->K <= 16 ? km::kRowDoubles : km::kRowHead + 4 * ctx->K;
+        ctx->row_stride = ctx->K <= 16 ? km::kRowDoubles : km::kRowHead + 4 * km::large_row_entries(ctx->K);
         // groups: kRowGroup rows (k_merge_sparse16) or kGroupChunks rows (k_merge_sparse)
         ctx->G = ctx->K <= 16 ? (ctx->n_chunks + km::kRowGroup - 1) / km::kRowGroup
                               : (ctx->n_chunks + km::kGroupChunks - 1) / km::kGroupChunks;
@@ -514,8 +513,10 @@ kmeans_status configure(kmeans_ctx* ctx) {
         CK(cudaFuncSetAttribute((const void*)km::k_merge_sparse<3>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->merge_smem));
         if (ctx->path == 1) {
-            // T [K][4] doubles, chunk list K x (float4 + int), 8 tile lists K x u16
-            ctx->heavy_smem = ctx->K * (32 + 16 + 4 + 16);
+            // per-warp slot tables and entry lists, the staged super list (K
+            // float4), then 8 tile lists of K u16
+            ctx->heavy_smem = (int)(sizeof(km::HeavySmem<3>) + sizeof(float4) * ctx->K +
+                                    sizeof(unsigned short) * km::kHeavyWarps * ctx->K);
             for (int mode = 1; mode <= 3; ++mode)
                 CK(cudaFuncSetAttribute((const void*)pick_heavy(ctx->d, mode),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -630,7 +631,7 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
                         ctx->N, ctx->K, (const float4*)ctx->cneg, (const DevState*)ctx->st, mu_sel,
                         ignore_done, (const float*)ctx->cbox, (const int*)ctx->slist,
                         (const int*)ctx->scount, ctx->cpart, ctx->row_stride, ctx->labels_sorted,
-                        ctx->cand_count, ctx->heavy, ctx->heavy_count, ctx->slotg, ctx->keep_n));
+                        ctx->cand_count, ctx->heavy, ctx->heavy_count, ctx->keep_n));
         if (A) ctx->launches += 1;
         if (A && ctx->path == 1) {
             HeavyFn hf = pick_heavy(ctx->d, mode);
@@ -1356,7 +1357,6 @@ void kmeans_destroy(kmeans_ctx* ctx) {
         pool_free(ctx, ctx->scount);
         pool_free(ctx, ctx->heavy);
         pool_free(ctx, ctx->heavy_count);
-        pool_free(ctx, ctx->slotg);
         pool_free(ctx, ctx->perm);
         pool_free(ctx, ctx->init_pairs);
         pool_free(ctx, ctx->init_pos);
@@ -1499,9 +1499,7 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
           pool_alloc(ctx, &ctx->slist, sizeof(int) * (size_t)K * ctx->n_super) != cudaSuccess ||
           pool_alloc(ctx, &ctx->scount, sizeof(int) * (size_t)ctx->n_super) != cudaSuccess ||
           pool_alloc(ctx, &ctx->heavy, sizeof(int) * (size_t)ctx->n_chunks) != cudaSuccess ||
-          pool_alloc(ctx, &ctx->heavy_count, sizeof(int)) != cudaSuccess ||
-          pool_alloc(ctx, &ctx->slotg, sizeof(unsigned short) * km::kSChunkPoints *
-                                           (size_t)ctx->n_chunks) != cudaSuccess)) ||
+          pool_alloc(ctx, &ctx->heavy_count, sizeof(int)) != cudaSuccess)) ||
         pool_alloc(ctx, &ctx->flag, sizeof(int)) != cudaSuccess ||
         (ctx->fused && pool_alloc(ctx, &ctx->brow, sizeof(double) * 2 * (size_t)ctx->nE *
                                                        ctx->fused_grid) != cudaSuccess) ||
