@@ -303,6 +303,20 @@ kmeans_status kmeans_generate(const kmeans_mixture* mix, int64_t start, int64_t 
  * kmeans_p2p_disable; every rank must then disable). */
 kmeans_status kmeans_p2p_handle(kmeans_ctx* ctx, unsigned char handle[64]);
 kmeans_status kmeans_p2p_open(kmeans_ctx* ctx, const unsigned char* handles);
+/* Diagnostic of an opened P2P group, run by ONE rank while the others are idle:
+ * all nranks ranks of the exchange protocol emulated by the blocks of one
+ * cooperative launch on this rank's GPU, over the REAL buffers -- this rank's
+ * own and its peers' (mapped by CUDA IPC, possibly in other processes) --
+ * with epochs no real exchange uses.  Round i: emulated rank r contributes
+ * vals[i][r][0..n) (host, rounds x nranks x n doubles); out[i][r][0..n) (host)
+ * receives what it computed, the rank-ordered sum over q of vals[i][q].
+ * Checks that every mapping works both ways (remote stores and loads, system-
+ * scope flags) without ranks waiting on one another across processes.
+ * Synchronous.  KMEANS_EINVAL without an opened group, for rounds < 1, n < 1
+ * or n > K (d + 1) + 1; KMEANS_ENCCL if an emulated rank timed out. */
+kmeans_status kmeans_p2p_loopback(kmeans_ctx* ctx, int rounds, int n, const double* vals,
+                                  double* out);
+
 /* Back to the NCCL allreduce (e.g. when some rank could not map its peers;
  * every rank must then disable).  Synchronises the context's stream. */
 kmeans_status kmeans_p2p_disable(kmeans_ctx* ctx);

@@ -2785,7 +2785,7 @@ __global__ void k_p2p_update(P2PView v, double* __restrict__ red, int nE, double
 __global__ void k_p2p_emulate(double* const* xb, uint64_t* const* xf, int P, int cap, int n,
                               int rounds, const double* __restrict__ vals, double* __restrict__ out,
                               double* __restrict__ scratch, int dead_rank, uint64_t timeout_ns,
-                              int* __restrict__ failed) {
+                              int* __restrict__ failed, uint64_t epoch_base) {
     P2PView v{xb, xf, P, (int)blockIdx.x, cap, timeout_ns};
     double* loc = scratch + (size_t)blockIdx.x * cap;
     if ((int)blockIdx.x == dead_rank) return;   // a rank that never publishes
@@ -2793,7 +2793,7 @@ __global__ void k_p2p_emulate(double* const* xb, uint64_t* const* xf, int P, int
         for (int e = threadIdx.x; e < n; e += blockDim.x)
             loc[e] = vals[((size_t)i * P + blockIdx.x) * n + e];
         __syncthreads();
-        if (!p2p_exchange(v, loc, n, i & 1, (1ull << 40) + (uint64_t)i + 1, loc)) {
+        if (!p2p_exchange(v, loc, n, 2 + (i & 1), epoch_base + (uint64_t)i + 1, loc)) {
             if (threadIdx.x == 0) failed[blockIdx.x] = i + 1;   // round of the failure
             return;
         }

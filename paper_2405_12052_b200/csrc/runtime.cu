@@ -1171,6 +1171,66 @@ kmeans_status kmeans_p2p_open(kmeans_ctx* ctx, const unsigned char* handles) {
     return KMEANS_OK;
 }
 
+kmeans_status kmeans_p2p_loopback(kmeans_ctx* ctx, int rounds, int n, const double* vals,
+                                  double* out) {
+    CHECK_CTX(ctx);
+    if (!ctx->p2p || rounds < 1 || n < 1 || n > ctx->xcap || !vals || !out) {
+        set_error("kmeans_p2p_loopback: needs an opened P2P group, rounds >= 1, 1 <= n <= %d",
+                  ctx->xcap);
+        return KMEANS_EINVAL;
+    }
+    DeviceGuard g(ctx->device);
+    int coop = 0;
+    CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device));
+    if (!coop) {
+        set_error("kmeans_p2p_loopback: no cooperative launch on this device");
+        return KMEANS_ECUDA;
+    }
+    const int P = ctx->nranks;
+    const size_t nv = (size_t)rounds * P * n;
+    double *dv = nullptr, *dout = nullptr, *scratch = nullptr;
+    int* dfail = nullptr;
+    CK(cudaStreamSynchronize(ctx->stream));   // no exchange of this context in flight
+    cudaError_t e = cudaMalloc(&dv, sizeof(double) * nv);
+    if (e == cudaSuccess) e = cudaMalloc(&dout, sizeof(double) * nv);
+    if (e == cudaSuccess) e = cudaMalloc(&scratch, sizeof(double) * P * (size_t)ctx->xcap);
+    if (e == cudaSuccess) e = cudaMalloc(&dfail, sizeof(int) * P);
+    if (e == cudaSuccess) e = cudaMemset(dfail, 0, sizeof(int) * P);
+    if (e == cudaSuccess) e = cudaMemcpy(dv, vals, sizeof(double) * nv, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        // every rank of the group emulated by one block, over the real buffers:
+        // this rank's own and the peers' (mapped by CUDA IPC); epochs of their
+        // own (bit 41) so no iteration or host-driven exchange can match them
+        double* const* xb = reinterpret_cast<double* const*>(ctx->xtab);
+        uint64_t* const* xf = reinterpret_cast<uint64_t* const*>(ctx->xtab + P);
+        int P_ = P, cap_ = ctx->xcap, n_ = n, r_ = rounds, dead = -1;
+        uint64_t tmo = (uint64_t)(ctx->comm_timeout_s * 1e9);
+        ctx->xcount += 1;
+        uint64_t ebase = (1ull << 41) + (ctx->xcount << 16);
+        void* args[] = {(void*)&xb,      (void*)&xf,   (void*)&P_,      (void*)&cap_,
+                        (void*)&n_,      (void*)&r_,   (void*)&dv,      (void*)&dout,
+                        (void*)&scratch, (void*)&dead, (void*)&tmo,     (void*)&dfail,
+                        (void*)&ebase};
+        e = cudaLaunchCooperativeKernel((const void*)km::k_p2p_emulate, dim3(P), dim3(128), args,
+                                        0, ctx->stream);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    std::vector<int> hf(P, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(hf.data(), dfail, sizeof(int) * P, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(out, dout, sizeof(double) * nv, cudaMemcpyDeviceToHost);
+    cudaFree(dv);
+    cudaFree(dout);
+    cudaFree(scratch);
+    cudaFree(dfail);
+    CK(e);
+    for (int r = 0; r < P; ++r)
+        if (hf[r]) {
+            set_error("kmeans_p2p_loopback: emulated rank %d timed out in round %d", r, hf[r]);
+            return KMEANS_ENCCL;
+        }
+    return KMEANS_OK;
+}
+
 kmeans_status kmeans_p2p_disable(kmeans_ctx* ctx) {
     CHECK_CTX(ctx);
     DeviceGuard g(ctx->device);
@@ -1223,10 +1283,11 @@ kmeans_status kmeans_p2p_selftest(int device, int P, int n, int rounds, const do
         double* const* xb = reinterpret_cast<double* const*>(tab);
         uint64_t* const* xf = reinterpret_cast<uint64_t* const*>(tab + P);
         int cap_ = cap, P_ = P, n_ = n, r_ = rounds, dead = dead_rank;
-        uint64_t tmo_ = tmo;
+        uint64_t tmo_ = tmo, ebase = 1ull << 40;
         void* args[] = {(void*)&xb,   (void*)&xf,    (void*)&P_,      (void*)&cap_,
                         (void*)&n_,   (void*)&r_,    (void*)&dv,      (void*)&dout,
-                        (void*)&scratch, (void*)&dead, (void*)&tmo_, (void*)&dfail};
+                        (void*)&scratch, (void*)&dead, (void*)&tmo_, (void*)&dfail,
+                        (void*)&ebase};
         // all P "ranks" co-resident (they wait on one another): a cooperative launch
         e = coop ? cudaLaunchCooperativeKernel((const void*)km::k_p2p_emulate, dim3(P), dim3(128),
                                                args, 0, 0)

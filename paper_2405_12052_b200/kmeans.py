@@ -95,6 +95,7 @@ SIGNATURES = {
     "kmeans_p2p_open": (I, [P, P]),
     "kmeans_p2p_disable": (I, [P]),
     "kmeans_p2p_selftest": (I, [I, I, I, I, P, P, I, D, P]),
+    "kmeans_p2p_loopback": (I, [P, I, I, P, P]),
 }
 
 _lib = None
@@ -333,6 +334,16 @@ class Context:
         blob = b"".join(handles)
         buf = (ctypes.c_ubyte * len(blob)).from_buffer_copy(blob)
         _check(lib().kmeans_p2p_open(self._h, buf), "kmeans_p2p_open")
+
+    def p2p_loopback(self, vals):
+        """kmeans_p2p_loopback: every rank of the opened group emulated on this
+        GPU over the real (IPC-mapped) buffers; vals (rounds, nranks, n)."""
+        v = np.ascontiguousarray(vals, dtype=np.float64)
+        rounds, P, n = v.shape
+        out = np.empty_like(v)
+        _check(lib().kmeans_p2p_loopback(self._h, int(rounds), int(n), _ptr(v), _ptr(out)),
+               "kmeans_p2p_loopback")
+        return out
 
     def p2p_disable(self):
         """Back to the NCCL allreduce (kmeans_p2p_disable)."""

@@ -97,6 +97,7 @@ def test_invalid_arguments_rejected_before_device_work(km):
     assert L.kmeans_p2p_handle(None, None) == -1
     assert L.kmeans_p2p_open(None, None) == -1
     assert L.kmeans_p2p_disable(None) == -1
+    assert L.kmeans_p2p_loopback(None, 1, 1, None, None) == -1
     assert L.kmeans_p2p_selftest(0, 0, 5, 1, None, None, -1, 0.0, None) == -1     # P < 1
     assert L.kmeans_p2p_selftest(0, 65, 5, 1, None, None, -1, 0.0, None) == -1    # P > 64
     v = np.zeros((1, 2, 5))
