@@ -693,13 +693,41 @@ __device__ __forceinline__ unsigned long long part1by2_64(unsigned long long x) 
     return x;
 }
 
+// Hilbert index of a grid cell (d = 2 or 3 axes of `bits` bits each): J.
+// Skilling's transform ("Programming the Hilbert curve", AIP Conf. Proc. 707,
+// 2004) turns the coordinates into the curve's "transposed" index in place;
+// interleaving their bits (axis 0 most significant) gives the index.  Unlike
+// the Z-curve, consecutive cells are always adjacent, so a run of consecutive
+// points never jumps across the box: chunk boxes stay compact and the pruning
+// keeps fewer candidates.
+__device__ __forceinline__ void hilbert_transpose(unsigned (&x)[3], int d, int bits) {
+    const unsigned M = 1u << (bits - 1);
+    for (unsigned Q = M; Q > 1; Q >>= 1) {   // inverse undo excess work (branch-free)
+        const unsigned P = Q - 1;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            if (i >= d) break;
+            const unsigned hit = 0u - ((x[i] & Q) != 0u);   // all ones: invert, else exchange
+            x[0] ^= P & hit;
+            const unsigned t = (x[0] ^ x[i]) & P & ~hit;
+            x[0] ^= t;
+            x[i] ^= t;
+        }
+    }
+    for (int i = 1; i < d; ++i) x[i] ^= x[i - 1];   // Gray encode
+    unsigned t = 0;
+    for (unsigned Q = M; Q > 1; Q >>= 1)
+        if (x[d - 1] & Q) t ^= Q - 1;
+    for (int i = 0; i < d; ++i) x[i] ^= t;
+}
+
 // 64-bit Morton key of every point (qbits <= 21 bits per axis in 3D, <= 32 in 2D) on an
 // isotropic grid over the global box -- cubic cells keep chunk boxes compact
 // even when the box is very elongated (C5's far outliers), and the fine grid
 // keeps the dense regions resolved -- with the identity permutation as values.
 template <typename KeyT>   // uint32 (d * qbits <= 32) or uint64 keys
 __global__ void k_morton(const float* __restrict__ in, int64_t N, int d, int64_t si, int64_t sj,
-                         const unsigned* __restrict__ box, int qbits,
+                         const unsigned* __restrict__ box, int qbits, int hilbert,
                          KeyT* __restrict__ keys, int32_t* __restrict__ iota) {
     const double qmax = (double)((1ull << qbits) - 1ull);   // qbits <= 32 (2D), <= 21 (3D)
     double lo[3], sc[3], ext = 0.0;
@@ -715,6 +743,13 @@ __global__ void k_morton(const float* __restrict__ in, int64_t N, int d, int64_t
             double t = ((double)in[i * si + (int64_t)j * sj] - lo[j]) * sc[j];
             t = fmin(fmax(t, 0.0), qmax);
             q[j] = (unsigned long long)t;
+        }
+        if (hilbert) {   // transposed Hilbert index; axis 0 the most significant
+            unsigned x[3] = {(unsigned)q[0], (unsigned)q[1], (unsigned)q[2]};
+            hilbert_transpose(x, d, qbits);
+            q[0] = x[d - 1];
+            q[1] = x[d - 2];
+            q[2] = d == 3 ? x[0] : 0ull;
         }
         keys[i] = (KeyT)((d == 2) ? (part1by1_64(q[0]) | (part1by1_64(q[1]) << 1))
                                   : (part1by2_64(q[0]) | (part1by2_64(q[1]) << 1) |

@@ -257,6 +257,9 @@ struct CreateTrace {
 #ifndef KM_MORTON_EXTRA
 #define KM_MORTON_EXTRA 6   // Morton bits per axis beyond log2(N) / d
 #endif
+#ifndef KM_HILBERT
+#define KM_HILBERT -1   // point order: 1 Hilbert curve, 0 Z-curve, -1 by shard (sort_points)
+#endif
 #ifndef KM_MORTON32
 #define KM_MORTON32 0   // 32-bit Morton keys (see sort_points): 2 ms faster create at
                         // NS, but 10 bits per axis over a box stretched by far outliers
@@ -1032,6 +1035,12 @@ kmeans_status sort_points(kmeans_ctx* ctx, const float* src, int64_t si, int64_t
     const int qcap = k32 ? 32 / d : (d == 2 ? 32 : 21);
     const int qbits = std::min(qcap, (lg + d - 1) / d + KM_MORTON_EXTRA);
     const size_t ksz = k32 ? sizeof(uint32_t) : sizeof(unsigned long long);
+    // the Hilbert curve (no jumps: compact chunk boxes, fewer candidates) in
+    // 3D, and in 2D below the 2048-point-chunk sizes; measured (DESIGN.md
+    // section 4): C5 6.9 -> 5.0 candidates per chunk, 0.420 -> 0.380 ms per
+    // iteration, NS 1.25e7-point shard 37.7 -> 34.8 us; C3 (2D, 1e8) 122 -> 126 us
+    const int hilbert = KM_HILBERT >= 0 ? KM_HILBERT
+                                        : (d == 3 || N < (int64_t)KM_BIG_CHUNK_MIN_N ? 1 : 0);
     if (pool_alloc(ctx, &ctx->perm, sizeof(int32_t) * N) != cudaSuccess ||
         pool_alloc(ctx, &ctx->init_pairs, sizeof(int2) * ctx->K) != cudaSuccess ||
         pool_alloc(ctx, &ctx->init_pos, sizeof(int32_t) * ctx->K) != cudaSuccess ||
@@ -1055,7 +1064,8 @@ kmeans_status sort_points(kmeans_ctx* ctx, const float* src, int64_t si, int64_t
     cudaError_t e = cudaMemcpyAsync(box, hb2, sizeof(unsigned) * 2 * d, cudaMemcpyHostToDevice,
                                     ctx->stream);
     auto radix = [&](auto* k1, auto* k2) {
-        km::k_morton<<<blocks, 256, 0, ctx->stream>>>(src, N, d, si, sj, box, qbits, k1, iota);
+        km::k_morton<<<blocks, 256, 0, ctx->stream>>>(src, N, d, si, sj, box, qbits, hilbert, k1,
+                                                      iota);
         ctx->launches += 1;
         tr.mark(ctx->stream, "bbox + morton keys");
         cudaError_t r = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k1, k2, iota,
