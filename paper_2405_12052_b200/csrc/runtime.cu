@@ -168,6 +168,8 @@ struct kmeans_ctx {
     double* part = nullptr;      // nE x G per-block partials
     double* red = nullptr;       // nE merged partials
     DevState* st = nullptr;
+    DevState* st_host = nullptr;  // pinned: reading the state never blocks the host in
+                                  // cudaMemcpy (so sync() can poll NCCL while it waits)
     double* trace_E = nullptr;
     double* trace_J = nullptr;
     int trace_cap = 0;
@@ -494,9 +496,13 @@ kmeans_status configure(kmeans_ctx* ctx) {
                          (ctx->flags & KMEANS_FLAG_BIG_CHUNKS);
         ctx->chunk_points = (ctx->K <= 16 && big) ? KM_BIG_CHUNK_TILES * km::kLaneTile
                                                   : km::kSChunkPoints;
-        {   // L2-resident prefix of the point stream (small K; tuning: KMEANS_L2_KEEP_MB)
+        {   // L2-resident prefix of the point stream (small K): shards of up to
+            // ~2.5x the 126 MB L2 keep their first 64 MB evict_last across
+            // iterations (measured: the 1.25e7-point NS shard 35.2 -> 34.0 us per
+            // iteration; 2.5e7 points unchanged); tuning: KMEANS_L2_KEEP_MB
+            const double shard_mb = 4.0 * ctx->d * (double)ctx->N / 1e6;
             const char* e = getenv("KMEANS_L2_KEEP_MB");
-            const double mb = e ? atof(e) : 0.0;
+            const double mb = e ? atof(e) : (shard_mb <= 320.0 ? 64.0 : 0.0);
             ctx->keep_n = (int64_t)(mb * 1e6 / (4.0 * ctx->d));
         }
         for (int mode = 1; mode <= 3; ++mode)
@@ -903,9 +909,13 @@ kmeans_status sync(kmeans_ctx* ctx) {
 }
 
 kmeans_status read_state(kmeans_ctx* ctx, DevState* h) {
-    CK(cudaMemcpyAsync(h, ctx->st, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
+    // through the context's pinned staging copy: a copy to pageable memory
+    // would block right here until the whole stream drained
+    CK(cudaMemcpyAsync(ctx->st_host, ctx->st, sizeof(DevState), cudaMemcpyDeviceToHost,
+                       ctx->stream));
     kmeans_status s = sync(ctx);
     if (s != KMEANS_OK) return s;
+    *h = *ctx->st_host;
     if (h->err == km::kErrExchangeTimeout) {   // a P2P exchange timed out (the run was stopped)
         set_error("P2P exchange: a peer did not publish within %.1f s (dead or hung rank)",
                   ctx->comm_timeout_s);
@@ -1417,6 +1427,7 @@ void kmeans_destroy(kmeans_ctx* ctx) {
         pool_free(ctx, ctx->part);
         pool_free(ctx, ctx->red);
         pool_free(ctx, ctx->st);
+        if (ctx->st_host) cudaFreeHost(ctx->st_host);
         pool_free(ctx, ctx->trace_E);
         pool_free(ctx, ctx->trace_J);
         pool_free(ctx, ctx->labels);
@@ -1561,6 +1572,7 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
         pool_alloc(ctx, &ctx->part, sizeof(double) * (size_t)ctx->nE * ctx->G) != cudaSuccess ||
         pool_alloc(ctx, &ctx->red, sizeof(double) * ctx->nE) != cudaSuccess ||
         pool_alloc(ctx, &ctx->st, sizeof(DevState)) != cudaSuccess ||
+        cudaMallocHost(&ctx->st_host, sizeof(DevState)) != cudaSuccess ||
         pool_alloc(ctx, &ctx->idx_dev, sizeof(int64_t) * K) != cudaSuccess ||
         ((ctx->path == 0 || ctx->sorted) &&
          pool_alloc(ctx, &ctx->cpart, sizeof(double) * ctx->row_stride * (size_t)ctx->n_chunks) !=

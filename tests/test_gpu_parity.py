@@ -979,3 +979,30 @@ def test_persistent_deterministic_and_p2p_single_rank():
         assert np.array_equal(r["labels"], runs[0]["labels"])
         assert np.array_equal(r["centroids"], runs[0]["centroids"])
         assert np.array_equal(r["E_trace"], runs[0]["E_trace"])
+
+
+def test_nccl_wait_is_bounded_and_aborts():
+    """With an NCCL communicator the host wait polls the stream and the
+    communicator; a collective that does not finish within comm_timeout_s
+    (here a deliberately tiny 1 us, so the first long wait trips it) aborts
+    the communicator and fails with a sticky KMEANS_ENCCL instead of
+    blocking; kmeans_comm_destroy then skips the aborted communicator."""
+    w = datagen.WORKLOADS["C2"]
+    N = 2_000_000
+    X = datagen.generate(w, N=N)
+    init = datagen.init_indices(w, N=N)
+    comm = km.comm_init(1, km.comm_unique_id(), 0, 0)
+    c = km.Context(X, w.K, comm=comm, global_offset=0, global_N=N, comm_timeout_s=1e-6)
+    try:
+        c.start(init_idx=init, tol=0.0, max_iter=1000)   # (its own waits may trip first)
+        c.iterate(500)
+        c.poll()
+        raised = None
+    except km.KMeansError as e:
+        raised = e
+    assert raised is not None and raised.name == "KMEANS_ENCCL", raised
+    with pytest.raises(km.KMeansError) as e2:   # sticky
+        c.poll()
+    assert e2.value.name == "KMEANS_ENCCL"
+    c.close()
+    km.comm_destroy(comm)   # already aborted: skipped, no double free
