@@ -31,6 +31,7 @@
 #pragma once
 #include <cooperative_groups.h>
 #include <cstdio>
+#include <type_traits>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -1173,11 +1174,15 @@ __device__ __forceinline__ void pruned_body(const float4* cand, const int* candk
     // the 4 points of a lane (a0, a1, b0, b1) at once: per slot present in
     // the warp, each lane sums its points of that slot in that order, then
     // one fixed butterfly over the lanes; counts by ballot
-    auto agg4 = [&](const bool (&v)[4], const int (&sl)[4], const float (&px)[4],
-                    const float (&py)[4], const float (&pz)[4]) {
+    // the NP points of a lane at once (a warp-tile: 4 -- a whole TMA unit, 8,
+    // measured no faster): per slot present in the warp, each lane sums its
+    // points of that slot in point order, then one fixed butterfly over the lanes
+    auto agg = [&](auto np_tag, const bool* v, const int* sl, const float* px, const float* py,
+                   const float* pz) {
+        constexpr int NP = decltype(np_tag)::value;
         unsigned long long mine_bits = 0ull;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < NP; ++i)
             if (v[i]) mine_bits |= 1ull << sl[i];
         unsigned long long pres = __reduce_or_sync(0xffffffffu, (unsigned)mine_bits);
         if (SLOTS > 32)
@@ -1189,7 +1194,7 @@ __device__ __forceinline__ void pruned_body(const float4* cand, const int* candk
             double sx = 0.0, sy = 0.0, sz = 0.0;
             unsigned c = 0u;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
+            for (int i = 0; i < NP; ++i) {
                 if (v[i] && sl[i] == q) {   // predicated adds (no selects)
                     sx += (double)px[i];
                     sy += (double)py[i];
@@ -1218,6 +1223,8 @@ __device__ __forceinline__ void pruned_body(const float4* cand, const int* candk
     for (int u = 0; u < nunit; ++u) {
         LanePts P[kUnitSub];
         fetch(u, P);
+        bool uv[4 * kUnitSub];   // the unit's points of this lane: valid, slot
+        int us[4 * kUnitSub];
 #pragma unroll
         for (int h = 0; h < kUnitSub; ++h) {
             const int off = u * kSortedUnit + h * kLaneTile + 2 * lane;   // in-chunk index
@@ -1265,12 +1272,18 @@ __device__ __forceinline__ void pruned_body(const float4* cand, const int* candk
                 if (pa + 1 < n) J += (double)ba.y;
                 if (pb < n) J += (double)bb.x;
                 if (pb + 1 < n) J += (double)bb.y;
-                const bool vv[4] = {pa < n, pa + 1 < n, pb < n, pb + 1 < n};
-                const int ss[4] = {s0, s1, s2, s3};
+                uv[4 * h + 0] = pa < n;
+                uv[4 * h + 1] = pa + 1 < n;
+                uv[4 * h + 2] = pb < n;
+                uv[4 * h + 3] = pb + 1 < n;
+                us[4 * h + 0] = s0;
+                us[4 * h + 1] = s1;
+                us[4 * h + 2] = s2;
+                us[4 * h + 3] = s3;
                 const float xx[4] = {P[h].xa.x, P[h].xa.y, P[h].xb.x, P[h].xb.y};
                 const float yy[4] = {P[h].ya.x, P[h].ya.y, P[h].yb.x, P[h].yb.y};
                 const float zz[4] = {P[h].za.x, P[h].za.y, P[h].zb.x, P[h].zb.y};
-                agg4(vv, ss, xx, yy, zz);
+                agg(std::integral_constant<int, 4>{}, uv + 4 * h, us + 4 * h, xx, yy, zz);
             }
         }
     }
@@ -1580,15 +1593,56 @@ __host__ __device__ constexpr int large_row_entries(int K) {
     return K < 128 ? (8 * K < kSChunkPoints ? 8 * K : kSChunkPoints) : kSChunkPoints;
 }
 
+constexpr int kHeavySplit = 64;   // tile lists longer than this are walked by all 8 warps
+
 template <int D>
 struct HeavySmem {
     double T[kHeavyWarps][kHeavySlots * 4];   // per warp: slot table of the current window
     double4 ent[kHeavyWarps][kLaneTile];      // per warp: {Sx, Sy, Sz, (k, n)} entries
+    float2 part[kHeavyWarps][4][32];          // split walks: (distance, slot) per warp, point, lane
     double wJ[kHeavyWarps];
     int went[kHeavyWarps];
+    int wnt[kHeavyWarps];
     // followed by the super list's staged centroids float4 cl[K] and the tile
     // lists unsigned short list[kHeavyWarps][K] (super-list positions)
 };
+
+// Strict-< argmin of a lane's 4 points over list positions [t0, t1) of a
+// tile list (slots ascending), two candidates per step (independent chains;
+// the updates stay in ascending slot order).  t0 < t1.
+template <int D>
+__device__ __forceinline__ void argmin_walk(const unsigned short* list, const float4* cl, int t0,
+                                            int t1, float2 xa, float2 ya, float2 za, float2 xb,
+                                            float2 yb, float2 zb, float (&best)[4], int (&sl)[4]) {
+    {
+        const float4 cc = cl[list[t0]];
+        const float2 da = form_d2<D>(xa, ya, za, cc), db = form_d2<D>(xb, yb, zb, cc);
+        best[0] = da.x; best[1] = da.y; best[2] = db.x; best[3] = db.y;
+        sl[0] = sl[1] = sl[2] = sl[3] = t0;
+    }
+    int t = t0 + 1;
+    for (; t + 1 < t1; t += 2) {
+        const float4 c0 = cl[list[t]], c1 = cl[list[t + 1]];
+        const float2 da = form_d2<D>(xa, ya, za, c0), db = form_d2<D>(xb, yb, zb, c0);
+        const float2 ea = form_d2<D>(xa, ya, za, c1), eb = form_d2<D>(xb, yb, zb, c1);
+        if (da.x < best[0]) { best[0] = da.x; sl[0] = t; }
+        if (da.y < best[1]) { best[1] = da.y; sl[1] = t; }
+        if (db.x < best[2]) { best[2] = db.x; sl[2] = t; }
+        if (db.y < best[3]) { best[3] = db.y; sl[3] = t; }
+        if (ea.x < best[0]) { best[0] = ea.x; sl[0] = t + 1; }
+        if (ea.y < best[1]) { best[1] = ea.y; sl[1] = t + 1; }
+        if (eb.x < best[2]) { best[2] = eb.x; sl[2] = t + 1; }
+        if (eb.y < best[3]) { best[3] = eb.y; sl[3] = t + 1; }
+    }
+    if (t < t1) {
+        const float4 cc = cl[list[t]];
+        const float2 da = form_d2<D>(xa, ya, za, cc), db = form_d2<D>(xb, yb, zb, cc);
+        if (da.x < best[0]) { best[0] = da.x; sl[0] = t; }
+        if (da.y < best[1]) { best[1] = da.y; sl[1] = t; }
+        if (db.x < best[2]) { best[2] = db.x; sl[2] = t; }
+        if (db.y < best[3]) { best[3] = db.y; sl[3] = t; }
+    }
+}
 
 template <int D, int MODE>
 __global__ void __launch_bounds__(kHeavyWarps * 32)
@@ -1682,21 +1736,51 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
         KM_CHECK(nt >= 1 && nt <= gc);
         __syncwarp();
         // ---- exact argmin over the tile list (ascending k; strict <) ----
+        // A long list (a tile spanning a sparse gap, e.g. to a far site) is
+        // walked by all 8 warps, each over a contiguous eighth; the partial
+        // (distance, slot) pairs are combined in ascending eighths with
+        // strict <, which is the serial walk's result (lowest slot on ties).
+        if (lane == 0) S.wnt[warp] = nt;
+        __syncthreads();   // every tile's list length
         float best[4];
         int sl[4];
-        {
-            const float4 cc = cl[my[0]];
-            const float2 da = form_d2<D>(xa, ya, za, cc), db = form_d2<D>(xb, yb, zb, cc);
-            best[0] = da.x; best[1] = da.y; best[2] = db.x; best[3] = db.y;
-            sl[0] = sl[1] = sl[2] = sl[3] = 0;
-        }
-        for (int t = 1; t < nt; ++t) {
-            const float4 cc = cl[my[t]];
-            const float2 da = form_d2<D>(xa, ya, za, cc), db = form_d2<D>(xb, yb, zb, cc);
-            if (da.x < best[0]) { best[0] = da.x; sl[0] = t; }
-            if (da.y < best[1]) { best[1] = da.y; sl[1] = t; }
-            if (db.x < best[2]) { best[2] = db.x; sl[2] = t; }
-            if (db.y < best[3]) { best[3] = db.y; sl[3] = t; }
+        if (nt <= kHeavySplit) argmin_walk<D>(my, cl, 0, nt, xa, ya, za, xb, yb, zb, best, sl);
+        for (int T = 0; T < kHeavyWarps; ++T) {   // block-uniform
+            const int ntT = S.wnt[T];
+            if (ntT <= kHeavySplit) continue;
+            const int64_t qa = (int64_t)chunk * kSChunkPoints + T * kLaneTile + 2 * lane;
+            const int64_t qb = qa + kWarpTile;
+            const float2 txa = ld_stream2(tile_coord<D>(X, qa, 0));
+            const float2 tya = ld_stream2(tile_coord<D>(X, qa, 1));
+            const float2 tza = (D == 3) ? ld_stream2(tile_coord<D>(X, qa, 2)) : make_float2(0.f, 0.f);
+            const float2 txb = ld_stream2(tile_coord<D>(X, qb, 0));
+            const float2 tyb = ld_stream2(tile_coord<D>(X, qb, 1));
+            const float2 tzb = (D == 3) ? ld_stream2(tile_coord<D>(X, qb, 2)) : make_float2(0.f, 0.f);
+            const unsigned short* listT = my - (size_t)warp * K + (size_t)T * K;
+            const int t0 = (int)((int64_t)ntT * warp / kHeavyWarps);
+            const int t1 = (int)((int64_t)ntT * (warp + 1) / kHeavyWarps);
+            float pb_[4];
+            int ps_[4];
+            argmin_walk<D>(listT, cl, t0, t1, txa, tya, tza, txb, tyb, tzb, pb_, ps_);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) S.part[warp][i][lane] = make_float2(pb_[i], __int_as_float(ps_[i]));
+            __syncthreads();
+            if (warp == T) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    float2 b2 = S.part[0][i][lane];
+                    best[i] = b2.x;
+                    sl[i] = __float_as_int(b2.y);
+                    for (int w = 1; w < kHeavyWarps; ++w) {
+                        const float2 c2 = S.part[w][i][lane];
+                        if (c2.x < best[i]) {
+                            best[i] = c2.x;
+                            sl[i] = __float_as_int(c2.y);
+                        }
+                    }
+                }
+            }
+            __syncthreads();   // the partials are reused by the next long tile
         }
         if (MODE & kModeLabels) {
             *reinterpret_cast<int2*>(labels + pa) =
