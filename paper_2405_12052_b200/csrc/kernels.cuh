@@ -957,6 +957,36 @@ __device__ __forceinline__ double prune_threshold(double M) {
     return (M > 1e37) ? (double)pos_inf() : M * (1.0 + 1e-5) + 0x1p-100;
 }
 
+#ifndef KM_BISECTOR
+#define KM_BISECTOR 1   // the bisector test on top of the box test
+#endif
+// Bisector test (the "filtering" test of Kanungo et al.'s kd-tree k-means):
+// centroid b can neither win nor tie anywhere in the box if the whole box
+// lies on a's side of the bisector of a and b, with margin.  For x in the box
+//   ||x - b||^2 - ||x - a||^2 = sum_j (a_j - b_j)(2 x_j - a_j - b_j)
+// is linear in x, so its minimum over the box is the sum over axes of the
+// smaller of the two corner values (fp64, from fp32 inputs: no cancellation
+// of large squares).  b is excluded when that minimum exceeds
+// 1e-5 (dmax2_a + dmax2_b) + 2^-100: form D's fp32 results are within
+// (d+2) 2^-24 relative (plus a few subnormal ulps) of the exact squares,
+// each at most its dmax2 over the box, so D(x, b) > D(x, a) strictly.  a is
+// the centroid attaining M = min dmax2 (any centroid would be sound).
+// Never when M could overflow fp32 (then nothing is pruned).
+template <int D>
+__device__ __forceinline__ bool bisector_excludes(const float (&b)[3], const float (&a)[3],
+                                                  const double (&lo)[3], const double (&hi)[3],
+                                                  double dmax2_b, double M) {
+    if (!KM_BISECTOR || M > 1e37) return false;
+    double f = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        const double aj = (double)a[j], bj = (double)b[j];
+        const double dj = aj - bj;
+        f += fmin(dj * (2.0 * lo[j] - aj - bj), dj * (2.0 * hi[j] - aj - bj));
+    }
+    return f > 1e-5 * (M + dmax2_b) + 0x1p-100;
+}
+
 // ---------------------------------------------------------------------------
 // small_chunk (sorted path, K <= 16): one warp, one chunk of points
 // [base, base + npts) streamed as nunit 256-point units by `fetch` (which waits
@@ -1353,7 +1383,13 @@ __device__ __forceinline__ void small_chunk(PrunedSmem<D, false>& S, int lane, i
         double M = is_k ? dmax2 : (double)pos_inf();
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
-        const bool cand = is_k && dmin2 <= prune_threshold(M);
+        // a = the centroid attaining M (lowest such lane)
+        const int al = __ffs(__ballot_sync(0xffffffffu, is_k && dmax2 == M)) - 1;
+        float a[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) a[j] = __shfl_sync(0xffffffffu, c[j], al & 31);
+        const bool cand = is_k && dmin2 <= prune_threshold(M) &&
+                          !bisector_excludes<D>(c, a, lo, hi, dmax2, M);
         const unsigned mask = __ballot_sync(0xffffffffu, cand);
         nc = __popc(mask);
         if (cand) {
@@ -1516,15 +1552,25 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
             const int sup = chunk / kSuperChunks;
             glist = slist + (size_t)sup * K;
             gcount = sup_count;
-            double M = (double)pos_inf();
+            double Ml = (double)pos_inf();   // this lane's min dmax2 and its position
+            int Mil = 0x7fffffff;
             for (int i = lane; i < gcount; i += 32) {
                 float c[3];
                 stage_c(__ldg(&glist[i]), c);
                 double a, b;
                 bounds(c, a, b);
-                M = fmin(M, b);
+                if (b < Ml) {
+                    Ml = b;
+                    Mil = i;
+                }
             }
-            const double thr = threshold(warp_min(M));
+            const double M = warp_min(Ml);
+            int Mi = (Ml == M) ? Mil : 0x7fffffff;   // the lowest position attaining M
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) Mi = min(Mi, __shfl_xor_sync(0xffffffffu, Mi, o));
+            float ca[3];   // a = the centroid attaining M
+            stage_c(__ldg(&glist[Mi]), ca);
+            const double thr = threshold(M);
             for (int i0 = 0; i0 < gcount; i0 += 32) {
                 const int i = i0 + lane;
                 float c[3] = {0.f, 0.f, 0.f};
@@ -1535,7 +1581,7 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
                     stage_c(k, c);
                     double a, b;
                     bounds(c, a, b);
-                    cand = a <= thr;
+                    cand = a <= thr && !bisector_excludes<D>(c, ca, lo, hi, b, M);
                 }
                 const unsigned mask = __ballot_sync(0xffffffffu, cand);
                 const int sl = nc + __popc(mask & ((1u << lane) - 1u));
@@ -1704,16 +1750,26 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
         // ---- the super list refined against the tile box (ascending k) ----
         int nt = 0;
         if (any_valid) {
-            double M = (double)pos_inf();
+            double Ml = (double)pos_inf();   // this lane's min dmax2 and its position
+            int Mil = 0x7fffffff;
             for (int i = lane; i < gc; i += 32) {
                 const float4 c4 = cl[i];
                 const float c[3] = {-c4.x, -c4.y, -c4.z};
                 double a, b;
                 box_bounds<D>(c, tlo, thi, a, b);
-                M = fmin(M, b);
+                if (b < Ml) {
+                    Ml = b;
+                    Mil = i;
+                }
             }
+            double M = Ml;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
+            int Mi = (Ml == M) ? Mil : 0x7fffffff;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) Mi = min(Mi, __shfl_xor_sync(0xffffffffu, Mi, o));
+            const float4 a4 = cl[Mi];   // a = the centroid attaining M
+            const float ca[3] = {-a4.x, -a4.y, -a4.z};
             const double thr = prune_threshold(M);
             for (int i0 = 0; i0 < gc; i0 += 32) {
                 const int i = i0 + lane;
@@ -1723,7 +1779,7 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
                     const float c[3] = {-c4.x, -c4.y, -c4.z};
                     double a, b;
                     box_bounds<D>(c, tlo, thi, a, b);
-                    cand = a <= thr;
+                    cand = a <= thr && !bisector_excludes<D>(c, ca, tlo, thi, b, M);
                 }
                 const unsigned m = __ballot_sync(0xffffffffu, cand);
                 if (cand) my[nt + __popc(m & ((1u << lane) - 1u))] = (unsigned short)i;
@@ -1876,6 +1932,7 @@ k_prune(const float4* __restrict__ cneg_buf, const DevState* __restrict__ st, in
     if (blockIdx.x == 0 && threadIdx.x == 0) *heavy_count = 0;   // the assign's heavy list
     __shared__ double wmin[8];
     __shared__ int wcnt[8];
+    __shared__ int wmi[8];
     __shared__ int base_s;
     const int s = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const float4* cneg = cneg_buf + (size_t)mu_sel * K;
@@ -1899,27 +1956,45 @@ k_prune(const float4* __restrict__ cneg_buf, const DevState* __restrict__ st, in
             dmax2 += dx * dx;
         }
     };
-    double M = (double)pos_inf();
+    double Mt = (double)pos_inf();   // this thread's min dmax2 and its centroid
+    int Mkt = 0x7fffffff;
     for (int k = tid; k < K; k += blockDim.x) {
         double a, b;
         bounds(k, a, b);
-        M = fmin(M, b);
+        if (b < Mt) {
+            Mt = b;
+            Mkt = k;
+        }
     }
+    double M = Mt;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
-    if (lane == 0) wmin[warp] = M;
+    int Mk = (Mt == M) ? Mkt : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) Mk = min(Mk, __shfl_xor_sync(0xffffffffu, Mk, o));
+    if (lane == 0) {
+        wmin[warp] = M;
+        wmi[warp] = Mk;
+    }
     if (tid == 0) base_s = 0;
     __syncthreads();
     M = wmin[0];
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) M = fmin(M, wmin[w]);
-    const double thr = (M > 1e37) ? (double)pos_inf() : M * (1.0 + 1e-5) + 0x1p-100;
+    Mk = 0x7fffffff;   // the lowest centroid attaining M: a
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+        if (wmin[w] == M) Mk = min(Mk, wmi[w]);
+    const float4 av = cneg[Mk];
+    const float ca[3] = {-av.x, -av.y, -av.z};
+    const double thr = prune_threshold(M);
     for (int k0 = 0; k0 < K; k0 += blockDim.x) {
         const int k = k0 + tid;
         bool cand = false;
         if (k < K) {
             double a, b;
             bounds(k, a, b);
-            cand = a <= thr;
+            const float4 v = cneg[k];
+            const float c[3] = {-v.x, -v.y, -v.z};
+            cand = a <= thr && !bisector_excludes<D>(c, ca, lo, hi, b, M);
         }
         const unsigned mask = __ballot_sync(0xffffffffu, cand);
         if (lane == 0) wcnt[warp] = __popc(mask);
