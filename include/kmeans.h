@@ -88,7 +88,8 @@ typedef struct kmeans_opts {
                                communicator's rank and size are used and these are ignored. */
     int expected_iters;     /* hint for the path choice: Lloyd iterations the caller will run on
                                this context (0 = unknown).  The sorted path costs a one-time
-                               Morton sort at create (about 0.1 ms per million points) that
+                               space-filling-curve sort at create (about 0.1 ms per million
+                               points) that
                                pays off only over enough iterations; kmeans_fit passes
                                max_iter. */
     double comm_timeout_s;  /* distributed: seconds to wait for a peer in an exchange before
@@ -111,8 +112,9 @@ typedef struct kmeans_opts {
                                      multi-iteration kernel (k_fused_iterate) that
                                      kmeans_iterate / kmeans_fit_ctx use for small
                                      single-GPU shards (<= 4 x 8 x SMs chunks of 2048) */
-/* Default (neither flag): the sorted path -- the shard is put in Morton order
- * once at create and each 1024-point chunk prunes the centroids that provably
+/* Default (neither flag): the sorted path -- the shard is put in space-filling-
+ * curve order (Hilbert in 3D and for 2D shards below 4e7 points, Z-curve
+ * otherwise) once at create and each 1024-point chunk prunes the centroids that provably
  * cannot be its points' argmin (exact; labels are returned in the caller's
  * order) -- when K > 16 or N*K*d >= 3.84e8 (N >= 8e6 at K = 16, d = 3);
  * below that the full scan is faster (the pruned kernel has a fixed per-chunk
@@ -234,7 +236,7 @@ typedef struct kmeans_info {
     int kernels_per_iter;   /* kernels of this library launched per iteration */
     int64_t kernel_launches;/* kernels of this library launched so far by this context */
     int nranks, rank;
-    int sorted;             /* 1 = Morton-sorted shard with per-chunk pruning */
+    int sorted;             /* 1 = curve-sorted shard with per-chunk pruning */
     int fused;              /* 1 = kmeans_iterate runs k_fused_iterate (grid = fused_grid) */
     int fused_grid;         /* its cooperative grid (blocks of 256 threads) */
     int persistent;         /* 1 = kmeans_iterate runs k_persist_iterate (KMEANS_FLAG_PERSIST) */

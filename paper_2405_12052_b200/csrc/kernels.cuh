@@ -2,12 +2,13 @@
 //
 // Step map (DESIGN.md section 1 / section 5):
 //   k_prep / k_input_bbox / k_morton / k_gather_sorted / k_chunk_bbox
-//                   create: input -> padded AoSoA fp32 tiles (Morton-sorted by
-//                   default), non-finite check, per-chunk / super-box boxes
+//                   create: input -> padded AoSoA fp32 tiles (Hilbert- or
+//                   Z-curve-sorted by default), non-finite check, per-chunk /
+//                   super-box boxes
 //   k_init_gather   mu^0_k = (double) x[init_idx[k]]
 //   k_assign_pruned sorted shard (default): one warp per 1024-point chunk fed by
-//                   TMA bulk copies; an exact box bound keeps only the centroids
-//                   that can be a point's argmin; form-D distances (packed
+//                   TMA bulk copies; exact box and bisector bounds keep only the
+//                   centroids that can be a point's argmin; form-D distances (packed
 //                   f32x2), strict-< argmin (lowest index on ties), fused fp64
 //                   sums / counts / inertia -> one sparse row per chunk
 //                                                                        PAPER.md:45-52
@@ -631,8 +632,8 @@ k_assign_chunk(const float* __restrict__ X, int64_t n, int K,
 // ---------------------------------------------------------------------------
 // Spatially sorted path (default for K <= 16): preprocessing kernels.
 //
-// At kmeans_create the shard's points are put in Morton (Z-curve) order once
-// (CUB radix sort of up to 64-bit keys; stable, so deterministic), and each
+// At kmeans_create the shard's points are put in Hilbert-curve order (3D, and
+// 2D below KM_BIG_CHUNK_MIN_N) or Morton (Z-curve) order once (CUB radix sort of up to 64-bit keys; stable, so deterministic), and each
 // 1024-point chunk gets its bounding box.  The order is an internal layout:
 // labels are scattered back to the caller's order, and every result of the
 // iteration is unchanged (sums are accumulated in a different fixed order).
@@ -1318,7 +1319,7 @@ __device__ __forceinline__ void pruned_body(const float4* cand, const int* candk
         }
     }
     if (!(MODE & kModeReduce)) return;
-    if (ACC) {   // slots in ascending k order
+    if constexpr (ACC) {   // slots in ascending k order
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
         if (lane == 0) {
@@ -1332,28 +1333,28 @@ __device__ __forceinline__ void pruned_body(const float4* cand, const int* candk
             }
             acc[64] += J;
         }
-        return;
-    }
-    // the non-empty slots, compacted in ascending slot (= ascending k) order
+    } else {
+        // the non-empty slots, compacted in ascending slot (= ascending k) order
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
-    int outc = 0;
-    for (int s0 = 0; s0 < ncand; s0 += 32) {
-        const int sl = s0 + lane;
-        const bool nz = sl < ncand && T[4 * sl + 3] > 0.0;
-        const unsigned m = __ballot_sync(0xffffffffu, nz);
-        if (nz) {
-            const int o = outc + __popc(m & ((1u << lane) - 1u));
-            const double* t = T + 4 * sl;
-            double2* e = reinterpret_cast<double2*>(row + kRowHead) + 2 * o;
-            e[0] = make_double2(t[0], t[1]);
-            e[1] = make_double2(t[2], pack_kn(candk[sl], (int)t[3]));
+        for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
+        int outc = 0;
+        for (int s0 = 0; s0 < ncand; s0 += 32) {
+            const int sl = s0 + lane;
+            const bool nz = sl < ncand && T[4 * sl + 3] > 0.0;
+            const unsigned m = __ballot_sync(0xffffffffu, nz);
+            if (nz) {
+                const int o = outc + __popc(m & ((1u << lane) - 1u));
+                const double* t = T + 4 * sl;
+                double2* e = reinterpret_cast<double2*>(row + kRowHead) + 2 * o;
+                e[0] = make_double2(t[0], t[1]);
+                e[1] = make_double2(t[2], pack_kn(candk[sl], (int)t[3]));
+            }
+            outc += __popc(m);
         }
-        outc += __popc(m);
-    }
-    if (lane == 0) {
-        row[0] = J;
-        row[1] = (double)outc;
+        if (lane == 0) {
+            row[0] = J;
+            row[1] = (double)outc;
+        }
     }
 }
 

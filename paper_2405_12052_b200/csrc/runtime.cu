@@ -80,14 +80,14 @@ void arm_red_zone(void* p, size_t bytes) {
 }
 
 void check_red_zone(void* p, const Live& l) {
-    if (!kRedZone) return;
+    if constexpr (kRedZone == 0) return;
     std::vector<unsigned char> h(kRedZone);
     if (cudaMemcpy(h.data(), static_cast<char*>(p) + l.bytes, kRedZone, cudaMemcpyDeviceToHost) !=
         cudaSuccess) {
         cudaGetLastError();
         return;
     }
-    for (size_t i = 0; i < kRedZone; ++i)
+    for (size_t i = 0; i < h.size(); ++i)
         if (h[i] != 0xA5) {
             fprintf(stderr, "KM_CHECKS: device buffer of %zu bytes overrun at byte %zu past its end\n",
                     l.bytes, i);
