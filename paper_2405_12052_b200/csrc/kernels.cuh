@@ -2383,38 +2383,104 @@ k_merge_rows(const double* __restrict__ cpart, int n_chunks, int K, double* __re
 }
 
 // ---------------------------------------------------------------------------
-// Large-K path (16 < K <= 1024).  Centroids staged in smem as float4
-// {-cx, -cy, -cz, 0}; each warp owns fp64 accumulators accS[w][k][D] and int
-// counts accN[w][k]; the 32 lanes of a warp update them in ascending lane order
-// (lanes with equal labels are serialised in rounds; distinct labels update in
-// parallel), so the sums are deterministic.
+// Large-K full scan (16 < K <= 1024; KMEANS_FLAG_NO_SORT and shards the sorted
+// path does not take).  The work is K form-D distances per point (6 FP32
+// lane-ops each): FP32-pipe bound, so the design is about
+// issue slots per (point, centroid) pair.
+//   - Each warp step covers NPL 128-point sub-tiles (4 points per lane
+//     each, packed f32x2 pairs), the next step's points prefetched into
+//     registers while this one runs.
+//   - Centroids staged once per launch in smem as negated float4, padded to a
+//     multiple of kLargeKT with +inf (their distances are +inf); one broadcast
+//     LDS.128 feeds 4 x NPL points.  NPL = 2 (more independent chains per
+//     warp) when the smem accumulators allow one block per SM only, else 1
+//     (fewer registers: two or more blocks per SM).
+//   - Argmin in steps of kLargeKT centroids: per point, a 3-input min tree
+//     (FMNMX3) over the step's distances and the running best, then one
+//     compare-select of the step index when the min strictly drops -- ~0.75
+//     issue slots per pair at 8 instead of a compare and two selects.  Strict < keeps the
+//     first step reaching the minimum; after the scan the winning step's 8
+//     distances are recomputed (the same RN operations, so bit-identical) and
+//     the lowest k with d_k == min is the label: exactly the serial strict-<
+//     argmin (lowest index on ties).  All distances +inf -> label 0.
+//   - Sums: per-warp fp64 accumulators accS[w][k][D] and counts accN[w][k] in
+//     smem.  Per point slot the lanes with equal labels (match_any) are summed
+//     in a fixed tree over their ranks and the group's lowest lane adds the
+//     result, so the sums are deterministic and a warp whose 32 points share
+//     one label costs 5 shuffle levels, not 32 serial rounds; the block row is
+//     the sum over warps in warp order.
 // ---------------------------------------------------------------------------
-template <int D, int MODE>
+#ifndef KM_LARGE_KT
+#define KM_LARGE_KT 8    // centroids per argmin step
+#endif
+constexpr int kLargeKT = KM_LARGE_KT;
+static_assert(kLargeKT == 8 || kLargeKT == 16, "argmin step: 8 or 16 centroids");
+
+__host__ __device__ constexpr int large_kpad(int K) {
+    return (K + kLargeKT - 1) / kLargeKT * kLargeKT;
+}
+
+template <int D>
+__device__ __forceinline__ void load_lane_pts(const float* __restrict__ X, int64_t sub, int lane,
+                                              LanePts& P) {
+    const int64_t pa = sub * kLaneTile + 2 * lane, pb = pa + kWarpTile;
+    P.xa = ld_stream2(tile_coord<D>(X, pa, 0));
+    P.ya = ld_stream2(tile_coord<D>(X, pa, 1));
+    P.za = (D == 3) ? ld_stream2(tile_coord<D>(X, pa, 2)) : make_float2(0.f, 0.f);
+    P.xb = ld_stream2(tile_coord<D>(X, pb, 0));
+    P.yb = ld_stream2(tile_coord<D>(X, pb, 1));
+    P.zb = (D == 3) ? ld_stream2(tile_coord<D>(X, pb, 2)) : make_float2(0.f, 0.f);
+}
+
+// min(best, v[0..KT)) by a 3-input min tree (FMNMX3)
+template <int KT>
+__device__ __forceinline__ float min_tree(const float (&v)[KT], float best) {
+    if constexpr (KT == 8) {
+        const float a = fminf(fminf(v[0], v[1]), v[2]);
+        const float b = fminf(fminf(v[3], v[4]), v[5]);
+        const float c = fminf(fminf(v[6], v[7]), best);
+        return fminf(fminf(a, b), c);
+    } else {
+        const float a = fminf(fminf(v[0], v[1]), v[2]);
+        const float b = fminf(fminf(v[3], v[4]), v[5]);
+        const float c = fminf(fminf(v[6], v[7]), v[8]);
+        const float d = fminf(fminf(v[9], v[10]), v[11]);
+        const float e = fminf(fminf(v[12], v[13]), v[14]);
+        const float f = fminf(v[15], best);
+        return fminf(fminf(fminf(a, b), c), fminf(fminf(d, e), f));
+    }
+}
+
+template <int D, int MODE, int NPL>
 __global__ void __launch_bounds__(kLargeTPBMax)
 k_assign_large(const float* __restrict__ X, int64_t ldx, int64_t n, int K,
                const double* __restrict__ mu_buf, const DevState* __restrict__ st,
                int mu_sel, int ignore_done, double* __restrict__ part,
                int32_t* __restrict__ labels) {
+    (void)ldx;   // whole 128-point sub-tiles: the padded tail of X is zeros
     if (!ignore_done && st->done) return;
+    constexpr int NP = 4 * NPL;   // points per lane per step
     const int t_it = st->t;
     const double* mu = mu_buf + (size_t)((t_it - mu_sel) & 1) * K * D;
+    const int Kp = large_kpad(K);
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x;
     const int nthr = blockDim.x;
     const int W = nthr >> 5;
     const int lane = tid & 31, warp = tid >> 5;
-    float4* cen = reinterpret_cast<float4*>(smem_raw);                  // [K]
-    double* accS = reinterpret_cast<double*>(cen + K);                  // [W][K][D]
+    float4* cen = reinterpret_cast<float4*>(smem_raw);                  // [Kp]
+    double* accS = reinterpret_cast<double*>(cen + Kp);                 // [W][K][D]
     int* accN = reinterpret_cast<int*>(accS + (size_t)W * K * D);        // [W][K]
     double* warpJ = reinterpret_cast<double*>(accN + W * K + ((W * K) & 1));  // [W]
 
-    for (int k = tid; k < K; k += nthr) {
-        float4 c;
-        c.x = -__double2float_rn(mu[k * D + 0]);
-        c.y = -__double2float_rn(mu[k * D + 1]);
-        c.z = (D == 3) ? -__double2float_rn(mu[k * D + 2]) : 0.0f;
-        c.w = 0.0f;
+    for (int k = tid; k < Kp; k += nthr) {
+        float4 c = make_float4(pos_inf(), pos_inf(), pos_inf(), 0.0f);
+        if (k < K) {
+            c.x = -__double2float_rn(mu[k * D + 0]);
+            c.y = -__double2float_rn(mu[k * D + 1]);
+            c.z = (D == 3) ? -__double2float_rn(mu[k * D + 2]) : 0.0f;
+        }
         cen[k] = c;
     }
     if (MODE & kModeReduce) {
@@ -2427,74 +2493,129 @@ k_assign_large(const float* __restrict__ X, int64_t ldx, int64_t n, int K,
     int* myN = accN + warp * K;
     double J = 0.0;
 
-    const int tileN = 2 * nthr;
-    const int64_t n_tiles = (n + tileN - 1) / tileN;
-
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int64_t p = tile * tileN + 2 * tid;
-        const float2 x = ld_stream2(tile_coord<D>(X, p, 0));
-        const float2 y = ld_stream2(tile_coord<D>(X, p, 1));
-        const float2 z = (D == 3) ? ld_stream2(tile_coord<D>(X, p, 2)) : make_float2(0.f, 0.f);
-
-        float b0 = pos_inf(), b1 = pos_inf();
-        int l0 = 0, l1 = 0;
-        // k = 0 sets the initial best (a +inf distance must still yield label 0)
-        {
-            const float4 c = cen[0];
-            float2 e0 = __fadd2_rn(x, make_float2(c.x, c.x));
-            float2 e1 = __fadd2_rn(y, make_float2(c.y, c.y));
-            float2 s = __fmul2_rn(e0, e0);
-            s = __ffma2_rn(e1, e1, s);
-            if (D == 3) {
-                float2 e2 = __fadd2_rn(z, make_float2(c.z, c.z));
-                s = __ffma2_rn(e2, e2, s);
-            }
-            b0 = s.x;
-            b1 = s.y;
-        }
-#pragma unroll 4
-        for (int k = 1; k < K; ++k) {
-            const float4 c = cen[k];
-            float2 e0 = __fadd2_rn(x, make_float2(c.x, c.x));
-            float2 e1 = __fadd2_rn(y, make_float2(c.y, c.y));
-            float2 s = __fmul2_rn(e0, e0);
-            s = __ffma2_rn(e1, e1, s);
-            if (D == 3) {
-                float2 e2 = __fadd2_rn(z, make_float2(c.z, c.z));
-                s = __ffma2_rn(e2, e2, s);
-            }
-            if (s.x < b0) { b0 = s.x; l0 = k; }
-            if (s.y < b1) { b1 = s.y; l1 = k; }
-        }
-
-        const bool v0 = p < n, v1 = p + 1 < n;
-        if (MODE & kModeLabels) *reinterpret_cast<int2*>(labels + p) = make_int2(l0, l1);
-        if (MODE & kModeReduce) {
-            if (v0) J += (double)b0;
-            if (v1) J += (double)b1;
-            // point 0 of every lane, then point 1 of every lane (fixed order)
+    // warp step = NPL consecutive 128-point sub-tiles
+    const int64_t n_tiles = (n + NPL * kLaneTile - 1) / (NPL * kLaneTile);
+    const int64_t stride = (int64_t)gridDim.x * W;
+    int64_t tile = (int64_t)blockIdx.x * W + warp;
+    LanePts P[NPL];
+    if (tile < n_tiles) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const bool v = h ? v1 : v0;
-                const int lab = h ? l1 : l0;
-                const float cx = h ? x.y : x.x, cy = h ? y.y : y.x, cz = h ? z.y : z.x;
-                unsigned pending = __ballot_sync(0xffffffffu, v);
-                while (pending) {
-                    // lanes still pending with my label
-                    const unsigned peers = __match_any_sync(0xffffffffu, v ? lab : -1 - lane) & pending;
-                    const bool mine = v && (pending >> lane & 1u) && ((peers & ((1u << lane) - 1u)) == 0u);
-                    if (mine) {
-                        double* s = myS + (size_t)lab * D;
-                        s[0] += (double)cx;
-                        s[1] += (double)cy;
-                        if (D == 3) s[2] += (double)cz;
-                        myN[lab] += 1;
+        for (int h = 0; h < NPL; ++h) load_lane_pts<D>(X, tile * NPL + h, lane, P[h]);
+    }
+#pragma unroll 1
+    for (; tile < n_tiles; tile += stride) {
+        LanePts Q[NPL];
+#pragma unroll
+        for (int h = 0; h < NPL; ++h) Q[h] = P[h];
+        if (tile + stride < n_tiles) {
+#pragma unroll
+            for (int h = 0; h < NPL; ++h)
+                load_lane_pts<D>(X, (tile + stride) * NPL + h, lane, Q[h]);
+        }
+
+        float best[NP];
+        int bt[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            best[i] = pos_inf();
+            bt[i] = 0;
+        }
+#pragma unroll 1
+        for (int k0 = 0; k0 < Kp; k0 += kLargeKT) {
+            float s[NP][kLargeKT];
+#pragma unroll
+            for (int u = 0; u < kLargeKT; ++u) {
+                const float4 cc = cen[k0 + u];
+#pragma unroll
+                for (int h = 0; h < NPL; ++h) {
+                    const float2 da = form_d2<D>(P[h].xa, P[h].ya, P[h].za, cc);
+                    const float2 db = form_d2<D>(P[h].xb, P[h].yb, P[h].zb, cc);
+                    s[4 * h + 0][u] = da.x;
+                    s[4 * h + 1][u] = da.y;
+                    s[4 * h + 2][u] = db.x;
+                    s[4 * h + 3][u] = db.y;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < NP; ++i) {
+                const float m = min_tree<kLargeKT>(s[i], best[i]);
+                bt[i] = (m < best[i]) ? k0 : bt[i];
+                best[i] = m;
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < NPL; ++h) {
+            const float px[4] = {P[h].xa.x, P[h].xa.y, P[h].xb.x, P[h].xb.y};
+            const float py[4] = {P[h].ya.x, P[h].ya.y, P[h].yb.x, P[h].yb.y};
+            const float pz[4] = {P[h].za.x, P[h].za.y, P[h].zb.x, P[h].zb.y};
+            int lab[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {   // lowest k of the winning step with d_k == best
+                const int b0 = bt[4 * h + i];
+                const float bv = best[4 * h + i];
+                int l = b0 + kLargeKT;
+#pragma unroll
+                for (int u = kLargeKT - 1; u >= 0; --u) {
+                    const float4 cc = cen[b0 + u];
+                    const float e0 = __fadd_rn(px[i], cc.x), e1 = __fadd_rn(py[i], cc.y);
+                    float d2 = __fmul_rn(e0, e0);
+                    d2 = __fmaf_rn(e1, e1, d2);
+                    if (D == 3) {
+                        const float e2 = __fadd_rn(pz[i], cc.z);
+                        d2 = __fmaf_rn(e2, e2, d2);
+                    }
+                    l = (d2 == bv) ? b0 + u : l;
+                }
+                KM_CHECK(l < K);
+                lab[i] = l;
+            }
+            const int64_t pa = (tile * NPL + h) * kLaneTile + 2 * lane, pb = pa + kWarpTile;
+            if (MODE & kModeLabels) {
+                *reinterpret_cast<int2*>(labels + pa) = make_int2(lab[0], lab[1]);
+                *reinterpret_cast<int2*>(labels + pb) = make_int2(lab[2], lab[3]);
+            }
+            if (MODE & kModeReduce) {
+                const bool v[4] = {pa < n, pa + 1 < n, pb < n, pb + 1 < n};
+                // per point slot i: the lanes sharing a label (match_any) form a
+                // group; its sum is a fixed tree over the group's ranks (pointer
+                // jumping through the next member), and the group's lowest lane
+                // adds it and the group size to the warp's accumulator.  Cost
+                // ~log2(group size) shuffle levels whatever the label mix.
+                const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    if (v[i]) J += (double)best[4 * h + i];
+                    const unsigned peers = __match_any_sync(0xffffffffu, v[i] ? lab[i] : -1 - lane);
+                    const int r = __popc(peers & lt), g = __popc(peers);
+                    const int maxg = __reduce_max_sync(0xffffffffu, (unsigned)g);
+                    double ax = (double)px[i], ay = (double)py[i], az = (double)pz[i];
+                    const unsigned above = peers & (0xfffffffeu << lane);
+                    int nxt = above ? __ffs(above) - 1 : lane;   // rank r + 1
+                    for (int st = 1; st < maxg; st <<= 1) {       // nxt = rank r + st
+                        const double ox = __shfl_sync(0xffffffffu, ax, nxt);
+                        const double oy = __shfl_sync(0xffffffffu, ay, nxt);
+                        const double oz = (D == 3) ? __shfl_sync(0xffffffffu, az, nxt) : 0.0;
+                        const int nn = __shfl_sync(0xffffffffu, nxt, nxt);
+                        if ((r & (2 * st - 1)) == 0 && r + st < g) {
+                            ax += ox;
+                            ay += oy;
+                            if (D == 3) az += oz;
+                        }
+                        nxt = nn;
+                    }
+                    if (v[i] && r == 0) {
+                        double* sp = myS + (size_t)lab[i] * D;
+                        sp[0] += ax;
+                        sp[1] += ay;
+                        if (D == 3) sp[2] += az;
+                        myN[lab[i]] += g;
                     }
                     __syncwarp();
-                    pending &= ~__ballot_sync(0xffffffffu, mine);
                 }
             }
         }
+#pragma unroll
+        for (int h = 0; h < NPL; ++h) P[h] = Q[h];
     }
 
     if (!(MODE & kModeReduce)) return;

@@ -178,6 +178,7 @@ struct kmeans_ctx {
     int* flag = nullptr;
 
     int G = 0, tpb = 0, smem = 0, path = 0;   // G = columns of part (blocks or groups)
+    int large_npl = 1;            // k_assign_large: 128-point sub-tiles per warp step
     int n_chunks = 0;
     int chunk_points = 0;         // points per chunk row (sorted / unsorted differ)
     double* cpart = nullptr;      // n_chunks x row_stride chunk rows (path 0 / sorted)
@@ -463,20 +464,34 @@ int chunk_smem(int d, int K) {
                    : (kp == 8 ? sizeof(km::ChunkSmem<3, 8>) : sizeof(km::ChunkSmem<3, 16>));
 }
 
-LargeFn pick_large(int d, int mode) {
+LargeFn pick_large(int d, int mode, int npl) {
     if (d == 2) {
-        if (mode == 1) return km::k_assign_large<2, 1>;
-        if (mode == 2) return km::k_assign_large<2, 2>;
-        return km::k_assign_large<2, 3>;
+        if (npl == 2) {
+            if (mode == 1) return km::k_assign_large<2, 1, 2>;
+            if (mode == 2) return km::k_assign_large<2, 2, 2>;
+            return km::k_assign_large<2, 3, 2>;
+        }
+        if (mode == 1) return km::k_assign_large<2, 1, 1>;
+        if (mode == 2) return km::k_assign_large<2, 2, 1>;
+        return km::k_assign_large<2, 3, 1>;
     }
-    if (mode == 1) return km::k_assign_large<3, 1>;
-    if (mode == 2) return km::k_assign_large<3, 2>;
-    return km::k_assign_large<3, 3>;
+    if (npl == 2) {
+        if (mode == 1) return km::k_assign_large<3, 1, 2>;
+        if (mode == 2) return km::k_assign_large<3, 2, 2>;
+        return km::k_assign_large<3, 3, 2>;
+    }
+    if (mode == 1) return km::k_assign_large<3, 1, 1>;
+    if (mode == 2) return km::k_assign_large<3, 2, 1>;
+    return km::k_assign_large<3, 3, 1>;
 }
+
+#ifndef KM_LARGE_NPL2
+#define KM_LARGE_NPL2 1   // allow k_assign_large<.., 2> (see configure)
+#endif
 
 int large_smem(int d, int K, int tpb) {
     const int W = tpb / 32;
-    return K * 16 + W * K * d * 8 + (W * K + 1) * 4 + 8 + W * 8;
+    return km::large_kpad(K) * 16 + W * K * d * 8 + (W * K + 1) * 4 + 8 + W * 8;
 }
 
 kmeans_status configure(kmeans_ctx* ctx) {
@@ -599,12 +614,18 @@ kmeans_status configure(kmeans_ctx* ctx) {
             set_error("K=%d needs %d B of shared memory (max %d)", ctx->K, ctx->smem, maxSmem);
             return KMEANS_EINVAL;
         }
-        for (int mode = 1; mode <= 3; ++mode)
-            CK(cudaFuncSetAttribute((const void*)pick_large(ctx->d, mode),
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
+        // two 128-point sub-tiles per warp step where the accumulators leave
+        // room for one block per SM anyway; one (fewer registers) otherwise
         int occ = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &occ, (const void*)pick_large(ctx->d, 1), ctx->tpb, ctx->smem));
+        for (int npl = 1; npl <= 2; ++npl) {
+            for (int mode = 1; mode <= 3; ++mode)
+                CK(cudaFuncSetAttribute((const void*)pick_large(ctx->d, mode, npl),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &occ, (const void*)pick_large(ctx->d, 1, npl), ctx->tpb, ctx->smem));
+            ctx->large_npl = npl;
+            if (occ >= 2 || KM_LARGE_NPL2 == 0) break;
+        }
         occ = std::max(occ, 1);
         ctx->G = sms * occ;  // persistent grid: every SM busy, static tile schedule
     }
@@ -686,7 +707,7 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
             ctx->launches += 1;
         }
     } else {
-        LargeFn f = pick_large(ctx->d, mode);
+        LargeFn f = pick_large(ctx->d, mode, ctx->large_npl);
         if (A) ctx->launches += 1;
         if (A) f<<<ctx->G, ctx->tpb, ctx->smem, ctx->stream>>>(ctx->X, ctx->ldx, ctx->N, ctx->K, ctx->mu,
                                                         ctx->st, mu_sel, ignore_done, ctx->part,

@@ -122,6 +122,22 @@ def test_step_parity_ragged_n(N, sort):
 
 
 @pytest.mark.parametrize("sort", SORT)
+@pytest.mark.parametrize("K,frac", [(40, 1.0), (64, 0.9), (257, 0.5), (1024, 0.97)])
+def test_step_parity_dominant_label(K, frac, sort):
+    """A label mix where one cluster takes most points of every warp (the
+    large-K full scan sums equal labels by a rank tree; up to all 32 lanes of
+    a slot in one group), the rest spread over the other centroids, ragged N."""
+    rng = np.random.default_rng(K)
+    N = 70_001
+    mu = np.zeros((K, 3))
+    mu[1:] = rng.uniform(-50, 50, (K - 1, 3)) + np.sign(rng.standard_normal((K - 1, 3))) * 20
+    own = rng.random(N) < frac
+    X = np.where(own[:, None], rng.normal(0, 1.0, (N, 3)),
+                 mu[rng.integers(1, K, N)] + rng.normal(0, 0.5, (N, 3))).astype(np.float32)
+    check_step(X, mu + rng.normal(0, 1e-3, mu.shape), tag=f"K={K} frac={frac}", sort=sort)
+
+
+@pytest.mark.parametrize("sort", SORT)
 def test_step_parity_exact_ties_and_empty_clusters(sort):
     """Integer data -> exact fp32 distances -> genuine ties (lowest k wins);
     duplicated centroids -> clusters that stay empty (keep mu^t)."""

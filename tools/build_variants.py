@@ -4,6 +4,8 @@ sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(_
 from paper_2405_12052_b200 import build as kb
 
 VARIANTS = {
+    "lnpl1": ("KM_LARGE_NPL2=0",),    # k_assign_large: 4 points per lane at every K
+    "lk16": ("KM_LARGE_KT=16",),      # k_assign_large: 16 centroids per argmin step
     "base": (),
     "c32": ("KM_CHUNK_TILES=32",),
     "st6": ("KM_SORTED_STAGES=6",),
