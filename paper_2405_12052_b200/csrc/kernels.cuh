@@ -2415,6 +2415,10 @@ k_merge_rows(const double* __restrict__ cpart, int n_chunks, int K, double* __re
 #endif
 constexpr int kLargeKT = KM_LARGE_KT;
 static_assert(kLargeKT == 8 || kLargeKT == 16, "argmin step: 8 or 16 centroids");
+#ifndef KM_LARGE_UNROLL
+#define KM_LARGE_UNROLL 1   // argmin steps per loop iteration
+#endif
+constexpr int kLargeUnroll = KM_LARGE_UNROLL;
 
 __host__ __device__ constexpr int large_kpad(int K) {
     return (K + kLargeKT - 1) / kLargeKT * kLargeKT;
@@ -2451,7 +2455,89 @@ __device__ __forceinline__ float min_tree(const float (&v)[KT], float best) {
     }
 }
 
-template <int D, int MODE, int NPL>
+// Negated fl32 centroids (RN) in smem, +inf past K.
+template <int D>
+__device__ __forceinline__ void large_stage(float4* cen, const double* mu, int K, int Kp, int tid,
+                                            int nthr) {
+    for (int k = tid; k < Kp; k += nthr) {
+        float4 c = make_float4(pos_inf(), pos_inf(), pos_inf(), 0.0f);
+        if (k < K) {
+            c.x = -__double2float_rn(mu[k * D + 0]);
+            c.y = -__double2float_rn(mu[k * D + 1]);
+            c.z = (D == 3) ? -__double2float_rn(mu[k * D + 2]) : 0.0f;
+        }
+        cen[k] = c;
+    }
+}
+
+// One point slot of a warp into its accumulators: the lanes sharing a label
+// (match_any) form a group; its sum is a fixed tree over the group's ranks
+// (pointer jumping through the next member), and the group's lowest lane adds
+// it and the group size -- ~log2(group size) shuffle levels whatever the mix.
+template <int D>
+__device__ __forceinline__ void large_accum_slot(bool v, int lab, float x, float y, float z,
+                                                 double* __restrict__ myS, int* __restrict__ myN,
+                                                 int lane) {
+    const unsigned peers = __match_any_sync(0xffffffffu, v ? lab : -1 - lane);
+    const int r = __popc(peers & ((1u << lane) - 1u)), g = __popc(peers);
+    const int maxg = __reduce_max_sync(0xffffffffu, (unsigned)g);
+    double ax = (double)x, ay = (double)y, az = (double)z;
+    const unsigned above = peers & (0xfffffffeu << lane);
+    int nxt = above ? __ffs(above) - 1 : lane;   // rank r + 1
+    for (int st = 1; st < maxg; st <<= 1) {       // nxt = rank r + st
+        const double ox = __shfl_sync(0xffffffffu, ax, nxt);
+        const double oy = __shfl_sync(0xffffffffu, ay, nxt);
+        const double oz = (D == 3) ? __shfl_sync(0xffffffffu, az, nxt) : 0.0;
+        const int nn = __shfl_sync(0xffffffffu, nxt, nxt);
+        if ((r & (2 * st - 1)) == 0 && r + st < g) {
+            ax += ox;
+            ay += oy;
+            if (D == 3) az += oz;
+        }
+        nxt = nn;
+    }
+    if (v && r == 0) {
+        double* sp = myS + (size_t)lab * D;
+        sp[0] += ax;
+        sp[1] += ay;
+        if (D == 3) sp[2] += az;
+        myN[lab] += g;
+    }
+    __syncwarp();
+}
+
+// The block's row: part[e][blockIdx] = sum over warps (warp order) of the
+// per-warp accumulators; J from each warp's lane-order butterfly.
+template <int D>
+__device__ __forceinline__ void large_block_row(const double* accS, const int* accN,
+                                                double* warpJ, double J, int K, int W, int tid,
+                                                int nthr, double* __restrict__ part) {
+    const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) J += __shfl_xor_sync(0xffffffffu, J, o);
+    if (lane == 0) warpJ[warp] = J;
+    __syncthreads();
+    const int G = gridDim.x;
+    const int nE = K * D + K + 1;
+    for (int e = tid; e < nE; e += nthr) {
+        double v = 0.0;
+        if (e < K * D) {
+            for (int w = 0; w < W; ++w) v += accS[(size_t)w * K * D + e];
+        } else if (e < K * D + K) {
+            long long c = 0;
+            for (int w = 0; w < W; ++w) c += accN[w * K + (e - K * D)];
+            v = (double)c;
+        } else {
+            for (int w = 0; w < W; ++w) v += warpJ[w];
+        }
+        part[(size_t)e * G + blockIdx.x] = v;
+    }
+}
+
+// MODE as elsewhere; SPLIT: labels only, no accumulators in smem (the sums
+// come from k_accum_large over the written labels), for K where the per-warp
+// accumulators would cap the warps per SM.
+template <int D, int MODE, int NPL, bool SPLIT = false>
 __global__ void __launch_bounds__(kLargeTPBMax)
 k_assign_large(const float* __restrict__ X, int64_t ldx, int64_t n, int K,
                const double* __restrict__ mu_buf, const DevState* __restrict__ st,
@@ -2460,6 +2546,8 @@ k_assign_large(const float* __restrict__ X, int64_t ldx, int64_t n, int K,
     (void)ldx;   // whole 128-point sub-tiles: the padded tail of X is zeros
     if (!ignore_done && st->done) return;
     constexpr int NP = 4 * NPL;   // points per lane per step
+    constexpr bool RED = !SPLIT && (MODE & kModeReduce);
+    constexpr bool LAB = SPLIT || (MODE & kModeLabels);
     const int t_it = st->t;
     const double* mu = mu_buf + (size_t)((t_it - mu_sel) & 1) * K * D;
     const int Kp = large_kpad(K);
@@ -2474,16 +2562,8 @@ k_assign_large(const float* __restrict__ X, int64_t ldx, int64_t n, int K,
     int* accN = reinterpret_cast<int*>(accS + (size_t)W * K * D);        // [W][K]
     double* warpJ = reinterpret_cast<double*>(accN + W * K + ((W * K) & 1));  // [W]
 
-    for (int k = tid; k < Kp; k += nthr) {
-        float4 c = make_float4(pos_inf(), pos_inf(), pos_inf(), 0.0f);
-        if (k < K) {
-            c.x = -__double2float_rn(mu[k * D + 0]);
-            c.y = -__double2float_rn(mu[k * D + 1]);
-            c.z = (D == 3) ? -__double2float_rn(mu[k * D + 2]) : 0.0f;
-        }
-        cen[k] = c;
-    }
-    if (MODE & kModeReduce) {
+    large_stage<D>(cen, mu, K, Kp, tid, nthr);
+    if (RED) {
         for (int q = tid; q < W * K * D; q += nthr) accS[q] = 0.0;
         for (int q = tid; q < W * K; q += nthr) accN[q] = 0;
     }
@@ -2520,7 +2600,7 @@ k_assign_large(const float* __restrict__ X, int64_t ldx, int64_t n, int K,
             best[i] = pos_inf();
             bt[i] = 0;
         }
-#pragma unroll 1
+#pragma unroll kLargeUnroll
         for (int k0 = 0; k0 < Kp; k0 += kLargeKT) {
             float s[NP][kLargeKT];
 #pragma unroll
@@ -2570,77 +2650,94 @@ k_assign_large(const float* __restrict__ X, int64_t ldx, int64_t n, int K,
                 lab[i] = l;
             }
             const int64_t pa = (tile * NPL + h) * kLaneTile + 2 * lane, pb = pa + kWarpTile;
-            if (MODE & kModeLabels) {
+            if (LAB) {
                 *reinterpret_cast<int2*>(labels + pa) = make_int2(lab[0], lab[1]);
                 *reinterpret_cast<int2*>(labels + pb) = make_int2(lab[2], lab[3]);
             }
-            if (MODE & kModeReduce) {
+            if (RED) {
                 const bool v[4] = {pa < n, pa + 1 < n, pb < n, pb + 1 < n};
-                // per point slot i: the lanes sharing a label (match_any) form a
-                // group; its sum is a fixed tree over the group's ranks (pointer
-                // jumping through the next member), and the group's lowest lane
-                // adds it and the group size to the warp's accumulator.  Cost
-                // ~log2(group size) shuffle levels whatever the label mix.
-                const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
+                for (int i = 0; i < 4; ++i) {   // slot i of every lane, sub-tile order
                     if (v[i]) J += (double)best[4 * h + i];
-                    const unsigned peers = __match_any_sync(0xffffffffu, v[i] ? lab[i] : -1 - lane);
-                    const int r = __popc(peers & lt), g = __popc(peers);
-                    const int maxg = __reduce_max_sync(0xffffffffu, (unsigned)g);
-                    double ax = (double)px[i], ay = (double)py[i], az = (double)pz[i];
-                    const unsigned above = peers & (0xfffffffeu << lane);
-                    int nxt = above ? __ffs(above) - 1 : lane;   // rank r + 1
-                    for (int st = 1; st < maxg; st <<= 1) {       // nxt = rank r + st
-                        const double ox = __shfl_sync(0xffffffffu, ax, nxt);
-                        const double oy = __shfl_sync(0xffffffffu, ay, nxt);
-                        const double oz = (D == 3) ? __shfl_sync(0xffffffffu, az, nxt) : 0.0;
-                        const int nn = __shfl_sync(0xffffffffu, nxt, nxt);
-                        if ((r & (2 * st - 1)) == 0 && r + st < g) {
-                            ax += ox;
-                            ay += oy;
-                            if (D == 3) az += oz;
-                        }
-                        nxt = nn;
-                    }
-                    if (v[i] && r == 0) {
-                        double* sp = myS + (size_t)lab[i] * D;
-                        sp[0] += ax;
-                        sp[1] += ay;
-                        if (D == 3) sp[2] += az;
-                        myN[lab[i]] += g;
-                    }
-                    __syncwarp();
+                    large_accum_slot<D>(v[i], lab[i], px[i], py[i], pz[i], myS, myN, lane);
                 }
             }
         }
 #pragma unroll
         for (int h = 0; h < NPL; ++h) P[h] = Q[h];
     }
+    if (RED) large_block_row<D>(accS, accN, warpJ, J, K, W, tid, nthr, part);
+}
 
-    if (!(MODE & kModeReduce)) return;
-    {
-        double j = J;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) j += __shfl_xor_sync(0xffffffffu, j, o);
-        if (lane == 0) warpJ[warp] = j;
-    }
+// Second pass of the split large-K path: points + their labels -> the block
+// rows.  J re-evaluates form D against the assigned centroid with the same RN
+// operations as the argmin (bit-identical to its minimum); sums as in the
+// fused kernel.  HBM-bound (16 or 12 B per point).
+template <int D>
+__global__ void __launch_bounds__(kLargeTPBMax)
+k_accum_large(const float* __restrict__ X, int64_t n, int K, const double* __restrict__ mu_buf,
+              const DevState* __restrict__ st, int mu_sel, int ignore_done,
+              const int32_t* __restrict__ labels, double* __restrict__ part) {
+    if (!ignore_done && st->done) return;
+    const double* mu = mu_buf + (size_t)((st->t - mu_sel) & 1) * K * D;
+    const int Kp = large_kpad(K);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x, nthr = blockDim.x, W = nthr >> 5;
+    const int lane = tid & 31, warp = tid >> 5;
+    float4* cen = reinterpret_cast<float4*>(smem_raw);
+    double* accS = reinterpret_cast<double*>(cen + Kp);
+    int* accN = reinterpret_cast<int*>(accS + (size_t)W * K * D);
+    double* warpJ = reinterpret_cast<double*>(accN + W * K + ((W * K) & 1));
+    large_stage<D>(cen, mu, K, Kp, tid, nthr);
+    for (int q = tid; q < W * K * D; q += nthr) accS[q] = 0.0;
+    for (int q = tid; q < W * K; q += nthr) accN[q] = 0;
     __syncthreads();
-    const int G = gridDim.x;
-    const int nE = K * D + K + 1;
-    for (int e = tid; e < nE; e += nthr) {
-        double v = 0.0;
-        if (e < K * D) {
-            for (int w = 0; w < W; ++w) v += accS[(size_t)w * K * D + e];
-        } else if (e < K * D + K) {
-            long long c = 0;
-            for (int w = 0; w < W; ++w) c += accN[w * K + (e - K * D)];
-            v = (double)c;
-        } else {
-            for (int w = 0; w < W; ++w) v += warpJ[w];
+    double* myS = accS + (size_t)warp * K * D;
+    int* myN = accN + warp * K;
+    double J = 0.0;
+    const int64_t n_sub = (n + kLaneTile - 1) / kLaneTile;
+    const int64_t stride = (int64_t)gridDim.x * W;
+    int64_t sub = (int64_t)blockIdx.x * W + warp;
+    LanePts P;
+    int2 la = make_int2(0, 0), lb = make_int2(0, 0);
+    auto fetch = [&](int64_t t, LanePts& Q, int2& qa, int2& qb) {
+        load_lane_pts<D>(X, t, lane, Q);
+        const int64_t pa = t * kLaneTile + 2 * lane;
+        qa = __ldcs(reinterpret_cast<const int2*>(labels + pa));
+        qb = __ldcs(reinterpret_cast<const int2*>(labels + pa + kWarpTile));
+    };
+    if (sub < n_sub) fetch(sub, P, la, lb);
+#pragma unroll 1
+    for (; sub < n_sub; sub += stride) {
+        LanePts Q = P;
+        int2 qa = la, qb = lb;
+        if (sub + stride < n_sub) fetch(sub + stride, Q, qa, qb);
+        const int64_t pa = sub * kLaneTile + 2 * lane, pb = pa + kWarpTile;
+        const bool v[4] = {pa < n, pa + 1 < n, pb < n, pb + 1 < n};
+        const int lab[4] = {la.x, la.y, lb.x, lb.y};
+        const float px[4] = {P.xa.x, P.xa.y, P.xb.x, P.xb.y};
+        const float py[4] = {P.ya.x, P.ya.y, P.yb.x, P.yb.y};
+        const float pz[4] = {P.za.x, P.za.y, P.zb.x, P.zb.y};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int l = v[i] ? lab[i] : 0;
+            KM_CHECK(l >= 0 && l < K);
+            const float4 cc = cen[l];
+            const float e0 = __fadd_rn(px[i], cc.x), e1 = __fadd_rn(py[i], cc.y);
+            float d2 = __fmul_rn(e0, e0);
+            d2 = __fmaf_rn(e1, e1, d2);
+            if (D == 3) {
+                const float e2 = __fadd_rn(pz[i], cc.z);
+                d2 = __fmaf_rn(e2, e2, d2);
+            }
+            if (v[i]) J += (double)d2;
+            large_accum_slot<D>(v[i], l, px[i], py[i], pz[i], myS, myN, lane);
         }
-        part[(size_t)e * G + blockIdx.x] = v;
+        P = Q;
+        la = qa;
+        lb = qb;
     }
+    large_block_row<D>(accS, accN, warpJ, J, K, W, tid, nthr, part);
 }
 
 // ---------------------------------------------------------------------------

@@ -179,6 +179,8 @@ struct kmeans_ctx {
 
     int G = 0, tpb = 0, smem = 0, path = 0;   // G = columns of part (blocks or groups)
     int large_npl = 1;            // k_assign_large: 128-point sub-tiles per warp step
+    bool large_split = false;     // large K: labels pass + k_accum_large (see configure)
+    int large_grid1 = 0, large_tpb1 = 0, large_smem1 = 0;   // its labels pass
     int n_chunks = 0;
     int chunk_points = 0;         // points per chunk row (sorted / unsorted differ)
     double* cpart = nullptr;      // n_chunks x row_stride chunk rows (path 0 / sorted)
@@ -312,6 +314,7 @@ bool persist_active(const kmeans_ctx* ctx);
 int kernels_per_iter(const kmeans_ctx* ctx) {
     if (ctx->fused || persist_active(ctx)) return 1;   // one launch covers many iterations
     int n = ctx->sorted ? (ctx->path == 1 ? 6 : 4) : (ctx->path == 0 ? 4 : 3);
+    if (!ctx->sorted && ctx->large_split) n += 1;
     if (fused_update(ctx) || p2p_one_kernel(ctx)) n -= 1;
     return n;
 }
@@ -464,30 +467,48 @@ int chunk_smem(int d, int K) {
                    : (kp == 8 ? sizeof(km::ChunkSmem<3, 8>) : sizeof(km::ChunkSmem<3, 16>));
 }
 
+#ifndef KM_LARGE_SPLIT_WARPS
+#define KM_LARGE_SPLIT_WARPS 8    // split the large-K full scan below this many fused warps / SM
+#endif
+#ifndef KM_LARGE_SPLIT_NPL
+#define KM_LARGE_SPLIT_NPL 3      // sub-tiles per warp step of the labels pass
+#endif
+#ifndef KM_LARGE_SPLIT_TPB
+#define KM_LARGE_SPLIT_TPB 128    // threads per block of the labels pass
+#endif
+#ifndef KM_LARGE_NPL2
+#define KM_LARGE_NPL2 1   // allow the wide k_assign_large step (see configure)
+#endif
+#ifndef KM_LARGE_NPL_BIG
+#define KM_LARGE_NPL_BIG 2   // its 128-point sub-tiles per warp step
+#endif
+
 LargeFn pick_large(int d, int mode, int npl) {
     if (d == 2) {
         if (npl == 2) {
-            if (mode == 1) return km::k_assign_large<2, 1, 2>;
-            if (mode == 2) return km::k_assign_large<2, 2, 2>;
-            return km::k_assign_large<2, 3, 2>;
+            if (mode == 1) return km::k_assign_large<2, 1, KM_LARGE_NPL_BIG>;
+            if (mode == 2) return km::k_assign_large<2, 2, KM_LARGE_NPL_BIG>;
+            return km::k_assign_large<2, 3, KM_LARGE_NPL_BIG>;
         }
         if (mode == 1) return km::k_assign_large<2, 1, 1>;
         if (mode == 2) return km::k_assign_large<2, 2, 1>;
         return km::k_assign_large<2, 3, 1>;
     }
     if (npl == 2) {
-        if (mode == 1) return km::k_assign_large<3, 1, 2>;
-        if (mode == 2) return km::k_assign_large<3, 2, 2>;
-        return km::k_assign_large<3, 3, 2>;
+        if (mode == 1) return km::k_assign_large<3, 1, KM_LARGE_NPL_BIG>;
+        if (mode == 2) return km::k_assign_large<3, 2, KM_LARGE_NPL_BIG>;
+        return km::k_assign_large<3, 3, KM_LARGE_NPL_BIG>;
     }
     if (mode == 1) return km::k_assign_large<3, 1, 1>;
     if (mode == 2) return km::k_assign_large<3, 2, 1>;
     return km::k_assign_large<3, 3, 1>;
 }
 
-#ifndef KM_LARGE_NPL2
-#define KM_LARGE_NPL2 1   // allow k_assign_large<.., 2> (see configure)
-#endif
+
+LargeFn pick_large_labels(int d) {
+    return d == 2 ? km::k_assign_large<2, 2, KM_LARGE_SPLIT_NPL, true>
+                  : km::k_assign_large<3, 2, KM_LARGE_SPLIT_NPL, true>;
+}
 
 int large_smem(int d, int K, int tpb) {
     const int W = tpb / 32;
@@ -628,6 +649,31 @@ kmeans_status configure(kmeans_ctx* ctx) {
         }
         occ = std::max(occ, 1);
         ctx->G = sms * occ;  // persistent grid: every SM busy, static tile schedule
+        // Where the per-warp accumulators cap the fused kernel below
+        // KM_LARGE_SPLIT_WARPS warps per SM (K >= ~500 in 3D), split it: an
+        // argmin pass with only the centroids in smem (occupancy set by
+        // registers) writes the labels, then k_accum_large (the fused
+        // kernel's grid, block and smem) sums points by label -- 16 B per
+        // point more HBM traffic for ~2x the warps on the FP32-bound pass.
+        ctx->large_split = occ * (ctx->tpb / 32) < KM_LARGE_SPLIT_WARPS;
+        if (ctx->large_split) {
+            auto acc = ctx->d == 2 ? km::k_accum_large<2> : km::k_accum_large<3>;
+            CK(cudaFuncSetAttribute((const void*)acc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    ctx->smem));
+            int occ2 = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, (const void*)acc, ctx->tpb,
+                                                             ctx->smem));
+            ctx->G = sms * std::max(occ2, 1);
+            ctx->large_tpb1 = KM_LARGE_SPLIT_TPB;
+            ctx->large_smem1 = km::large_kpad(ctx->K) * 16;
+            int occ1 = 0;
+            CK(cudaFuncSetAttribute((const void*)pick_large_labels(ctx->d),
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->large_smem1));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &occ1, (const void*)pick_large_labels(ctx->d), ctx->large_tpb1, ctx->large_smem1));
+            ctx->large_grid1 = sms * std::max(occ1, 1);
+            if (!ctx->labels) CK(pool_alloc(ctx, &ctx->labels, sizeof(int32_t) * ctx->ldx));
+        }
     }
     return KMEANS_OK;
 }
@@ -707,11 +753,26 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
             ctx->launches += 1;
         }
     } else {
-        LargeFn f = pick_large(ctx->d, mode, ctx->large_npl);
-        if (A) ctx->launches += 1;
-        if (A) f<<<ctx->G, ctx->tpb, ctx->smem, ctx->stream>>>(ctx->X, ctx->ldx, ctx->N, ctx->K, ctx->mu,
-                                                        ctx->st, mu_sel, ignore_done, ctx->part,
-                                                        ctx->labels);
+        if (A && ctx->large_split) {
+            pick_large_labels(ctx->d)<<<ctx->large_grid1, ctx->large_tpb1, ctx->large_smem1,
+                                        ctx->stream>>>(ctx->X, ctx->ldx, ctx->N, ctx->K, ctx->mu,
+                                                       ctx->st, mu_sel, ignore_done, nullptr,
+                                                       ctx->labels);
+            ctx->launches += 1;
+            if (mode & km::kModeReduce) {
+                (ctx->d == 2 ? km::k_accum_large<2> : km::k_accum_large<3>)
+                    <<<ctx->G, ctx->tpb, ctx->smem, ctx->stream>>>(
+                        ctx->X, ctx->N, ctx->K, ctx->mu, ctx->st, mu_sel, ignore_done,
+                        ctx->labels, ctx->part);
+                ctx->launches += 1;
+            }
+        } else if (A) {
+            LargeFn f = pick_large(ctx->d, mode, ctx->large_npl);
+            ctx->launches += 1;
+            f<<<ctx->G, ctx->tpb, ctx->smem, ctx->stream>>>(ctx->X, ctx->ldx, ctx->N, ctx->K,
+                                                            ctx->mu, ctx->st, mu_sel, ignore_done,
+                                                            ctx->part, ctx->labels);
+        }
     }
     CK(cudaGetLastError());
     if (A && (mode & km::kModeLabels) && ctx->sorted) {

@@ -6,6 +6,14 @@ from paper_2405_12052_b200 import build as kb
 VARIANTS = {
     "lnpl1": ("KM_LARGE_NPL2=0",),    # k_assign_large: 4 points per lane at every K
     "lk16": ("KM_LARGE_KT=16",),      # k_assign_large: 16 centroids per argmin step
+    "lnpl3": ("KM_LARGE_NPL_BIG=3",),  # k_assign_large: 12 points per lane at large K
+    "lu2": ("KM_LARGE_UNROLL=2",),     # k_assign_large: two argmin steps per loop trip
+    "lnosplit": ("KM_LARGE_SPLIT_WARPS=0",),   # large K: never split into labels + accumulate
+    "lsnpl1": ("KM_LARGE_SPLIT_NPL=1",),       # split labels pass: 4 points per lane
+    "lsnpl2": ("KM_LARGE_SPLIT_NPL=2",),       # split labels pass: 8 points per lane
+    "lnb3": ("KM_LARGE_NPL_BIG=3",),           # fused, one block per SM: 12 points per lane
+    "lsplit64": ("KM_LARGE_SPLIT_WARPS=64",),  # split at every large K
+    "lsplit12": ("KM_LARGE_SPLIT_WARPS=12",),  # split below 12 fused warps per SM
     "base": (),
     "c32": ("KM_CHUNK_TILES=32",),
     "st6": ("KM_SORTED_STAGES=6",),
