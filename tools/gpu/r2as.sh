@@ -1,0 +1,8 @@
+# round 2, call as: label groups by per-bit ballots instead of MATCH.ANY
+set -x
+timeout -s KILL 600 python -m pytest tests/test_gpu_parity.py -x -q -k "k_sweep or ragged or ties or dominant or configs or full_size_c5 or deterministic" > gpurun_out/r2as_tests.txt 2>&1; echo "rc=$?" >> gpurun_out/r2as_tests.txt
+timeout -s KILL 300 python tools/sweep.py paper_2405_12052_b200/libkmeans.so --workload C5 --no-sort --reps 5 --iters 2 >> gpurun_out/r2as_sweep.txt 2>&1
+for K in 64 200 600; do
+timeout -s KILL 300 python tools/sweep.py paper_2405_12052_b200/libkmeans.so --workload C5 --no-sort --K $K --N 20000000 --reps 10 --iters 2 >> gpurun_out/r2as_sweep.txt 2>&1
+done
+timeout -s KILL 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k "regex:k_accum_large" -c 2 --csv --log-file gpurun_out/r2as_accum.csv python tools/sweep.py paper_2405_12052_b200/libkmeans.so --workload C5 --no-sort --reps 1 --iters 1 > gpurun_out/r2as_ncu.log 2>&1
