@@ -263,6 +263,9 @@ constexpr int kLaneTile = 2 * kWarpTile;                 // 128 points per warp-
 #ifndef KM_TWO_CAND_PRED
 #define KM_TWO_CAND_PRED 1   // two-candidate chunks: predicated adds instead of +0.0 selects
 #endif
+#ifndef KM_AGG_TRANSPOSE
+#define KM_AGG_TRANSPOSE 1   // slot sums by a transposing butterfly (see pruned_body's agg)
+#endif
 #ifndef KM_CAND_UNROLL2
 #define KM_CAND_UNROLL2 1   // multi-candidate argmin: two candidates per loop step
 #endif
@@ -1233,6 +1236,23 @@ __device__ __forceinline__ void pruned_body(const float4* cand, const int* candk
                     ++c;
                 }
             }
+#if KM_AGG_TRANSPOSE
+            // (Sx, Sy, Sz, n) over the 32 lanes by a transposing butterfly:
+            // the offset-16 step trades half the values (each half-warp keeps
+            // a pair), the offset-8 step half again, then three plain steps
+            // on one value -- 7 fp64 shuffles and 6 adds instead of 15 and 15
+            // plus a REDUX; lane 8 j ends with value j (fixed order).
+            const bool up16 = lane & 16, up8 = lane & 8;
+            double k0 = up16 ? sz : sx, k1 = up16 ? (double)c : sy;
+            const double o0 = up16 ? sx : sz, o1 = up16 ? sy : (double)c;
+            k0 += __shfl_xor_sync(0xffffffffu, o0, 16);
+            k1 += __shfl_xor_sync(0xffffffffu, o1, 16);
+            double kv = up8 ? k1 : k0;
+            kv += __shfl_xor_sync(0xffffffffu, up8 ? k0 : k1, 8);
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) kv += __shfl_xor_sync(0xffffffffu, kv, o);
+            if ((lane & 7) == 0) T[4 * q + (lane >> 3)] += kv;
+#else
             const unsigned cnt = __reduce_add_sync(0xffffffffu, c);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
@@ -1247,6 +1267,7 @@ __device__ __forceinline__ void pruned_body(const float4* cand, const int* candk
                 t[2] += sz;
                 t[3] += (double)cnt;
             }
+#endif
         }
         __syncwarp();
     };

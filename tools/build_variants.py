@@ -8,6 +8,7 @@ VARIANTS = {
     "lk16": ("KM_LARGE_KT=16",),      # k_assign_large: 16 centroids per argmin step
     "lnpl3": ("KM_LARGE_NPL_BIG=3",),  # k_assign_large: 12 points per lane at large K
     "lu2": ("KM_LARGE_UNROLL=2",),     # k_assign_large: two argmin steps per loop trip
+    "aggbfly": ("KM_AGG_TRANSPOSE=0",),      # pruned slot sums: plain 5-level butterflies
     "lnosplit": ("KM_LARGE_SPLIT_WARPS=0",),   # large K: never split into labels + accumulate
     "lsnpl1": ("KM_LARGE_SPLIT_NPL=1",),       # split labels pass: 4 points per lane
     "lsnpl2": ("KM_LARGE_SPLIT_NPL=2",),       # split labels pass: 8 points per lane
