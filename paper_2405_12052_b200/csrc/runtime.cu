@@ -122,6 +122,29 @@ cudaError_t cached_malloc(int dev, void** p, size_t bytes) {
     return e;
 }
 
+// Pinned host blocks for the device state mirror (one per context):
+// cudaMallocHost / cudaFreeHost synchronise the device and page-lock memory,
+// milliseconds per create / destroy, so idle blocks are kept for the next one.
+std::vector<void*> g_pinned_state;
+
+cudaError_t pinned_state_get(void** p, size_t bytes) {
+    {
+        std::lock_guard<std::mutex> lk(g_mem_mu);
+        if (!g_pinned_state.empty()) {
+            *p = g_pinned_state.back();
+            g_pinned_state.pop_back();
+            return cudaSuccess;
+        }
+    }
+    return cudaMallocHost(p, bytes);
+}
+
+void pinned_state_put(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_mem_mu);
+    g_pinned_state.push_back(p);
+}
+
 void cached_free(void* p) {
     if (!p) return;
     std::lock_guard<std::mutex> lk(g_mem_mu);
@@ -235,18 +258,19 @@ namespace {
 // (synchronising the stream at every mark -- a tuning aid, off by default).
 struct CreateTrace {
     bool on = false;
+    const char* tag;
     std::chrono::steady_clock::time_point t0;
-    CreateTrace() {
+    explicit CreateTrace(const char* t = "kmeans_create") : tag(t) {
         const char* e = getenv("KMEANS_TRACE");
         on = e && *e && *e != '0';
         t0 = std::chrono::steady_clock::now();
     }
     void mark(cudaStream_t s, const char* what) {
         if (!on) return;
-        cudaStreamSynchronize(s);
+        if (s) cudaStreamSynchronize(s);
         const double ms =
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-        fprintf(stderr, "[kmeans_create] %8.2f ms  %s\n", ms, what);
+        fprintf(stderr, "[%s] %8.2f ms  %s\n", tag, ms, what);
     }
 };
 
@@ -1500,16 +1524,19 @@ void kmeans_destroy(kmeans_ctx* ctx) {
     if (!ctx) return;
     {
         DeviceGuard g(ctx->device);
+        CreateTrace tr("kmeans_destroy");
         if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+        tr.mark(nullptr, "stream idle");
         if (ctx->graph) cudaGraphExecDestroy(ctx->graph);
         if (ctx->graph_u) cudaGraphExecDestroy(ctx->graph_u);
+        tr.mark(nullptr, "graphs destroyed");
         pool_free(ctx, ctx->X);
         pool_free(ctx, ctx->mu);
         pool_free(ctx, ctx->cneg);
         pool_free(ctx, ctx->part);
         pool_free(ctx, ctx->red);
         pool_free(ctx, ctx->st);
-        if (ctx->st_host) cudaFreeHost(ctx->st_host);
+        pinned_state_put(ctx->st_host);
         pool_free(ctx, ctx->trace_E);
         pool_free(ctx, ctx->trace_J);
         pool_free(ctx, ctx->labels);
@@ -1533,7 +1560,9 @@ void kmeans_destroy(kmeans_ctx* ctx) {
         for (void* p : ctx->xopened) cudaIpcCloseMemHandle(p);
         if (ctx->xown) cudaFree(ctx->xown);
         pool_free(ctx, ctx->xtab);
+        tr.mark(nullptr, "buffers back to the cache");
         if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+        tr.mark(nullptr, "stream destroyed");
         cudaGetLastError();
     }
     delete ctx;
@@ -1654,7 +1683,7 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
         pool_alloc(ctx, &ctx->part, sizeof(double) * (size_t)ctx->nE * ctx->G) != cudaSuccess ||
         pool_alloc(ctx, &ctx->red, sizeof(double) * ctx->nE) != cudaSuccess ||
         pool_alloc(ctx, &ctx->st, sizeof(DevState)) != cudaSuccess ||
-        cudaMallocHost(&ctx->st_host, sizeof(DevState)) != cudaSuccess ||
+        pinned_state_get(reinterpret_cast<void**>(&ctx->st_host), sizeof(DevState)) != cudaSuccess ||
         pool_alloc(ctx, &ctx->idx_dev, sizeof(int64_t) * K) != cudaSuccess ||
         ((ctx->path == 0 || ctx->sorted) &&
          pool_alloc(ctx, &ctx->cpart, sizeof(double) * ctx->row_stride * (size_t)ctx->n_chunks) !=
