@@ -566,6 +566,31 @@ def test_generator_and_memory_cache_edges():
     assert np.array_equal(a["centroids"], b["centroids"])
 
 
+def test_interleaved_contexts_reuse_cached_blocks():
+    """Contexts created and destroyed in an interleaved order (device blocks
+    and the pinned state mirrors come back from the caches) each keep their
+    own state: every run matches a run on a fresh context, and the stop rule
+    of one does not leak into another."""
+    w = datagen.WORKLOADS["C2"]
+    X = datagen.generate(w, N=40_000)
+    init = datagen.init_indices(w, N=40_000)
+    with km.Context(X, 8) as c:
+        ref = c.fit(init, 0.0, 4)
+        ref_conv = c.fit(init, 1e-6, 100)
+    live = []
+    for i in range(24):
+        live.append(km.Context(X, 8, sort=bool(i % 2)))
+        if i % 3 == 2:   # destroy an older one while others stay alive
+            live.pop(0).close()
+    for i, c in enumerate(live):
+        r = c.fit(init, 0.0, 4) if i % 2 else c.fit(init, 1e-6, 100)
+        e = ref if i % 2 else ref_conv
+        assert r["iters"] == e["iters"], i
+        assert np.allclose(r["centroids"], e["centroids"], rtol=1e-9, atol=1e-9), i
+    for c in live:
+        c.close()
+
+
 @pytest.mark.parametrize("P,n,rounds", [(1, 5, 3), (2, 65, 6), (3, 1, 4), (8, 4097, 5),
                                          (16, 33, 9), (64, 200, 3)])
 def test_p2p_exchange_protocol_emulated(P, n, rounds):
