@@ -2197,21 +2197,24 @@ k_merge_sparse(const double* __restrict__ rows, int row_stride, int n_chunks, in
 // entries w, w + nwarp, ... four at a time so that 16 loads are in flight per
 // lane.
 // ---------------------------------------------------------------------------
+template <int R = 4>   // entries per warp per pass (all loads of a pass in flight at once)
 __device__ __forceinline__ void block_merge_groups(const double* part, int G, int nE,
                                                    double* rs, double* red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-    for (int e0 = warp; e0 < nE; e0 += 4 * nwarp) {
-        double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int e0 = warp; e0 < nE; e0 += R * nwarp) {
+        double v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = 0.0;
 #pragma unroll 4
         for (int b = lane; b < G; b += 32) {
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
+            for (int r = 0; r < R; ++r) {
                 const int e = e0 + r * nwarp;
                 if (e < nE) v[r] += __ldcg(part + (size_t)e * G + b);   // L2: may be written by other blocks of this kernel
             }
         }
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < R; ++r) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) v[r] += __shfl_xor_sync(0xffffffffu, v[r], o);
             const int e = e0 + r * nwarp;
@@ -3055,7 +3058,9 @@ k_fused_iterate(const float* __restrict__ X, int64_t n, int K, int n_chunks,
         }
         grid.sync();
         // every block: the merged vector (k_merge order) and the update
-        block_merge_groups(bp, G, nE, rs, b == 0 ? red : nullptr);
+        // one pass: every entry's loads in flight at once (nE <= 8 R)
+        block_merge_groups<(KP * (D + 1) + 1 + kFusedWarps - 1) / kFusedWarps>(
+            bp, G, nE, rs, b == 0 ? red : nullptr);
         __syncthreads();
         for (int q = tid; q < K * D; q += blockDim.x) {
             const double nk = rs[K * D + q / D];
