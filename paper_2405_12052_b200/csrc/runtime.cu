@@ -385,6 +385,22 @@ using ChunkFn = void (*)(const float*, int64_t, int, const double*, const DevSta
 using LargeFn = void (*)(const float*, int64_t, int64_t, int, const double*, const DevState*,
                          int, int, double*, int32_t*);
 
+// Raise (never lower) a kernel's dynamic shared memory limit: the attribute
+// is per function and process-wide, so contexts with different sizes (K, N)
+// must not shrink it under one another.
+cudaError_t allow_smem(const void* f, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, int> set;   // (device, kernel) -> bytes
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    int& cur = set[{dev, f}];
+    if (bytes <= cur) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) cur = bytes;
+    return e;
+}
+
 int small_kp(int K) { return K <= 4 ? 4 : (K <= 8 ? 8 : 16); }
 
 using FusedFn = void (*)(const float*, int64_t, int, int, double*, DevState*, double*, double*,
@@ -566,9 +582,7 @@ kmeans_status configure(kmeans_ctx* ctx) {
             ctx->keep_n = (int64_t)(mb * 1e6 / (4.0 * ctx->d));
         }
         for (int mode = 1; mode <= 3; ++mode)
-            CK(cudaFuncSetAttribute(
-                (const void*)pick_pruned(ctx->d, ctx->K, mode, ctx->chunk_points),
-                cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
+            CK(allow_smem((const void*)pick_pruned(ctx->d, ctx->K, mode, ctx->chunk_points), ctx->smem));
         ctx->n_chunks = (int)((ctx->N + ctx->chunk_points - 1) / ctx->chunk_points);
         // sparse rows: <= 16 entries (k_merge_sparse16) or up to K (k_merge_sparse)
         ctx->row_stride = ctx->K <= 16 ? km::kRowDoubles : km::kRowHead + 4 * km::large_row_entries(ctx->K);
@@ -577,19 +591,15 @@ kmeans_status configure(kmeans_ctx* ctx) {
                               : (ctx->n_chunks + km::kGroupChunks - 1) / km::kGroupChunks;
         ctx->n_super = (ctx->n_chunks + km::kSuperChunks - 1) / km::kSuperChunks;
         ctx->merge_smem = 4 * ctx->K * (int)sizeof(double);   // k_merge_sparse table
-        CK(cudaFuncSetAttribute((const void*)km::k_merge_sparse<2>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->merge_smem));
-        CK(cudaFuncSetAttribute((const void*)km::k_merge_sparse<3>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->merge_smem));
+        CK(allow_smem((const void*)km::k_merge_sparse<2>, ctx->merge_smem));
+        CK(allow_smem((const void*)km::k_merge_sparse<3>, ctx->merge_smem));
         if (ctx->path == 1) {
             // per-warp slot tables and entry lists, the staged super list (K
             // float4), then 8 tile lists of K u16
             ctx->heavy_smem = (int)(sizeof(km::HeavySmem<3>) + sizeof(float4) * ctx->K +
                                     sizeof(unsigned short) * km::kHeavyWarps * ctx->K);
             for (int mode = 1; mode <= 3; ++mode)
-                CK(cudaFuncSetAttribute((const void*)pick_heavy(ctx->d, mode),
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        ctx->heavy_smem));
+                CK(allow_smem((const void*)pick_heavy(ctx->d, mode), ctx->heavy_smem));
             int hocc = 0;   // one resident block per heavy chunk when possible
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &hocc, (const void*)pick_heavy(ctx->d, 1), 256, ctx->heavy_smem));
@@ -605,8 +615,7 @@ kmeans_status configure(kmeans_ctx* ctx) {
                 cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device) ==
                     cudaSuccess &&
                 coop &&
-                cudaFuncSetAttribute((const void*)pf, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     ctx->persist_smem) == cudaSuccess &&
+                allow_smem((const void*)pf, ctx->persist_smem) == cudaSuccess &&
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)pf, W * 32,
                                                               ctx->persist_smem) == cudaSuccess &&
                 occ >= 1) {
@@ -621,8 +630,7 @@ kmeans_status configure(kmeans_ctx* ctx) {
         ctx->tpb = 32;
         ctx->smem = chunk_smem(ctx->d, ctx->K);
         for (int mode = 1; mode <= 3; ++mode)
-            CK(cudaFuncSetAttribute((const void*)pick_chunk(ctx->d, ctx->K, mode),
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
+            CK(allow_smem((const void*)pick_chunk(ctx->d, ctx->K, mode), ctx->smem));
         ctx->chunk_points = km::kChunkPoints;
         ctx->n_chunks = (int)((ctx->N + ctx->chunk_points - 1) / ctx->chunk_points);
         ctx->row_stride = km::kRowDoubles;
@@ -634,8 +642,7 @@ kmeans_status configure(kmeans_ctx* ctx) {
             FusedFn ff = pick_fused(ctx->d, ctx->K);
             int occ = 0;
             if (ctx->fused_smem <= maxSmem &&
-                cudaFuncSetAttribute((const void*)ff, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     ctx->fused_smem) == cudaSuccess &&
+                allow_smem((const void*)ff, ctx->fused_smem) == cudaSuccess &&
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)ff,
                                                               km::kFusedWarps * 32,
                                                               ctx->fused_smem) == cudaSuccess &&
@@ -664,8 +671,7 @@ kmeans_status configure(kmeans_ctx* ctx) {
         int occ = 0;
         for (int npl = 1; npl <= 2; ++npl) {
             for (int mode = 1; mode <= 3; ++mode)
-                CK(cudaFuncSetAttribute((const void*)pick_large(ctx->d, mode, npl),
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->smem));
+                CK(allow_smem((const void*)pick_large(ctx->d, mode, npl), ctx->smem));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &occ, (const void*)pick_large(ctx->d, 1, npl), ctx->tpb, ctx->smem));
             ctx->large_npl = npl;
@@ -682,8 +688,7 @@ kmeans_status configure(kmeans_ctx* ctx) {
         ctx->large_split = occ * (ctx->tpb / 32) < KM_LARGE_SPLIT_WARPS;
         if (ctx->large_split) {
             auto acc = ctx->d == 2 ? km::k_accum_large<2> : km::k_accum_large<3>;
-            CK(cudaFuncSetAttribute((const void*)acc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    ctx->smem));
+            CK(allow_smem((const void*)acc, ctx->smem));
             int occ2 = 0;
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, (const void*)acc, ctx->tpb,
                                                              ctx->smem));
@@ -691,8 +696,7 @@ kmeans_status configure(kmeans_ctx* ctx) {
             ctx->large_tpb1 = KM_LARGE_SPLIT_TPB;
             ctx->large_smem1 = km::large_kpad(ctx->K) * 16;
             int occ1 = 0;
-            CK(cudaFuncSetAttribute((const void*)pick_large_labels(ctx->d),
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->large_smem1));
+            CK(allow_smem((const void*)pick_large_labels(ctx->d), ctx->large_smem1));
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                 &occ1, (const void*)pick_large_labels(ctx->d), ctx->large_tpb1, ctx->large_smem1));
             ctx->large_grid1 = sms * std::max(occ1, 1);

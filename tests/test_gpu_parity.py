@@ -566,6 +566,43 @@ def test_generator_and_memory_cache_edges():
     assert np.array_equal(a["centroids"], b["centroids"])
 
 
+def test_contexts_with_different_smem_sizes_interleave():
+    """Kernels' shared-memory limits are process-wide: a context needing
+    less (smaller K, smaller shard) must not shrink the limit under a live
+    context that needs more (the large-K full scan)."""
+    w = datagen.WORKLOADS["C5"]
+    X = datagen.generate(w, N=60_000)
+    # the same k_assign_large instance (8 points per lane, one block per SM)
+    # at ~144 KB and ~120 KB of shared memory
+    big = km.Context(X, 600, sort=False)
+    small = km.Context(X[:20_000], 500, sort=False)
+    mu_b = perturbed_centroids(X, 600, 7)
+    mu_s = perturbed_centroids(X[:20_000], 500, 8)
+    try:
+        gb = big.assign(mu_b)
+        gs = small.assign(mu_s)
+        gb2 = big.assign(mu_b)                # after the small context configured
+        assert np.array_equal(gb["labels"], gb2["labels"])
+        assert np.array_equal(gb["labels"], oracle.step(X, mu_b)["labels"])
+        assert np.array_equal(gs["labels"], oracle.step(X[:20_000], mu_s)["labels"])
+    finally:
+        big.close()
+        small.close()
+    w2 = datagen.WORKLOADS["C2"]
+    Xa = datagen.generate(w2, N=400_000)      # fused kernel
+    init = datagen.init_indices(w2, N=400_000)
+    a = km.Context(Xa, 8)
+    b = km.Context(Xa[:5_000], 8)             # fused, smaller grid
+    try:
+        ra = a.fit(init, 0.0, 3)
+        b.fit(datagen.init_indices(w2, N=5_000), 0.0, 3)
+        ra2 = a.fit(init, 0.0, 3)
+        assert np.array_equal(ra["centroids"], ra2["centroids"])
+    finally:
+        a.close()
+        b.close()
+
+
 def test_interleaved_contexts_reuse_cached_blocks():
     """Contexts created and destroyed in an interleaved order (device blocks
     and the pinned state mirrors come back from the caches) each keep their
