@@ -2168,6 +2168,13 @@ kmeans_status kmeans_candidate_stats(kmeans_ctx* ctx, double* mean, int* max, in
         mx = std::max(mx, v);
         one += (v == 1);
     }
+    if (getenv("KMEANS_TRACE") && *getenv("KMEANS_TRACE") && *getenv("KMEANS_TRACE") != '0') {
+        std::map<int, int64_t> h;   // candidates per chunk -> chunks (tuning aid)
+        for (int v : c) h[std::min(v, 65)] += 1;
+        fprintf(stderr, "[kmeans_candidate_stats] chunks by candidate count:");
+        for (auto& kv : h) fprintf(stderr, " %d:%lld", kv.first, (long long)kv.second);
+        fprintf(stderr, "\n");
+    }
     if (mean) *mean = c.empty() ? 0.0 : sum / c.size();
     if (max) *max = mx;
     if (single) *single = one;
