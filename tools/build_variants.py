@@ -33,6 +33,7 @@ VARIANTS = {
     "c8u1st3": ("KM_CHUNK_TILES=8", "KM_SORTED_UNIT_SUB=1", "KM_SORTED_STAGES=3"),
     "c8st2": ("KM_CHUNK_TILES=8", "KM_SORTED_STAGES=2"),
     "c2u1st2": ("KM_CHUNK_TILES=2", "KM_SORTED_UNIT_SUB=1", "KM_SORTED_STAGES=2"),
+    "rg64": ("KM_ROW_GROUP=64",),
     "rg128": ("KM_ROW_GROUP=128",),
     "rg256": ("KM_ROW_GROUP=256",),
     "rg512": ("KM_ROW_GROUP=512",),
