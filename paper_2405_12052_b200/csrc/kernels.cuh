@@ -263,6 +263,9 @@ constexpr int kLaneTile = 2 * kWarpTile;                 // 128 points per warp-
 #ifndef KM_TWO_CAND_PRED
 #define KM_TWO_CAND_PRED 1   // two-candidate chunks: predicated adds instead of +0.0 selects
 #endif
+#ifndef KM_AGG_UNIT
+#define KM_AGG_UNIT 1   // large K: slot sums per TMA unit (8 points per lane), not per warp-tile
+#endif
 #ifndef KM_AGG_TRANSPOSE
 #define KM_AGG_TRANSPOSE 1   // slot sums by a transposing butterfly (see pruned_body's agg)
 #endif
@@ -1271,6 +1274,10 @@ __device__ __forceinline__ void pruned_body(const float4* cand, const int* candk
         }
         __syncwarp();
     };
+    // large K: one slot aggregation per 256-point TMA unit (8 points per lane;
+    // fewer butterflies: C5 assign 0.276 -> 0.265 ms); small K (where >= 3
+    // candidates are rare) per warp-tile (the unit form measured slower there)
+    constexpr bool kUnitAgg = KM_AGG_UNIT && SLOTS > 16;
 #pragma unroll 1
     for (int u = 0; u < nunit; ++u) {
         LanePts P[kUnitSub];
@@ -1332,11 +1339,26 @@ __device__ __forceinline__ void pruned_body(const float4* cand, const int* candk
                 us[4 * h + 1] = s1;
                 us[4 * h + 2] = s2;
                 us[4 * h + 3] = s3;
-                const float xx[4] = {P[h].xa.x, P[h].xa.y, P[h].xb.x, P[h].xb.y};
-                const float yy[4] = {P[h].ya.x, P[h].ya.y, P[h].yb.x, P[h].yb.y};
-                const float zz[4] = {P[h].za.x, P[h].za.y, P[h].zb.x, P[h].zb.y};
-                agg(std::integral_constant<int, 4>{}, uv + 4 * h, us + 4 * h, xx, yy, zz);
+                if constexpr (!kUnitAgg) {
+                    const float xx[4] = {P[h].xa.x, P[h].xa.y, P[h].xb.x, P[h].xb.y};
+                    const float yy[4] = {P[h].ya.x, P[h].ya.y, P[h].yb.x, P[h].yb.y};
+                    const float zz[4] = {P[h].za.x, P[h].za.y, P[h].zb.x, P[h].zb.y};
+                    agg(std::integral_constant<int, 4>{}, uv + 4 * h, us + 4 * h, xx, yy, zz);
+                }
             }
+        }
+        if constexpr (kUnitAgg && (MODE & kModeReduce)) {   // the whole unit's points at once
+            float xx[4 * kUnitSub], yy[4 * kUnitSub], zz[4 * kUnitSub];
+#pragma unroll
+            for (int h = 0; h < kUnitSub; ++h) {
+                xx[4 * h + 0] = P[h].xa.x; xx[4 * h + 1] = P[h].xa.y;
+                xx[4 * h + 2] = P[h].xb.x; xx[4 * h + 3] = P[h].xb.y;
+                yy[4 * h + 0] = P[h].ya.x; yy[4 * h + 1] = P[h].ya.y;
+                yy[4 * h + 2] = P[h].yb.x; yy[4 * h + 3] = P[h].yb.y;
+                zz[4 * h + 0] = P[h].za.x; zz[4 * h + 1] = P[h].za.y;
+                zz[4 * h + 2] = P[h].zb.x; zz[4 * h + 3] = P[h].zb.y;
+            }
+            agg(std::integral_constant<int, 4 * kUnitSub>{}, uv, us, xx, yy, zz);
         }
     }
     if (!(MODE & kModeReduce)) return;
