@@ -1278,6 +1278,7 @@ __device__ __forceinline__ void pruned_body(const float4* cand, const int* candk
     // fewer butterflies: C5 assign 0.276 -> 0.265 ms); small K (where >= 3
     // candidates are rare) per warp-tile (the unit form measured slower there)
     constexpr bool kUnitAgg = KM_AGG_UNIT && SLOTS > 16;
+    const int remc = rem < (int64_t)0x7fffffff ? (int)rem : 0x7fffffff;
 #pragma unroll 1
     for (int u = 0; u < nunit; ++u) {
         LanePts P[kUnitSub];
@@ -1327,14 +1328,18 @@ __device__ __forceinline__ void pruned_body(const float4* cand, const int* candk
                 *reinterpret_cast<int2*>(labels + pb) = make_int2(cand_at(s2, t), cand_at(s3, t));
             }
             if (MODE & kModeReduce) {
-                if (pa < n) J += (double)ba.x;
-                if (pa + 1 < n) J += (double)ba.y;
-                if (pb < n) J += (double)bb.x;
-                if (pb + 1 < n) J += (double)bb.y;
-                uv[4 * h + 0] = pa < n;
-                uv[4 * h + 1] = pa + 1 < n;
-                uv[4 * h + 2] = pb < n;
-                uv[4 * h + 3] = pb + 1 < n;
+                // validity from the in-chunk offset (32-bit compares; every
+                // point of all but the shard's last chunk is valid)
+                const bool v0 = off < remc, v1 = off + 1 < remc;
+                const bool v2 = off + kWarpTile < remc, v3 = off + kWarpTile + 1 < remc;
+                if (v0) J += (double)ba.x;
+                if (v1) J += (double)ba.y;
+                if (v2) J += (double)bb.x;
+                if (v3) J += (double)bb.y;
+                uv[4 * h + 0] = v0;
+                uv[4 * h + 1] = v1;
+                uv[4 * h + 2] = v2;
+                uv[4 * h + 3] = v3;
                 us[4 * h + 0] = s0;
                 us[4 * h + 1] = s1;
                 us[4 * h + 2] = s2;
