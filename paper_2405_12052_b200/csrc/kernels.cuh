@@ -1024,6 +1024,7 @@ __device__ __forceinline__ void pruned_body(const float4* cand, const int* candk
                                            int32_t* __restrict__ labels, Fetch&& fetch,
                                            double* acc) {
     const int64_t rem = n - base;
+    const int remc = rem < (int64_t)0x7fffffff ? (int)rem : 0x7fffffff;   // valid: offset < remc
     auto cand_at = [&](int j, float4& cc) -> int {   // candidate j: negated centroid, index
         cc = cand[j];
         return candk[j];
@@ -1154,10 +1155,13 @@ __device__ __forceinline__ void pruned_body(const float4* cand, const int* candk
                         make_int2(b1.x < b0.x ? k1 : k0, b1.y < b0.y ? k1 : k0);
                 }
                 if (MODE & kModeReduce) {
-                    if (pa < n) add(0, P[h].xa.x, P[h].ya.x, P[h].za.x, a0.x, a1.x);
-                    if (pa + 1 < n) add(0, P[h].xa.y, P[h].ya.y, P[h].za.y, a0.y, a1.y);
-                    if (pb < n) add(1, P[h].xb.x, P[h].yb.x, P[h].zb.x, b0.x, b1.x);
-                    if (pb + 1 < n) add(1, P[h].xb.y, P[h].yb.y, P[h].zb.y, b0.y, b1.y);
+                    // validity from the in-chunk offset (32-bit compares)
+                    const int off = u * kSortedUnit + h * kLaneTile + 2 * lane;
+                    if (off < remc) add(0, P[h].xa.x, P[h].ya.x, P[h].za.x, a0.x, a1.x);
+                    if (off + 1 < remc) add(0, P[h].xa.y, P[h].ya.y, P[h].za.y, a0.y, a1.y);
+                    if (off + kWarpTile < remc) add(1, P[h].xb.x, P[h].yb.x, P[h].zb.x, b0.x, b1.x);
+                    if (off + kWarpTile + 1 < remc)
+                        add(1, P[h].xb.y, P[h].yb.y, P[h].zb.y, b0.y, b1.y);
                 }
             }
         }
@@ -1278,7 +1282,6 @@ __device__ __forceinline__ void pruned_body(const float4* cand, const int* candk
     // fewer butterflies: C5 assign 0.276 -> 0.265 ms); small K (where >= 3
     // candidates are rare) per warp-tile (the unit form measured slower there)
     constexpr bool kUnitAgg = KM_AGG_UNIT && SLOTS > 16;
-    const int remc = rem < (int64_t)0x7fffffff ? (int)rem : 0x7fffffff;
 #pragma unroll 1
     for (int u = 0; u < nunit; ++u) {
         LanePts P[kUnitSub];
