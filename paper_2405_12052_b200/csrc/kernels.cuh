@@ -1471,7 +1471,8 @@ __global__ void __launch_bounds__(32, LARGE ? KM_PRUNED_MINB_LARGE : KM_PRUNED_M
 k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
                 const float4* __restrict__ cneg_buf, const DevState* __restrict__ st,
                 int mu_sel, int ignore_done, const float* __restrict__ cbox,
-                const int* __restrict__ slist, const int* __restrict__ scount,
+                const int* __restrict__ slist, const float4* __restrict__ scl,
+                const int* __restrict__ scount,
                 double* __restrict__ rows, int row_stride, int32_t* __restrict__ labels,
                 int* __restrict__ cand_count, int* __restrict__ heavy,
                 int* __restrict__ heavy_count, int64_t keep_n) {
@@ -1570,12 +1571,6 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
             lo[j] = (double)__shfl_sync(0xffffffffu, bx, j);
             hi[j] = (double)__shfl_sync(0xffffffffu, bx, D + j);
         }
-        auto stage_c = [&](int k, float (&c)[3]) {   // staged fp32 centroid k
-            const float4 v = __ldg(&cneg[k]);
-            c[0] = -v.x;
-            c[1] = -v.y;
-            c[2] = -v.z;
-        };
         auto bounds = [&](const float (&c)[3], double& dmin2, double& dmax2) {
             dmin2 = 0.0;
             dmax2 = 0.0;
@@ -1599,16 +1594,18 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
         int nc = 0;          // refined candidates
         bool big = false;    // candidates = the unrefined super list (global)
         const int* glist = nullptr;
+        const float4* gcl = nullptr;   // the super list's staged centroids, k in .w
         int gcount = 0;
         {
             const int sup = chunk / kSuperChunks;
             glist = slist + (size_t)sup * K;
+            gcl = scl + (size_t)sup * K;
             gcount = sup_count;
             double Ml = (double)pos_inf();   // this lane's min dmax2 and its position
             int Mil = 0x7fffffff;
             for (int i = lane; i < gcount; i += 32) {
-                float c[3];
-                stage_c(__ldg(&glist[i]), c);
+                const float4 v = __ldg(&gcl[i]);
+                const float c[3] = {-v.x, -v.y, -v.z};
                 double a, b;
                 bounds(c, a, b);
                 if (b < Ml) {
@@ -1620,8 +1617,8 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
             int Mi = (Ml == M) ? Mil : 0x7fffffff;   // the lowest position attaining M
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) Mi = min(Mi, __shfl_xor_sync(0xffffffffu, Mi, o));
-            float ca[3];   // a = the centroid attaining M
-            stage_c(__ldg(&glist[Mi]), ca);
+            const float4 av = __ldg(&gcl[Mi]);   // a = the centroid attaining M
+            const float ca[3] = {-av.x, -av.y, -av.z};
             const double thr = threshold(M);
             for (int i0 = 0; i0 < gcount; i0 += 32) {
                 const int i = i0 + lane;
@@ -1629,8 +1626,11 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
                 int k = 0;
                 bool cand = false;
                 if (i < gcount) {
-                    k = __ldg(&glist[i]);
-                    stage_c(k, c);
+                    const float4 v = __ldg(&gcl[i]);
+                    k = __float_as_int(v.w);
+                    c[0] = -v.x;
+                    c[1] = -v.y;
+                    c[2] = -v.z;
                     double a, b;
                     bounds(c, a, b);
                     cand = a <= thr && !bisector_excludes<D>(c, ca, lo, hi, b, M);
@@ -1747,6 +1747,7 @@ __global__ void __launch_bounds__(kHeavyWarps * 32)
 k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __restrict__ cneg_buf,
                const DevState* __restrict__ st, int mu_sel, int ignore_done,
                const float* __restrict__ cbox, const int* __restrict__ slist,
+               const float4* __restrict__ scl,
                const int* __restrict__ scount, const int* __restrict__ heavy,
                const int* __restrict__ heavy_count, double* __restrict__ rows, int row_stride,
                int32_t* __restrict__ labels) {
@@ -1759,13 +1760,15 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
     float4* cl = reinterpret_cast<float4*>(smem_raw + sizeof(HeavySmem<D>));   // [K]
     unsigned short* my = reinterpret_cast<unsigned short*>(cl + K) + (size_t)warp * K;
     double* T = S.T[warp];
-    const float4* cneg = cneg_buf + (size_t)mu_sel * K;
+    (void)cneg_buf;   // the super lists carry the staged centroids (scl)
+    (void)mu_sel;
     const int nh = *heavy_count;
     for (int h = blockIdx.x; h < nh; h += gridDim.x) {
         const int chunk = heavy[h];
         const int* list = slist + (size_t)(chunk / kSuperChunks) * K;
         const int gc = scount[chunk / kSuperChunks];
-        for (int i = tid; i < gc; i += blockDim.x) cl[i] = __ldg(&cneg[__ldg(&list[i])]);
+        const float4* lcl = scl + (size_t)(chunk / kSuperChunks) * K;
+        for (int i = tid; i < gc; i += blockDim.x) cl[i] = __ldg(&lcl[i]);
         __syncthreads();   // the super list's centroids are staged
         // ---- this warp's sub-tile: points and box ----
         const int64_t pa = (int64_t)chunk * kSChunkPoints + warp * kLaneTile + 2 * lane;
@@ -1979,6 +1982,7 @@ template <int D>
 __global__ void __launch_bounds__(256)
 k_prune(const float4* __restrict__ cneg_buf, const DevState* __restrict__ st, int mu_sel,
         int ignore_done, int K, const float* __restrict__ sbox, int* __restrict__ slist,
+        float4* __restrict__ scl,
         int* __restrict__ scount, int* __restrict__ heavy_count) {
     if (!ignore_done && st->done) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) *heavy_count = 0;   // the assign's heavy list
@@ -2041,10 +2045,11 @@ k_prune(const float4* __restrict__ cneg_buf, const DevState* __restrict__ st, in
     for (int k0 = 0; k0 < K; k0 += blockDim.x) {
         const int k = k0 + tid;
         bool cand = false;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (k < K) {
             double a, b;
             bounds(k, a, b);
-            const float4 v = cneg[k];
+            v = cneg[k];
             const float c[3] = {-v.x, -v.y, -v.z};
             cand = a <= thr && !bisector_excludes<D>(c, ca, lo, hi, b, M);
         }
@@ -2053,7 +2058,11 @@ k_prune(const float4* __restrict__ cneg_buf, const DevState* __restrict__ st, in
         __syncthreads();
         int off = base_s;
         for (int w = 0; w < warp; ++w) off += wcnt[w];
-        if (cand) slist[(size_t)s * K + off + __popc(mask & ((1u << lane) - 1u))] = k;
+        if (cand) {
+            const size_t at = (size_t)s * K + off + __popc(mask & ((1u << lane) - 1u));
+            slist[at] = k;
+            scl[at] = make_float4(v.x, v.y, v.z, __int_as_float(k));   // staged centroid, k
+        }
         __syncthreads();
         if (tid == 0) {
             int t = 0;

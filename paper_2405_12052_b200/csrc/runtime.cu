@@ -211,6 +211,7 @@ struct kmeans_ctx {
     int n_super = 0;              // prune super-boxes (sorted, large K)
     float* sbox = nullptr;        // super-box bounding boxes
     int* slist = nullptr;         // n_super x K candidate lists
+    float4* scl = nullptr;        // the same lists' staged centroids (k in .w)
     int* scount = nullptr;        // candidates per super-box
     int merge_smem = 0;           // k_merge_sparse dynamic shared memory (K x 4 doubles)
     int* heavy = nullptr;         // chunks deferred to k_assign_heavy (sorted, large K)
@@ -442,11 +443,11 @@ ChunkFn pick_chunk(int d, int K, int mode) {
 }
 
 using PrunedFn = void (*)(const float*, int64_t, int, const float4*, const DevState*, int, int,
-                          const float*, const int*, const int*, double*, int, int32_t*, int*,
-                          int*, int*, int64_t);
+                          const float*, const int*, const float4*, const int*, double*, int,
+                          int32_t*, int*, int*, int*, int64_t);
 using HeavyFn = void (*)(const float*, int64_t, int, const float4*, const DevState*, int, int,
-                         const float*, const int*, const int*, const int*, const int*, double*, int,
-                         int32_t*);
+                         const float*, const int*, const float4*, const int*, const int*,
+                         const int*, double*, int, int32_t*);
 
 HeavyFn pick_heavy(int d, int mode) {
     if (d == 2) {
@@ -722,11 +723,11 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
             if (ctx->d == 2)
                 km::k_prune<2><<<ctx->n_super, 256, 0, ctx->stream>>>(
                     ctx->cneg, ctx->st, mu_sel, ignore_done, ctx->K, ctx->sbox, ctx->slist,
-                    ctx->scount, ctx->heavy_count);
+                    ctx->scl, ctx->scount, ctx->heavy_count);
             else
                 km::k_prune<3><<<ctx->n_super, 256, 0, ctx->stream>>>(
                     ctx->cneg, ctx->st, mu_sel, ignore_done, ctx->K, ctx->sbox, ctx->slist,
-                    ctx->scount, ctx->heavy_count);
+                    ctx->scl, ctx->scount, ctx->heavy_count);
             ctx->launches += 1;
         }
         PrunedFn f = pick_pruned(ctx->d, ctx->K, mode, ctx->chunk_points);
@@ -734,15 +735,16 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
             CK(launch_k(f, ctx->n_chunks, 32, ctx->smem, ctx->stream, ctx->path == 0, ctx->X,
                         ctx->N, ctx->K, (const float4*)ctx->cneg, (const DevState*)ctx->st, mu_sel,
                         ignore_done, (const float*)ctx->cbox, (const int*)ctx->slist,
-                        (const int*)ctx->scount, ctx->cpart, ctx->row_stride, ctx->labels_sorted,
+                        (const float4*)ctx->scl, (const int*)ctx->scount, ctx->cpart,
+                        ctx->row_stride, ctx->labels_sorted,
                         ctx->cand_count, ctx->heavy, ctx->heavy_count, ctx->keep_n));
         if (A) ctx->launches += 1;
         if (A && ctx->path == 1) {
             HeavyFn hf = pick_heavy(ctx->d, mode);
             hf<<<ctx->heavy_grid, 256, ctx->heavy_smem, ctx->stream>>>(
                 ctx->X, ctx->N, ctx->K, ctx->cneg, ctx->st, mu_sel, ignore_done, ctx->cbox,
-                ctx->slist, ctx->scount, ctx->heavy, ctx->heavy_count, ctx->cpart, ctx->row_stride,
-                ctx->labels_sorted);
+                ctx->slist, ctx->scl, ctx->scount, ctx->heavy, ctx->heavy_count, ctx->cpart,
+                ctx->row_stride, ctx->labels_sorted);
             ctx->launches += 1;
         }
         if (Mg && ctx->path == 0) {
@@ -1549,6 +1551,7 @@ void kmeans_destroy(kmeans_ctx* ctx) {
         pool_free(ctx, ctx->cpart);
         pool_free(ctx, ctx->sbox);
         pool_free(ctx, ctx->slist);
+        pool_free(ctx, ctx->scl);
         pool_free(ctx, ctx->scount);
         pool_free(ctx, ctx->heavy);
         pool_free(ctx, ctx->heavy_count);
@@ -1695,6 +1698,7 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
         (ctx->sorted && ctx->path == 1 &&
          (pool_alloc(ctx, &ctx->sbox, sizeof(float) * 2 * d * (size_t)ctx->n_super) != cudaSuccess ||
           pool_alloc(ctx, &ctx->slist, sizeof(int) * (size_t)K * ctx->n_super) != cudaSuccess ||
+          pool_alloc(ctx, &ctx->scl, sizeof(float4) * (size_t)K * ctx->n_super) != cudaSuccess ||
           pool_alloc(ctx, &ctx->scount, sizeof(int) * (size_t)ctx->n_super) != cudaSuccess ||
           pool_alloc(ctx, &ctx->heavy, sizeof(int) * (size_t)ctx->n_chunks) != cudaSuccess ||
           pool_alloc(ctx, &ctx->heavy_count, sizeof(int)) != cudaSuccess)) ||
