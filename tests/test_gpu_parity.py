@@ -232,6 +232,20 @@ def test_full_run_parity_one_init_per_blob(name, N, sort):
     np.testing.assert_allclose(g["centroids"], w.centers(), atol=0.05)
 
 
+@pytest.mark.parametrize("sort", SORT)
+@pytest.mark.parametrize("K", [600, 1024])
+def test_full_run_large_k(K, sort):
+    """kmeans_fit at large K on every path: the iteration graph and the final
+    labels pass (unsorted K = 1024: the labels pass + k_accum_large split;
+    K = 600: the fused kernel at 8 points per lane; sorted: prune + pruned +
+    heavy), against the oracle's run -- iterations, labels, centroids, J."""
+    w = datagen.WORKLOADS["C5"]
+    N = 80_000
+    X = datagen.generate(w, N=N)
+    init = datagen.init_indices(w, N=N, K=K)
+    check_fit(X, K, init, 0.0, 3, tag=f"K={K}", sort=sort)
+
+
 @pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("name,N,K", [("C1", 10_000, 4), ("C2", 1_000_000, 8), ("C2", 77_777, 3),
                                       ("NS", 3_000_000, 16), ("C3", 2_100_000, 13)])
