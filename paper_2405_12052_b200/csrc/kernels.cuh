@@ -1695,9 +1695,10 @@ constexpr int kHeavySplit = 64;   // tile lists longer than this are walked by a
 
 template <int D>
 struct HeavySmem {
-    double T[kHeavyWarps][kHeavySlots * 4];   // per warp: slot table of the current window
     double4 ent[kHeavyWarps][kLaneTile];      // per warp: {Sx, Sy, Sz, (k, n)} entries
-    float2 part[kHeavyWarps][4][32];          // split walks: (distance, slot) per warp, point, lane
+    float2 part[kHeavyWarps][kHeavyWarps][4][32];   // split walks: (distance, slot) per
+                                                    // tile, warp, point, lane
+    float2 pts[kHeavyWarps][6][32];           // each tile's points (xa ya za xb yb zb per lane)
     double wJ[kHeavyWarps];
     int went[kHeavyWarps];
     int wnt[kHeavyWarps];
@@ -1759,7 +1760,6 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     float4* cl = reinterpret_cast<float4*>(smem_raw + sizeof(HeavySmem<D>));   // [K]
     unsigned short* my = reinterpret_cast<unsigned short*>(cl + K) + (size_t)warp * K;
-    double* T = S.T[warp];
     (void)cneg_buf;   // the super lists carry the staged centroids (scl)
     (void)mu_sel;
     const int nh = *heavy_count;
@@ -1767,10 +1767,7 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
         const int chunk = heavy[h];
         const int* list = slist + (size_t)(chunk / kSuperChunks) * K;
         const int gc = scount[chunk / kSuperChunks];
-        const float4* lcl = scl + (size_t)(chunk / kSuperChunks) * K;
-        for (int i = tid; i < gc; i += blockDim.x) cl[i] = __ldg(&lcl[i]);
-        __syncthreads();   // the super list's centroids are staged
-        // ---- this warp's sub-tile: points and box ----
+        // ---- this warp's sub-tile: points (loads issued before the staging) ----
         const int64_t pa = (int64_t)chunk * kSChunkPoints + warp * kLaneTile + 2 * lane;
         const int64_t pb = pa + kWarpTile;
         const float2 xa = ld_stream2(tile_coord<D>(X, pa, 0));
@@ -1779,6 +1776,16 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
         const float2 xb = ld_stream2(tile_coord<D>(X, pb, 0));
         const float2 yb = ld_stream2(tile_coord<D>(X, pb, 1));
         const float2 zb = (D == 3) ? ld_stream2(tile_coord<D>(X, pb, 2)) : make_float2(0.f, 0.f);
+        const float4* lcl = scl + (size_t)(chunk / kSuperChunks) * K;
+        for (int i = tid; i < gc; i += blockDim.x) cl[i] = __ldg(&lcl[i]);
+        // the tile's points for the split walks of the other warps
+        S.pts[warp][0][lane] = xa;
+        S.pts[warp][1][lane] = ya;
+        S.pts[warp][2][lane] = za;
+        S.pts[warp][3][lane] = xb;
+        S.pts[warp][4][lane] = yb;
+        S.pts[warp][5][lane] = zb;
+        __syncthreads();   // the super list's centroids (and the tiles' points) are staged
         const bool v[4] = {pa < n, pa + 1 < n, pb < n, pb + 1 < n};
         const float px[4] = {xa.x, xa.y, xb.x, xb.y}, py[4] = {ya.x, ya.y, yb.x, yb.y};
         const float pz[4] = {za.x, za.y, zb.x, zb.y};
@@ -1856,34 +1863,37 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
         float best[4];
         int sl[4];
         if (nt <= kHeavySplit) argmin_walk<D>(my, cl, 0, nt, xa, ya, za, xb, yb, zb, best, sl);
+        // every long tile in one round: warp w walks the w-th eighth of each
+        // (the tile's points from shared memory), one barrier, then the tile's
+        // own warp combines the eighths in ascending order (strict <)
+        bool any_long = false;
         for (int T = 0; T < kHeavyWarps; ++T) {   // block-uniform
             const int ntT = S.wnt[T];
             if (ntT <= kHeavySplit) continue;
-            const int64_t qa = (int64_t)chunk * kSChunkPoints + T * kLaneTile + 2 * lane;
-            const int64_t qb = qa + kWarpTile;
-            const float2 txa = ld_stream2(tile_coord<D>(X, qa, 0));
-            const float2 tya = ld_stream2(tile_coord<D>(X, qa, 1));
-            const float2 tza = (D == 3) ? ld_stream2(tile_coord<D>(X, qa, 2)) : make_float2(0.f, 0.f);
-            const float2 txb = ld_stream2(tile_coord<D>(X, qb, 0));
-            const float2 tyb = ld_stream2(tile_coord<D>(X, qb, 1));
-            const float2 tzb = (D == 3) ? ld_stream2(tile_coord<D>(X, qb, 2)) : make_float2(0.f, 0.f);
+            any_long = true;
+            const float2* tp = &S.pts[T][0][0];
             const unsigned short* listT = my - (size_t)warp * K + (size_t)T * K;
             const int t0 = (int)((int64_t)ntT * warp / kHeavyWarps);
             const int t1 = (int)((int64_t)ntT * (warp + 1) / kHeavyWarps);
             float pb_[4];
             int ps_[4];
-            argmin_walk<D>(listT, cl, t0, t1, txa, tya, tza, txb, tyb, tzb, pb_, ps_);
+            argmin_walk<D>(listT, cl, t0, t1, tp[0 * 32 + lane], tp[1 * 32 + lane],
+                           tp[2 * 32 + lane], tp[3 * 32 + lane], tp[4 * 32 + lane],
+                           tp[5 * 32 + lane], pb_, ps_);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) S.part[warp][i][lane] = make_float2(pb_[i], __int_as_float(ps_[i]));
-            __syncthreads();
-            if (warp == T) {
+            for (int i = 0; i < 4; ++i)
+                S.part[T][warp][i][lane] = make_float2(pb_[i], __int_as_float(ps_[i]));
+        }
+        if (any_long) {
+            __syncthreads();   // every eighth of every long tile
+            if (nt > kHeavySplit) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    float2 b2 = S.part[0][i][lane];
+                    float2 b2 = S.part[warp][0][i][lane];
                     best[i] = b2.x;
                     sl[i] = __float_as_int(b2.y);
                     for (int w = 1; w < kHeavyWarps; ++w) {
-                        const float2 c2 = S.part[w][i][lane];
+                        const float2 c2 = S.part[warp][w][i][lane];
                         if (c2.x < best[i]) {
                             best[i] = c2.x;
                             sl[i] = __float_as_int(c2.y);
@@ -1891,7 +1901,6 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
                     }
                 }
             }
-            __syncthreads();   // the partials are reused by the next long tile
         }
         if (MODE & kModeLabels) {
             *reinterpret_cast<int2*>(labels + pa) =
