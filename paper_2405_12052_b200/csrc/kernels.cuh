@@ -263,6 +263,13 @@ constexpr int kLaneTile = 2 * kWarpTile;                 // 128 points per warp-
 #ifndef KM_TWO_CAND_PRED
 #define KM_TWO_CAND_PRED 1   // two-candidate chunks: predicated adds instead of +0.0 selects
 #endif
+#ifndef KM_REFINE_UNROLL
+#define KM_REFINE_UNROLL 4   // heavy kernel's refinement loops: entries in flight per lane
+#endif
+constexpr int kRefineUnroll = KM_REFINE_UNROLL;
+#ifndef KM_HEAVY_PROF
+#define KM_HEAVY_PROF 0   // tuning aid: per-chunk phase times of k_assign_heavy (printf)
+#endif
 #ifndef KM_AGG_UNIT
 #define KM_AGG_UNIT 1   // large K: slot sums per TMA unit (8 points per lane), not per warp-tile
 #endif
@@ -1765,6 +1772,9 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
     const int nh = *heavy_count;
     for (int h = blockIdx.x; h < nh; h += gridDim.x) {
         const int chunk = heavy[h];
+#if KM_HEAVY_PROF
+        const unsigned long long tp0 = (unsigned long long)global_ns();
+#endif
         const int* list = slist + (size_t)(chunk / kSuperChunks) * K;
         const int gc = scount[chunk / kSuperChunks];
         // ---- this warp's sub-tile: points (loads issued before the staging) ----
@@ -1786,6 +1796,9 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
         S.pts[warp][4][lane] = yb;
         S.pts[warp][5][lane] = zb;
         __syncthreads();   // the super list's centroids (and the tiles' points) are staged
+#if KM_HEAVY_PROF
+        const unsigned long long tp1 = (unsigned long long)global_ns();
+#endif
         const bool v[4] = {pa < n, pa + 1 < n, pb < n, pb + 1 < n};
         const float px[4] = {xa.x, xa.y, xb.x, xb.y}, py[4] = {ya.x, ya.y, yb.x, yb.y};
         const float pz[4] = {za.x, za.y, zb.x, zb.y};
@@ -1814,6 +1827,7 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
         if (any_valid) {
             double Ml = (double)pos_inf();   // this lane's min dmax2 and its position
             int Mil = 0x7fffffff;
+#pragma unroll kRefineUnroll
             for (int i = lane; i < gc; i += 32) {
                 const float4 c4 = cl[i];
                 const float c[3] = {-c4.x, -c4.y, -c4.z};
@@ -1833,6 +1847,7 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
             const float4 a4 = cl[Mi];   // a = the centroid attaining M
             const float ca[3] = {-a4.x, -a4.y, -a4.z};
             const double thr = prune_threshold(M);
+#pragma unroll kRefineUnroll
             for (int i0 = 0; i0 < gc; i0 += 32) {
                 const int i = i0 + lane;
                 bool cand = false;
@@ -1860,6 +1875,9 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
         // strict <, which is the serial walk's result (lowest slot on ties).
         if (lane == 0) S.wnt[warp] = nt;
         __syncthreads();   // every tile's list length
+#if KM_HEAVY_PROF
+        const unsigned long long tp2 = (unsigned long long)global_ns();
+#endif
         float best[4];
         int sl[4];
         if (nt <= kHeavySplit) argmin_walk<D>(my, cl, 0, nt, xa, ya, za, xb, yb, zb, best, sl);
@@ -1957,6 +1975,9 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
             }
         }
         __syncthreads();   // every tile's entries are in shared memory
+#if KM_HEAVY_PROF
+        const unsigned long long tp3 = (unsigned long long)global_ns();
+#endif
         if ((MODE & kModeReduce) && warp == 0) {
             // the chunk row: tiles in order, each tile's entries in ascending k
             double* row = rows + (size_t)chunk * row_stride;
@@ -1980,6 +2001,12 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
             }
         }
         __syncthreads();   // shared memory is reused by the next heavy chunk
+#if KM_HEAVY_PROF
+        if (tid == 0)
+            printf("heavy h=%d chunk=%d gc=%d nt=%d,%d,%d,%d,%d,%d,%d,%d stage=%llu refine=%llu walk+agg=%llu row=%llu\n",
+                   h, chunk, gc, S.wnt[0], S.wnt[1], S.wnt[2], S.wnt[3], S.wnt[4], S.wnt[5],
+                   S.wnt[6], S.wnt[7], tp1 - tp0, tp2 - tp1, tp3 - tp2, (unsigned long long)global_ns() - tp3);
+#endif
     }
 }
 

@@ -10,6 +10,8 @@ VARIANTS = {
     "lu2": ("KM_LARGE_UNROLL=2",),     # k_assign_large: two argmin steps per loop trip
     "aggbfly": ("KM_AGG_TRANSPOSE=0",),      # pruned slot sums: plain 5-level butterflies
     "aggtile": ("KM_AGG_UNIT=0",),             # pruned, large K: slot sums per warp-tile
+    "hprof": ("KM_HEAVY_PROF=1",),
+    "ru1": ("KM_REFINE_UNROLL=1",),            # list refinement loops not unrolled             # per-chunk phase times of k_assign_heavy (printf)
     "lnosplit": ("KM_LARGE_SPLIT_WARPS=0",),   # large K: never split into labels + accumulate
     "lsnpl1": ("KM_LARGE_SPLIT_NPL=1",),       # split labels pass: 4 points per lane
     "lsnpl2": ("KM_LARGE_SPLIT_NPL=2",),       # split labels pass: 8 points per lane
