@@ -888,7 +888,10 @@ constexpr int kSortedUnit = kUnitSub * kLaneTile;      // points per TMA stage
 constexpr int kSChunkPoints = KM_SORTED_CHUNK_TILES * kLaneTile;   // 1024
 constexpr int kSortedUnits = kSChunkPoints / kSortedUnit;          // 4 per chunk
 constexpr int kSortedStages = KM_SORTED_STAGES;
-constexpr int kSuperChunks = 64;                        // chunks per prune super-box
+#ifndef KM_SUPER_CHUNKS
+#define KM_SUPER_CHUNKS 64
+#endif
+constexpr int kSuperChunks = KM_SUPER_CHUNKS;           // chunks per prune super-box
 constexpr int kRowHead = 2;                             // J, count
 
 template <bool LARGE>

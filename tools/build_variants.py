@@ -12,6 +12,9 @@ VARIANTS = {
     "aggtile": ("KM_AGG_UNIT=0",),             # pruned, large K: slot sums per warp-tile
     "hprof": ("KM_HEAVY_PROF=1",),
     "ru1": ("KM_REFINE_UNROLL=1",),            # list refinement loops not unrolled             # per-chunk phase times of k_assign_heavy (printf)
+    "sup16": ("KM_SUPER_CHUNKS=16",),          # large K: 16 chunks per prune super box
+    "sup32": ("KM_SUPER_CHUNKS=32",),
+    "sup128": ("KM_SUPER_CHUNKS=128",),
     "lnosplit": ("KM_LARGE_SPLIT_WARPS=0",),   # large K: never split into labels + accumulate
     "lsnpl1": ("KM_LARGE_SPLIT_NPL=1",),       # split labels pass: 4 points per lane
     "lsnpl2": ("KM_LARGE_SPLIT_NPL=2",),       # split labels pass: 8 points per lane
