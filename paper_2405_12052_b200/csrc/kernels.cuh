@@ -267,6 +267,9 @@ constexpr int kLaneTile = 2 * kWarpTile;                 // 128 points per warp-
 #define KM_REFINE_UNROLL 4   // heavy kernel's refinement loops: entries in flight per lane
 #endif
 constexpr int kRefineUnroll = KM_REFINE_UNROLL;
+#ifndef KM_LARGE_REVERSE
+#define KM_LARGE_REVERSE 1   // large-K pruned kernel: chunks in reverse order
+#endif
 #ifndef KM_HEAVY_PROF
 #define KM_HEAVY_PROF 0   // tuning aid: per-chunk phase times of k_assign_heavy (printf)
 #endif
@@ -1491,7 +1494,11 @@ k_assign_pruned(const float* __restrict__ X, int64_t n, int K,
     // chunk box and the points (the TMA ring is filled here, so with PDL the
     // first units stream in while the previous update finishes).
     const int lane = threadIdx.x;
-    const int chunk = blockIdx.x;
+    // large K: chunks in reverse curve order -- the far end of the curve
+    // (outlier sites) makes the widest super boxes and the longest chunk
+    // prologues, which then start first instead of stretching the tail
+    const int chunk = (LARGE && KM_LARGE_REVERSE) ? (int)gridDim.x - 1 - (int)blockIdx.x
+                                                  : (int)blockIdx.x;
     const float4* cneg = cneg_buf + (size_t)mu_sel * K;   // -fl32(mu^t) (or mu^{t-1})
     const float bx = (lane < 2 * D) ? __ldg(&cbox[(size_t)chunk * 2 * D + lane]) : 0.0f;
     extern __shared__ __align__(16) unsigned char smem_raw[];

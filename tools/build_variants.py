@@ -15,6 +15,7 @@ VARIANTS = {
     "sup16": ("KM_SUPER_CHUNKS=16",),          # large K: 16 chunks per prune super box
     "sup32": ("KM_SUPER_CHUNKS=32",),
     "sup128": ("KM_SUPER_CHUNKS=128",),
+    "lfwd": ("KM_LARGE_REVERSE=0",),          # large-K pruned kernel: chunks in curve order
     "lnosplit": ("KM_LARGE_SPLIT_WARPS=0",),   # large K: never split into labels + accumulate
     "lsnpl1": ("KM_LARGE_SPLIT_NPL=1",),       # split labels pass: 4 points per lane
     "lsnpl2": ("KM_LARGE_SPLIT_NPL=2",),       # split labels pass: 8 points per lane
