@@ -2021,6 +2021,369 @@ k_assign_heavy(const float* __restrict__ X, int64_t n, int K, const float4* __re
 }
 
 // ---------------------------------------------------------------------------
+// k_assign_heavy_tiles (large K, KM_HEAVY_TILES): the same heavy chunks, one
+// 8-warp block per 128-point TILE instead of per chunk.  k_assign_heavy's
+// length is its slowest chunk, and there one warp refines the whole super
+// list (1024 entries: 2 x 32 dependent passes) and aggregates up to 128 slots
+// alone; here the block's 8 warps share every step of one tile:
+//   * the refinement: warp w tests list positions [128 w, 128 w + 128); the
+//     minimiser of dmax2 (lowest position on ties) and the ascending tile list
+//     are assembled across warps -- the same list as k_assign_heavy's;
+//   * the argmin: the split walk (eighths, ascending strict-< combine) for
+//     lists longer than kHeavySplit, else warp 0 alone;
+//   * the sums: slot windows of 64 spread over the warps, each window's
+//     entries at its prefix offset -- the same butterflies, so every entry is
+//     bit-identical to k_assign_heavy's.
+// A tile's entries go to its own stretch [T ts, T ts + ne) of the chunk row
+// (ts = min(K, 128) >= its entry count) and its (J, ne) to htile; the block
+// that completes the chunk's 8th tile (gpu fence + ticket, as in the
+// threadfence reduction) moves the entries together in tile order and writes
+// the row head with J summed in tile order: the row k_assign_heavy writes.
+// ---------------------------------------------------------------------------
+#ifndef KM_HEAVY_TILES
+#define KM_HEAVY_TILES 1   // 1: k_assign_heavy_tiles, 0: k_assign_heavy (one block per chunk)
+#endif
+#ifndef KM_HEAVY_TILE_MINB
+#define KM_HEAVY_TILE_MINB 4   // k_assign_heavy_tiles: resident blocks per SM (register cap)
+#endif
+constexpr int kHeavyTileSplit = kHeavyWarps;      // tile lists this long are walked by all 8 warps
+
+// position of the r-th (0-based, ascending) set bit of m (r < popc(m))
+__device__ __forceinline__ int nth_set_bit(unsigned m, int r) {
+    int pos = 0;
+#pragma unroll
+    for (int w = 16; w > 0; w >>= 1) {
+        const unsigned lowm = m & ((1u << w) - 1u);
+        const int c = __popc(lowm);
+        if (r >= c) {
+            r -= c;
+            m >>= w;
+            pos += w;
+        } else {
+            m = lowm;
+        }
+    }
+    return pos;
+}
+
+struct alignas(16) HeavyTileSmem {   // size a multiple of 16: float4 cl[] follows
+    float2 part[kHeavyWarps][4][32];   // split walk: (distance, slot) per warp, point, lane
+    float2 fin[4][32];                 // the tile's (distance, slot) per point and lane
+    double wM[kHeavyWarps];
+    int wMi[kHeavyWarps];
+    int wcnt[kHeavyWarps];
+    int last;
+    // followed by float4 cl[K] (the super list's staged centroids) and
+    // unsigned short tl[K] (the tile list: super-list positions)
+};
+
+template <int D, int MODE>
+__global__ void __launch_bounds__(kHeavyWarps * 32, KM_HEAVY_TILE_MINB)
+k_assign_heavy_tiles(const float* __restrict__ X, int64_t n, int K, const DevState* __restrict__ st,
+                     int ignore_done, const int* __restrict__ slist,
+                     const float4* __restrict__ scl, const int* __restrict__ scount,
+                     const int* __restrict__ heavy, const int* __restrict__ heavy_count,
+                     double* __restrict__ rows, int row_stride, int32_t* __restrict__ labels,
+                     double2* __restrict__ htile, int* __restrict__ hctr) {
+    if (!ignore_done && st->done) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    HeavyTileSmem& S = *reinterpret_cast<HeavyTileSmem*>(smem_raw);
+    float4* cl = reinterpret_cast<float4*>(smem_raw + sizeof(HeavyTileSmem));   // [K]
+    unsigned short* tl = reinterpret_cast<unsigned short*>(cl + K);             // [K]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ts = K < kLaneTile ? K : kLaneTile;   // row entries reserved per tile
+    const int nitems = *heavy_count * kHeavyWarps;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const int h = it / kHeavyWarps, T = it % kHeavyWarps;
+        const int chunk = heavy[h];
+#if KM_HEAVY_PROF
+        const unsigned long long q0 = (unsigned long long)global_ns();
+        unsigned long long q1 = 0, q2 = 0, q3 = 0, q4 = 0;
+#endif
+        const int* list = slist + (size_t)(chunk / kSuperChunks) * K;
+        const int gc = scount[chunk / kSuperChunks];
+        KM_CHECK(gc >= 1 && gc <= K && K <= 1024);
+        // the tile's points: every warp holds all 128 (4 per lane)
+        const int64_t pa = (int64_t)chunk * kSChunkPoints + T * kLaneTile + 2 * lane;
+        const int64_t pb = pa + kWarpTile;
+        const float2 xa = ld_stream2(tile_coord<D>(X, pa, 0));
+        const float2 ya = ld_stream2(tile_coord<D>(X, pa, 1));
+        const float2 za = (D == 3) ? ld_stream2(tile_coord<D>(X, pa, 2)) : make_float2(0.f, 0.f);
+        const float2 xb = ld_stream2(tile_coord<D>(X, pb, 0));
+        const float2 yb = ld_stream2(tile_coord<D>(X, pb, 1));
+        const float2 zb = (D == 3) ? ld_stream2(tile_coord<D>(X, pb, 2)) : make_float2(0.f, 0.f);
+        const float4* lcl = scl + (size_t)(chunk / kSuperChunks) * K;
+        for (int i = tid; i < gc; i += blockDim.x) cl[i] = __ldg(&lcl[i]);
+        const bool v[4] = {pa < n, pa + 1 < n, pb < n, pb + 1 < n};
+        const float px[4] = {xa.x, xa.y, xb.x, xb.y}, py[4] = {ya.x, ya.y, yb.x, yb.y};
+        const float pz[4] = {za.x, za.y, zb.x, zb.y};
+        double tlo[3] = {0, 0, 0}, thi[3] = {0, 0, 0};
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            const float* pj = j == 0 ? px : (j == 1 ? py : pz);
+            float l_ = pos_inf(), h_ = -pos_inf();
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (v[i]) {
+                    l_ = fminf(l_, pj[i]);
+                    h_ = fmaxf(h_, pj[i]);
+                }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                l_ = fminf(l_, __shfl_xor_sync(0xffffffffu, l_, o));
+                h_ = fmaxf(h_, __shfl_xor_sync(0xffffffffu, h_, o));
+            }
+            tlo[j] = (double)l_;
+            thi[j] = (double)h_;
+        }
+        const bool any_valid = tlo[0] <= thi[0];   // block-uniform; false for an all-padding tile
+        __syncthreads();   // the super list's centroids are staged
+#if KM_HEAVY_PROF
+        q1 = (unsigned long long)global_ns();
+#endif
+        // ---- the super list refined against the tile box, across the warps ----
+        int nt = 1;
+        if (any_valid) {
+            double Ml = (double)pos_inf();
+            int Mil = 0x7fffffff;
+#pragma unroll 4
+            for (int i = warp * 32 + lane; i < gc; i += kHeavyWarps * 32) {
+                const float4 c4 = cl[i];
+                const float c[3] = {-c4.x, -c4.y, -c4.z};
+                double a, b;
+                box_bounds<D>(c, tlo, thi, a, b);
+                if (b < Ml) {
+                    Ml = b;
+                    Mil = i;
+                }
+            }
+            double M = Ml;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
+            int Mi = (Ml == M) ? Mil : 0x7fffffff;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) Mi = min(Mi, __shfl_xor_sync(0xffffffffu, Mi, o));
+            if (lane == 0) {
+                S.wM[warp] = M;
+                S.wMi[warp] = Mi;
+            }
+            __syncthreads();
+            M = S.wM[0];
+#pragma unroll
+            for (int w = 1; w < kHeavyWarps; ++w) M = fmin(M, S.wM[w]);
+            Mi = 0x7fffffff;   // the lowest position attaining M
+#pragma unroll
+            for (int w = 0; w < kHeavyWarps; ++w)
+                if (S.wM[w] == M) Mi = min(Mi, S.wMi[w]);
+            const float4 a4 = cl[Mi];
+            const float ca[3] = {-a4.x, -a4.y, -a4.z};
+            const double thr = prune_threshold(M);
+            // warp w: positions [128 w, 128 w + 128) in 4 ballots; its candidates
+            // follow those of warps < w (ascending positions = ascending k)
+            unsigned m[4];
+            int cnt = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int i = (warp * 4 + q) * 32 + lane;
+                bool cand = false;
+                if (i < gc) {
+                    const float4 c4 = cl[i];
+                    const float c[3] = {-c4.x, -c4.y, -c4.z};
+                    double a, b;
+                    box_bounds<D>(c, tlo, thi, a, b);
+                    cand = a <= thr && !bisector_excludes<D>(c, ca, tlo, thi, b, M);
+                }
+                m[q] = __ballot_sync(0xffffffffu, cand);
+                cnt += __popc(m[q]);
+            }
+            if (lane == 0) S.wcnt[warp] = cnt;
+            __syncthreads();
+            int off = 0;
+            nt = 0;
+#pragma unroll
+            for (int w = 0; w < kHeavyWarps; ++w) {
+                off += (w < warp) ? S.wcnt[w] : 0;
+                nt += S.wcnt[w];
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if ((m[q] >> lane) & 1u)
+                    tl[off + __popc(m[q] & ((1u << lane) - 1u))] = (unsigned short)((warp * 4 + q) * 32 + lane);
+                off += __popc(m[q]);
+            }
+        } else if (tid == 0) {
+            tl[0] = 0;   // an all-padding tile: list {position 0}, as k_assign_heavy
+        }
+        KM_CHECK(nt >= 1 && nt <= gc);
+        __syncthreads();   // the tile list is complete
+#if KM_HEAVY_PROF
+        q2 = (unsigned long long)global_ns();
+#endif
+        // ---- exact argmin over the tile list (ascending k; strict <) ----
+        float best[4];
+        int sl[4];
+        const bool split = nt >= kHeavyTileSplit;   // every eighth non-empty
+        if (split) {
+            const int t0 = (int)((int64_t)nt * warp / kHeavyWarps);
+            const int t1 = (int)((int64_t)nt * (warp + 1) / kHeavyWarps);
+            argmin_walk<D>(tl, cl, t0, t1, xa, ya, za, xb, yb, zb, best, sl);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) S.part[warp][i][lane] = make_float2(best[i], __int_as_float(sl[i]));
+            __syncthreads();
+        } else if (warp == 0) {
+            argmin_walk<D>(tl, cl, 0, nt, xa, ya, za, xb, yb, zb, best, sl);
+        }
+        if (warp == 0) {
+            if (split) {   // ascending eighths, strict <
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    for (int w = 1; w < kHeavyWarps; ++w) {
+                        const float2 c2 = S.part[w][i][lane];
+                        if (c2.x < best[i]) {
+                            best[i] = c2.x;
+                            sl[i] = __float_as_int(c2.y);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) S.fin[i][lane] = make_float2(best[i], __int_as_float(sl[i]));
+            if (MODE & kModeLabels) {
+                *reinterpret_cast<int2*>(labels + pa) =
+                    make_int2(__ldg(&list[tl[sl[0]]]), __ldg(&list[tl[sl[1]]]));
+                *reinterpret_cast<int2*>(labels + pb) =
+                    make_int2(__ldg(&list[tl[sl[2]]]), __ldg(&list[tl[sl[3]]]));
+            }
+        }
+        if (MODE & kModeReduce) {
+            __syncthreads();   // the tile's slots
+#if KM_HEAVY_PROF
+            q3 = (unsigned long long)global_ns();
+#endif
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float2 f = S.fin[i][lane];
+                best[i] = f.x;
+                sl[i] = __float_as_int(f.y);
+            }
+            double* row = rows + (size_t)chunk * row_stride;
+            const int nwin = any_valid ? (nt + kHeavySlots - 1) / kHeavySlots : 0;
+            // slot windows of 64 in ascending order (block-uniform); the present
+            // slots of a window are dealt round-robin to the warps, each entry
+            // written at its rank -- entries stay in ascending k
+            int ne = T * ts;   // the next entry of this tile's stretch
+            for (int wi = 0; wi < nwin; ++wi) {
+                const int w0 = wi * kHeavySlots;
+                unsigned long long mine = 0ull;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (v[i] && sl[i] >= w0 && sl[i] < w0 + kHeavySlots) mine |= 1ull << (sl[i] - w0);
+                const unsigned plo = __reduce_or_sync(0xffffffffu, (unsigned)mine);
+                const unsigned phi = __reduce_or_sync(0xffffffffu, (unsigned)(mine >> 32));
+                const int nlo = __popc(plo), np = nlo + __popc(phi);
+                for (int r = warp; r < np; r += kHeavyWarps) {
+                    const int q = r < nlo ? nth_set_bit(plo, r) : 32 + nth_set_bit(phi, r - nlo);
+                    double sx = 0.0, sy = 0.0, sz = 0.0;
+                    unsigned cnt = 0u;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const bool mm = v[i] && sl[i] == w0 + q;
+                        sx += mm ? (double)px[i] : 0.0;
+                        sy += mm ? (double)py[i] : 0.0;
+                        sz += mm ? (double)pz[i] : 0.0;
+                        cnt += __popc(__ballot_sync(0xffffffffu, mm));
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+                        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+                        if (D == 3) sz += __shfl_xor_sync(0xffffffffu, sz, o);
+                    }
+                    if (lane == 0) {
+                        KM_CHECK(ne + r < (T + 1) * ts);
+                        double2* d2 = reinterpret_cast<double2*>(row + kRowHead) + 2 * (ne + r);
+                        d2[0] = make_double2(sx, sy);
+                        d2[1] = make_double2(sz, pack_kn(__ldg(&list[tl[w0 + q]]), (int)cnt));
+                    }
+                }
+                ne += np;
+            }
+            if (warp == 0) {
+                double j4 = 0.0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (v[i]) j4 += (double)best[i];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) j4 += __shfl_xor_sync(0xffffffffu, j4, o);
+                if (lane == 0) htile[(size_t)h * kHeavyWarps + T] = make_double2(j4, (double)(ne - T * ts));
+            }
+            // ---- the chunk's last tile assembles the row ----
+#if KM_HEAVY_PROF
+            __syncthreads();
+            q4 = (unsigned long long)global_ns();
+#endif
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) S.last = atomicAdd(&hctr[h], 1) == kHeavyWarps - 1;
+            __syncthreads();
+            if (S.last) {   // block-uniform
+                __threadfence();
+                int cnt[kHeavyWarps], tot = 0;
+                double J = 0.0;
+#pragma unroll
+                for (int u = 0; u < kHeavyWarps; ++u) {
+                    const double2 jn = __ldcg(&htile[(size_t)h * kHeavyWarps + u]);
+                    cnt[u] = (int)jn.y;
+                    tot += cnt[u];
+                    J += jn.x;
+                }
+                // every entry read before any is moved (the moves overlap)
+                constexpr int kPer = kSChunkPoints / (kHeavyWarps * 32);   // 4 entries per thread
+                double2 e0[kPer], e1[kPer];
+                int dst[kPer];
+#pragma unroll
+                for (int r = 0; r < kPer; ++r) {
+                    const int g = tid + r * kHeavyWarps * 32;   // position in the compacted row
+                    dst[r] = -1;
+                    if (g < tot) {
+                        int u = 0, base = 0;
+                        while (g >= base + cnt[u]) base += cnt[u++];
+                        const double2* s2 = reinterpret_cast<const double2*>(row + kRowHead) +
+                                            2 * (u * ts + g - base);
+                        e0[r] = __ldcg(s2);
+                        e1[r] = __ldcg(s2 + 1);
+                        dst[r] = g;
+                    }
+                }
+                __syncthreads();
+#pragma unroll
+                for (int r = 0; r < kPer; ++r)
+                    if (dst[r] >= 0) {
+                        double2* d2 = reinterpret_cast<double2*>(row + kRowHead) + 2 * dst[r];
+                        d2[0] = e0[r];
+                        d2[1] = e1[r];
+                    }
+                if (tid == 0) {
+                    KM_CHECK(kRowHead + 4 * tot <= row_stride);
+                    row[0] = J;
+                    row[1] = (double)tot;
+                    hctr[h] = 0;   // ready for the next iteration
+                }
+            }
+        } else {
+            __syncthreads();
+        }
+        __syncthreads();   // shared memory is reused by the next tile
+#if KM_HEAVY_PROF
+        if (tid == 0)
+            printf("htile blk=%d h=%d T=%d chunk=%d gc=%d nt=%d start=%llu stage=%llu refine=%llu walk=%llu sums=%llu row=%llu\n",
+                   blockIdx.x, h, T, chunk, gc, nt, q0, q1 - q0, q2 - q1, q3 - q2, q4 - q3,
+                   (unsigned long long)global_ns() - q4);
+#endif
+    }
+}
+
+// ---------------------------------------------------------------------------
 // k_prune (large K): candidates of each super box (kSuperChunks chunks) by the
 // same exclusion test, listed in ascending k.
 // ---------------------------------------------------------------------------

@@ -218,6 +218,8 @@ struct kmeans_ctx {
     int* heavy_count = nullptr;
     int heavy_smem = 0;
     int heavy_grid = 0;
+    double2* htile = nullptr;     // KM_HEAVY_TILES: per heavy chunk and tile (J, entries)
+    int* hctr = nullptr;          // KM_HEAVY_TILES: tiles done per heavy chunk (0 between launches)
     bool sorted = false;          // points held in Morton order (path 0 default)
     int64_t keep_n = 0;           // sorted small K: points [0, keep_n) kept resident in L2
     int32_t* perm = nullptr;      // sorted position -> caller's index (sorted only)
@@ -449,6 +451,21 @@ using HeavyFn = void (*)(const float*, int64_t, int, const float4*, const DevSta
                          const float*, const int*, const float4*, const int*, const int*,
                          const int*, double*, int, int32_t*);
 
+using HeavyTileFn = void (*)(const float*, int64_t, int, const DevState*, int, const int*,
+                             const float4*, const int*, const int*, const int*, double*, int,
+                             int32_t*, double2*, int*);
+
+HeavyTileFn pick_heavy_tiles(int d, int mode) {
+    if (d == 2) {
+        if (mode == 1) return km::k_assign_heavy_tiles<2, 1>;
+        if (mode == 2) return km::k_assign_heavy_tiles<2, 2>;
+        return km::k_assign_heavy_tiles<2, 3>;
+    }
+    if (mode == 1) return km::k_assign_heavy_tiles<3, 1>;
+    if (mode == 2) return km::k_assign_heavy_tiles<3, 2>;
+    return km::k_assign_heavy_tiles<3, 3>;
+}
+
 HeavyFn pick_heavy(int d, int mode) {
     if (d == 2) {
         if (mode == 1) return km::k_assign_heavy<2, 1>;
@@ -597,13 +614,23 @@ kmeans_status configure(kmeans_ctx* ctx) {
         if (ctx->path == 1) {
             // per-warp slot tables and entry lists, the staged super list (K
             // float4), then 8 tile lists of K u16
-            ctx->heavy_smem = (int)(sizeof(km::HeavySmem<3>) + sizeof(float4) * ctx->K +
-                                    sizeof(unsigned short) * km::kHeavyWarps * ctx->K);
-            for (int mode = 1; mode <= 3; ++mode)
-                CK(allow_smem((const void*)pick_heavy(ctx->d, mode), ctx->heavy_smem));
-            int hocc = 0;   // one resident block per heavy chunk when possible
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &hocc, (const void*)pick_heavy(ctx->d, 1), 256, ctx->heavy_smem));
+            int hocc = 0;   // one resident block per heavy chunk (tile) when possible
+            if (KM_HEAVY_TILES) {
+                // the staged super list (K float4) and one tile list (K u16)
+                ctx->heavy_smem = (int)(sizeof(km::HeavyTileSmem) + sizeof(float4) * ctx->K +
+                                        sizeof(unsigned short) * ctx->K);
+                for (int mode = 1; mode <= 3; ++mode)
+                    CK(allow_smem((const void*)pick_heavy_tiles(ctx->d, mode), ctx->heavy_smem));
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                    &hocc, (const void*)pick_heavy_tiles(ctx->d, 1), 256, ctx->heavy_smem));
+            } else {
+                ctx->heavy_smem = (int)(sizeof(km::HeavySmem<3>) + sizeof(float4) * ctx->K +
+                                        sizeof(unsigned short) * km::kHeavyWarps * ctx->K);
+                for (int mode = 1; mode <= 3; ++mode)
+                    CK(allow_smem((const void*)pick_heavy(ctx->d, mode), ctx->heavy_smem));
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                    &hocc, (const void*)pick_heavy(ctx->d, 1), 256, ctx->heavy_smem));
+            }
             ctx->heavy_grid = sms * std::max(hocc, 1);
         }
         if (ctx->path == 0 && (ctx->flags & KMEANS_FLAG_PERSIST)) {
@@ -739,7 +766,14 @@ kmeans_status launch_assign(kmeans_ctx* ctx, int mode, int mu_sel, int ignore_do
                         ctx->row_stride, ctx->labels_sorted,
                         ctx->cand_count, ctx->heavy, ctx->heavy_count, ctx->keep_n));
         if (A) ctx->launches += 1;
-        if (A && ctx->path == 1) {
+        if (A && ctx->path == 1 && KM_HEAVY_TILES) {
+            HeavyTileFn hf = pick_heavy_tiles(ctx->d, mode);
+            hf<<<ctx->heavy_grid, 256, ctx->heavy_smem, ctx->stream>>>(
+                ctx->X, ctx->N, ctx->K, ctx->st, ignore_done, ctx->slist, ctx->scl, ctx->scount,
+                ctx->heavy, ctx->heavy_count, ctx->cpart, ctx->row_stride, ctx->labels_sorted,
+                ctx->htile, ctx->hctr);
+            ctx->launches += 1;
+        } else if (A && ctx->path == 1) {
             HeavyFn hf = pick_heavy(ctx->d, mode);
             hf<<<ctx->heavy_grid, 256, ctx->heavy_smem, ctx->stream>>>(
                 ctx->X, ctx->N, ctx->K, ctx->cneg, ctx->st, mu_sel, ignore_done, ctx->cbox,
@@ -1555,6 +1589,8 @@ void kmeans_destroy(kmeans_ctx* ctx) {
         pool_free(ctx, ctx->scount);
         pool_free(ctx, ctx->heavy);
         pool_free(ctx, ctx->heavy_count);
+        pool_free(ctx, ctx->htile);
+        pool_free(ctx, ctx->hctr);
         pool_free(ctx, ctx->perm);
         pool_free(ctx, ctx->init_pairs);
         pool_free(ctx, ctx->init_pos);
@@ -1701,7 +1737,10 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
           pool_alloc(ctx, &ctx->scl, sizeof(float4) * (size_t)K * ctx->n_super) != cudaSuccess ||
           pool_alloc(ctx, &ctx->scount, sizeof(int) * (size_t)ctx->n_super) != cudaSuccess ||
           pool_alloc(ctx, &ctx->heavy, sizeof(int) * (size_t)ctx->n_chunks) != cudaSuccess ||
-          pool_alloc(ctx, &ctx->heavy_count, sizeof(int)) != cudaSuccess)) ||
+          pool_alloc(ctx, &ctx->heavy_count, sizeof(int)) != cudaSuccess ||
+          pool_alloc(ctx, &ctx->htile, sizeof(double2) * km::kHeavyWarps * (size_t)ctx->n_chunks) !=
+              cudaSuccess ||
+          pool_alloc(ctx, &ctx->hctr, sizeof(int) * (size_t)ctx->n_chunks) != cudaSuccess)) ||
         pool_alloc(ctx, &ctx->flag, sizeof(int)) != cudaSuccess ||
         (ctx->fused && pool_alloc(ctx, &ctx->brow, sizeof(double) * 2 * (size_t)ctx->nE *
                                                        ctx->fused_grid) != cudaSuccess) ||
@@ -1721,7 +1760,9 @@ kmeans_status kmeans_create(kmeans_ctx** out, const float* points, int64_t N, in
         ((ctx->path == 0 || ctx->sorted) &&
          cudaMemsetAsync(ctx->cpart, 0, sizeof(double) * ctx->row_stride * (size_t)ctx->n_chunks,
                          ctx->stream) != cudaSuccess) ||
-        cudaMemsetAsync(ctx->st, 0, sizeof(DevState), ctx->stream) != cudaSuccess) {
+        cudaMemsetAsync(ctx->st, 0, sizeof(DevState), ctx->stream) != cudaSuccess ||
+        (ctx->hctr &&
+         cudaMemsetAsync(ctx->hctr, 0, sizeof(int) * (size_t)ctx->n_chunks, ctx->stream) != cudaSuccess)) {
         cuda_fail(ctx, cudaGetLastError(), "cudaMemsetAsync");
         return fail(KMEANS_ECUDA);
     }

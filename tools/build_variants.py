@@ -16,6 +16,9 @@ VARIANTS = {
     "sup32": ("KM_SUPER_CHUNKS=32",),
     "sup128": ("KM_SUPER_CHUNKS=128",),
     "lfwd": ("KM_LARGE_REVERSE=0",),          # large-K pruned kernel: chunks in curve order
+    "htold": ("KM_HEAVY_TILES=0",),
+    "htb3": ("KM_HEAVY_TILE_MINB=3",),        # k_assign_heavy_tiles: <= 85 registers
+    "htb4": ("KM_HEAVY_TILE_MINB=4",),        # k_assign_heavy_tiles: <= 64 registers           # heavy chunks: one block per chunk (k_assign_heavy)
     "lnosplit": ("KM_LARGE_SPLIT_WARPS=0",),   # large K: never split into labels + accumulate
     "lsnpl1": ("KM_LARGE_SPLIT_NPL=1",),       # split labels pass: 4 points per lane
     "lsnpl2": ("KM_LARGE_SPLIT_NPL=2",),       # split labels pass: 8 points per lane
