@@ -12,8 +12,9 @@
 //                   f32x2), strict-< argmin (lowest index on ties), fused fp64
 //                   sums / counts / inertia -> one sparse row per chunk
 //                                                                        PAPER.md:45-52
-//   k_prune / k_assign_heavy   K > 16: super-box candidate lists; chunks with
-//                   more than 64 candidates, one 8-warp block each
+//   k_prune / k_assign_heavy_tiles   K > 16: super-box candidate lists; chunks
+//                   with more than 64 candidates, one 8-warp block per 128-point
+//                   tile (k_assign_heavy: one block per chunk, KM_HEAVY_TILES=0)
 //   k_assign_chunk  full scan (small shards, KMEANS_FLAG_NO_SORT), K <= 16:
 //                   one warp per 2048-point chunk, centroids in registers,
 //                   exact argmin via FMNMX3 + select, per-lane fp64 columns
@@ -664,12 +665,16 @@ __device__ __forceinline__ float unord_f32(unsigned u) {
 
 // Global bounding box of the input (ordered-int min/max atomics: order-free)
 // plus the non-finite check.  box[0..d) = min, box[d..2d) = max (ordered ints).
-__global__ void k_input_bbox(const float* __restrict__ in, int64_t N, int d, int64_t si, int64_t sj,
+// d is a template argument: the per-axis registers stay registers (a runtime d
+// put them on the stack: 3x slower at create).
+template <int d>
+__global__ void k_input_bbox(const float* __restrict__ in, int64_t N, int64_t si, int64_t sj,
                              unsigned* __restrict__ box, int* __restrict__ flag) {
     unsigned mn[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, mx[3] = {0u, 0u, 0u};
     int bad = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) {
+#pragma unroll
         for (int j = 0; j < d; ++j) {
             const float v = in[i * si + (int64_t)j * sj];
             bad |= !isfinite(v);
@@ -678,6 +683,7 @@ __global__ void k_input_bbox(const float* __restrict__ in, int64_t N, int d, int
             mx[j] = max(mx[j], o);
         }
     }
+#pragma unroll
     for (int j = 0; j < d; ++j) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -743,20 +749,23 @@ __device__ __forceinline__ void hilbert_transpose(unsigned (&x)[3], int d, int b
 // isotropic grid over the global box -- cubic cells keep chunk boxes compact
 // even when the box is very elongated (C5's far outliers), and the fine grid
 // keeps the dense regions resolved -- with the identity permutation as values.
-template <typename KeyT>   // uint32 (d * qbits <= 32) or uint64 keys
-__global__ void k_morton(const float* __restrict__ in, int64_t N, int d, int64_t si, int64_t sj,
+template <typename KeyT, int d>   // uint32 (d * qbits <= 32) or uint64 keys; d = 2 or 3
+__global__ void k_morton(const float* __restrict__ in, int64_t N, int64_t si, int64_t sj,
                          const unsigned* __restrict__ box, int qbits, int hilbert,
                          KeyT* __restrict__ keys, int32_t* __restrict__ iota) {
     const double qmax = (double)((1ull << qbits) - 1ull);   // qbits <= 32 (2D), <= 21 (3D)
     double lo[3], sc[3], ext = 0.0;
+#pragma unroll
     for (int j = 0; j < d; ++j) {
         lo[j] = (double)unord_f32(box[j]);
         ext = fmax(ext, (double)unord_f32(box[d + j]) - lo[j]);
     }
+#pragma unroll
     for (int j = 0; j < d; ++j) sc[j] = (ext > 0.0) ? qmax / ext : 0.0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) {
         unsigned long long q[3] = {0ull, 0ull, 0ull};
+#pragma unroll
         for (int j = 0; j < d; ++j) {
             double t = ((double)in[i * si + (int64_t)j * sj] - lo[j]) * sc[j];
             t = fmin(fmax(t, 0.0), qmax);

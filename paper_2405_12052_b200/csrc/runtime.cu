@@ -6,6 +6,7 @@
 // into a CUDA graph [assign+reduce -> merge -> (NCCL allreduce) -> update] and
 // replayed; the stop rule lives on the device (DevState::done), so the host only
 // polls between graph replays.
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -1220,8 +1221,9 @@ kmeans_status sort_points(kmeans_ctx* ctx, const float* src, int64_t si, int64_t
     cudaError_t e = cudaMemcpyAsync(box, hb2, sizeof(unsigned) * 2 * d, cudaMemcpyHostToDevice,
                                     ctx->stream);
     auto radix = [&](auto* k1, auto* k2) {
-        km::k_morton<<<blocks, 256, 0, ctx->stream>>>(src, N, d, si, sj, box, qbits, hilbert, k1,
-                                                      iota);
+        using KeyT = std::remove_pointer_t<decltype(k1)>;
+        (d == 2 ? km::k_morton<KeyT, 2> : km::k_morton<KeyT, 3>)<<<blocks, 256, 0, ctx->stream>>>(
+            src, N, si, sj, box, qbits, hilbert, k1, iota);
         ctx->launches += 1;
         tr.mark(ctx->stream, "bbox + morton keys");
         cudaError_t r = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k1, k2, iota,
@@ -1233,7 +1235,8 @@ kmeans_status sort_points(kmeans_ctx* ctx, const float* src, int64_t si, int64_t
         return r;
     };
     if (e == cudaSuccess) {
-        km::k_input_bbox<<<blocks, 256, 0, ctx->stream>>>(src, N, d, si, sj, box, ctx->flag);
+        (d == 2 ? km::k_input_bbox<2> : km::k_input_bbox<3>)<<<blocks, 256, 0, ctx->stream>>>(
+            src, N, si, sj, box, ctx->flag);
         ctx->launches += 1;
         e = k32 ? radix((uint32_t*)keys, (uint32_t*)keys2)
                 : radix((unsigned long long*)keys, (unsigned long long*)keys2);
