@@ -420,7 +420,7 @@ def main():
         t_assign = 0.5 * (pre_assign + post_assign)
         if info["sorted"]:
             kname = ("k_assign_pruned" if info["path"] == 0
-                     else "k_prune+k_assign_pruned+k_assign_heavy")
+                     else "k_prune+k_assign_pruned+k_assign_heavy_tiles")
         else:
             kname = "k_assign_chunk" if info["path"] == 0 else "k_assign_large"
         # per-stage device time (each stage alone, back-to-back launches)

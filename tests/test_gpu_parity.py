@@ -848,8 +848,8 @@ def test_full_size_c5_parity():
 
 def test_heavy_chunks_large_k():
     """Large K with far outliers and sparse tails: chunk boxes that span huge
-    empty regions keep more than 64 candidates and go to k_assign_heavy (one
-    block per chunk, candidates in batches); labels must stay bit-exact."""
+    empty regions keep more than 64 candidates and go to k_assign_heavy_tiles
+    (one block per 128-point tile); labels must stay bit-exact."""
     rng = np.random.default_rng(21)
     w = datagen.WORKLOADS["C5"]
     X = datagen.generate(w, N=200_000)
