@@ -846,6 +846,29 @@ def test_full_size_c5_parity():
         assert np.array_equal(mu_next[ks[1:]], mu[ks[1:]])
 
 
+@pytest.mark.parametrize("d,K", [(3, 100), (3, 128), (2, 100), (2, 300)])
+def test_heavy_tiles_mid_k(d, K):
+    """Heavy chunks at 64 < K <= 128 (each tile's stretch of the chunk row is
+    K < 128 entries) and in 2D: k_assign_heavy_tiles against the oracle, one
+    step and a 2-iteration fit through the iteration graph."""
+    rng = np.random.default_rng(1000 + 10 * K + d)
+    w = datagen.WORKLOADS["NS" if d == 3 else "C3"]
+    N = 100_003
+    X = datagen.generate(w, N=N)
+    far = rng.uniform(-3000, 3000, (5000, d)).astype(np.float32)
+    X[rng.choice(N, 5000, replace=False)] = far
+    init = rng.choice(N, K, replace=False)
+    mu = X[init].astype(np.float64)
+    with km.Context(X, K, sort=True) as c:
+        check_step(X, mu, ctx=c, tag=f"heavy d={d} K={K}")
+        st = c.candidate_stats()
+    assert st["max"] > 64, st   # the heavy path was exercised
+    o1 = oracle.fit(X, K, init, 0.0, 2)
+    with km.Context(X, K, sort=True) as c:
+        r = c.fit(init, 0.0, 2)
+    assert np.array_equal(r["labels"], o1["labels"])
+
+
 def test_heavy_chunks_large_k():
     """Large K with far outliers and sparse tails: chunk boxes that span huge
     empty regions keep more than 64 candidates and go to k_assign_heavy_tiles
