@@ -2075,6 +2075,51 @@ __device__ __forceinline__ int nth_set_bit(unsigned m, int r) {
     return pos;
 }
 
+// Strict-< argmin of a lane's 4 points over positions [t0, t1) of a tile list
+// whose centroids are gathered contiguously (tcl[t] = staged centroid of
+// list position t): one LDS.128 per entry, four entries in flight per step;
+// the updates stay in ascending position order (lowest position on ties).
+template <int D>
+__device__ __forceinline__ void argmin_walk_gathered(const float4* tcl, int t0, int t1, float2 xa,
+                                                     float2 ya, float2 za, float2 xb, float2 yb,
+                                                     float2 zb, float (&best)[4], int (&sl)[4]) {
+    {
+        const float4 cc = tcl[t0];
+        const float2 da = form_d2<D>(xa, ya, za, cc), db = form_d2<D>(xb, yb, zb, cc);
+        best[0] = da.x; best[1] = da.y; best[2] = db.x; best[3] = db.y;
+        sl[0] = sl[1] = sl[2] = sl[3] = t0;
+    }
+    int t = t0 + 1;
+    for (; t + 3 < t1; t += 4) {
+        float2 da[4], db[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float4 cc = tcl[t + u];
+            da[u] = form_d2<D>(xa, ya, za, cc);
+            db[u] = form_d2<D>(xb, yb, zb, cc);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (da[u].x < best[0]) { best[0] = da[u].x; sl[0] = t + u; }
+            if (da[u].y < best[1]) { best[1] = da[u].y; sl[1] = t + u; }
+            if (db[u].x < best[2]) { best[2] = db[u].x; sl[2] = t + u; }
+            if (db[u].y < best[3]) { best[3] = db[u].y; sl[3] = t + u; }
+        }
+    }
+    for (; t < t1; ++t) {
+        const float4 cc = tcl[t];
+        const float2 da = form_d2<D>(xa, ya, za, cc), db = form_d2<D>(xb, yb, zb, cc);
+        if (da.x < best[0]) { best[0] = da.x; sl[0] = t; }
+        if (da.y < best[1]) { best[1] = da.y; sl[1] = t; }
+        if (db.x < best[2]) { best[2] = db.x; sl[2] = t; }
+        if (db.y < best[3]) { best[3] = db.y; sl[3] = t; }
+    }
+}
+
+#ifndef KM_HEAVY_GATHER
+#define KM_HEAVY_GATHER 1   // k_assign_heavy_tiles: tile-list centroids gathered before the walk
+#endif
+
 struct alignas(16) HeavyTileSmem {   // size a multiple of 16: float4 cl[] follows
     float2 part[kHeavyWarps][4][32];   // split walk: (distance, slot) per warp, point, lane
     float2 fin[4][32];                 // the tile's (distance, slot) per point and lane
@@ -2082,7 +2127,8 @@ struct alignas(16) HeavyTileSmem {   // size a multiple of 16: float4 cl[] follo
     int wMi[kHeavyWarps];
     int wcnt[kHeavyWarps];
     int last;
-    // followed by float4 cl[K] (the super list's staged centroids) and
+    // followed by float4 cl[K] (the super list's staged centroids), with
+    // KM_HEAVY_GATHER float4 tcl[K] (the tile list's centroids), and
     // unsigned short tl[K] (the tile list: super-list positions)
 };
 
@@ -2098,9 +2144,11 @@ k_assign_heavy_tiles(const float* __restrict__ X, int64_t n, int K, const DevSta
     extern __shared__ __align__(16) unsigned char smem_raw[];
     HeavyTileSmem& S = *reinterpret_cast<HeavyTileSmem*>(smem_raw);
     float4* cl = reinterpret_cast<float4*>(smem_raw + sizeof(HeavyTileSmem));   // [K]
-    unsigned short* tl = reinterpret_cast<unsigned short*>(cl + K);             // [K]
+    float4* tcl = cl + K;                                                       // [K] (gather)
+    unsigned short* tl = reinterpret_cast<unsigned short*>(cl + (KM_HEAVY_GATHER ? 2 : 1) * K);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ts = K < kLaneTile ? K : kLaneTile;   // row entries reserved per tile
+    (void)tcl;
     const int nitems = *heavy_count * kHeavyWarps;
     for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
         const int h = it / kHeavyWarps, T = it % kHeavyWarps;
@@ -2232,10 +2280,20 @@ k_assign_heavy_tiles(const float* __restrict__ X, int64_t n, int K, const DevSta
         float best[4];
         int sl[4];
         const bool split = nt >= kHeavyTileSplit;   // every eighth non-empty
+#if KM_HEAVY_GATHER
+        if (split) {   // long lists: the tile list's centroids made contiguous
+            for (int i = tid; i < nt; i += blockDim.x) tcl[i] = cl[tl[i]];
+            __syncthreads();
+        }
+#endif
         if (split) {
             const int t0 = (int)((int64_t)nt * warp / kHeavyWarps);
             const int t1 = (int)((int64_t)nt * (warp + 1) / kHeavyWarps);
+#if KM_HEAVY_GATHER
+            argmin_walk_gathered<D>(tcl, t0, t1, xa, ya, za, xb, yb, zb, best, sl);
+#else
             argmin_walk<D>(tl, cl, t0, t1, xa, ya, za, xb, yb, zb, best, sl);
+#endif
 #pragma unroll
             for (int i = 0; i < 4; ++i) S.part[warp][i][lane] = make_float2(best[i], __int_as_float(sl[i]));
             __syncthreads();

@@ -618,7 +618,8 @@ kmeans_status configure(kmeans_ctx* ctx) {
             int hocc = 0;   // one resident block per heavy chunk (tile) when possible
             if (KM_HEAVY_TILES) {
                 // the staged super list (K float4) and one tile list (K u16)
-                ctx->heavy_smem = (int)(sizeof(km::HeavyTileSmem) + sizeof(float4) * ctx->K +
+                ctx->heavy_smem = (int)(sizeof(km::HeavyTileSmem) +
+                                        sizeof(float4) * (KM_HEAVY_GATHER ? 2 : 1) * ctx->K +
                                         sizeof(unsigned short) * ctx->K);
                 for (int mode = 1; mode <= 3; ++mode)
                     CK(allow_smem((const void*)pick_heavy_tiles(ctx->d, mode), ctx->heavy_smem));
