@@ -2488,14 +2488,26 @@ k_prune(const float4* __restrict__ cneg_buf, const DevState* __restrict__ st, in
             dmax2 += dx * dx;
         }
     };
+    // thread tid takes centroids tid + 256 j (K <= 1024: j < 4); both passes
+    // use the same bounds and centroid, kept in registers
+    constexpr int kPer = 1024 / 256;
+    KM_CHECK(K <= kPer * 256 && blockDim.x == 256);
+    double ca_[kPer], cb_[kPer];
+    float4 cv_[kPer];
     double Mt = (double)pos_inf();   // this thread's min dmax2 and its centroid
     int Mkt = 0x7fffffff;
-    for (int k = tid; k < K; k += blockDim.x) {
-        double a, b;
-        bounds(k, a, b);
-        if (b < Mt) {
-            Mt = b;
-            Mkt = k;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const int k = tid + 256 * j;
+        ca_[j] = cb_[j] = 0.0;
+        cv_[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k < K) {
+            bounds(k, ca_[j], cb_[j]);
+            cv_[j] = cneg[k];
+            if (cb_[j] < Mt) {
+                Mt = cb_[j];
+                Mkt = k;
+            }
         }
     }
     double M = Mt;
@@ -2518,16 +2530,15 @@ k_prune(const float4* __restrict__ cneg_buf, const DevState* __restrict__ st, in
     const float4 av = cneg[Mk];
     const float ca[3] = {-av.x, -av.y, -av.z};
     const double thr = prune_threshold(M);
-    for (int k0 = 0; k0 < K; k0 += blockDim.x) {
-        const int k = k0 + tid;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        if (256 * j >= K) break;   // block-uniform
+        const int k = tid + 256 * j;
         bool cand = false;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 v = cv_[j];
         if (k < K) {
-            double a, b;
-            bounds(k, a, b);
-            v = cneg[k];
             const float c[3] = {-v.x, -v.y, -v.z};
-            cand = a <= thr && !bisector_excludes<D>(c, ca, lo, hi, b, M);
+            cand = ca_[j] <= thr && !bisector_excludes<D>(c, ca, lo, hi, cb_[j], M);
         }
         const unsigned mask = __ballot_sync(0xffffffffu, cand);
         if (lane == 0) wcnt[warp] = __popc(mask);
