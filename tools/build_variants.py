@@ -18,8 +18,8 @@ VARIANTS = {
     "lfwd": ("KM_LARGE_REVERSE=0",),          # large-K pruned kernel: chunks in curve order
     "htold": ("KM_HEAVY_TILES=0",),            # heavy chunks: one block per chunk (k_assign_heavy)
     "hnog": ("KM_HEAVY_GATHER=0",),            # heavy tiles: walk through the tile list (no gathered centroids)
-    "htb3": ("KM_HEAVY_TILE_MINB=3",),        # k_assign_heavy_tiles: <= 85 registers
-    "htb4": ("KM_HEAVY_TILE_MINB=4",),        # k_assign_heavy_tiles: <= 64 registers           # heavy chunks: one block per chunk (k_assign_heavy)
+    "htb3": ("KM_HEAVY_TILE_MINB=3",),         # k_assign_heavy_tiles: <= 85 registers
+    "htb4": ("KM_HEAVY_TILE_MINB=4",),         # k_assign_heavy_tiles: <= 64 registers
     "lnosplit": ("KM_LARGE_SPLIT_WARPS=0",),   # large K: never split into labels + accumulate
     "lsnpl1": ("KM_LARGE_SPLIT_NPL=1",),       # split labels pass: 4 points per lane
     "lsnpl2": ("KM_LARGE_SPLIT_NPL=2",),       # split labels pass: 8 points per lane
